@@ -1,0 +1,219 @@
+"""O4 — rank-k column-pivoted QR in the paper's low precision, written plainly.
+
+TEST INFRASTRUCTURE ONLY (see oracle/rounding.py header).  Never imported by
+the product path; imports nothing from it.
+
+What is computed:
+  * Algorithm 2 line 2: A_L = fl(A) — done by the caller with
+    `rounding.round_to`, optionally after range scaling (`scale_matrix`).
+  * Algorithm 2 line 4 and Eq. (6)-(7): A Z = Q R, rank k,
+    column pivoting on the largest remaining column norm.  The paper's QR is
+    modified Gram-Schmidt; BASELINE.json's north_star asks for Householder.
+    `qrcp_householder` is the Householder form (reading R3) and
+    `qrcp_mgs` is the paper-literal MGS form of SPEC S:189-197, kept as an
+    independent cross-check (same pivots and |R| in exact arithmetic).
+  * Simulated low precision: values are "cast to half or single" but
+    "accumulate error exclusively in single precision".  Precision model used by
+    both this oracle and the CUDA path (readings R4-R6):
+      - element arithmetic (the reflector update W <- W - v f^T) in fp32;
+      - the working matrix is re-stored (rounded) to the low format every `nb`
+        steps — nb = 1 is SPEC's store-after-every-update, nb > 1 the blocked
+        implementation the paper names as future work;
+      - reductions over rows (column norms, W^T u) accumulated in fp64 (reading
+        R5: sequential fp32 sums stagnate at m = 2^24 rows);
+      - pivot norms recomputed from the current working matrix every step;
+      - ties broken toward the lowest original column index;
+      - R rows normalised so that R_jj >= 0.
+    fmt = "fp64" runs the same algorithm entirely in fp64 (Algorithm 1).
+  * Tolerance-driven rank (reading R8; "||A - BC|| << eps"): stop before
+    step j when sqrt(sum_{i>=j} ||W(j:m, i)||^2) <= eps * ||A_L||_F.
+  * Underflow: status "underflow" when the selected pivot norm
+    squared underflows the fp32 normal range or the pivot column is zero.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .rounding import fmt_of, round_to, DOUBLE, SINGLE
+
+
+@dataclass
+class QRCPResult:
+    perm: np.ndarray            # (n,) 0-based original column index at each position
+    R: np.ndarray               # (k_out, n) float64 holding working-precision values, pivoted order
+    k_out: int
+    status: str                 # "ok" | "underflow"
+    V: np.ndarray               # (m, k_out) Householder vectors (v_j = 1, zeros above)
+    tau: np.ndarray             # (k_out,)
+    top2: np.ndarray            # (k_out, 2) the two largest candidate norms at each step
+    maxnorm0: float             # max_i ||A_L(:, i)|| (scale for tie certification)
+    normAL: float               # ||A_L||_F
+    resid: list = field(default_factory=list)   # sqrt(sum of remaining norms^2) before each step (+ after the last)
+
+    @property
+    def I(self) -> np.ndarray:
+        return self.perm[: self.k_out].copy()
+
+
+def scale_factor(A_D: np.ndarray, scaling: str) -> float:
+    """Range scaling s applied before rounding (BASELINE.json configs[1]; reading R7).
+
+    "none": s = 1; "maxabs": s = 1/max|a_ij| (literal C2 text); "pow2":
+    s = 2^-ceil(log2 max|a_ij|), an exact power of two.
+    """
+    if scaling == "none":
+        return 1.0
+    mx = float(np.max(np.abs(A_D)))
+    if mx == 0.0:
+        return 1.0
+    if scaling == "maxabs":
+        return 1.0 / mx
+    if scaling == "pow2":
+        return math.ldexp(1.0, -math.ceil(math.log2(mx)))
+    raise ValueError(scaling)
+
+
+def make_AL(A_D: np.ndarray, fmt: str, scaling: str = "none"):
+    """A_L = fl_L(s * A_D) with a single RNE rounding from fp64 (reading R7)."""
+    s = scale_factor(A_D, scaling)
+    AL = round_to(np.asarray(A_D, dtype=np.float64) * s, fmt).reshape(A_D.shape)
+    return np.asfortranarray(AL), s
+
+
+def _work_dtype(fmt):
+    return np.float64 if fmt_of(fmt) is DOUBLE else np.float32
+
+
+def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1,
+                     eps: float = 0.0) -> QRCPResult:
+    """Householder QRCP of the already-rounded A_L, in the precision model above.
+
+    Step j (0-based), following Eq. (6)-(7):
+      0. every nb steps (j > 0, j % nb == 0): W(j:, j:) <- fl_L(W(j:, j:))     [store point]
+      1. s_i = ||W(j:m, i)||^2, i >= j (fp64 sum of exact fp32 squares)         [norms]
+      2. p = argmax s_i (ties: lowest original index); swap columns j <-> p     [pivot, Z]
+      3. u = W(j:m, j); beta = -sign(u_0) sqrt(s_j); v = u / (u_0 - beta), v_0 = 1;
+         tau = (beta - u_0) / beta                                              [reflector]
+      4. w = W(j:m, j:)^T u (fp64 accumulation); R(j, i) = w_i / beta; the new
+         row j equals x_i - f_i with x = W(j, j:), so f = x - w / beta
+         (= tau * W^T v); W(j:m, j:) <- W - v f^T in fp32                       [update]
+      5. R(j, :) *= sign(beta) so that R_jj = |beta| >= 0.
+    """
+    fmtL = fmt_of(fmt)
+    wdt = _work_dtype(fmt)
+    A_L = np.asarray(A_L, dtype=np.float64)
+    m, n = A_L.shape
+    if not (1 <= k_max <= min(m, n)):
+        raise ValueError("k out of range (DimensionError)")
+    W = np.array(A_L, dtype=wdt, order="F")
+    perm = np.arange(n)
+    R = np.zeros((k_max, n), dtype=np.float64)
+    V = np.zeros((m, k_max), dtype=np.float64)
+    tau = np.zeros(k_max)
+    top2 = np.zeros((k_max, 2))
+    col2 = np.sum(A_L * A_L, axis=0)
+    normAL = math.sqrt(float(np.sum(col2)))
+    maxnorm0 = math.sqrt(float(np.max(col2))) if n else 0.0
+    resid = []
+    status, k_out = "ok", k_max
+    for j in range(k_max):
+        if j > 0 and j % nb == 0 and fmtL is not DOUBLE:
+            W[j:, j:] = round_to(W[j:, j:].astype(np.float64), fmtL).reshape(m - j, n - j)
+        Wt = W[j:, j:].astype(np.float64)
+        s = np.sum(Wt * Wt, axis=0)                           # step 1
+        resid.append(math.sqrt(float(np.sum(s))))
+        if eps > 0.0 and j > 0 and resid[-1] <= eps * normAL:
+            k_out = j
+            break
+        cand = np.flatnonzero(s == s.max())                    # step 2, tie -> lowest original index
+        best = int(cand[np.argmin(perm[j + cand])])
+        srt = np.sort(s)[::-1]
+        top2[j] = [math.sqrt(srt[0]), math.sqrt(srt[1]) if len(srt) > 1 else 0.0]
+        p = j + best
+        tiny = DOUBLE.min_normal if fmtL is DOUBLE else SINGLE.min_normal
+        if s[best] < tiny or s[best] == 0.0:
+            status, k_out = "underflow", j
+            break
+        if p != j:
+            W[:, [j, p]] = W[:, [p, j]]
+            Wt[:, [0, best]] = Wt[:, [best, 0]]
+            R[:j, [j, p]] = R[:j, [p, j]]
+            perm[[j, p]] = perm[[p, j]]
+            s[[0, best]] = s[[best, 0]]
+        u = Wt[:, 0]                                           # step 3
+        sj = float(s[0])
+        u0 = float(u[0])
+        beta = -math.copysign(math.sqrt(sj), u0)
+        c = 1.0 / (u0 - beta)
+        v = (u * c).astype(wdt)
+        v[0] = 1.0
+        tau[j] = (beta - u0) / beta
+        w = Wt.T @ u                                           # step 4
+        Rraw = w / beta
+        x = Wt[0, :]
+        f = (x - Rraw).astype(wdt)
+        W[j:, j:] = W[j:, j:] - np.outer(v, f).astype(wdt)
+        R[j, j:] = (Rraw * math.copysign(1.0, beta)).astype(wdt)   # step 5
+        V[j:, j] = v
+    if status == "ok" and k_out == k_max and k_max < min(m, n):
+        Wt = W[k_max:, k_max:].astype(np.float64)
+        resid.append(math.sqrt(float(np.sum(Wt * Wt))))       # remaining mass after k steps
+    R = R[:k_out]
+    return QRCPResult(perm, R, k_out, status, V[:, :k_out], tau[:k_out], top2[:k_out],
+                      maxnorm0, normAL, resid)
+
+
+def qrcp_mgs(A_L: np.ndarray, k: int, fmt: str = "fp64"):
+    """Paper-literal pivoted MGS, the O4b cross-check.
+
+    For j = 1..k: (a) recompute the norms of the trailing columns; (b) swap the
+    max-norm column (ties: lowest index) into position j; (c) r_jj = norm;
+    (d) q_j = w_j / r_jj stored to the low format; (e) for i > j:
+    r_ji = fl_L(q_j . w_i), w_i = fl_L(w_i - r_ji q_j).  Arithmetic in the
+    accumulation format (fp32 for fp16/fp32, fp64 for fp64).
+    Returns (perm, R (k x n), Q (m x k)).
+    """
+    fmtL = fmt_of(fmt)
+    wdt = _work_dtype(fmt)
+    st = (lambda a: a.astype(wdt)) if fmtL is DOUBLE else (
+        lambda a: round_to(np.asarray(a, dtype=np.float64), fmtL).astype(wdt))
+    A = np.array(A_L, dtype=wdt, order="F")
+    m, n = A.shape
+    perm = np.arange(n)
+    R = np.zeros((k, n))
+    Q = np.zeros((m, k))
+    for j in range(k):
+        nrm = np.sqrt(np.sum(A[:, j:].astype(np.float64) ** 2, axis=0))
+        p = j + int(np.argmax(nrm))          # argmax returns the first (lowest index) maximum
+        if p != j:
+            A[:, [j, p]] = A[:, [p, j]]
+            R[:j, [j, p]] = R[:j, [p, j]]
+            perm[[j, p]] = perm[[p, j]]
+        rjj = float(st(np.array([math.sqrt(float(np.sum(A[:, j].astype(np.float64) ** 2)))]))[0])
+        q = st(A[:, j].astype(np.float64) / rjj)
+        R[j, j] = rjj
+        qd = q.astype(np.float64)
+        rj = st(qd @ A[:, j + 1:].astype(np.float64)).astype(np.float64)   # r_ji = fl_L(q_j . w_i)
+        R[j, j + 1:] = rj
+        A[:, j + 1:] = st(A[:, j + 1:].astype(np.float64) - np.outer(qd, rj)).reshape(m, n - j - 1)
+        Q[:, j] = q
+    return perm, R, Q
+
+
+def form_Q(V: np.ndarray, tau: np.ndarray) -> np.ndarray:
+    """Q(:, 0:k) = H_0 H_1 ... H_{k-1} I(:, 0:k) in fp64, H_j = I - tau_j v_j v_j^T."""
+    m, k = V.shape
+    Q = np.eye(m, k)
+    for j in reversed(range(k)):
+        v = V[:, j]
+        Q -= tau[j] * np.outer(v, v @ Q)
+    return Q
+
+
+def certified_steps(res: QRCPResult, c_tie: float = 64.0, u_acc: float = SINGLE.u) -> np.ndarray:
+    """Boolean per step: top-2 margin > c_tie * u_acc * max_i ||a_i|| (reading R10)."""
+    thr = c_tie * u_acc * res.maxnorm0
+    return (res.top2[:, 0] - res.top2[:, 1]) > thr
