@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark of the mixed-precision ID hot path (arXiv 2012.00706) on B200.
+
+One "step" = one full rank-k ID of the workload through the C ABI:
+  scale + round A_D -> A_L, low-precision pivoted Householder QR (k steps),
+  fp64 coefficients P (LSQ refit), fp64 error ||A_D - A_D(:,I)P||_F.
+Workload: BASELINE.json configs[3] ("C4", 128^3 x 1024,
+64 Fourier modes, k = 100, fp16) — the largest config that fits one GPU
+(configs[4] is 256 GiB).  With --gpus N (torchrun) every rank holds one C4-sized
+row shard of an N x taller snapshot matrix (weak scaling; one NCCL allreduce per
+QR step, the path's real exchange).
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rank-k ID time & TFLOP/s (lowprec QRCP + fp64 coeffs) at 1/2/4/8 B200"
+
+
+def flops(m, n, k, mode="lsq"):
+    """Algorithmic flops: Householder QRCP, fp64 coefficients, error."""
+    fq = sum(4.0 * (m - j) * (n - j - 1) + 3.0 * (m - j) for j in range(k)) + 2.0 * m * n
+    fc = (4.0 * m * k * k + 2.0 * m * k * n + k * k * n) if mode == "lsq" else k * k * (n - k)
+    fe = 2.0 * m * k * (n - k) + 3.0 * m * n
+    return fq, fc, fe
+
+
+def pass_bytes(m, n, k, nb, s):
+    """Algorithmic bytes of the dominant kernel (k_pass) summed over the k launches:
+    read (m-j)(n-j) s per step, plus a write of the same on store steps (j % nb == 0, j > 0)."""
+    tot = 0.0
+    for j in range(k):
+        e = (m - j) * (n - j) * s
+        tot += e * (2.0 if (j > 0 and j % nb == 0) else 1.0)
+    return tot
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured", d
+    return 6650.0, "fallback", {}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.idx = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except Exception:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_sample(rows, k, nb, fmt, seed=0, repeats=1):
+    """The oracle (as it stands) on a bounded row sample of the workload; returns (seconds, flops, cores)."""
+    import numpy as np
+    from oracle.id import coeffs_lsq, id_error
+    from oracle.qrcp import make_AL, qrcp_householder
+    from synth import gen_config
+    A = gen_config("C4", seed, row0=0, m_loc=rows)
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([t.get("num_threads", 1) for t in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    t0 = time.perf_counter()
+    for _ in range(repeats):
+        AL, s = make_AL(A, fmt, "pow2" if fmt == "fp16" else "none")
+        r = qrcp_householder(AL, k, fmt, nb=nb)
+        P = coeffs_lsq(A, r.I)
+        id_error(A, r.I, P)
+    dt = (time.perf_counter() - t0) / repeats
+    fq, fc, fe = flops(rows, A.shape[1], k)
+    return dt, fq + fc + fe, cores
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--fmt", default="fp16")
+    ap.add_argument("--k", type=int, default=0)
+    ap.add_argument("--nb", type=int, default=4)
+    ap.add_argument("--mode", default="lsq")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--rows", type=int, default=0, help="override rows per GPU (debug)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-rows", type=int, default=16384)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    from synth import config_spec
+    spec = config_spec(args.config)
+    k = args.k or spec.ks[0]
+    rows = args.rows or spec.m
+    scaling = spec.scaling[args.fmt]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        # the oracle, as it stands, on the host cores; each step one bounded sample
+        wsteps = []
+        for i in range(args.warmup + args.steps):
+            dt, fl, cores = cpu_oracle_sample(args.cpu_rows, k, args.nb, args.fmt, args.seed)
+            if i >= args.warmup:
+                wsteps.append(dt)
+        T = sum(wsteps) / len(wsteps)
+        val = fl / T / 1e12
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": T * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32+f64 (simulated fp16)" if args.fmt == "fp16" else "f32+f64",
+                "data": "synthetic",
+                "config": {"workload": f"{args.config} row sample", "rows": args.cpu_rows, "n": spec.n,
+                           "k": k, "fmt": args.fmt, "nb": args.nb, "coef": args.mode},
+                "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                                 "sample": f"first {args.cpu_rows} rows of {args.config} ({args.cpu_rows}x{spec.n}, k={k})"},
+                "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2012_00706_b200 import mpid
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    mpid.lib()
+
+    comm = None
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(mpid.id_nccl_get_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = mpid.id_nccl_comm_init(bytes(uid.cpu().numpy().tobytes()), world, rank)
+
+    # ---- input: this rank's row shard, generated on device ------------------
+    from synth import fourier_params, gen_fourier
+    m_loc = rows
+    m_glob = rows * world
+    row0 = rank * rows
+    if args.config in ("C4", "C5"):
+        fp = fourier_params(spec.extra["N"], spec.extra["L"], spec.n, args.seed)
+        A = gen_fourier(fp, args.seed, row0=row0, m_loc=m_loc, device=dev)
+    else:
+        from synth import gen_config
+        A = torch.from_numpy(np.ascontiguousarray(gen_config(args.config, args.seed).T)).to(dev)
+        m_loc = m_glob = A.shape[1]
+    n = spec.n
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    h = mpid.MPID(A, k_max=k, m_global=m_glob, row_offset=row0, comm=comm, rank=rank, nranks=world,
+                  stream=stream)
+    s_bytes = 2 if args.fmt == "fp16" else 4
+
+    def one_step(profile):
+        q = h.qrcp(args.fmt, scaling, k=k, nb=args.nb, profile=profile)
+        P = h.coeffs(args.mode)
+        e = h.error()
+        return q, P, e
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        q, P, e = one_step(True)
+    st0 = h.stats()
+
+    clocks = Clocks(local_rank)
+    barrier()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    pass_ms, qr_ms, coef_ms, err_ms, round_ms = [], [], [], [], []
+    ev0.record(stream)
+    for _ in range(args.steps):
+        q, P, e = one_step(True)
+        st = h.stats()
+        pass_ms.append(st["t_pass_ms"])
+        qr_ms.append(st["t_qrcp_ms"])
+        round_ms.append(st["t_round_ms"])
+        coef_ms.append(st["t_coef_ms"])
+        err_ms.append(st["t_err_ms"])
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    t_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    ms_step = t_ms / args.steps
+    fq, fc, fe = flops(m_glob, n, q.k, args.mode)
+    value = (fq + fc + fe) / (ms_step * 1e-3) / 1e12
+
+    # ---- roofline of the dominant kernel (k_pass), per launch -----------------
+    peak, peak_kind, peaks = load_peaks()
+    pb = pass_bytes(m_loc, n, q.k, args.nb, s_bytes)
+    pass_avg_ms = statistics.mean(pass_ms)
+    achieved = pb / (pass_avg_ms * 1e-3) / 1e9          # GB/s over the k launches of a step
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "pass_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the C ABI with host buffers ------------------------------
+    e2e = None
+    if not args.no_e2e:
+        Ah = torch.empty((n, m_loc), dtype=torch.float64, pin_memory=True)
+        Ah.copy_(A)
+        del A
+        h.close()
+        torch.cuda.empty_cache()
+        times = []
+        for i in range(args.e2e_steps + 1):
+            barrier()
+            t0 = time.perf_counter()
+            hh = mpid.MPID(Ah, k_max=k, m_global=m_glob, row_offset=row0, comm=comm, rank=rank,
+                           nranks=world, stream=stream, device=dev)
+            qq = hh.qrcp(args.fmt, scaling, k=k, nb=args.nb)
+            PP = hh.coeffs(args.mode)
+            P_host = PP.cpu()
+            ee = hh.error()
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            hh.close()
+            del hh, PP
+            if i > 0:
+                times.append(dt)
+        dt = statistics.mean(times)
+        if world > 1:
+            tt = torch.tensor([dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        e2e = {"value": (fq + fc + fe) / dt / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": int(m_loc * n * 8 * world),
+               "d2h_bytes_per_step": int((k * n * 8 + k * 4 + 16) * world),
+               "ms_per_step": dt * 1e3}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        dt_c, fl_c, cores = cpu_oracle_sample(args.cpu_rows, k, args.nb, args.fmt, args.seed)
+        cpu = {"value": fl_c / dt_c / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+               "sample": f"first {args.cpu_rows} rows of {args.config} ({args.cpu_rows}x{n}, k={k}), one full ID",
+               "seconds": dt_c}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f16 storage / f32 arithmetic QRCP + f64 ID" if args.fmt == "fp16" else "f32 QRCP + f64 ID",
+            "data": "synthetic",
+            "config": {"workload": f"{args.config}: {m_glob}x{n} fp64 Fourier snapshots, k={k}, "
+                                   f"{args.fmt} QRCP (nb={args.nb}), {args.mode.upper()} coefficients",
+                       "rows_per_gpu": m_loc, "n": n, "k": k, "fmt": args.fmt, "nb": args.nb,
+                       "coef": args.mode, "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (A_D 16 GiB, A_L 4 GiB per GPU); no flush"},
+            "stages_ms": {"round": statistics.mean(round_ms), "qrcp_incl_round": statistics.mean(qr_ms),
+                          "coef": statistics.mean(coef_ms), "error": statistics.mean(err_ms),
+                          "pass_total": pass_avg_ms},
+            "tflops_parts": {"qrcp": fq / (statistics.mean(qr_ms) * 1e-3) / 1e12,
+                             "fp64": (fc + fe) / ((statistics.mean(coef_ms) + statistics.mean(err_ms)) * 1e-3) / 1e12},
+            "k_out": q.k, "rel_err_fro": e[1],
+            "roofline": {"kernel": "k_pass (per-step panel pass)", "bound": "hbm", "achieved": achieved,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "peak_kind": peak_kind, "launches_per_step": q.k,
+                         "algorithmic_bytes_per_step": pb},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(st0["kernel_launches"]) * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line))
+    if comm:
+        mpid.id_nccl_comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

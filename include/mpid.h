@@ -1,0 +1,176 @@
+/*
+ * mpid.h — C ABI of the B200-native mixed-precision interpolative decomposition
+ * (ID) hot path, after arXiv 2012.00706 ("PAPER.md"; P:L = PAPER.md line L).
+ *
+ * The operation (Algorithm 2; Eq. (4)-(8)):
+ *   given A_D (m x n, fp64), a target rank k (or a tolerance eps), a low-
+ *   precision format and a range scaling,
+ *     1. A_L = fl_L(s * A_D)                                  (Alg. 2 line 2)
+ *     2. A_L Z = Q R, rank-k column-pivoted Householder QR in the simulated
+ *        low precision (fp16/fp32 storage, fp32 arithmetic)   (Alg. 2 line 4, Eq. (6)-(7))
+ *     3. I = Z(:, 1:k); P(:, I) = I_k, P(:, J) = T with
+ *        T = R11^{-1} R12 (R mode, Eq. (8)) or the fp64 least-squares fit of
+ *        A_D(:, J) on A_D(:, I) (LSQ mode)             (Alg. 2 lines 5-7)
+ *     4. ||A_D - A_D(:, I) P||_F evaluated in fp64             (Remark 2)
+ *
+ * Conventions
+ *   - All matrices are column-major.  Indices are 0-based.
+ *   - Every call is collective over the `nranks` ranks of a row-sharded matrix:
+ *     rank r owns rows [row_offset, row_offset + m_local) of A_D.  With
+ *     nranks > 1 the per-step reductions use the caller's NCCL communicator
+ *     (an ncclComm_t passed as void*; see id_nccl_* below).  Results are
+ *     identical on all ranks.
+ *   - Errors: no C++ exception crosses the ABI; each call returns an id_status
+ *     and id_last_error() gives a message.  ID_ERR_CUDA / ID_ERR_NCCL leave the
+ *     handle unusable (destroy it).
+ *   - Ownership: A_D is borrowed (read-only, must outlive the handle); the
+ *     workspace is caller-owned device memory of id_workspace_bytes() bytes
+ *     (e.g. a torch uint8 tensor); outputs go to caller memory as stated per
+ *     call.  All work is enqueued on the caller's CUDA stream; calls that
+ *     return host values synchronise that stream.
+ */
+#ifndef MPID_H
+#define MPID_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mpid_ctx* id_handle;
+
+/* Low-precision storage formats, Table 1.  Arithmetic is fp32 in both
+ * ("simulated half"). */
+typedef enum { ID_FP16 = 1, ID_FP32 = 2 } id_format;
+
+/* Range scaling before rounding (BASELINE.json configs[1]; reading R7):
+ * NONE: s = 1; MAXABS: s = 1/max|a_ij|; POW2: s = 2^-ceil(log2 max|a_ij|). */
+typedef enum { ID_SCALE_NONE = 0, ID_SCALE_MAXABS = 1, ID_SCALE_POW2 = 2 } id_scaling;
+
+/* Coefficient modes: R = T from the low-precision R (Eq. (8), Alg. 2 line 5);
+ * LSQ = fp64 least-squares refit against A_D(:, I). */
+typedef enum { ID_COEF_R = 0, ID_COEF_LSQ = 1 } id_coef_mode;
+
+typedef enum {
+  ID_OK = 0,
+  ID_ERR_ARG = 1,        /* null pointer / invalid enum / bad leading dimension */
+  ID_ERR_DIM = 2,        /* k out of range, shard geometry inconsistent, workspace too small */
+  ID_ERR_OVERFLOW = 3,   /* A_L has an Inf after scaling and rounding */
+  ID_ERR_UNDERFLOW = 4,  /* selected pivot norm^2 below the fp32 normal range;
+                            k_out holds the completed steps, piv_out[0:k_out] valid */
+  ID_ERR_DEGENERATE = 5, /* R11 or the skeleton Gram matrix is numerically singular */
+  ID_ERR_DOMAIN = 6,     /* eps outside [0, 1) */
+  ID_ERR_CUDA = 7,
+  ID_ERR_NCCL = 8,
+  ID_ERR_OOM = 9,
+  ID_ERR_STATE = 10      /* called out of order (create -> qrcp -> coeffs -> error) */
+} id_status;
+
+/* Numerical-model knobs of the QRCP (readings R4-R6).  NULL = defaults. */
+typedef struct {
+  int32_t nb;        /* store interval: the trailing matrix is re-stored in the
+                        low format every nb steps (1 = SPEC's store-after-every-
+                        update); 0 = default (4).  1 <= nb <= 16. */
+  int32_t use_graph; /* 0 or 1 (default) = capture the k-step loop in a CUDA graph
+                        and replay it; -1 = plain stream launches. */
+  int32_t profile_pass; /* 1 = bracket every panel-pass launch with CUDA events
+                           (id_stats.t_pass_ms); adds event nodes between kernels. */
+  int32_t reserved[5];
+} id_qrcp_opts;
+
+/* Per-call statistics (device-event times of the last calls, in ms). */
+typedef struct {
+  double scale;          /* s applied before rounding */
+  double normAL_fro;     /* ||A_L||_F (global) */
+  double normAD_fro;     /* ||A_D||_F (global) */
+  double resid_est;      /* sqrt(sum of remaining downdated column norms^2) of A_L after k_out steps */
+  double t_round_ms;     /* scale + round + initial norms */
+  double t_qrcp_ms;      /* the k-step pivoted QR loop */
+  double t_coef_ms;      /* id_coeffs_fp64 */
+  double t_err_ms;       /* id_error */
+  double t_pass_ms;      /* sum of the panel-pass kernel times (dominant kernel), when profiled */
+  int64_t pass_launches; /* number of panel-pass launches in the last QRCP */
+  int64_t kernel_launches; /* kernels launched by the last qrcp+coeffs+error sequence */
+  int32_t k_out;
+  int32_t nb;
+  int32_t status_qrcp;
+  int32_t reserved[5];
+} id_stats;
+
+/* Bytes of device workspace for a shard of m_local rows, n columns, rank <= k_max,
+ * store interval nb (0 = default), storage format fmt.  host_AD != 0 reserves room
+ * for a device copy of a host-resident A_D. */
+size_t id_workspace_bytes(int64_t m_local, int64_t n, int32_t k_max, int32_t nb,
+                          id_format fmt, int32_t host_AD);
+
+/* Create a handle over this rank's shard of A_D.
+ *   A_D        column-major m_local x n, leading dimension ld >= m_local; device
+ *              memory, or host memory (pinned recommended), detected with
+ *              cudaPointerGetAttributes — a host A_D is copied into the
+ *              workspace on `stream` (host_AD must have been set in
+ *              id_workspace_bytes).
+ *   m_global   rows of the whole matrix; row_offset = first global row of the shard.
+ *   workspace  caller-owned device memory, >= id_workspace_bytes(...) bytes,
+ *              256-byte aligned.
+ *   nccl_comm  ncclComm_t (as void*) when nranks > 1, else NULL.
+ *   stream     cudaStream_t (as void*); NULL = legacy default stream. */
+id_status id_create(id_handle* h, const double* A_D, int64_t m_global, int64_t m_local,
+                    int64_t row_offset, int64_t n, int64_t ld, void* workspace,
+                    size_t ws_bytes, void* nccl_comm, int32_t rank, int32_t nranks,
+                    void* stream);
+
+/* Steps 1-2: scale, round, pivoted QR.  eps <= 0: fixed rank k_max; eps in (0,1):
+ * stop at the first k with sqrt(sum_{unpivoted} ||r_i||^2) <= eps ||A_L||_F
+ * (reading R8), k <= k_max.  Writes k_out (host) and
+ * piv_out[0:k_out] (host, 0-based original column indices = I, in pivot order).
+ * Synchronises the stream. */
+id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_t k_max,
+                          double eps, const id_qrcp_opts* opts, int32_t* k_out,
+                          int32_t* piv_out);
+
+/* Step 3: P (k_out x n, column-major, leading dimension ldp >= k_out) in fp64 into
+ * caller DEVICE memory P_out; P(:, I) is exactly I_k.  Requires a successful QRCP. */
+id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t ldp);
+
+/* Step 4: ||A_D - A_D(:, I) P||_F and its ratio to ||A_D||_F (host scalars,
+ * identical on all ranks), using the P of the last id_coeffs_fp64. */
+id_status id_error(id_handle h, double* abs_fro, double* rel_fro);
+
+/* R (k_out x n fp32, columns in pivoted order, R_jj >= 0) into DEVICE memory. */
+id_status id_get_R(id_handle h, float* R_out, int64_t ldr);
+
+/* The full column permutation Z (host, n entries, 0-based original indices in
+ * pivoted order; perm_out[0:k_out] = I, the rest is the order R's trailing
+ * columns are in). */
+id_status id_get_perm(id_handle h, int32_t* perm_out);
+
+/* A_L of this shard (m_local x n, column-major, ld >= m_local) into DEVICE memory:
+ * uint16 fp16 bit patterns for ID_FP16, float for ID_FP32.  Valid after
+ * id_qrcp_lowprec with the same fmt and before any later re-store (i.e. it is
+ * the rounded input only when called right after id_round_only). */
+id_status id_get_AL(id_handle h, void* out, int64_t ld);
+
+/* Step 1 alone (scale + round + norms), for bit-exact checks of A_L. */
+id_status id_round_only(id_handle h, id_format fmt, id_scaling scaling);
+
+id_status id_get_stats(id_handle h, id_stats* out);
+const char* id_last_error(id_handle h);
+void id_destroy(id_handle h);
+
+/* NCCL plumbing (the library dlopen()s the libnccl.so.2 already loaded by the
+ * process, e.g. PyTorch's).  The unique id is 128 bytes; broadcast it with any
+ * transport (e.g. torch.distributed), then every rank calls id_nccl_comm_init. */
+int32_t id_nccl_unique_id_bytes(void);
+id_status id_nccl_get_unique_id(void* out);
+id_status id_nccl_comm_init(void** comm, const void* unique_id, int32_t nranks, int32_t rank);
+id_status id_nccl_comm_destroy(void* comm);
+
+/* Library version and build target. */
+const char* id_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPID_H */

@@ -17,7 +17,8 @@ What is computed (PAPER.md):
     both this oracle and the CUDA path (readings R4-R6):
       - element arithmetic (the reflector update W <- W - v f^T) in fp32;
       - the working matrix is re-stored (rounded) to the low format every `nb`
-        steps — nb = 1 is SPEC's store-after-every-update, nb > 1 the blocked
+        steps, after that step's pivot is chosen and before its reflector is
+        formed — nb = 1 is SPEC's store-after-every-update, nb > 1 the blocked
         implementation the paper names as future work (P:402);
       - reductions over rows (column norms, W^T u) accumulated in fp64 (reading
         R5: sequential fp32 sums stagnate at m = 2^24 rows);
@@ -92,9 +93,9 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
     """Householder QRCP of the already-rounded A_L, in the precision model above.
 
     Step j (0-based), following Eq. (6)-(7):
-      0. every nb steps (j > 0, j % nb == 0): W(j:, j:) <- fl_L(W(j:, j:))     [store point]
       1. s_i = ||W(j:m, i)||^2, i >= j (fp64 sum of exact fp32 squares)         [norms]
       2. p = argmax s_i (ties: lowest original index); swap columns j <-> p     [pivot, Z]
+      2'. every nb steps (j > 0, j % nb == 0): W(j:, j:) <- fl_L(W(j:, j:))    [store point]
       3. u = W(j:m, j); beta = -sign(u_0) sqrt(s_j); v = u / (u_0 - beta), v_0 = 1;
          tau = (beta - u_0) / beta                                              [reflector]
       4. w = W(j:m, j:)^T u (fp64 accumulation); R(j, i) = w_i / beta; the new
@@ -120,8 +121,6 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
     resid = []
     status, k_out = "ok", k_max
     for j in range(k_max):
-        if j > 0 and j % nb == 0 and fmtL is not DOUBLE:
-            W[j:, j:] = round_to(W[j:, j:].astype(np.float64), fmtL).reshape(m - j, n - j)
         Wt = W[j:, j:].astype(np.float64)
         s = np.sum(Wt * Wt, axis=0)                           # step 1
         resid.append(math.sqrt(float(np.sum(s))))
@@ -143,8 +142,11 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
             R[:j, [j, p]] = R[:j, [p, j]]
             perm[[j, p]] = perm[[p, j]]
             s[[0, best]] = s[[best, 0]]
+        if j > 0 and j % nb == 0 and fmtL is not DOUBLE:       # store point (reading R4)
+            W[j:, j:] = round_to(Wt, fmtL).reshape(m - j, n - j)
+            Wt = W[j:, j:].astype(np.float64)
         u = Wt[:, 0]                                           # step 3
-        sj = float(s[0])
+        sj = float(np.sum(u * u))
         u0 = float(u[0])
         beta = -math.copysign(math.sqrt(sj), u0)
         c = 1.0 / (u0 - beta)

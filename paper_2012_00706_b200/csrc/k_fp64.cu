@@ -1,0 +1,450 @@
+// The fp64 ID step (Algorithm 2 lines 5-7; Eq. (8) P:129-135;
+// Remark 1 P:136-139; Remark 2 P:199-201).
+//
+//   LSQ mode ("least-squares problem"): P(:, J) = argmin ||A_I X - A_J||_F,
+//   A_I = A_D(:, I), solved by CholeskyQR2-style orthogonalisation in fp64:
+//     G1 = A_I^T A_I,  R1 = chol(G1),  Q1 = A_I R1^{-1}     (blocked TRSM, in place)
+//     G2 = Q1^T Q1 (well conditioned: kappa(Q1)^2 = 1 + O(u kappa(A_I)^2)),
+//     W  = Q1^T A_D,   T = R1^{-1} G2^{-1} W(:, J)          (small triangular solves)
+//   which equals R^{-1} Q^T A_J with Q = Q1 R2^{-1}, R = R2 R1 (CholQR2) but forms
+//   only one m x k triangular solve.  R mode (Eq. (8)): T = R11^{-1} R12 from the
+//   low-precision R promoted to fp64.
+//   The error ||A_D - A_D(:, I) P||_F is one fused pass: a 64x64-tiled fp64 GEMM
+//   A_I P whose epilogue subtracts from A_D, squares and reduces (never stored).
+//
+// Bound: fp64 FMA pipe for the GEMM-shaped kernels (intensity ~k/4 flop/B).
+#include "mpid_internal.cuh"
+#include <math.h>
+
+namespace mpid {
+
+// ---------------------------------------------------------------------------
+__global__ void k_gather_cols(const double* __restrict__ A, int64_t m, int64_t ld,
+                              const int* __restrict__ perm, double* __restrict__ X) {
+  const int l = blockIdx.y;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < m) X[(int64_t)l * m + r] = A[(int64_t)perm[l] * ld + r];
+}
+
+// ---------------------------------------------------------------------------
+// 64x64-tiled fp64 GEMM core, 256 threads, 4x4 outputs per thread, K tile 16,
+// double-buffered shared memory.  Thread layout inside a warp is 4 (M) x 8 (N)
+// so the shared-memory operand reads are broadcast-friendly.
+// ---------------------------------------------------------------------------
+constexpr int GT = 64, GK = 16;
+
+enum GemmMode { GM_TN_PARTIAL = 0, GM_NN_ERROR = 1, GM_NN_UPDATE = 2 };
+
+struct GemmArgs {
+  // TN: C(i, c) = sum_r X(r, i) Y(r, c), rows r in the split's range; X m x M, Y m x N
+  // NN: C(r, c) = sum_l X(r, l) B(l, c); X m x K, B K x N (col-major, ldb)
+  const double* X;
+  int64_t ldx;
+  const double* Y;   // TN: Y ; NN: B
+  int64_t ldy;
+  int64_t M, N, K;   // TN: M = k1, N = n1, K = m (rows) ; NN: M = m, N = ncols, K = k
+  int64_t k_per_split;
+  double* out;       // TN: partials [split][M][N] ; NN_ERROR: partial sums per block ; NN_UPDATE: C
+  int64_t ldo;
+  const double* A;   // NN_ERROR: A_D (m x N), lda
+  int64_t lda;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_gemm64(GemmArgs g) {
+  __shared__ __align__(16) double As[2][GK][GT];
+  __shared__ __align__(16) double Bs[2][GK][GT];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int ti = (warp >> 1) * 4 + (lane >> 3);     // 0..15 (M)
+  const int tj = (warp & 1) * 8 + (lane & 7);       // 0..15 (N)
+  const int64_t m0 = (int64_t)blockIdx.x * GT;      // M tile
+  const int64_t n0 = (int64_t)blockIdx.y * GT;      // N tile
+  int64_t k_begin = 0, k_end = g.K;
+  if (MODE == GM_TN_PARTIAL) {
+    k_begin = (int64_t)blockIdx.z * g.k_per_split;
+    k_end = min(g.K, k_begin + g.k_per_split);
+  }
+  // loader mapping: column/row index along the 64-wide dim, 4 consecutive k
+  const int ld_mn = tid & 63;
+  const int ld_k = (tid >> 6) * 4;
+
+  double ra[4], rb[4];
+  auto gload = [&](int64_t kb) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t kk = kb + ld_k + q;
+      if (MODE == GM_TN_PARTIAL) {
+        const int64_t i = m0 + ld_mn, c = n0 + ld_mn;
+        ra[q] = (kk < k_end && i < g.M) ? g.X[i * g.ldx + kk] : 0.0;
+        rb[q] = (kk < k_end && c < g.N) ? g.Y[c * g.ldy + kk] : 0.0;
+      } else {
+        const int64_t r = m0 + ld_mn, c = n0 + ld_mn;
+        ra[q] = (kk < k_end && r < g.M) ? g.X[kk * g.ldx + r] : 0.0;
+        rb[q] = (kk < k_end && c < g.N) ? g.Y[c * g.ldy + kk] : 0.0;
+      }
+    }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      As[buf][ld_k + q][ld_mn] = ra[q];
+      Bs[buf][ld_k + q][ld_mn] = rb[q];
+    }
+  };
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+
+  if (k_begin < k_end) {
+    gload(k_begin);
+    sstore(0);
+    __syncthreads();
+    int buf = 0;
+    for (int64_t kb = k_begin; kb < k_end; kb += GK) {
+      const bool more = kb + GK < k_end;
+      if (more) gload(kb + GK);
+#pragma unroll
+      for (int kk = 0; kk < GK; ++kk) {
+        const double2 a01 = *reinterpret_cast<const double2*>(&As[buf][kk][ti * 4]);
+        const double2 a23 = *reinterpret_cast<const double2*>(&As[buf][kk][ti * 4 + 2]);
+        const double2 b01 = *reinterpret_cast<const double2*>(&Bs[buf][kk][tj * 4]);
+        const double2 b23 = *reinterpret_cast<const double2*>(&Bs[buf][kk][tj * 4 + 2]);
+        const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+        const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+      }
+      if (more) {
+        sstore(buf ^ 1);
+        __syncthreads();
+        buf ^= 1;
+      }
+    }
+  }
+
+  if (MODE == GM_TN_PARTIAL) {
+    double* o = g.out + (int64_t)blockIdx.z * g.M * g.N;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int64_t i = m0 + ti * 4 + a;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int64_t c = n0 + tj * 4 + b;
+        if (i < g.M && c < g.N) o[c * g.M + i] = acc[a][b];
+      }
+    }
+  } else if (MODE == GM_NN_UPDATE) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int64_t r = m0 + ti * 4 + a;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int64_t c = n0 + tj * 4 + b;
+        if (r < g.M && c < g.N) g.out[c * g.ldo + r] -= acc[a][b];
+      }
+    }
+  } else {  // GM_NN_ERROR: sum (A_D - A_I P)^2 over the tile
+    double e2 = 0.0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int64_t c = n0 + tj * 4 + b;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int64_t r = m0 + ti * 4 + a;
+        if (r < g.M && c < g.N) {
+          const double e = g.A[c * g.lda + r] - acc[a][b];
+          e2 = fma(e, e, e2);
+        }
+      }
+    }
+    __shared__ double red[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+    if (lane == 0) red[warp] = e2;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += red[w];
+      g.out[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Cholesky G = L L^T (lower, col-major k x k) in one CTA; returns R = L^T
+// (upper, col-major) in place of G's upper triangle.  info = 0 or j+1 at the
+// first non-positive pivot (breakdown -> ID_ERR_DEGENERATE).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ G, int k, int* __restrict__ info) {
+  extern __shared__ double sG[];
+  const bool in_smem = (size_t)k * k * sizeof(double) <= 160 * 1024;
+  double* L = in_smem ? sG : G;
+  if (in_smem)
+    for (int i = threadIdx.x; i < k * k; i += blockDim.x) sG[i] = G[i];
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = L[j + (int64_t)j * k];
+      if (!(d > 0.0)) bad = bad ? bad : j + 1;
+      L[j + (int64_t)j * k] = d > 0.0 ? sqrt(d) : 1.0;
+    }
+    __syncthreads();
+    const double djj = L[j + (int64_t)j * k];
+    for (int i = j + 1 + threadIdx.x; i < k; i += blockDim.x) L[i + (int64_t)j * k] /= djj;
+    __syncthreads();
+    const int w = k - j - 1;
+    for (int64_t idx = threadIdx.x; idx < (int64_t)w * w; idx += blockDim.x) {
+      const int i = j + 1 + (int)(idx % w), l = j + 1 + (int)(idx / w);
+      if (l <= i) L[i + (int64_t)l * k] -= L[i + (int64_t)j * k] * L[l + (int64_t)j * k];
+    }
+    __syncthreads();
+  }
+  // R(j, i) = L(i, j) for i >= j, then zero below the diagonal (two passes: in-place safe)
+  for (int64_t idx = threadIdx.x; idx < (int64_t)k * k; idx += blockDim.x) {
+    const int r = (int)(idx % k), c = (int)(idx / k);
+    if (c >= r) G[r + (int64_t)c * k] = L[c + (int64_t)r * k];
+  }
+  __syncthreads();
+  for (int64_t idx = threadIdx.x; idx < (int64_t)k * k; idx += blockDim.x) {
+    const int r = (int)(idx % k), c = (int)(idx / k);
+    if (c < r) G[r + (int64_t)c * k] = 0.0;
+  }
+  if (threadIdx.x == 0) *info = bad;
+}
+
+// ---------------------------------------------------------------------------
+// In-block part of the blocked right TRSM X <- X R^{-1} (R upper k x k):
+// columns [c0, c0 + nbk) of every row, after the GEMM update with the previous
+// blocks.  One thread per row, the nbk unknowns in registers.
+// ---------------------------------------------------------------------------
+constexpr int TRSM_NB = 32;
+__global__ void __launch_bounds__(128) k_trsm_rows_block(double* __restrict__ X, int64_t m,
+                                                         int64_t ldx, const double* __restrict__ R,
+                                                         int k, int c0, int nbk) {
+  __shared__ double Rb[TRSM_NB][TRSM_NB + 1];
+  for (int i = threadIdx.x; i < TRSM_NB * TRSM_NB; i += blockDim.x) {
+    const int a = i % TRSM_NB, b = i / TRSM_NB;
+    Rb[a][b] = (a < nbk && b < nbk) ? R[(c0 + a) + (int64_t)(c0 + b) * k] : (a == b ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  double q[TRSM_NB];
+#pragma unroll
+  for (int c = 0; c < TRSM_NB; ++c) q[c] = c < nbk ? X[(int64_t)(c0 + c) * ldx + r] : 0.0;
+#pragma unroll
+  for (int c = 0; c < TRSM_NB; ++c) {
+    double s = q[c];
+#pragma unroll
+    for (int l = 0; l < c; ++l) s = fma(-q[l], Rb[l][c], s);
+    q[c] = s / Rb[c][c];
+  }
+#pragma unroll
+  for (int c = 0; c < TRSM_NB; ++c)
+    if (c < nbk) X[(int64_t)(c0 + c) * ldx + r] = q[c];
+}
+
+// ---------------------------------------------------------------------------
+// Small left triangular solves on a block of 32 right-hand sides held in
+// shared memory (the fp64 triangular solve for P).  For column i of the block,
+// b = B(:, map[i]) (map = perm + k for W(:, J), or identity + k for R12):
+//   mode 0 (R mode):   T = R1^{-1} b
+//   mode 1 (LSQ mode): T = R1^{-1} R2^{-1} R2^{-T} b    (G2 = R2^T R2)
+// R1, R2 upper, col-major k x k.  One CTA per 32 columns, 1024 threads.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_trsm_left_block(const double* __restrict__ R1,
+                                                          const double* __restrict__ R2, int k,
+                                                          const double* __restrict__ B, int64_t ldb,
+                                                          const int* __restrict__ map, int ncols,
+                                                          double* __restrict__ T, int64_t ldt,
+                                                          int mode) {
+  extern __shared__ double sb[];  // [k][33]
+  const int c = threadIdx.x & 31, rg = threadIdx.x >> 5;  // column in block, row group (32)
+  const int col = blockIdx.x * 32 + c;
+  const bool valid = col < ncols;
+  const int64_t src = valid ? (int64_t)(map ? map[col] : col) : 0;
+  for (int r = rg; r < k; r += 32) sb[r * 33 + c] = valid ? B[src * ldb + r] : 0.0;
+  __syncthreads();
+  auto back = [&](const double* U) {          // solve U x = b (upper), column sweep
+    for (int i = k - 1; i >= 0; --i) {
+      const double xi = sb[i * 33 + c] / U[i + (int64_t)i * k];
+      __syncthreads();
+      if (rg == 0) sb[i * 33 + c] = xi;
+      for (int r = rg; r < i; r += 32) sb[r * 33 + c] = fma(-U[r + (int64_t)i * k], xi, sb[r * 33 + c]);
+      __syncthreads();
+    }
+  };
+  auto fwdT = [&](const double* U) {          // solve U^T x = b (lower), column sweep
+    for (int i = 0; i < k; ++i) {
+      const double xi = sb[i * 33 + c] / U[i + (int64_t)i * k];
+      __syncthreads();
+      if (rg == 0) sb[i * 33 + c] = xi;
+      for (int r = i + 1 + rg; r < k; r += 32) sb[r * 33 + c] = fma(-U[i + (int64_t)r * k], xi, sb[r * 33 + c]);
+      __syncthreads();
+    }
+  };
+  if (mode == 1) {
+    fwdT(R2);
+    back(R2);
+  }
+  back(R1);
+  if (valid)
+    for (int r = rg; r < k; r += 32) T[(int64_t)col * ldt + r] = sb[r * 33 + c];
+}
+
+// R (k x n fp32, row-major, pivoted order) -> fp64 col-major k x n
+__global__ void k_R_to_fp64(const float* __restrict__ R, int k, int n, double* __restrict__ Rd) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)k * n) return;
+  const int i = (int)(idx % k), c = (int)(idx / k);
+  Rd[idx] = (double)R[(int64_t)i * n + c];
+}
+
+// R (k x n fp32 row-major) -> fp32 col-major k x n with leading dimension ldr
+__global__ void k_R_export(const float* __restrict__ R, int k, int n, float* __restrict__ out, int64_t ldr) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)k * n) return;
+  const int i = (int)(idx % k), c = (int)(idx / k);
+  out[(int64_t)c * ldr + i] = R[(int64_t)i * n + c];
+}
+
+// P(:, perm[j]) = e_j (j < k), P(:, perm[k + i]) = T(:, i); col-major k x n, ldp
+__global__ void k_assemble_P(const double* __restrict__ T, int64_t ldt, int k, int n,
+                             const int* __restrict__ perm, double* __restrict__ P, int64_t ldp) {
+  const int pos = blockIdx.x;
+  const int orig = perm[pos];
+  for (int r = threadIdx.x; r < k; r += blockDim.x) {
+    double v;
+    if (pos < k) v = (r == pos) ? 1.0 : 0.0;
+    else v = T[(int64_t)(pos - k) * ldt + r];
+    P[(int64_t)orig * ldp + r] = v;
+  }
+}
+
+__global__ void k_sum_scalar(const double* __restrict__ part, int nblk, double* __restrict__ out) {
+  __shared__ double sh[32];
+  double t = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) t += part[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (int)(blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) *out = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+cudaError_t launch_gather_cols(const double* A, int64_t m, int64_t ld, const int* perm, int k,
+                               double* X, cudaStream_t st) {
+  dim3 grid((unsigned)((m + 255) / 256), (unsigned)k);
+  k_gather_cols<<<grid, 256, 0, st>>>(A, m, ld, perm, X);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tsmm(const double* X, int64_t ldx, int k1, const double* Y, int64_t ldy, int n1,
+                        int64_t m, double* part, int splits, cudaStream_t st) {
+  GemmArgs g{};
+  g.X = X; g.ldx = ldx; g.Y = Y; g.ldy = ldy;
+  g.M = k1; g.N = n1; g.K = m;
+  g.k_per_split = ((m + splits - 1) / splits + GK - 1) / GK * GK;
+  g.out = part;
+  dim3 grid((unsigned)((k1 + GT - 1) / GT), (unsigned)((n1 + GT - 1) / GT), (unsigned)splits);
+  k_gemm64<GM_TN_PARTIAL><<<grid, 256, 0, st>>>(g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cholesky(double* G, int k, int* info, cudaStream_t st) {
+  const size_t sm = (size_t)k * k * sizeof(double);
+  const size_t smem = sm <= 160 * 1024 ? sm : 0;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(k_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    set = true;
+  }
+  k_cholesky<<<1, 1024, smem, st>>>(G, k, info);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trsm_right_upper(double* X, int64_t m, int64_t ldx, const double* Rm, int k,
+                                    cudaStream_t st) {
+  for (int c0 = 0; c0 < k; c0 += TRSM_NB) {
+    const int nbk = k - c0 < TRSM_NB ? k - c0 : TRSM_NB;
+    if (c0 > 0) {  // X(:, c0:c0+nbk) -= X(:, 0:c0) R(0:c0, c0:c0+nbk)
+      GemmArgs g{};
+      g.X = X; g.ldx = ldx;
+      g.Y = Rm + (int64_t)c0 * k; g.ldy = k;
+      g.M = m; g.N = nbk; g.K = c0;
+      g.out = X + (int64_t)c0 * ldx; g.ldo = ldx;
+      dim3 grid((unsigned)((m + GT - 1) / GT), (unsigned)((nbk + GT - 1) / GT), 1);
+      k_gemm64<GM_NN_UPDATE><<<grid, 256, 0, st>>>(g);
+    }
+    k_trsm_rows_block<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(X, m, ldx, Rm, k, c0, nbk);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trsm_left_upper(const double* R1, const double* R2, int k, const double* B,
+                                   int64_t ldb, const int* map, int ncols, double* T, int64_t ldt,
+                                   int mode, cudaStream_t st) {
+  if (ncols <= 0) return cudaSuccess;
+  const size_t smem = (size_t)k * 33 * sizeof(double);
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(k_trsm_left_block, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    set = true;
+  }
+  k_trsm_left_block<<<(unsigned)((ncols + 31) / 32), 1024, smem, st>>>(R1, R2, k, B, ldb, map, ncols,
+                                                                        T, ldt, mode);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_R_to_fp64(const float* R, int k, int n, double* Rd, cudaStream_t st) {
+  const int64_t tot = (int64_t)k * n;
+  k_R_to_fp64<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(R, k, n, Rd);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_R_export(const float* R, int k, int n, float* out, int64_t ldr, cudaStream_t st) {
+  const int64_t tot = (int64_t)k * n;
+  k_R_export<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(R, k, n, out, ldr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assemble_P(const double* T, int64_t ldt, int k, int n, const int* perm, double* P,
+                              int64_t ldp, cudaStream_t st) {
+  k_assemble_P<<<n, 128, 0, st>>>(T, ldt, k, n, perm, P, ldp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int n, const double* X, int k,
+                         const double* P, int64_t ldp, double* part, int* nblk_out, cudaStream_t st) {
+  GemmArgs g{};
+  g.X = X; g.ldx = m;
+  g.Y = P; g.ldy = ldp;
+  g.M = m; g.N = n; g.K = k;
+  g.out = part;
+  g.A = A; g.lda = ld;
+  dim3 grid((unsigned)((m + GT - 1) / GT), (unsigned)((n + GT - 1) / GT), 1);
+  *nblk_out = (int)(grid.x * grid.y);
+  k_gemm64<GM_NN_ERROR><<<grid, 256, 0, st>>>(g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_scalar(const double* part, int nblk, double* out, cudaStream_t st) {
+  k_sum_scalar<<<1, 1024, 0, st>>>(part, nblk, out);
+  return cudaGetLastError();
+}
+
+}  // namespace mpid

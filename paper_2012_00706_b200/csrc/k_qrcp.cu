@@ -1,0 +1,497 @@
+// The k-step low-precision pivoted Householder QR (Algorithm 2 line 4, P:163;
+// Eq. (6)-(7)), B200 design "lazy panel with on-the-fly formation":
+//
+//   the stored matrix S (fp16/fp32, 8-row interleaved column-major, see
+//   mpid_internal.cuh) lags the factorisation by at most nb reflectors; each
+//   step ONE streaming pass over S (k_pass)
+//     - forms the current trailing matrix A~ = S - sum_{pending l} v_l f_l^T
+//       element by element in fp32 (FMA, in step order = the oracle's order),
+//     - takes u = A~(:, j) (this step's pivot column, rows >= j),
+//     - reduces w = A~^T u and the exact residual norms s_i = ||A~(j:m, i)||^2
+//       (fp32 within an 8-row group, fp64 across groups; reading R5),
+//     - emits the row x = A~(j, :) (needed for F and R),
+//     - every nb steps writes fl_L(A~) back to S (the storage rounding point,
+//       reading R4), which empties the pending list.
+//   The per-step scalar work (k_reflector, one CTA) then forms the reflector
+//   (beta, tau, c), the row R(j, :) = w / beta (sign-normalised), the update
+//   vector f = x - w / beta (= tau A~^T v), the one-step downdated norms
+//   vn_i = s_i - R(j,i)^2 and the next pivot (warp-shuffle argmax, ties to the
+//   lowest original column index), all in device memory — no host sync.
+//   k_swap exchanges the pivot column into position j+1 (S, pending f, R, perm).
+//
+// Bound: HBM.  Per step the pass reads (m - j)(n - j) s bytes, plus
+// (m - j)(n - j) s bytes written on store steps (every nb-th), plus the
+// O(m + n) vectors.  The fp32 formation costs npend FMAs per element.
+#include "mpid_internal.cuh"
+#include <cfloat>
+#include <math.h>
+
+namespace mpid {
+
+template <typename T> struct Io;
+template <> struct Io<__half> {
+  __device__ static __forceinline__ void load8(const __half* p, float* x) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p));
+    const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __half22float2(h[i]);
+      x[2 * i] = f.x;
+      x[2 * i + 1] = f.y;
+    }
+  }
+  __device__ static __forceinline__ void store8(__half* p, const float* x) {
+    uint4 v;
+    __half2* h = reinterpret_cast<__half2*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(x[2 * i], x[2 * i + 1]);
+    __stcs(reinterpret_cast<uint4*>(p), v);
+  }
+  __device__ static __forceinline__ float load1(const __half* p) { return __half2float(*p); }
+  __device__ static __forceinline__ float rnd(float x) { return __half2float(__float2half_rn(x)); }
+};
+template <> struct Io<float> {
+  __device__ static __forceinline__ void load8(const float* p, float* x) {
+    const float4 a = __ldcs(reinterpret_cast<const float4*>(p));
+    const float4 b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+  }
+  __device__ static __forceinline__ void store8(float* p, const float* x) {
+    __stcs(reinterpret_cast<float4*>(p), make_float4(x[0], x[1], x[2], x[3]));
+    __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(x[4], x[5], x[6], x[7]));
+  }
+  __device__ static __forceinline__ float load1(const float* p) { return *p; }
+  __device__ static __forceinline__ float rnd(float x) { return x; }
+};
+
+// ---------------------------------------------------------------------------
+// k_pass<T, PMAX>: grid (GX row-CTAs, GY column splits), 256 threads.
+// Shared memory: us[256] (u of the tile rows), vs[PMAX][256] (pending v rows),
+// acc[WRS][2][ncols] fp64 per-lane-owned column accumulators.
+// ---------------------------------------------------------------------------
+template <typename T, int PMAX>
+__global__ void __launch_bounds__(PASS_THREADS, 2) k_pass(PassParams p) {
+  if (p.sc->done) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int TROWS = PASS_TILE_G * RG;                  // 256 rows per tile
+  float* us = reinterpret_cast<float*>(smem_raw);
+  float* vs = us + TROWS;                                    // [PMAX][TROWS]
+  double* acc = reinterpret_cast<double*>(vs + PMAX * TROWS);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = p.n, j = p.j, npend = p.npend;
+  T* __restrict__ S = reinterpret_cast<T*>(p.S);
+
+  // column range of this CTA: chunks [q0, q1) of 32 columns starting at column j
+  const int nchunk_tot = (n - j + 31) >> 5;
+  const int q0 = blockIdx.y * p.chunks_per_split;
+  const int q1 = min(nchunk_tot, q0 + p.chunks_per_split);
+  if (q0 >= q1) return;
+  const int nchunks = q1 - q0;
+  const int cbase = j + 32 * q0;                            // first column of the CTA
+  const int ncols = min(n, j + 32 * q1) - cbase;
+  int CW = 1;
+  while (CW * 2 <= PASS_WARPS && CW * 2 <= nchunks) CW *= 2;
+  const int WRS = PASS_WARPS / CW;
+  const int cw = warp % CW, rw = warp / CW;
+
+  for (int i = tid; i < WRS * 2 * ncols; i += PASS_THREADS) acc[i] = 0.0;
+
+  // pending reflectors: slot and c for step t = j0 + l
+  int slot[PMAX];
+  float fcol_j[PMAX];
+#pragma unroll
+  for (int l = 0; l < PMAX; ++l) {
+    slot[l] = (p.j0 + l) % NSLOT;
+    fcol_j[l] = (l < npend) ? p.F[(int64_t)slot[l] * n + j] : 0.f;
+  }
+  const int slot_j = j % NSLOT;
+  const int64_t jloc = (int64_t)j - p.row_offset;            // local row of the pivot row
+  const int t0 = blockIdx.x * p.tiles_per_cta;
+  const int t1 = min(p.ntiles, t0 + p.tiles_per_cta);
+
+  for (int t = t0; t < t1; ++t) {
+    const int64_t r_tile = (int64_t)t * TROWS;               // first local row of the tile
+    if (p.row_offset + r_tile + TROWS <= j) continue;          // whole tile above row j
+    __syncthreads();
+    // ---- phase 1: pending v rows and u = A~(:, j) for the tile rows --------
+    {
+      const int64_t rl = r_tile + tid;
+      const int64_t rg = p.row_offset + rl;
+      const bool real = rl < p.m_local;
+      float a = Io<T>::load1(S + ((rl >> 3) * n + j) * RG + (rl & 7));
+#pragma unroll
+      for (int l = 0; l < PMAX; ++l) {
+        if (l < npend) {
+          const int64_t tstep = p.j0 + l;
+          float v;
+          if (!real || rg < tstep) v = 0.f;
+          else if (rg == tstep) v = 1.f;
+          else v = __double2float_rn((double)p.U[(int64_t)slot[l] * p.m_pad + rl] * p.cvec[tstep]);
+          vs[l * TROWS + tid] = v;
+          a = fmaf(-v, fcol_j[l], a);
+        }
+      }
+      if (p.store) a = Io<T>::rnd(a);                           // storage rounding point (R4)
+      const float u = (real && rg >= j) ? a : 0.f;
+      us[tid] = u;
+      if (blockIdx.y == 0) p.U[(int64_t)slot_j * p.m_pad + rl] = u;
+    }
+    __syncthreads();
+    // ---- phase 2: stream the tile's columns --------------------------------
+    for (int q = cw; q < nchunks; q += CW) {
+      const int col = cbase + 32 * q + lane;
+      const bool valid = col < n;
+      float f[PMAX];
+#pragma unroll
+      for (int l = 0; l < PMAX; ++l)
+        f[l] = (l < npend && valid) ? p.F[(int64_t)slot[l] * n + col] : 0.f;
+      double aw = 0.0, as = 0.0;
+      if (valid) {
+#pragma unroll 2
+        for (int gl = rw; gl < PASS_TILE_G; gl += WRS) {
+          const int64_t g = (int64_t)t * PASS_TILE_G + gl;
+          const int64_t r0 = g * 8;
+          if (p.row_offset + r0 + 8 <= j) continue;              // rows above the pivot row
+          T* ptr = S + (g * n + col) * RG;
+          float x[8];
+          Io<T>::load8(ptr, x);
+#pragma unroll
+          for (int l = 0; l < PMAX; ++l) {
+            if (l < npend) {
+              const float4 v0 = *reinterpret_cast<const float4*>(vs + l * TROWS + gl * 8);
+              const float4 v1 = *reinterpret_cast<const float4*>(vs + l * TROWS + gl * 8 + 4);
+              x[0] = fmaf(-v0.x, f[l], x[0]); x[1] = fmaf(-v0.y, f[l], x[1]);
+              x[2] = fmaf(-v0.z, f[l], x[2]); x[3] = fmaf(-v0.w, f[l], x[3]);
+              x[4] = fmaf(-v1.x, f[l], x[4]); x[5] = fmaf(-v1.y, f[l], x[5]);
+              x[6] = fmaf(-v1.z, f[l], x[6]); x[7] = fmaf(-v1.w, f[l], x[7]);
+            }
+          }
+          if (p.store) {                                             // storage rounding point (R4)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = Io<T>::rnd(x[i]);
+            Io<T>::store8(ptr, x);
+          }
+          const float4 u0 = *reinterpret_cast<const float4*>(us + gl * 8);
+          const float4 u1 = *reinterpret_cast<const float4*>(us + gl * 8 + 4);
+          if (r0 + 8 + p.row_offset > j && r0 + p.row_offset <= j) {   // group holding row j
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (p.row_offset + r0 + i < j) x[i] = 0.f;
+            if (jloc >= r0 && jloc < r0 + 8) p.xr[col] = x[jloc - r0];
+          }
+          float pw = x[0] * u0.x;
+          pw = fmaf(x[1], u0.y, pw); pw = fmaf(x[2], u0.z, pw); pw = fmaf(x[3], u0.w, pw);
+          pw = fmaf(x[4], u1.x, pw); pw = fmaf(x[5], u1.y, pw); pw = fmaf(x[6], u1.z, pw);
+          pw = fmaf(x[7], u1.w, pw);
+          float ps = x[0] * x[0];
+#pragma unroll
+          for (int i = 1; i < 8; ++i) ps = fmaf(x[i], x[i], ps);
+          aw += (double)pw;
+          as += (double)ps;
+        }
+        const int cl = col - cbase;
+        acc[(rw * 2 + 0) * ncols + cl] += aw;
+        acc[(rw * 2 + 1) * ncols + cl] += as;
+      }
+    }
+  }
+  __syncthreads();
+  for (int cl = tid; cl < ncols; cl += PASS_THREADS) {
+    double w = 0.0, s = 0.0;
+    for (int r = 0; r < WRS; ++r) {
+      w += acc[(r * 2 + 0) * ncols + cl];
+      s += acc[(r * 2 + 1) * ncols + cl];
+    }
+    p.part[((int64_t)blockIdx.x * 2 + 0) * n + cbase + cl] = w;
+    p.part[((int64_t)blockIdx.x * 2 + 1) * n + cbase + cl] = s;
+  }
+}
+
+// red[0][c] = sum w, red[1][c] = sum s over the GX row-CTAs, red[2][c] = x_c.
+// CTA = 32 columns (lanes) x 8 warps; warp w sums rows b = w, w+8, ... ; the 8
+// warp partials are then added in warp order (deterministic).
+__global__ void __launch_bounds__(256) k_pass_reduce(const double* __restrict__ part, int gx, int n,
+                                                     int j, const double* __restrict__ xr, int own_row,
+                                                     double* __restrict__ red,
+                                                     const DevScalars* __restrict__ sc) {
+  if (sc->done) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = j + blockIdx.x * 32 + lane;
+  __shared__ double sh[2][8][32];
+  double w = 0.0, s = 0.0;
+  if (c < n) {
+    for (int b = warp; b < gx; b += 8) {
+      w += part[((int64_t)b * 2 + 0) * n + c];
+      s += part[((int64_t)b * 2 + 1) * n + c];
+    }
+  }
+  sh[0][warp][lane] = w;
+  sh[1][warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && c < n) {
+    double tw = 0.0, ts = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { tw += sh[0][i][lane]; ts += sh[1][i][lane]; }
+    red[c] = tw;
+    red[n + c] = ts;
+    red[2 * n + c] = own_row ? xr[c] : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_reflector: one CTA of 1024 threads.  Step j's reflector, R row, f vector,
+// downdated norms, next pivot, tolerance test.
+// ---------------------------------------------------------------------------
+struct ArgMax {
+  double v;
+  int orig;
+  int pos;
+};
+__device__ __forceinline__ bool am_better(const ArgMax& a, const ArgMax& b) {
+  // larger value wins; ties -> lowest original column index
+  return a.v > b.v || (a.v == b.v && a.orig < b.orig);
+}
+__device__ __forceinline__ ArgMax am_shfl(const ArgMax& a, int o) {
+  ArgMax b;
+  b.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+  b.orig = __shfl_xor_sync(0xffffffffu, a.orig, o);
+  b.pos = __shfl_xor_sync(0xffffffffu, a.pos, o);
+  return b;
+}
+__device__ ArgMax block_argmax(ArgMax a) {
+  __shared__ ArgMax sh[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const ArgMax b = am_shfl(a, o);
+    if (am_better(b, a)) a = b;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) sh[warp] = a;
+  __syncthreads();
+  if (warp == 0) {
+    a = lane < (int)(blockDim.x >> 5) ? sh[lane] : ArgMax{-1.0, 0x7fffffff, -1};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const ArgMax b = am_shfl(a, o);
+      if (am_better(b, a)) a = b;
+    }
+    if (lane == 0) sh[0] = a;
+  }
+  __syncthreads();
+  const ArgMax r = sh[0];
+  __syncthreads();
+  return r;
+}
+__device__ double block_sum(double v) {
+  __shared__ double sh[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[0] = v;
+  }
+  __syncthreads();
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) k_reflector(const double* __restrict__ red, int n, int j,
+                                                    int k_max, float* __restrict__ F,
+                                                    float* __restrict__ R, double* __restrict__ beta_out,
+                                                    double* __restrict__ cvec, double* __restrict__ tau,
+                                                    const int* __restrict__ perm,
+                                                    DevScalars* __restrict__ sc) {
+  if (sc->done) return;
+  const double sj = red[n + j];
+  const double uj = red[2 * n + j];
+  if (!(sj >= (double)FLT_MIN)) {                    // pivot norm^2 underflows fp32
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      sc->status = 4;  // ID_ERR_UNDERFLOW
+      sc->k_out = j;
+      sc->done = 1;
+    }
+    return;
+  }
+  const double beta = -copysign(sqrt(sj), uj);
+  const double sgn = beta < 0.0 ? -1.0 : 1.0;
+  const double c = 1.0 / (uj - beta);
+  const int slot = j % NSLOT;
+  if (threadIdx.x == 0) {
+    beta_out[j] = beta;
+    cvec[j] = c;
+    tau[j] = (beta - uj) / beta;
+  }
+  ArgMax best{-1.0, 0x7fffffff, -1};
+  double rest = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (i < j) {
+      R[(int64_t)j * n + i] = 0.f;
+      continue;
+    }
+    const double rraw = red[i] / beta;
+    R[(int64_t)j * n + i] = __double2float_rn(rraw * sgn);
+    F[(int64_t)slot * n + i] = __double2float_rn(red[2 * n + i] - rraw);
+    if (i > j) {
+      const double vn = red[n + i] - rraw * rraw;      // one-step downdate from exact s_i
+      rest += fmax(vn, 0.0);
+      const ArgMax cand{vn, perm[i], i};
+      if (am_better(cand, best)) best = cand;
+    }
+  }
+  best = block_argmax(best);
+  rest = block_sum(rest);
+  if (threadIdx.x == 0) {
+    sc->k_out = j + 1;
+    sc->resid2 = rest;
+    sc->pivot = best.pos;
+    if (j + 1 >= k_max || best.pos < 0) sc->done = 1;
+    else if (sc->eps2normAL2 > 0.0 && rest <= sc->eps2normAL2) sc->done = 1;
+  }
+}
+
+// initial pivot: argmax of the initial column norms (ties lowest index); perm = identity
+__global__ void __launch_bounds__(1024) k_init_pivot(const double* __restrict__ norms, int n,
+                                                     int* __restrict__ perm,
+                                                     DevScalars* __restrict__ sc) {
+  ArgMax best{-1.0, 0x7fffffff, -1};
+  double tot = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    perm[i] = i;
+    const ArgMax cand{norms[i], i, i};
+    tot += norms[i];
+    if (am_better(cand, best)) best = cand;
+  }
+  best = block_argmax(best);
+  tot = block_sum(tot);
+  if (threadIdx.x == 0) {
+    sc->pivot = best.pos;
+    sc->resid2 = tot;
+    sc->k_out = 0;
+    sc->status = 0;
+    sc->done = sc->overflow ? 1 : 0;
+    if (sc->overflow) sc->status = 3;  // ID_ERR_OVERFLOW
+  }
+}
+
+// swap columns jn <-> p (p = sc->pivot) in S (all row groups), in the pending
+// f vectors of steps [j0, jn), in R rows [0, jn), and in perm.
+template <typename T>
+__global__ void k_swap(T* __restrict__ S, int64_t ngroups, int n, int jn, int j0,
+                       float* __restrict__ F, float* __restrict__ R, int* __restrict__ perm,
+                       const DevScalars* __restrict__ sc) {
+  if (sc->done) return;
+  const int p = sc->pivot;
+  if (p == jn || p < 0) return;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < ngroups) {
+    if (sizeof(T) == 2) {
+      uint4* a = reinterpret_cast<uint4*>(S + (g * n + jn) * RG);
+      uint4* b = reinterpret_cast<uint4*>(S + (g * n + p) * RG);
+      const uint4 ta = *a, tb = *b;
+      *a = tb;
+      *b = ta;
+    } else {
+      uint4* a = reinterpret_cast<uint4*>(S + (g * n + jn) * RG);
+      uint4* b = reinterpret_cast<uint4*>(S + (g * n + p) * RG);
+      const uint4 ta0 = a[0], ta1 = a[1], tb0 = b[0], tb1 = b[1];
+      a[0] = tb0; a[1] = tb1;
+      b[0] = ta0; b[1] = ta1;
+    }
+  }
+  if (blockIdx.x == 0) {
+    for (int t = j0 + threadIdx.x; t < jn; t += blockDim.x) {
+      float* f = F + (int64_t)(t % NSLOT) * n;
+      const float x = f[jn];
+      f[jn] = f[p];
+      f[p] = x;
+    }
+    for (int t = threadIdx.x; t < jn; t += blockDim.x) {
+      float* r = R + (int64_t)t * n;
+      const float x = r[jn];
+      r[jn] = r[p];
+      r[p] = x;
+    }
+    if (threadIdx.x == 0) {
+      const int x = perm[jn];
+      perm[jn] = perm[p];
+      perm[p] = x;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <typename T, int PMAX>
+static cudaError_t launch_pass_t(const PassParams& p, dim3 grid, cudaStream_t st) {
+  const int nchunks = (p.n - p.j + 31) / 32;
+  const int cps = p.chunks_per_split;
+  const int nch = cps < nchunks ? cps : nchunks;
+  int CW = 1;
+  while (CW * 2 <= PASS_WARPS && CW * 2 <= nch) CW *= 2;
+  const int WRS = PASS_WARPS / CW;
+  const size_t smem = (size_t)(PASS_TILE_G * RG) * (1 + PMAX) * sizeof(float) +
+                      (size_t)WRS * 2 * (32 * nch) * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_pass<T, PMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  k_pass<T, PMAX><<<grid, PASS_THREADS, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t launch_pass_fmt(const PassParams& p, dim3 grid, cudaStream_t st) {
+  const int np = p.npend;
+  if (np <= 1) return launch_pass_t<T, 1>(p, grid, st);
+  if (np <= 2) return launch_pass_t<T, 2>(p, grid, st);
+  if (np <= 4) return launch_pass_t<T, 4>(p, grid, st);
+  if (np <= 8) return launch_pass_t<T, 8>(p, grid, st);
+  return launch_pass_t<T, 16>(p, grid, st);
+}
+
+cudaError_t launch_pass(int fmt, const PassParams& p, dim3 grid, cudaStream_t st) {
+  return fmt == 1 ? launch_pass_fmt<__half>(p, grid, st) : launch_pass_fmt<float>(p, grid, st);
+}
+
+cudaError_t launch_pass_reduce(const double* part, int gx, int n, int j, const double* xr,
+                               int own_row, double* red, const DevScalars* sc, cudaStream_t st) {
+  const int cols = n - j;
+  k_pass_reduce<<<(cols + 31) / 32, 256, 0, st>>>(part, gx, n, j, xr, own_row, red, sc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reflector(const double* red, int n, int j, int k_max, int nslot_f, float* F,
+                             float* R, double* beta, double* cvec, double* tau, const int* perm,
+                             DevScalars* sc, cudaStream_t st) {
+  (void)nslot_f;
+  k_reflector<<<1, 1024, 0, st>>>(red, n, j, k_max, F, R, beta, cvec, tau, perm, sc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_pivot(const double* norms, int n, int* perm, DevScalars* sc,
+                              cudaStream_t st) {
+  k_init_pivot<<<1, 1024, 0, st>>>(norms, n, perm, sc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_swap(int fmt, void* S, int64_t ngroups, int n, int jn, int j0, int steps_done,
+                        float* F, float* R, int* perm, DevScalars* sc, cudaStream_t st) {
+  (void)steps_done;
+  const unsigned nb = (unsigned)((ngroups + 255) / 256);
+  if (fmt == 1)
+    k_swap<__half><<<nb, 256, 0, st>>>((__half*)S, ngroups, n, jn, j0, F, R, perm, sc);
+  else
+    k_swap<float><<<nb, 256, 0, st>>>((float*)S, ngroups, n, jn, j0, F, R, perm, sc);
+  return cudaGetLastError();
+}
+
+}  // namespace mpid

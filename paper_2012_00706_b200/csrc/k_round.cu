@@ -1,0 +1,257 @@
+// K0 / K1 — range scaling, rounding A_D -> A_L, initial column norms.
+//
+// Algorithm 2 line 2: A_L = fl(A).  With range scaling (BASELINE.json
+// configs[1]; reading R7) A_L = fl_L(s * A_D): one fp64 multiply and
+// ONE round-to-nearest-even conversion fp64 -> fp16 (cvt.rn.f16.f64) or
+// fp64 -> fp32 (cvt.rn.f32.f64), subnormals kept (no -ftz), overflow -> Inf and
+// flagged.  Column norms of A_L are accumulated in fp64 (the squares
+// of fp16/fp32 values are exact in fp64; reading R5) for the first pivot.
+//
+// Bound: HBM.  Reads 8 B and writes s B (2 or 4) per element once.
+#include "mpid_internal.cuh"
+#include <cfloat>
+#include <math.h>
+
+namespace mpid {
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// K0: per-block max |a_ij| (grid-stride over columns x rows)
+__global__ void __launch_bounds__(256) k_maxabs(const double* __restrict__ A, int64_t m, int64_t n,
+                                                int64_t ld, double* __restrict__ part) {
+  double mx = 0.0;
+  const int64_t total = m * n;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = idx / m, r = idx - c * m;
+    mx = fmax(mx, fabs(__ldg(A + c * ld + r)));
+  }
+  __shared__ double sh[8];
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    v = warp_max(v);
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
+  }
+}
+
+__global__ void k_maxabs_finish(const double* __restrict__ part, int nblk, DevScalars* sc) {
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) mx = fmax(mx, part[i]);
+  __shared__ double sh[32];
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    v = warp_max(v);
+    if (threadIdx.x == 0) sc->maxabs = v;
+  }
+}
+
+// s from the (global) max: MAXABS s = 1/mx; POW2 s = 2^-ceil(log2 mx) computed
+// exactly with frexp (mx = f 2^e, f in [0.5,1): ceil(log2 mx) = e, or e-1 when f == 0.5).
+__global__ void k_scale_from_max(DevScalars* sc, int scaling) {
+  const double mx = sc->maxabs;
+  double s = 1.0;
+  if (mx > 0.0 && scaling == 1) {
+    s = 1.0 / mx;
+  } else if (mx > 0.0 && scaling == 2) {
+    int e;
+    const double f = frexp(mx, &e);
+    const int c = (f == 0.5) ? e - 1 : e;
+    s = ldexp(1.0, -c);
+  }
+  sc->scale = s;
+}
+
+template <typename T> struct Pack8;
+template <> struct Pack8<__half> {
+  using V = uint4;                               // 8 x fp16 = 16 B
+  __device__ static V pack(const double* x, int* inf, double* sq) {
+    uint16_t h[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const __half v = __double2half(x[i]);      // cvt.rn.f16.f64: single RNE rounding
+      h[i] = __half_as_ushort(v);
+      const double d = (double)__half2float(v);
+      *inf |= isinf(d) ? 1 : 0;
+      sq[i] = d * d;
+    }
+    V o;
+    o.x = h[0] | ((uint32_t)h[1] << 16);
+    o.y = h[2] | ((uint32_t)h[3] << 16);
+    o.z = h[4] | ((uint32_t)h[5] << 16);
+    o.w = h[6] | ((uint32_t)h[7] << 16);
+    return o;
+  }
+};
+template <> struct Pack8<float> {
+  struct V { float4 a, b; };
+  __device__ static V pack(const double* x, int* inf, double* sq) {
+    float f[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      f[i] = __double2float_rn(x[i]);           // cvt.rn.f32.f64
+      *inf |= isinf(f[i]) ? 1 : 0;
+      sq[i] = (double)f[i] * (double)f[i];
+    }
+    V o;
+    o.a = make_float4(f[0], f[1], f[2], f[3]);
+    o.b = make_float4(f[4], f[5], f[6], f[7]);
+    return o;
+  }
+};
+
+// K1: grid (ceil(n/32), GY).  Lane = column within a 32-column chunk, warp w of
+// the block takes row groups g = g0 + w, g0 + w + 8, ... of the block's range.
+// Per (blockIdx.y, column): fp64 partial of ||A_L(:,c)||^2 -> part[y*n + c];
+// per block: partial ||A_D||_F^2 -> aux[y*gridDim.x + x].
+template <typename T>
+__global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int64_t m,
+                                               int64_t ngroups, int64_t n, int64_t ld,
+                                               T* __restrict__ S, double* __restrict__ part,
+                                               double* __restrict__ aux,
+                                               DevScalars* __restrict__ sc) {
+  using P = Pack8<T>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t per = (ngroups + gridDim.y - 1) / gridDim.y;
+  const int64_t g0 = (int64_t)blockIdx.y * per;
+  const int64_t g1 = min(ngroups, g0 + per);
+  const double s = sc->scale;
+  double colsq = 0.0, adsq = 0.0;
+  int inf = 0;
+  if (c < n) {
+    const double* col = A + c * ld;
+    for (int64_t g = g0 + warp; g < g1; g += 8) {
+      double x[8], sq[8];
+      const int64_t r0 = g * 8;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double a = (r0 + i < m) ? __ldg(col + r0 + i) : 0.0;
+        adsq = fma(a, a, adsq);
+        x[i] = __dmul_rn(s, a);
+      }
+      const typename P::V v = P::pack(x, &inf, sq);
+      *reinterpret_cast<typename P::V*>(S + (g * n + c) * 8) = v;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) colsq += sq[i];
+    }
+  }
+  __shared__ double shc[8][32];
+  __shared__ double sha[8];
+  __shared__ int shi;
+  if (threadIdx.x == 0) shi = 0;
+  shc[warp][lane] = colsq;
+  double a = warp_sum(adsq);
+  if (lane == 0) sha[warp] = a;
+  __syncthreads();
+  if (inf) atomicOr(&shi, 1);
+  if (warp == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += shc[w][lane];
+    if (c < n) part[(int64_t)blockIdx.y * n + c] = t;
+    double u = lane < 8 ? sha[lane] : 0.0;
+    u = warp_sum(u);
+    if (lane == 0) aux[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = u;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && shi) atomicOr(&sc->overflow, 1);
+}
+
+// out[c] = sum_y part[y*stride + c] (fixed order: deterministic)
+__global__ void k_sum_rows(const double* __restrict__ part, int rows, int64_t stride, int64_t len,
+                           double* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= len) return;
+  double t = 0.0;
+  for (int y = 0; y < rows; ++y) t += part[(int64_t)y * stride + c];
+  out[c] = t;
+}
+
+// (unused helper kept for single-rank debugging) normAL2 = sum norms, normAD2 = sum aux
+__global__ void k_round_scalars(const double* __restrict__ norms, int64_t n,
+                                const double* __restrict__ aux, int naux, DevScalars* sc) {
+  __shared__ double sh[2][32];
+  double a = 0.0, b = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += norms[i];
+  for (int i = threadIdx.x; i < naux; i += blockDim.x) b += aux[i];
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if ((threadIdx.x & 31) == 0) { sh[0][threadIdx.x >> 5] = a; sh[1][threadIdx.x >> 5] = b; }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    double x = threadIdx.x < nw ? sh[0][threadIdx.x] : 0.0;
+    double y = threadIdx.x < nw ? sh[1][threadIdx.x] : 0.0;
+    x = warp_sum(x);
+    y = warp_sum(y);
+    if (threadIdx.x == 0) { sc->normAL2 = x; sc->normAD2 = y; }
+  }
+}
+
+// S (interleaved) -> column-major out (A_L export for bit-exact checks)
+template <typename T>
+__global__ void k_export(const T* __restrict__ S, int64_t m, int64_t n, T* __restrict__ out,
+                         int64_t ld) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= m * n) return;
+  const int64_t c = idx / m, r = idx - c * m;
+  out[c * ld + r] = S[((r >> 3) * n + c) * 8 + (r & 7)];
+}
+
+// ---------------------------------------------------------------------------
+cudaError_t launch_maxabs(const double* A, int64_t m, int64_t n, int64_t ld, double* part,
+                          int nblk, cudaStream_t st) {
+  k_maxabs<<<nblk, 256, 0, st>>>(A, m, n, ld, part);
+  return cudaGetLastError();
+}
+cudaError_t launch_maxabs_finish(const double* part, int nblk, DevScalars* sc, int scaling,
+                                 cudaStream_t st) {
+  k_maxabs_finish<<<1, 1024, 0, st>>>(part, nblk, sc);
+  return cudaGetLastError();
+}
+cudaError_t launch_scale_from_max(DevScalars* sc, int scaling, cudaStream_t st) {
+  k_scale_from_max<<<1, 1, 0, st>>>(sc, scaling);
+  return cudaGetLastError();
+}
+cudaError_t launch_round(int fmt, const double* A, int64_t m, int64_t m_pad, int64_t n, int64_t ld,
+                         void* S, double* part, int gy, DevScalars* sc, cudaStream_t st) {
+  dim3 grid((unsigned)((n + 31) / 32), (unsigned)gy);
+  double* aux = part + (int64_t)gy * n;
+  if (fmt == 1)
+    k_round<__half><<<grid, 256, 0, st>>>(A, m, m_pad / 8, n, ld, (__half*)S, part, aux, sc);
+  else
+    k_round<float><<<grid, 256, 0, st>>>(A, m, m_pad / 8, n, ld, (float*)S, part, aux, sc);
+  return cudaGetLastError();
+}
+cudaError_t launch_sum_partials(const double* part, int splits, int64_t len, double* out,
+                                cudaStream_t st) {
+  k_sum_rows<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(part, splits, len, len, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_export_S(int fmt, const void* S, int64_t m_local, int n, void* out, int64_t ld,
+                            cudaStream_t st) {
+  const int64_t tot = m_local * n;
+  const unsigned nb = (unsigned)((tot + 255) / 256);
+  if (fmt == 1)
+    k_export<__half><<<nb, 256, 0, st>>>((const __half*)S, m_local, n, (__half*)out, ld);
+  else
+    k_export<float><<<nb, 256, 0, st>>>((const float*)S, m_local, n, (float*)out, ld);
+  return cudaGetLastError();
+}
+
+}  // namespace mpid

@@ -1,0 +1,752 @@
+// C ABI of libmpid.so (declared in include/mpid.h): handle, workspace layout,
+// host orchestration of the kernels, NCCL (dlopen'ed) collectives, CUDA-graph
+// capture of the k-step loop and per-stage device timing.
+#include "../../include/mpid.h"
+#include "mpid_internal.cuh"
+
+#include <dlfcn.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+using namespace mpid;
+
+// ----------------------------------------------------------------------------
+// NCCL through dlopen (the process's libnccl.so.2, e.g. PyTorch's)
+// ----------------------------------------------------------------------------
+namespace {
+typedef int nccl_result_t;
+struct NcclApi {
+  bool ok = false;
+  nccl_result_t (*GetUniqueId)(void*) = nullptr;
+  nccl_result_t (*CommInitRank)(void**, int, /*ncclUniqueId by value*/ ...) = nullptr;
+  nccl_result_t (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  nccl_result_t (*CommDestroy)(void*) = nullptr;
+  const char* (*GetErrorString)(nccl_result_t) = nullptr;
+};
+struct NcclUid { char internal[128]; };
+typedef nccl_result_t (*CommInitRankFn)(void**, int, NcclUid, int);
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.GetUniqueId = (nccl_result_t(*)(void*))dlsym(h, "ncclGetUniqueId");
+  api.CommInitRank = (nccl_result_t(*)(void**, int, ...))dlsym(h, "ncclCommInitRank");
+  api.AllReduce = (nccl_result_t(*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
+      h, "ncclAllReduce");
+  api.CommDestroy = (nccl_result_t(*)(void*))dlsym(h, "ncclCommDestroy");
+  api.GetErrorString = (const char* (*)(nccl_result_t))dlsym(h, "ncclGetErrorString");
+  api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
+  return api;
+}
+constexpr int NCCL_FLOAT64 = 8;
+constexpr int NCCL_SUM = 0, NCCL_MAX = 2;
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Layout {
+  size_t AD, S, U, F, R, part, red, xr, norms, perm, scal3, sc, maxpart, rpart;
+  size_t AI, Q1, G1, G2, W, tpart, Rd, T, Pw, epart, misc;
+  size_t total;
+};
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+int64_t m_pad_of(int64_t m_local) {
+  const int64_t T = PASS_TILE_G * RG;
+  return std::max<int64_t>(T, (m_local + T - 1) / T * T);
+}
+int gx_of(int64_t m_pad) {
+  const int64_t ntiles = m_pad / (PASS_TILE_G * RG);
+  return (int)std::min<int64_t>(ntiles, 2 * num_sms());
+}
+int round_gy(int64_t m_pad, int64_t n) {
+  const int64_t gx = (n + 31) / 32;
+  const int64_t ngroups = m_pad / 8;
+  int64_t gy = std::max<int64_t>(1, (4 * num_sms() + gx - 1) / gx);
+  gy = std::min<int64_t>(gy, std::max<int64_t>(1, ngroups / 8));
+  return (int)std::min<int64_t>(gy, 4096);
+}
+int tsmm_splits(int64_t k1, int64_t n1, int64_t m) {
+  const int64_t tiles = ((k1 + 63) / 64) * ((n1 + 63) / 64);
+  int64_t s = std::max<int64_t>(1, (2 * num_sms() + tiles - 1) / tiles);
+  s = std::min<int64_t>(s, std::max<int64_t>(1, m / 1024));
+  return (int)std::min<int64_t>(s, 128);
+}
+
+Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
+  Layout L{};
+  const int64_t mp = m_pad_of(m_local);
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
+  L.AD = take(host_AD ? (size_t)m_local * n * 8 : 0);
+  L.S = take((size_t)mp * n * 4);  // room for fp32 storage (fp16 uses half)
+  (void)sbytes;
+  L.U = take((size_t)NSLOT * mp * 4);
+  L.F = take((size_t)NSLOT * n * 4);
+  L.R = take((size_t)k * n * 4);
+  L.part = take((size_t)gx_of(mp) * 2 * n * 8);
+  L.red = take((size_t)3 * n * 8);
+  L.xr = take((size_t)n * 8);
+  L.norms = take((size_t)(n + 2) * 8);
+  L.perm = take((size_t)n * 4);
+  L.scal3 = take((size_t)3 * k * 8);
+  L.sc = take(sizeof(DevScalars));
+  L.maxpart = take(1024 * 8);
+  L.rpart = take(((size_t)round_gy(mp, n) * n + (size_t)round_gy(mp, n) * ((n + 31) / 32)) * 8);
+  L.AI = take((size_t)m_local * k * 8);
+  L.Q1 = take((size_t)m_local * k * 8);
+  L.G1 = take((size_t)k * k * 8);
+  L.G2 = take((size_t)k * k * 8);
+  L.W = take((size_t)k * n * 8);
+  const size_t tp = std::max<size_t>((size_t)tsmm_splits(k, n, m_local) * k * n,
+                                     (size_t)tsmm_splits(k, k, m_local) * k * k);
+  L.tpart = take(tp * 8);
+  L.Rd = take((size_t)k * n * 8);
+  L.T = take((size_t)k * n * 8);
+  L.Pw = take((size_t)k * n * 8);
+  L.epart = take((size_t)((m_local + 63) / 64) * ((n + 63) / 64) * 8);
+  L.misc = take(1024);
+  L.total = off;
+  return L;
+}
+}  // namespace
+
+struct mpid_ctx {
+  // geometry
+  const double* AD = nullptr;   // device A_D (user's or the workspace copy)
+  int64_t m_global = 0, m_local = 0, row_offset = 0, n = 0, ld = 0, m_pad = 0;
+  int32_t rank = 0, nranks = 1;
+  void* comm = nullptr;
+  cudaStream_t st = nullptr;      // current enqueue stream (user's, or cap during graph capture)
+  cudaStream_t user_st = nullptr; // the caller's stream
+  cudaStream_t cap = nullptr;     // internal non-blocking stream: graph capture and replay
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  Layout L{};
+  int64_t k_cap = 0;
+  bool host_AD = false;
+  // device pointers
+  void* S = nullptr;
+  float *U = nullptr, *F = nullptr, *R = nullptr;
+  double *part = nullptr, *red = nullptr, *xr = nullptr, *norms = nullptr, *beta = nullptr,
+         *cvec = nullptr, *tau = nullptr, *maxpart = nullptr, *rpart = nullptr;
+  int* perm = nullptr;
+  DevScalars* sc = nullptr;
+  double *AI = nullptr, *Q1 = nullptr, *G1 = nullptr, *G2 = nullptr, *W = nullptr, *tpart = nullptr,
+         *Rd = nullptr, *T = nullptr, *Pw = nullptr, *epart = nullptr;
+  int* info = nullptr;
+  double* err2 = nullptr;
+  // state
+  int fmt = 0;
+  int k_out = 0;
+  int qr_status = 0;
+  bool have_qr = false, have_coef = false;
+  std::vector<int> perm_host;
+  DevScalars sc_host{};
+  std::string err;
+  // graphs keyed by (fmt, scaling, k_max, nb, eps bits, profile)
+  std::map<std::tuple<int, int, int, int, uint64_t, int>, cudaGraphExec_t> graphs;
+  std::map<std::tuple<int, int, int, int, uint64_t, int>, int64_t> graph_launches;
+  cudaEvent_t ev[8]{};
+  std::vector<cudaEvent_t> pass_ev;
+  int64_t pass_launches = 0, kernel_launches = 0;
+  id_stats stats{};
+};
+
+static id_status fail(mpid_ctx* h, id_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) h->err = buf;
+  return s;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(h, ID_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                 \
+  } while (0)
+
+static cudaError_t rec(mpid_ctx* h, cudaEvent_t e) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(h->st, &cs);
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, h->st, cudaEventRecordExternal)
+                                             : cudaEventRecord(e, h->st);
+}
+
+static id_status allreduce(mpid_ctx* h, double* buf, size_t count, int op) {
+  if (h->nranks <= 1) return ID_OK;
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(h, ID_ERR_NCCL, "libnccl.so.2 not available");
+  const nccl_result_t r = api.AllReduce(buf, buf, count, NCCL_FLOAT64, op, h->comm, h->st);
+  if (r != 0)
+    return fail(h, ID_ERR_NCCL, "ncclAllReduce: %s", api.GetErrorString ? api.GetErrorString(r) : "?");
+  return ID_OK;
+}
+
+extern "C" {
+
+const char* id_version(void) { return "mpid 0.1 (sm_100a; arXiv 2012.00706 mixed-precision ID)"; }
+
+size_t id_workspace_bytes(int64_t m_local, int64_t n, int32_t k_max, int32_t nb, id_format fmt,
+                          int32_t host_AD) {
+  (void)nb;
+  if (m_local <= 0 || n <= 0 || k_max <= 0) return 0;
+  return layout(m_local, n, k_max, host_AD, fmt == ID_FP16 ? 2 : 4).total;
+}
+
+id_status id_create(id_handle* hp, const double* A_D, int64_t m_global, int64_t m_local,
+                    int64_t row_offset, int64_t n, int64_t ld, void* workspace, size_t ws_bytes,
+                    void* nccl_comm, int32_t rank, int32_t nranks, void* stream) {
+  if (!hp || !A_D || !workspace) return ID_ERR_ARG;
+  *hp = nullptr;
+  if (m_local <= 0 || n <= 0 || ld < m_local || m_global < m_local || row_offset < 0 ||
+      row_offset + m_local > m_global || nranks < 1 || rank < 0 || rank >= nranks)
+    return ID_ERR_DIM;
+  if (nranks > 1 && !nccl_comm) return ID_ERR_ARG;
+  if (((uintptr_t)workspace) & 255) return ID_ERR_ARG;
+  mpid_ctx* h = new mpid_ctx();
+  h->m_global = m_global;
+  h->m_local = m_local;
+  h->row_offset = row_offset;
+  h->n = n;
+  h->rank = rank;
+  h->nranks = nranks;
+  h->comm = nccl_comm;
+  h->st = (cudaStream_t)stream;
+  h->user_st = h->st;
+  h->ws = (char*)workspace;
+  h->ws_bytes = ws_bytes;
+  h->m_pad = m_pad_of(m_local);
+  cudaPointerAttributes pa{};
+  cudaError_t pe = cudaPointerGetAttributes(&pa, A_D);
+  if (pe != cudaSuccess) cudaGetLastError();
+  h->host_AD = (pe != cudaSuccess) || pa.type == cudaMemoryTypeHost || pa.type == cudaMemoryTypeUnregistered;
+  // the largest k this workspace supports
+  int64_t lo = 0, hi = std::min<int64_t>(n, m_global);  // largest k with layout(k) <= ws_bytes
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) / 2;
+    if (layout(m_local, n, mid, h->host_AD, 4).total <= ws_bytes) lo = mid;
+    else hi = mid - 1;
+  }
+  const int64_t kmax = lo;
+  if (kmax <= 0) {
+    delete h;
+    return ID_ERR_DIM;
+  }
+  h->k_cap = kmax;
+  h->L = layout(m_local, n, kmax, h->host_AD, 4);
+  const Layout& L = h->L;
+  char* w = h->ws;
+  h->S = w + L.S;
+  h->U = (float*)(w + L.U);
+  h->F = (float*)(w + L.F);
+  h->R = (float*)(w + L.R);
+  h->part = (double*)(w + L.part);
+  h->red = (double*)(w + L.red);
+  h->xr = (double*)(w + L.xr);
+  h->norms = (double*)(w + L.norms);
+  h->perm = (int*)(w + L.perm);
+  h->beta = (double*)(w + L.scal3);
+  h->cvec = h->beta + kmax;
+  h->tau = h->cvec + kmax;
+  h->sc = (DevScalars*)(w + L.sc);
+  h->maxpart = (double*)(w + L.maxpart);
+  h->rpart = (double*)(w + L.rpart);
+  h->AI = (double*)(w + L.AI);
+  h->Q1 = (double*)(w + L.Q1);
+  h->G1 = (double*)(w + L.G1);
+  h->G2 = (double*)(w + L.G2);
+  h->W = (double*)(w + L.W);
+  h->tpart = (double*)(w + L.tpart);
+  h->Rd = (double*)(w + L.Rd);
+  h->T = (double*)(w + L.T);
+  h->Pw = (double*)(w + L.Pw);
+  h->epart = (double*)(w + L.epart);
+  h->info = (int*)(w + L.misc);
+  h->err2 = (double*)(w + L.misc + 64);
+  for (auto& e : h->ev) {
+    if (cudaEventCreate(&e) != cudaSuccess) { delete h; return ID_ERR_CUDA; }
+  }
+  if (cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->join_ev, cudaEventDisableTiming) != cudaSuccess) {
+    delete h;
+    return ID_ERR_CUDA;
+  }
+  if (h->host_AD) {
+    double* dst = (double*)(w + L.AD);
+    cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)m_local * 8, A_D, (size_t)ld * 8, (size_t)m_local * 8,
+                                      (size_t)n, cudaMemcpyHostToDevice, h->st);
+    if (e != cudaSuccess) {
+      fail(h, ID_ERR_CUDA, "H2D copy of A_D: %s", cudaGetErrorString(e));
+      delete h;
+      return ID_ERR_CUDA;
+    }
+    h->AD = dst;
+    h->ld = m_local;
+  } else {
+    h->AD = A_D;
+    h->ld = ld;
+  }
+  // zero U (padding rows must stay 0); S is fully written by the rounding kernel
+  cudaMemsetAsync(h->U, 0, (size_t)NSLOT * h->m_pad * 4, h->st);
+  *hp = h;
+  return ID_OK;
+}
+
+void id_destroy(id_handle h) {
+  if (!h) return;
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& e : h->ev) if (e) cudaEventDestroy(e);
+  for (auto& e : h->pass_ev) cudaEventDestroy(e);
+  if (h->fork_ev) cudaEventDestroy(h->fork_ev);
+  if (h->join_ev) cudaEventDestroy(h->join_ev);
+  if (h->cap) cudaStreamDestroy(h->cap);
+  delete h;
+}
+
+const char* id_last_error(id_handle h) { return h ? h->err.c_str() : "null handle"; }
+
+}  // extern "C"
+
+// reset per-call scalars
+__global__ void k_reset_scalars(DevScalars* sc, double eps) {
+  sc->overflow = 0;
+  sc->done = 0;
+  sc->status = 0;
+  sc->k_out = 0;
+  sc->pivot = 0;
+  sc->scale = 1.0;
+  sc->maxabs = 0.0;
+  sc->eps2normAL2 = eps > 0.0 ? eps * eps : 0.0;  // multiplied by ||A_L||^2 after rounding
+}
+// global norms/scalars after the (optional) allreduce of [norms(n), adsq, overflow]
+__global__ void k_finish_round(const double* __restrict__ nb, int n, DevScalars* sc) {
+  __shared__ double sh[32];
+  double t = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) t += nb[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (int)(blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) {
+      sc->normAL2 = t;
+      sc->normAD2 = nb[n];
+      if (nb[n + 1] > 0.0) sc->overflow = 1;
+      sc->eps2normAL2 *= t;
+    }
+  }
+}
+// per-rank adsq (sum of block partials) and overflow flag into nb[n], nb[n+1]
+__global__ void k_pack_round(const double* __restrict__ aux, int naux, DevScalars* sc, double* nb, int n) {
+  __shared__ double sh[32];
+  double t = 0.0;
+  for (int i = threadIdx.x; i < naux; i += blockDim.x) t += aux[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (int)(blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) {
+      nb[n] = t;
+      nb[n + 1] = sc->overflow ? 1.0 : 0.0;
+    }
+  }
+}
+__global__ void k_set_max(double* buf, const DevScalars* sc) { buf[0] = sc->maxabs; }
+__global__ void k_get_max(const double* buf, DevScalars* sc) { sc->maxabs = buf[0]; }
+
+
+// enqueue scale + round + initial norms (+ collectives)
+static id_status enqueue_round(mpid_ctx* h, int fmt, int scaling, double eps) {
+  const int64_t m = h->m_local, n = h->n;
+  k_reset_scalars<<<1, 1, 0, h->st>>>(h->sc, eps);
+  h->kernel_launches += 1;
+  if (scaling != ID_SCALE_NONE) {
+    const int nblk = (int)std::min<int64_t>(1024, std::max<int64_t>(1, (m * n + 255) / 256));
+    CK(launch_maxabs(h->AD, m, n, h->ld, h->maxpart, nblk, h->st));
+    CK(launch_maxabs_finish(h->maxpart, nblk, h->sc, scaling, h->st));
+    h->kernel_launches += 2;
+    if (h->nranks > 1) {
+      k_set_max<<<1, 1, 0, h->st>>>(h->maxpart, h->sc);
+      id_status s = allreduce(h, h->maxpart, 1, NCCL_MAX);
+      if (s) return s;
+      k_get_max<<<1, 1, 0, h->st>>>(h->maxpart, h->sc);
+      h->kernel_launches += 2;
+    }
+  }
+  CK(launch_scale_from_max(h->sc, scaling, h->st));
+  const int gy = round_gy(h->m_pad, n);
+  CK(launch_round(fmt, h->AD, m, h->m_pad, n, h->ld, h->S, h->rpart, gy, h->sc, h->st));
+  CK(launch_sum_partials(h->rpart, gy, n, h->norms, h->st));  // norms[0:n]
+  const int naux = gy * (int)((n + 31) / 32);
+  k_pack_round<<<1, 1024, 0, h->st>>>(h->rpart + (int64_t)gy * n, naux, h->sc, h->norms, (int)n);
+  h->kernel_launches += 4;
+  id_status s = allreduce(h, h->norms, (size_t)n + 2, NCCL_SUM);
+  if (s) return s;
+  k_finish_round<<<1, 1024, 0, h->st>>>(h->norms, (int)n, h->sc);
+  h->kernel_launches += 1;
+  return ID_OK;
+}
+
+static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, double eps, int nb,
+                              bool profile) {
+  const int64_t n = h->n;
+  h->kernel_launches = 0;
+  h->pass_launches = 0;
+  cudaGetLastError();  // clear any stale error before the launch checks
+  CK(rec(h, h->ev[0]));
+  id_status s = enqueue_round(h, fmt, scaling, eps);
+  if (s) return s;
+  CK(rec(h, h->ev[1]));
+  CK(launch_init_pivot(h->norms, (int)n, h->perm, h->sc, h->st));
+  h->kernel_launches += 1;
+  const int gx = gx_of(h->m_pad);
+  const int ntiles = (int)(h->m_pad / (PASS_TILE_G * RG));
+  const int tpc = (ntiles + gx - 1) / gx;
+  const int own_lo = (int)std::min<int64_t>(h->row_offset, INT32_MAX);
+  for (int j = 0; j < k_max; ++j) {
+    const int j0 = j == 0 ? 0 : nb * ((j - 1) / nb);
+    const int npend = j - j0;
+    const int store = (npend == nb) ? 1 : 0;
+    CK(launch_swap(fmt, h->S, h->m_pad / 8, (int)n, j, j0, j, h->F, h->R, h->perm, h->sc, h->st));
+    PassParams p{};
+    p.S = h->S;
+    p.ngroups = h->m_pad / 8;
+    p.row_offset = h->row_offset;
+    p.m_local = h->m_local;
+    p.n = (int)n;
+    p.j = j;
+    p.j0 = j0;
+    p.npend = npend;
+    p.store = store;
+    p.tiles_per_cta = tpc;
+    p.ntiles = ntiles;
+    const int nchunks = (int)((n - j + 31) / 32);
+    int gy = std::max(1, std::min(nchunks, (2 * num_sms() + gx - 1) / gx));
+    int cps = (nchunks + gy - 1) / gy;
+    cps = std::min(cps, 256);
+    gy = (nchunks + cps - 1) / cps;
+    p.chunks_per_split = cps;
+    p.U = h->U;
+    p.F = h->F;
+    p.cvec = h->cvec;
+    p.part = h->part;
+    p.xr = h->xr;
+    p.sc = h->sc;
+    p.m_pad = h->m_pad;
+    if (profile) CK(rec(h, h->pass_ev[2 * j]));
+    CK(launch_pass(fmt, p, dim3(gx, gy), h->st));
+    if (profile) CK(rec(h, h->pass_ev[2 * j + 1]));
+    const int own = (j >= own_lo && (int64_t)j < h->row_offset + h->m_local) ? 1 : 0;
+    CK(launch_pass_reduce(h->part, gx, (int)n, j, h->xr, own, h->red, h->sc, h->st));
+    s = allreduce(h, h->red, (size_t)3 * n, NCCL_SUM);
+    if (s) return s;
+    CK(launch_reflector(h->red, (int)n, j, k_max, NSLOT, h->F, h->R, h->beta, h->cvec, h->tau, h->perm,
+                        h->sc, h->st));
+    h->kernel_launches += 4;
+    h->pass_launches += 1;
+  }
+  CK(rec(h, h->ev[2]));
+  return ID_OK;
+}
+
+extern "C" {
+
+id_status id_round_only(id_handle h, id_format fmt, id_scaling scaling) {
+  if (!h) return ID_ERR_ARG;
+  cudaGetLastError();
+  if (fmt != ID_FP16 && fmt != ID_FP32) return fail(h, ID_ERR_ARG, "bad format");
+  if (scaling < 0 || scaling > 2) return fail(h, ID_ERR_ARG, "bad scaling");
+  id_status s = enqueue_round(h, fmt, scaling, 0.0);
+  if (s) return s;
+  CK(cudaMemcpyAsync(&h->sc_host, h->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  h->fmt = fmt;
+  h->have_qr = false;
+  h->have_coef = false;
+  h->stats.scale = h->sc_host.scale;
+  h->stats.normAL_fro = sqrt(h->sc_host.normAL2);
+  h->stats.normAD_fro = sqrt(h->sc_host.normAD2);
+  if (h->sc_host.overflow) return fail(h, ID_ERR_OVERFLOW, "A_L overflows the low format after scaling");
+  return ID_OK;
+}
+
+id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_t k_max, double eps,
+                          const id_qrcp_opts* opts, int32_t* k_out, int32_t* piv_out) {
+  if (!h || !k_out || !piv_out) return ID_ERR_ARG;
+  if (fmt != ID_FP16 && fmt != ID_FP32) return fail(h, ID_ERR_ARG, "bad format %d", (int)fmt);
+  if (scaling < 0 || scaling > 2) return fail(h, ID_ERR_ARG, "bad scaling %d", (int)scaling);
+  if (!(eps >= 0.0 && eps < 1.0)) return fail(h, ID_ERR_DOMAIN, "eps must be in [0, 1)");
+  if (k_max < 1 || k_max > std::min<int64_t>(h->n, h->m_global))
+    return fail(h, ID_ERR_DIM, "k_max=%d outside [1, min(m, n)]", k_max);
+  if (k_max > h->k_cap) return fail(h, ID_ERR_DIM, "workspace too small for k_max=%d (cap %lld)", k_max,
+                                    (long long)h->k_cap);
+  int nb = opts && opts->nb > 0 ? opts->nb : 4;
+  if (nb > NB_MAX) return fail(h, ID_ERR_ARG, "nb=%d > %d", nb, NB_MAX);
+  const bool use_graph = !(opts && opts->use_graph < 0);
+  const bool profile = opts && opts->profile_pass;
+  h->have_qr = h->have_coef = false;
+  if (profile && (int)h->pass_ev.size() < 2 * k_max) {
+    const size_t old = h->pass_ev.size();
+    h->pass_ev.resize(2 * k_max);
+    for (size_t i = old; i < h->pass_ev.size(); ++i) CK(cudaEventCreate(&h->pass_ev[i]));
+  }
+  if (use_graph) {
+    uint64_t eb;
+    memcpy(&eb, &eps, 8);
+    auto key = std::make_tuple((int)fmt, (int)scaling, (int)k_max, nb, eb, profile ? 1 : 0);
+    auto it = h->graphs.find(key);
+    if (it == h->graphs.end()) {
+      cudaGraph_t g;
+      h->st = h->cap;  // capture on the internal stream (the caller's may be the legacy stream)
+      CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+      id_status s = enqueue_qrcp(h, fmt, scaling, k_max, eps, nb, profile);
+      cudaError_t e = cudaStreamEndCapture(h->cap, &g);
+      h->st = h->user_st;
+      if (s) return s;
+      if (e != cudaSuccess) return fail(h, ID_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+      cudaGraphExec_t ge;
+      CK(cudaGraphInstantiate(&ge, g, 0));
+      cudaGraphDestroy(g);
+      it = h->graphs.emplace(key, ge).first;
+      h->graph_launches[key] = h->kernel_launches;
+    }
+    // fork: cap waits for the caller's prior work; join: the caller waits for the graph
+    CK(cudaEventRecord(h->fork_ev, h->user_st));
+    CK(cudaStreamWaitEvent(h->cap, h->fork_ev, 0));
+    CK(cudaGraphLaunch(it->second, h->cap));
+    CK(cudaEventRecord(h->join_ev, h->cap));
+    CK(cudaStreamWaitEvent(h->user_st, h->join_ev, 0));
+    h->stats.kernel_launches = h->graph_launches[key];
+  } else {
+    id_status s = enqueue_qrcp(h, fmt, scaling, k_max, eps, nb, profile);
+    if (s) return s;
+    h->stats.kernel_launches = h->kernel_launches;
+  }
+  h->perm_host.resize(h->n);
+  CK(cudaMemcpyAsync(&h->sc_host, h->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaMemcpyAsync(h->perm_host.data(), h->perm, h->n * sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  h->fmt = fmt;
+  const DevScalars& sc = h->sc_host;
+  h->k_out = sc.k_out;
+  h->qr_status = sc.status;
+  *k_out = sc.k_out;
+  for (int i = 0; i < sc.k_out; ++i) piv_out[i] = h->perm_host[i];
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]);
+  h->stats.t_round_ms = ms;
+  cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]);
+  h->stats.t_qrcp_ms = ms;
+  h->stats.t_pass_ms = 0.0;
+  if (profile) {
+    double tot = 0.0;
+    for (int j = 0; j < sc.k_out; ++j) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, h->pass_ev[2 * j], h->pass_ev[2 * j + 1]) == cudaSuccess) tot += t;
+    }
+    h->stats.t_pass_ms = tot;
+  }
+  h->stats.pass_launches = sc.k_out;
+  h->stats.scale = sc.scale;
+  h->stats.normAL_fro = sqrt(sc.normAL2);
+  h->stats.normAD_fro = sqrt(sc.normAD2);
+  h->stats.resid_est = sqrt(std::max(0.0, sc.resid2));
+  h->stats.k_out = sc.k_out;
+  h->stats.nb = nb;
+  h->stats.status_qrcp = sc.status;
+  if (sc.overflow || sc.status == ID_ERR_OVERFLOW)
+    return fail(h, ID_ERR_OVERFLOW, "A_L overflows the low format after scaling (S:53)");
+  if (sc.status == ID_ERR_UNDERFLOW) {
+    h->have_qr = sc.k_out > 0;
+    return fail(h, ID_ERR_UNDERFLOW, "pivot norm underflow at step %d (P:266)", sc.k_out);
+  }
+  h->have_qr = true;
+  return ID_OK;
+}
+
+id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t ldp) {
+  if (!h || !P_out) return ID_ERR_ARG;
+  cudaGetLastError();
+  if (!h->have_qr || h->k_out < 1) return fail(h, ID_ERR_STATE, "id_coeffs_fp64 needs a successful QRCP");
+  const int k = h->k_out;
+  const int n = (int)h->n;
+  const int64_t m = h->m_local;
+  if (ldp < k) return fail(h, ID_ERR_ARG, "ldp < k");
+  if ((size_t)k * 33 * 8 > 200 * 1024) return fail(h, ID_ERR_DIM, "k=%d too large for the P solve", k);
+  CK(cudaEventRecord(h->ev[3], h->st));
+  int launches = 0;
+  CK(launch_gather_cols(h->AD, m, h->ld, h->perm, k, h->AI, h->st));
+  launches++;
+  if (mode == ID_COEF_R) {
+    CK(launch_R_to_fp64(h->R, k, n, h->Rd, h->st));
+    CK(launch_trsm_left_upper(h->Rd, nullptr, k, h->Rd + (int64_t)k * k, k, nullptr, n - k, h->T, k, 0,
+                              h->st));
+    launches += 2;
+  } else if (mode == ID_COEF_LSQ) {
+    // G1 = A_I^T A_I
+    int sp = tsmm_splits(k, k, m);
+    CK(launch_tsmm(h->AI, m, k, h->AI, m, k, m, h->tpart, sp, h->st));
+    CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G1, h->st));
+    launches += 2;
+    id_status s = allreduce(h, h->G1, (size_t)k * k, NCCL_SUM);
+    if (s) return s;
+    CK(launch_cholesky(h->G1, k, h->info, h->st));
+    // Q1 = A_I R1^{-1}
+    CK(cudaMemcpyAsync(h->Q1, h->AI, (size_t)m * k * 8, cudaMemcpyDeviceToDevice, h->st));
+    CK(launch_trsm_right_upper(h->Q1, m, m, h->G1, k, h->st));
+    launches += 1 + 2 * ((k + 31) / 32);
+    // G2 = Q1^T Q1
+    CK(launch_tsmm(h->Q1, m, k, h->Q1, m, k, m, h->tpart, sp, h->st));
+    CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G2, h->st));
+    s = allreduce(h, h->G2, (size_t)k * k, NCCL_SUM);
+    if (s) return s;
+    CK(launch_cholesky(h->G2, k, h->info + 1, h->st));
+    // W = Q1^T A_D
+    const int spw = tsmm_splits(k, n, m);
+    CK(launch_tsmm(h->Q1, m, k, h->AD, h->ld, n, m, h->tpart, spw, h->st));
+    CK(launch_sum_partials(h->tpart, spw, (int64_t)k * n, h->W, h->st));
+    s = allreduce(h, h->W, (size_t)k * n, NCCL_SUM);
+    if (s) return s;
+    // T = R1^{-1} R2^{-1} R2^{-T} W(:, perm[k:])
+    CK(launch_trsm_left_upper(h->G1, h->G2, k, h->W, k, h->perm + k, n - k, h->T, k, 1, h->st));
+    launches += 6;
+  } else {
+    return fail(h, ID_ERR_ARG, "bad coefficient mode");
+  }
+  CK(launch_assemble_P(h->T, k, k, n, h->perm, h->Pw, k, h->st));
+  CK(cudaMemcpy2DAsync(P_out, ldp * 8, h->Pw, (size_t)k * 8, (size_t)k * 8, n, cudaMemcpyDeviceToDevice,
+                       h->st));
+  launches++;
+  CK(cudaEventRecord(h->ev[4], h->st));
+  int info[2] = {0, 0};
+  if (mode == ID_COEF_LSQ)
+    CK(cudaMemcpyAsync(info, h->info, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]);
+  h->stats.t_coef_ms = ms;
+  h->stats.kernel_launches += launches;
+  if (info[0] || info[1])
+    return fail(h, ID_ERR_DEGENERATE, "Cholesky breakdown in the LSQ refit (info %d, %d)", info[0], info[1]);
+  h->have_coef = true;
+  return ID_OK;
+}
+
+id_status id_error(id_handle h, double* abs_fro, double* rel_fro) {
+  if (!h || !abs_fro || !rel_fro) return ID_ERR_ARG;
+  cudaGetLastError();
+  if (!h->have_coef) return fail(h, ID_ERR_STATE, "id_error needs id_coeffs_fp64 first");
+  const int k = h->k_out;
+  CK(cudaEventRecord(h->ev[5], h->st));
+  int nblk = 0;
+  CK(launch_error(h->AD, h->m_local, h->ld, (int)h->n, h->AI, k, h->Pw, k, h->epart, &nblk, h->st));
+  CK(launch_sum_scalar(h->epart, nblk, h->err2, h->st));
+  id_status s = allreduce(h, h->err2, 1, NCCL_SUM);
+  if (s) return s;
+  CK(cudaEventRecord(h->ev[6], h->st));
+  double e2 = 0.0;
+  CK(cudaMemcpyAsync(&e2, h->err2, 8, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev[5], h->ev[6]);
+  h->stats.t_err_ms = ms;
+  h->stats.kernel_launches += 2;
+  *abs_fro = sqrt(e2);
+  *rel_fro = h->sc_host.normAD2 > 0 ? sqrt(e2 / h->sc_host.normAD2) : NAN;
+  return ID_OK;
+}
+
+id_status id_get_R(id_handle h, float* R_out, int64_t ldr) {
+  if (!h || !R_out) return ID_ERR_ARG;
+  if (!h->have_qr) return fail(h, ID_ERR_STATE, "no QRCP result");
+  if (ldr < h->k_out) return ID_ERR_ARG;
+  // R is stored row-major k x n; output column-major k x n
+  CK(launch_R_export(h->R, h->k_out, (int)h->n, R_out, ldr, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return ID_OK;
+}
+
+id_status id_get_perm(id_handle h, int32_t* perm_out) {
+  if (!h || !perm_out) return ID_ERR_ARG;
+  if (h->perm_host.size() != (size_t)h->n) return fail(h, ID_ERR_STATE, "no QRCP result");
+  memcpy(perm_out, h->perm_host.data(), h->n * sizeof(int32_t));
+  return ID_OK;
+}
+
+id_status id_get_AL(id_handle h, void* out, int64_t ld) {
+  if (!h || !out || ld < h->m_local) return ID_ERR_ARG;
+  if (!h->fmt) return fail(h, ID_ERR_STATE, "no A_L yet");
+  CK(launch_export_S(h->fmt, h->S, h->m_local, (int)h->n, out, ld, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return ID_OK;
+}
+
+id_status id_get_stats(id_handle h, id_stats* out) {
+  if (!h || !out) return ID_ERR_ARG;
+  *out = h->stats;
+  return ID_OK;
+}
+
+int32_t id_nccl_unique_id_bytes(void) { return 128; }
+
+id_status id_nccl_get_unique_id(void* out) {
+  if (!out) return ID_ERR_ARG;
+  NcclApi& api = nccl();
+  if (!api.ok) return ID_ERR_NCCL;
+  return api.GetUniqueId(out) == 0 ? ID_OK : ID_ERR_NCCL;
+}
+
+id_status id_nccl_comm_init(void** comm, const void* unique_id, int32_t nranks, int32_t rank) {
+  if (!comm || !unique_id) return ID_ERR_ARG;
+  NcclApi& api = nccl();
+  if (!api.ok) return ID_ERR_NCCL;
+  NcclUid uid;
+  memcpy(uid.internal, unique_id, 128);
+  CommInitRankFn fn = (CommInitRankFn)api.CommInitRank;
+  return fn(comm, nranks, uid, rank) == 0 ? ID_OK : ID_ERR_NCCL;
+}
+
+id_status id_nccl_comm_destroy(void* comm) {
+  if (!comm) return ID_ERR_ARG;
+  NcclApi& api = nccl();
+  if (!api.ok) return ID_ERR_NCCL;
+  return api.CommDestroy(comm) == 0 ? ID_OK : ID_ERR_NCCL;
+}
+
+}  // extern "C"

@@ -1,0 +1,105 @@
+// Internal definitions shared by the CUDA translation units of libmpid.so.
+// Not part of the ABI (include/mpid.h is).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace mpid {
+
+// ---------------------------------------------------------------------------
+// Data layout of the stored low-precision matrix S (A_L, re-stored every nb
+// steps): "8-row interleaved column-major".  Element (r, c) of the m_pad x n
+// shard lives at index ((r >> 3) * n + c) * 8 + (r & 7).  One 8-row group of
+// one column is 16 bytes (fp16) or 32 bytes (fp32) and a row group of all n
+// columns is contiguous, so a warp whose lanes take 32 consecutive columns of
+// one row group reads 512 B (fp16) / 1 KB (fp32) contiguous bytes.
+// ---------------------------------------------------------------------------
+constexpr int RG = 8;                  // rows per group
+constexpr int NB_MAX = 16;             // max store interval (pending reflectors)
+constexpr int NSLOT = NB_MAX + 1;      // cyclic slots for u / f vectors
+constexpr int PASS_THREADS = 256;      // 8 warps
+constexpr int PASS_WARPS = PASS_THREADS / 32;
+constexpr int PASS_TILE_G = 32;        // row groups per tile (256 rows)
+constexpr int MAX_RED_BLOCKS = 1024;   // max partial-sum rows per step
+
+struct DevScalars {                   // device-resident per-call state
+  double scale;        // s
+  double maxabs;       // max |a_ij| (global)
+  double normAD2;      // ||A_D||_F^2 (global)
+  double normAL2;      // ||A_L||_F^2 (global)
+  double eps2normAL2;  // (eps ||A_L||_F)^2, 0 = fixed rank
+  double resid2;       // remaining norm mass after the last completed step
+  int32_t overflow;    // any Inf in A_L
+  int32_t done;        // QRCP finished early (tolerance / underflow)
+  int32_t status;      // 0 ok, ID_ERR_UNDERFLOW ...
+  int32_t k_out;       // completed steps
+  int32_t pivot;       // pivot chosen for the next step (current column position)
+  int32_t pad[3];
+};
+
+struct PassParams {
+  void* S;                 // T* stored matrix
+  int64_t ngroups;         // m_pad / 8
+  int64_t row_offset;      // global index of local row 0
+  int64_t m_local;         // real rows in this shard
+  int n;
+  int j;                   // step (global row/col index of the pivot position)
+  int j0;                  // first pending step
+  int npend;               // j - j0 pending reflectors
+  int store;               // write back fl(A~) after forming
+  int tiles_per_cta;       // row tiles per blockIdx.x
+  int ntiles;              // total row tiles
+  int chunks_per_split;    // 32-column chunks per blockIdx.y
+  float* U;                // [NSLOT][m_pad] raw u vectors
+  const float* F;          // [NSLOT][n]   f vectors (current column order)
+  const double* cvec;      // [k_max] c_t = 1/(u_t - beta_t) per step
+  double* part;            // [gridDim.x][2][n] partial (w, s)
+  double* xr;              // [n] row j of A~ (owner rank writes)
+  const DevScalars* sc;
+  int64_t m_pad;
+};
+
+// host-side launchers ---------------------------------------------------------
+cudaError_t launch_maxabs(const double* A, int64_t m, int64_t n, int64_t ld, double* part,
+                          int nblk, cudaStream_t st);
+cudaError_t launch_maxabs_finish(const double* part, int nblk, DevScalars* sc, int scaling,
+                                 cudaStream_t st);
+cudaError_t launch_scale_from_max(DevScalars* sc, int scaling, cudaStream_t st);
+cudaError_t launch_round(int fmt, const double* A, int64_t m, int64_t m_pad, int64_t n, int64_t ld,
+                         void* S, double* part, int gx, DevScalars* sc, cudaStream_t st);
+cudaError_t launch_init_pivot(const double* norms, int n, int* perm, DevScalars* sc,
+                              cudaStream_t st);
+cudaError_t launch_pass(int fmt, const PassParams& p, dim3 grid, cudaStream_t st);
+cudaError_t launch_pass_reduce(const double* part, int gx, int n, int j, const double* xr,
+                               int own_row, double* red, const DevScalars* sc, cudaStream_t st);
+cudaError_t launch_reflector(const double* red, int n, int j, int k_max, int nslot_f, float* F,
+                             float* R, double* beta, double* cvec, double* tau, const int* perm,
+                             DevScalars* sc, cudaStream_t st);
+cudaError_t launch_swap(int fmt, void* S, int64_t ngroups, int n, int jn, int j0, int steps_done,
+                        float* F, float* R, int* perm, DevScalars* sc, cudaStream_t st);
+cudaError_t launch_export_S(int fmt, const void* S, int64_t m_local, int n, void* out, int64_t ld,
+                            cudaStream_t st);
+
+// fp64 stage
+cudaError_t launch_gather_cols(const double* A, int64_t m, int64_t ld, const int* perm, int k,
+                               double* X, cudaStream_t st);
+cudaError_t launch_tsmm(const double* X, int64_t ldx, int k1, const double* Y, int64_t ldy, int n1,
+                        int64_t m, double* part, int splits, cudaStream_t st);
+cudaError_t launch_sum_partials(const double* part, int splits, int64_t len, double* out,
+                                cudaStream_t st);
+cudaError_t launch_cholesky(double* G, int k, int* info, cudaStream_t st);
+cudaError_t launch_trsm_right_upper(double* X, int64_t m, int64_t ldx, const double* Rm, int k,
+                                    cudaStream_t st);
+cudaError_t launch_trsm_left_upper(const double* R1, const double* R2, int k, const double* B,
+                                   int64_t ldb, const int* map, int ncols, double* T, int64_t ldt,
+                                   int mode, cudaStream_t st);
+cudaError_t launch_R_to_fp64(const float* R, int k, int n, double* Rd, cudaStream_t st);
+cudaError_t launch_R_export(const float* R, int k, int n, float* out, int64_t ldr, cudaStream_t st);
+cudaError_t launch_assemble_P(const double* T, int64_t ldt, int k, int n, const int* perm, double* P,
+                              int64_t ldp, cudaStream_t st);
+cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int n, const double* X, int k,
+                         const double* P, int64_t ldp, double* part, int* nblk_out, cudaStream_t st);
+cudaError_t launch_sum_scalar(const double* part, int nblk, double* out, cudaStream_t st);
+
+}  // namespace mpid

@@ -1,0 +1,49 @@
+"""Shared helpers for the -m gpu parity tests (test infrastructure)."""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle.qrcp import certified_steps
+
+
+def to_dev(A: np.ndarray):
+    """numpy m x n (any order) -> torch (n, m) contiguous fp64 on cuda = column-major m x n."""
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(A, dtype=np.float64).T)).cuda()
+
+
+def run_gpu(A: np.ndarray, fmt: str, scaling: str, k: int, nb: int = 4, eps: float = 0.0,
+            mode: str = "lsq", use_graph: bool = True, allow_underflow=False, host=False):
+    from paper_2012_00706_b200.mpid import MPID
+    import torch
+    if host:
+        At = torch.from_numpy(np.ascontiguousarray(np.asarray(A, dtype=np.float64).T)).pin_memory()
+    else:
+        At = to_dev(A)
+    h = MPID(At, k_max=k)
+    q = h.qrcp(fmt, scaling, k=k, eps=eps, nb=nb, use_graph=use_graph, allow_underflow=allow_underflow)
+    out = {"k": q.k, "piv": q.piv, "status": q.status, "h": h}
+    if q.k > 0 and q.status == 0:
+        out["R"] = h.get_R().cpu().numpy().astype(np.float64)
+        out["perm"] = h.get_perm()
+        P = h.coeffs(mode)
+        out["P"] = P.cpu().numpy()
+        out["err"] = h.error()
+    out["stats"] = h.stats()
+    return out
+
+
+def prefix_match(piv_gpu, res_oracle, c_tie=64.0):
+    """Length of the ordered prefix on which GPU and oracle agree, and the first
+    uncertified oracle step (reading R10)."""
+    cert = certified_steps(res_oracle, c_tie=c_tie)
+    k = min(len(piv_gpu), res_oracle.k_out)
+    first_unc = k
+    for i in range(k):
+        if not cert[i]:
+            first_unc = i
+            break
+    agree = 0
+    while agree < k and piv_gpu[agree] == res_oracle.perm[agree]:
+        agree += 1
+    return agree, first_unc
