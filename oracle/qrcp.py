@@ -20,9 +20,13 @@ What is computed (PAPER.md):
         steps, after that step's pivot is chosen and before its reflector is
         formed — nb = 1 is SPEC's store-after-every-update, nb > 1 the blocked
         implementation the paper names as future work (P:402);
-      - reductions over rows (column norms, W^T u) accumulated in fp64 (reading
-        R5: sequential fp32 sums stagnate at m = 2^24 rows);
-      - pivot norms recomputed from the current working matrix every step (S:215);
+      - reductions over rows (column norms, W^T u): fp32 fused multiply-add
+        chains over 8-row groups ("accumulate in single"), the group
+        partials added in fp64 (reading R5: sequential fp32 sums stagnate at
+        m = 2^24 rows);
+      - pivot norms: the exact norms of the trailing matrix formed at step j-1,
+        downdated by one step (reading R6); the recompute-every-step form of
+        SPEC S:215 is kept as a cross-check (norms="recompute");
       - ties broken toward the lowest original column index (S:216);
       - R rows normalised so that R_jj >= 0.
     fmt = "fp64" runs the same algorithm entirely in fp64 (Algorithm 1).
@@ -52,7 +56,7 @@ class QRCPResult:
     top2: np.ndarray            # (k_out, 2) the two largest candidate norms at each step
     maxnorm0: float             # max_i ||A_L(:, i)|| (scale for tie certification)
     normAL: float               # ||A_L||_F
-    resid: list = field(default_factory=list)   # sqrt(sum of remaining norms^2) before each step (+ after the last)
+    resid: list = field(default_factory=list)   # exact sqrt(sum of remaining norms^2) before each step (+ after the last)
 
     @property
     def I(self) -> np.ndarray:
@@ -88,20 +92,45 @@ def _work_dtype(fmt):
     return np.float64 if fmt_of(fmt) is DOUBLE else np.float32
 
 
+def _fma(a, b, c, wdt):
+    """fl(a*b + c) with one rounding to the working precision (emulated: the
+    product of two fp32 values is exact in fp64; reading R4b)."""
+    return (a.astype(np.float64) * b.astype(np.float64) + c.astype(np.float64)).astype(wdt)
+
+
+def chain8(X: np.ndarray, Y: np.ndarray, wdt) -> np.ndarray:
+    """Column sums of X*Y in the blocked order of reading R5: within each group of
+    8 consecutive rows a working-precision FMA chain (p = x0*y0; p = fma(xi, yi, p)),
+    then the group partials added in fp64.  X: (8G, c); Y: (8G, c) or (8G, 1)."""
+    G = X.shape[0] // 8
+    Xg = X.reshape(G, 8, -1)
+    Yg = Y.reshape(G, 8, -1)
+    acc = (Xg[:, 0].astype(np.float64) * Yg[:, 0].astype(np.float64)).astype(wdt)
+    for i in range(1, 8):
+        acc = _fma(Xg[:, i], Yg[:, i], acc, wdt)
+    return acc.astype(np.float64).sum(axis=0)
+
+
 def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1,
-                     eps: float = 0.0) -> QRCPResult:
+                     eps: float = 0.0, norms: str = "downdate", acc: str = "chain8") -> QRCPResult:
     """Householder QRCP of the already-rounded A_L, in the precision model above.
 
     Step j (0-based), following Eq. (6)-(7):
-      1. s_i = ||W(j:m, i)||^2, i >= j (fp64 sum of exact fp32 squares)         [norms]
-      2. p = argmax s_i (ties: lowest original index); swap columns j <-> p     [pivot, Z]
-      2'. every nb steps (j > 0, j % nb == 0): W(j:, j:) <- fl_L(W(j:, j:))    [store point]
-      3. u = W(j:m, j); beta = -sign(u_0) sqrt(s_j); v = u / (u_0 - beta), v_0 = 1;
-         tau = (beta - u_0) / beta                                              [reflector]
-      4. w = W(j:m, j:)^T u (fp64 accumulation); R(j, i) = w_i / beta; the new
-         row j equals x_i - f_i with x = W(j, j:), so f = x - w / beta
-         (= tau * W^T v); W(j:m, j:) <- W - v f^T in fp32                       [update]
-      5. R(j, :) *= sign(beta) so that R_jj = |beta| >= 0.
+      1. p = argmax vn_i over i >= j (ties: lowest original index); swap j <-> p   [pivot, Z]
+         vn: initial exact column norms^2 of A_L; then (norms="downdate", reading
+         R6 / SURVEY A2) the one-step downdate vn_i = s_i - R(j-1, i)^2 of the
+         exact norms s of the previous step's trailing matrix; (norms="recompute")
+         the exact norms of the current trailing matrix (cross-check).
+      2. every nb steps (j > 0, j % nb == 0): W(j:, j:) <- fl_L(W(j:, j:))      [store point, R4]
+      3. s_i = ||W(j:m, i)||^2, w = W(j:m, j:)^T u with u = W(j:m, j), summed in
+         the blocked order `acc` ("chain8": 8-row fp32 FMA chains + fp64, R5;
+         "fp64": exact products summed in fp64)                                 [reductions]
+      4. beta = -sign(u_0) sqrt(s_j); c = 1/(u_0 - beta); v = fl(u c), v_0 = 1;
+         tau = (beta - u_0)/beta; R(j, i) = w_i / beta (row sign-normalised so
+         R_jj = |beta|); f = fl(x - w/beta) with x = W(j, j:) (= tau W^T v)
+      5. W(j:m, j:) <- fl(W - v f^T), one rounding per entry                     [update, R4b]
+    The tolerance stop (reading R8) is tested before step j >= 1 on the exact
+    norms of step 3: sqrt(sum_{i >= j} s_i) <= eps ||A_L||_F -> k = j.
     """
     fmtL = fmt_of(fmt)
     wdt = _work_dtype(fmt)
@@ -109,7 +138,9 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
     m, n = A_L.shape
     if not (1 <= k_max <= min(m, n)):
         raise ValueError("k out of range (DimensionError)")
-    W = np.array(A_L, dtype=wdt, order="F")
+    m8 = (m + 7) // 8 * 8
+    W = np.zeros((m8, n), dtype=wdt, order="F")
+    W[:m] = A_L
     perm = np.arange(n)
     R = np.zeros((k_max, n), dtype=np.float64)
     V = np.zeros((m, k_max), dtype=np.float64)
@@ -118,51 +149,67 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
     col2 = np.sum(A_L * A_L, axis=0)
     normAL = math.sqrt(float(np.sum(col2)))
     maxnorm0 = math.sqrt(float(np.max(col2))) if n else 0.0
+    vn = col2.copy()                                        # exact initial norms^2
+    tiny = DOUBLE.min_normal if fmtL is DOUBLE else SINGLE.min_normal
+
+    def reduce(X, Y):
+        if acc == "chain8":
+            return chain8(X, Y, wdt)
+        return np.sum(X.astype(np.float64) * Y.astype(np.float64), axis=0)
+
     resid = []
     status, k_out = "ok", k_max
     for j in range(k_max):
-        Wt = W[j:, j:].astype(np.float64)
-        s = np.sum(Wt * Wt, axis=0)                           # step 1
-        resid.append(math.sqrt(float(np.sum(s))))
-        if eps > 0.0 and j > 0 and resid[-1] <= eps * normAL:
-            k_out = j
-            break
-        cand = np.flatnonzero(s == s.max())                    # step 2, tie -> lowest original index
-        best = int(cand[np.argmin(perm[j + cand])])
-        srt = np.sort(s)[::-1]
-        top2[j] = [math.sqrt(srt[0]), math.sqrt(srt[1]) if len(srt) > 1 else 0.0]
+        g0 = (j // 8) * 8                                   # first row of j's 8-row group
+        if norms == "recompute":
+            Wj = W[g0:, j:].copy()
+            Wj[: j - g0] = 0
+            vn[j:] = reduce(Wj, Wj)
+        cand = vn[j:]
+        c_ = np.flatnonzero(cand == cand.max())             # step 1, tie -> lowest original index
+        best = int(c_[np.argmin(perm[j + c_])])
+        srt = np.sort(cand)[::-1]
+        top2[j] = [math.sqrt(max(srt[0], 0.0)), math.sqrt(max(srt[1], 0.0)) if len(srt) > 1 else 0.0]
         p = j + best
-        tiny = DOUBLE.min_normal if fmtL is DOUBLE else SINGLE.min_normal
-        if s[best] < tiny or s[best] == 0.0:
-            status, k_out = "underflow", j
-            break
         if p != j:
             W[:, [j, p]] = W[:, [p, j]]
-            Wt[:, [0, best]] = Wt[:, [best, 0]]
             R[:j, [j, p]] = R[:j, [p, j]]
             perm[[j, p]] = perm[[p, j]]
-            s[[0, best]] = s[[best, 0]]
-        if j > 0 and j % nb == 0 and fmtL is not DOUBLE:       # store point (reading R4)
-            W[j:, j:] = round_to(Wt, fmtL).reshape(m - j, n - j)
-            Wt = W[j:, j:].astype(np.float64)
-        u = Wt[:, 0]                                           # step 3
-        sj = float(np.sum(u * u))
-        u0 = float(u[0])
+            vn[[j, p]] = vn[[p, j]]
+        if j > 0 and j % nb == 0 and fmtL is not DOUBLE:    # step 2, store point
+            W[j:, j:] = round_to(W[j:, j:].astype(np.float64), fmtL).reshape(m8 - j, n - j)
+        Wj = W[g0:, j:].copy()                              # step 3 (rows < j masked to 0)
+        Wj[: j - g0] = 0
+        u = Wj[:, :1]
+        s = reduce(Wj, Wj)
+        resid.append(math.sqrt(float(np.sum(s))))           # exact remaining mass before step j
+        if eps > 0.0 and j > 0 and resid[-1] <= eps * normAL:
+            k_out = j                                       # tolerance stop (reading R8)
+            break
+        w = reduce(Wj, u)
+        sj = float(s[0])
+        if not (sj >= tiny):
+            status, k_out = "underflow", j
+            break
+        u0 = float(W[j, j])                                 # step 4
         beta = -math.copysign(math.sqrt(sj), u0)
         c = 1.0 / (u0 - beta)
-        v = (u * c).astype(wdt)
+        uu = W[j:, j].astype(np.float64)
+        v = (uu * c).astype(wdt)
         v[0] = 1.0
         tau[j] = (beta - u0) / beta
-        w = Wt.T @ u                                           # step 4
         Rraw = w / beta
-        x = Wt[0, :]
+        x = W[j, j:].astype(np.float64)
         f = (x - Rraw).astype(wdt)
-        W[j:, j:] = W[j:, j:] - np.outer(v, f).astype(wdt)
-        R[j, j:] = (Rraw * math.copysign(1.0, beta)).astype(wdt)   # step 5
-        V[j:, j] = v
+        R[j, j:] = (Rraw * math.copysign(1.0, beta)).astype(wdt)
+        vn[j + 1:] = s[1:] - Rraw[1:] ** 2                  # one-step downdate (R6)
+        W[j:, j:] = _fma(-v[:, None], f[None, :], W[j:, j:], wdt)   # step 5
+        V[j:, j] = v[: m - j]
     if status == "ok" and k_out == k_max and k_max < min(m, n):
-        Wt = W[k_max:, k_max:].astype(np.float64)
-        resid.append(math.sqrt(float(np.sum(Wt * Wt))))       # remaining mass after k steps
+        g0 = (k_max // 8) * 8
+        Wj = W[g0:, k_max:].copy()
+        Wj[: k_max - g0] = 0
+        resid.append(math.sqrt(float(np.sum(reduce(Wj, Wj)))))   # exact mass after k steps
     R = R[:k_out]
     return QRCPResult(perm, R, k_out, status, V[:, :k_out], tau[:k_out], top2[:k_out],
                       maxnorm0, normAL, resid)

@@ -310,6 +310,20 @@ __global__ void __launch_bounds__(1024) k_reflector(const double* __restrict__ r
                                                     const int* __restrict__ perm,
                                                     DevScalars* __restrict__ sc) {
   if (sc->done) return;
+  // tolerance stop on the exact norms of this step's formed trailing matrix (R8)
+  if (j > 0 && sc->eps2normAL2 > 0.0) {
+    double tot = 0.0;
+    for (int i = j + threadIdx.x; i < n; i += blockDim.x) tot += red[n + i];
+    tot = block_sum(tot);
+    if (tot <= sc->eps2normAL2) {
+      if (threadIdx.x == 0) {
+        sc->k_out = j;
+        sc->resid2 = tot;
+        sc->done = 1;
+      }
+      return;
+    }
+  }
   const double sj = red[n + j];
   const double uj = red[2 * n + j];
   if (!(sj >= (double)FLT_MIN)) {                    // pivot norm^2 underflows fp32
@@ -354,7 +368,6 @@ __global__ void __launch_bounds__(1024) k_reflector(const double* __restrict__ r
     sc->resid2 = rest;
     sc->pivot = best.pos;
     if (j + 1 >= k_max || best.pos < 0) sc->done = 1;
-    else if (sc->eps2normAL2 > 0.0 && rest <= sc->eps2normAL2) sc->done = 1;
   }
 }
 

@@ -76,94 +76,96 @@ __global__ void k_scale_from_max(DevScalars* sc, int scaling) {
   sc->scale = s;
 }
 
-template <typename T> struct Pack8;
-template <> struct Pack8<__half> {
-  using V = uint4;                               // 8 x fp16 = 16 B
-  __device__ static V pack(const double* x, int* inf, double* sq) {
-    uint16_t h[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const __half v = __double2half(x[i]);      // cvt.rn.f16.f64: single RNE rounding
-      h[i] = __half_as_ushort(v);
-      const double d = (double)__half2float(v);
-      *inf |= isinf(d) ? 1 : 0;
-      sq[i] = d * d;
-    }
-    V o;
-    o.x = h[0] | ((uint32_t)h[1] << 16);
-    o.y = h[2] | ((uint32_t)h[3] << 16);
-    o.z = h[4] | ((uint32_t)h[5] << 16);
-    o.w = h[6] | ((uint32_t)h[7] << 16);
-    return o;
-  }
-};
-template <> struct Pack8<float> {
-  struct V { float4 a, b; };
-  __device__ static V pack(const double* x, int* inf, double* sq) {
-    float f[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      f[i] = __double2float_rn(x[i]);           // cvt.rn.f32.f64
-      *inf |= isinf(f[i]) ? 1 : 0;
-      sq[i] = (double)f[i] * (double)f[i];
-    }
-    V o;
-    o.a = make_float4(f[0], f[1], f[2], f[3]);
-    o.b = make_float4(f[4], f[5], f[6], f[7]);
-    return o;
-  }
-};
-
-// K1: grid (ceil(n/32), GY).  Lane = column within a 32-column chunk, warp w of
-// the block takes row groups g = g0 + w, g0 + w + 8, ... of the block's range.
-// Per (blockIdx.y, column): fp64 partial of ||A_L(:,c)||^2 -> part[y*n + c];
-// per block: partial ||A_D||_F^2 -> aux[y*gridDim.x + x].
+// K1: grid (ceil(n/32), GY).  A CTA owns 32 columns and the row tiles
+// t = blockIdx.y, blockIdx.y + GY, ... of 256 rows.  Per tile: each warp reads
+// 4 whole columns of the tile (coalesced 256 B fp64 rows per instruction),
+// rounds once fp64 -> fp16/fp32 (cvt.rn), keeps exact fp64 squares for the
+// column norms, and stages the values in shared memory; the block then writes
+// the tile in the interleaved layout, 32 consecutive columns x 16 B per row
+// group (512 B contiguous per warp store).
+// Partials: part[y*n + c] = sum of ||A_L(rows, c)||^2 over the CTA's tiles,
+// aux[y*gridDim.x + x] = sum a_ij^2 (for ||A_D||_F).
 template <typename T>
 __global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int64_t m,
                                                int64_t ngroups, int64_t n, int64_t ld,
                                                T* __restrict__ S, double* __restrict__ part,
                                                double* __restrict__ aux,
                                                DevScalars* __restrict__ sc) {
-  using P = Pack8<T>;
+  constexpr int TR = 256;                          // rows per tile
+  constexpr int PAD = 16 / sizeof(T);              // keep 16 B alignment, spread banks
+  __shared__ __align__(16) T tile[32][TR + PAD];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
-  const int64_t per = (ngroups + gridDim.y - 1) / gridDim.y;
-  const int64_t g0 = (int64_t)blockIdx.y * per;
-  const int64_t g1 = min(ngroups, g0 + per);
+  const int64_t c0 = (int64_t)blockIdx.x * 32;
+  const int64_t ntiles = ngroups / (TR / 8);
   const double s = sc->scale;
-  double colsq = 0.0, adsq = 0.0;
+  double colsq[4] = {0.0, 0.0, 0.0, 0.0};
+  double adsq = 0.0;
   int inf = 0;
-  if (c < n) {
-    const double* col = A + c * ld;
-    for (int64_t g = g0 + warp; g < g1; g += 8) {
-      double x[8], sq[8];
-      const int64_t r0 = g * 8;
+  for (int64_t t = blockIdx.y; t < ntiles; t += gridDim.y) {
+    const int64_t r0 = t * TR;
+    __syncthreads();
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const double a = (r0 + i < m) ? __ldg(col + r0 + i) : 0.0;
+    for (int q = 0; q < 4; ++q) {
+      const int cl = warp * 4 + q;
+      const int64_t c = c0 + cl;
+      const double* col = A + c * ld;
+#pragma unroll
+      for (int i = 0; i < TR / 32; ++i) {
+        const int rr = i * 32 + lane;
+        const int64_t r = r0 + rr;
+        const double a = (c < n && r < m) ? __ldcs(col + r) : 0.0;
         adsq = fma(a, a, adsq);
-        x[i] = __dmul_rn(s, a);
+        const double x = __dmul_rn(s, a);
+        T v;
+        double d;
+        if (sizeof(T) == 2) {
+          const __half hv = __double2half(x);          // cvt.rn.f16.f64: single RNE rounding
+          d = (double)__half2float(hv);
+          v = *reinterpret_cast<const T*>(&hv);
+        } else {
+          const float fv = __double2float_rn(x);       // cvt.rn.f32.f64
+          d = (double)fv;
+          v = *reinterpret_cast<const T*>(&fv);
+        }
+        inf |= isinf(d) ? 1 : 0;
+        colsq[q] = fma(d, d, colsq[q]);
+        tile[cl][rr] = v;
       }
-      const typename P::V v = P::pack(x, &inf, sq);
-      *reinterpret_cast<typename P::V*>(S + (g * n + c) * 8) = v;
+    }
+    __syncthreads();
+    // write: thread -> (column lane, row group warp + 8 j)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) colsq += sq[i];
+    for (int jg = 0; jg < TR / 8 / 8; ++jg) {
+      const int g = warp + 8 * jg;
+      const int64_t c = c0 + lane;
+      if (c < n) {
+        const uint4* src = reinterpret_cast<const uint4*>(&tile[lane][g * 8]);
+        uint4* dst = reinterpret_cast<uint4*>(S + ((t * (TR / 8) + g) * n + c) * 8);
+        if (sizeof(T) == 2) {
+          __stcs(dst, src[0]);
+        } else {
+          __stcs(dst, src[0]);
+          __stcs(dst + 1, src[1]);
+        }
+      }
     }
   }
-  __shared__ double shc[8][32];
+  __shared__ double shc[32];
   __shared__ double sha[8];
   __shared__ int shi;
   if (threadIdx.x == 0) shi = 0;
-  shc[warp][lane] = colsq;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double v = warp_sum(colsq[q]);
+    if (lane == 0) shc[warp * 4 + q] = v;
+  }
   double a = warp_sum(adsq);
   if (lane == 0) sha[warp] = a;
   __syncthreads();
   if (inf) atomicOr(&shi, 1);
   if (warp == 0) {
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) t += shc[w][lane];
-    if (c < n) part[(int64_t)blockIdx.y * n + c] = t;
+    const int64_t c = c0 + lane;
+    if (c < n) part[(int64_t)blockIdx.y * n + c] = shc[lane];
     double u = lane < 8 ? sha[lane] : 0.0;
     u = warp_sum(u);
     if (lane == 0) aux[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = u;

@@ -154,3 +154,29 @@ def test_fp32_pivots_match_fp64_on_gapped_input():
     r64 = qrcp_householder(A, 48, "fp64")
     r32 = qrcp_householder(round_to(A, "fp32").reshape(A.shape), 48, "fp32", nb=16)
     assert np.array_equal(r64.perm[:48], r32.perm[:48])
+
+
+@pytest.mark.parametrize("fmt,nb", [("fp16", 4), ("fp32", 4), ("fp64", 1)])
+def test_norm_and_accumulation_variants_agree_on_certified_steps(fmt, nb):
+    """Reading R5/R6 cross-check: the one-step downdate vs recomputing the norms every
+    step, and the 8-row fp32 chains vs fp64 accumulation, give the same
+    pivots on every certified step."""
+    A = gen_config("C1")
+    AL, _ = make_AL(A, fmt, "pow2" if fmt == "fp16" else "none")
+    base = qrcp_householder(AL, 32, fmt, nb=nb)
+    cert = certified_steps(base)
+    fu = int(np.argmin(cert)) if not cert.all() else 32
+    assert fu >= 20
+    for kw in ({"norms": "recompute"}, {"acc": "fp64"}, {"norms": "recompute", "acc": "fp64"}):
+        alt = qrcp_householder(AL, 32, fmt, nb=nb, **kw)
+        assert np.array_equal(alt.perm[:fu], base.perm[:fu]), kw
+
+
+def test_chain8_is_an_accurate_sum():
+    """The blocked order stays within a few fp32 ulps of the exact (fsum) column sums."""
+    from oracle.qrcp import chain8
+    rng = np.random.default_rng(1)
+    X = rng.standard_normal((4096, 5)).astype(np.float32)
+    got = chain8(X, X, np.float32)
+    ref = np.array([math.fsum(float(v) ** 2 for v in X[:, c]) for c in range(5)])
+    assert np.all(np.abs(got - ref) <= 8 * SINGLE.u * ref)
