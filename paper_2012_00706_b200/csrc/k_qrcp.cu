@@ -28,187 +28,6 @@
 
 namespace mpid {
 
-template <typename T> struct Io;
-template <> struct Io<__half> {
-  __device__ static __forceinline__ void load8(const __half* p, float* x) {
-    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p));
-    const __half2* h = reinterpret_cast<const __half2*>(&v);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float2 f = __half22float2(h[i]);
-      x[2 * i] = f.x;
-      x[2 * i + 1] = f.y;
-    }
-  }
-  __device__ static __forceinline__ void store8(__half* p, const float* x) {
-    uint4 v;
-    __half2* h = reinterpret_cast<__half2*>(&v);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(x[2 * i], x[2 * i + 1]);
-    __stcs(reinterpret_cast<uint4*>(p), v);
-  }
-  __device__ static __forceinline__ float load1(const __half* p) { return __half2float(*p); }
-  __device__ static __forceinline__ float rnd(float x) { return __half2float(__float2half_rn(x)); }
-};
-template <> struct Io<float> {
-  __device__ static __forceinline__ void load8(const float* p, float* x) {
-    const float4 a = __ldcs(reinterpret_cast<const float4*>(p));
-    const float4 b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
-    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-  }
-  __device__ static __forceinline__ void store8(float* p, const float* x) {
-    __stcs(reinterpret_cast<float4*>(p), make_float4(x[0], x[1], x[2], x[3]));
-    __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(x[4], x[5], x[6], x[7]));
-  }
-  __device__ static __forceinline__ float load1(const float* p) { return *p; }
-  __device__ static __forceinline__ float rnd(float x) { return x; }
-};
-
-// ---------------------------------------------------------------------------
-// k_pass<T, PMAX>: grid (GX row-CTAs, GY column splits), 256 threads.
-// Shared memory: us[256] (u of the tile rows), vs[PMAX][256] (pending v rows),
-// acc[WRS][2][ncols] fp64 per-lane-owned column accumulators.
-// ---------------------------------------------------------------------------
-template <typename T, int PMAX>
-__global__ void __launch_bounds__(PASS_THREADS, 2) k_pass(PassParams p) {
-  if (p.sc->done) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int TROWS = PASS_TILE_G * RG;                  // 256 rows per tile
-  float* us = reinterpret_cast<float*>(smem_raw);
-  float* vs = us + TROWS;                                    // [PMAX][TROWS]
-  double* acc = reinterpret_cast<double*>(vs + PMAX * TROWS);
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n = p.n, j = p.j, npend = p.npend;
-  T* __restrict__ S = reinterpret_cast<T*>(p.S);
-
-  // column range of this CTA: chunks [q0, q1) of 32 columns starting at column j
-  const int nchunk_tot = (n - j + 31) >> 5;
-  const int q0 = blockIdx.y * p.chunks_per_split;
-  const int q1 = min(nchunk_tot, q0 + p.chunks_per_split);
-  if (q0 >= q1) return;
-  const int nchunks = q1 - q0;
-  const int cbase = j + 32 * q0;                            // first column of the CTA
-  const int ncols = min(n, j + 32 * q1) - cbase;
-  int CW = 1;
-  while (CW * 2 <= PASS_WARPS && CW * 2 <= nchunks) CW *= 2;
-  const int WRS = PASS_WARPS / CW;
-  const int cw = warp % CW, rw = warp / CW;
-
-  for (int i = tid; i < WRS * 2 * ncols; i += PASS_THREADS) acc[i] = 0.0;
-
-  // pending reflectors: slot and c for step t = j0 + l
-  int slot[PMAX];
-  float fcol_j[PMAX];
-#pragma unroll
-  for (int l = 0; l < PMAX; ++l) {
-    slot[l] = (p.j0 + l) % NSLOT;
-    fcol_j[l] = (l < npend) ? p.F[(int64_t)slot[l] * n + j] : 0.f;
-  }
-  const int slot_j = j % NSLOT;
-  const int64_t jloc = (int64_t)j - p.row_offset;            // local row of the pivot row
-  const int t0 = blockIdx.x * p.tiles_per_cta;
-  const int t1 = min(p.ntiles, t0 + p.tiles_per_cta);
-
-  for (int t = t0; t < t1; ++t) {
-    const int64_t r_tile = (int64_t)t * TROWS;               // first local row of the tile
-    if (p.row_offset + r_tile + TROWS <= j) continue;          // whole tile above row j
-    __syncthreads();
-    // ---- phase 1: pending v rows and u = A~(:, j) for the tile rows --------
-    {
-      const int64_t rl = r_tile + tid;
-      const int64_t rg = p.row_offset + rl;
-      const bool real = rl < p.m_local;
-      float a = Io<T>::load1(S + ((rl >> 3) * n + j) * RG + (rl & 7));
-#pragma unroll
-      for (int l = 0; l < PMAX; ++l) {
-        if (l < npend) {
-          const int64_t tstep = p.j0 + l;
-          float v;
-          if (!real || rg < tstep) v = 0.f;
-          else if (rg == tstep) v = 1.f;
-          else v = __double2float_rn((double)p.U[(int64_t)slot[l] * p.m_pad + rl] * p.cvec[tstep]);
-          vs[l * TROWS + tid] = v;
-          a = fmaf(-v, fcol_j[l], a);
-        }
-      }
-      if (p.store) a = Io<T>::rnd(a);                           // storage rounding point (R4)
-      const float u = (real && rg >= j) ? a : 0.f;
-      us[tid] = u;
-      if (blockIdx.y == 0) p.U[(int64_t)slot_j * p.m_pad + rl] = u;
-    }
-    __syncthreads();
-    // ---- phase 2: stream the tile's columns --------------------------------
-    for (int q = cw; q < nchunks; q += CW) {
-      const int col = cbase + 32 * q + lane;
-      const bool valid = col < n;
-      float f[PMAX];
-#pragma unroll
-      for (int l = 0; l < PMAX; ++l)
-        f[l] = (l < npend && valid) ? p.F[(int64_t)slot[l] * n + col] : 0.f;
-      double aw = 0.0, as = 0.0;
-      if (valid) {
-#pragma unroll 2
-        for (int gl = rw; gl < PASS_TILE_G; gl += WRS) {
-          const int64_t g = (int64_t)t * PASS_TILE_G + gl;
-          const int64_t r0 = g * 8;
-          if (p.row_offset + r0 + 8 <= j) continue;              // rows above the pivot row
-          T* ptr = S + (g * n + col) * RG;
-          float x[8];
-          Io<T>::load8(ptr, x);
-#pragma unroll
-          for (int l = 0; l < PMAX; ++l) {
-            if (l < npend) {
-              const float4 v0 = *reinterpret_cast<const float4*>(vs + l * TROWS + gl * 8);
-              const float4 v1 = *reinterpret_cast<const float4*>(vs + l * TROWS + gl * 8 + 4);
-              x[0] = fmaf(-v0.x, f[l], x[0]); x[1] = fmaf(-v0.y, f[l], x[1]);
-              x[2] = fmaf(-v0.z, f[l], x[2]); x[3] = fmaf(-v0.w, f[l], x[3]);
-              x[4] = fmaf(-v1.x, f[l], x[4]); x[5] = fmaf(-v1.y, f[l], x[5]);
-              x[6] = fmaf(-v1.z, f[l], x[6]); x[7] = fmaf(-v1.w, f[l], x[7]);
-            }
-          }
-          if (p.store) {                                             // storage rounding point (R4)
-#pragma unroll
-            for (int i = 0; i < 8; ++i) x[i] = Io<T>::rnd(x[i]);
-            Io<T>::store8(ptr, x);
-          }
-          const float4 u0 = *reinterpret_cast<const float4*>(us + gl * 8);
-          const float4 u1 = *reinterpret_cast<const float4*>(us + gl * 8 + 4);
-          if (r0 + 8 + p.row_offset > j && r0 + p.row_offset <= j) {   // group holding row j
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (p.row_offset + r0 + i < j) x[i] = 0.f;
-            if (jloc >= r0 && jloc < r0 + 8) p.xr[col] = x[jloc - r0];
-          }
-          float pw = x[0] * u0.x;
-          pw = fmaf(x[1], u0.y, pw); pw = fmaf(x[2], u0.z, pw); pw = fmaf(x[3], u0.w, pw);
-          pw = fmaf(x[4], u1.x, pw); pw = fmaf(x[5], u1.y, pw); pw = fmaf(x[6], u1.z, pw);
-          pw = fmaf(x[7], u1.w, pw);
-          float ps = x[0] * x[0];
-#pragma unroll
-          for (int i = 1; i < 8; ++i) ps = fmaf(x[i], x[i], ps);
-          aw += (double)pw;
-          as += (double)ps;
-        }
-        const int cl = col - cbase;
-        acc[(rw * 2 + 0) * ncols + cl] += aw;
-        acc[(rw * 2 + 1) * ncols + cl] += as;
-      }
-    }
-  }
-  __syncthreads();
-  for (int cl = tid; cl < ncols; cl += PASS_THREADS) {
-    double w = 0.0, s = 0.0;
-    for (int r = 0; r < WRS; ++r) {
-      w += acc[(r * 2 + 0) * ncols + cl];
-      s += acc[(r * 2 + 1) * ncols + cl];
-    }
-    p.part[((int64_t)blockIdx.x * 2 + 0) * n + cbase + cl] = w;
-    p.part[((int64_t)blockIdx.x * 2 + 1) * n + cbase + cl] = s;
-  }
-}
-
 // red[0][c] = sum w, red[1][c] = sum s over the GX row-CTAs, red[2][c] = x_c.
 // CTA = 32 columns (lanes) x 8 warps; warp w sums rows b = w, w+8, ... ; the 8
 // warp partials are then added in warp order (deterministic).
@@ -442,39 +261,6 @@ __global__ void k_swap(T* __restrict__ S, int64_t ngroups, int n, int jn, int j0
 }
 
 // ---------------------------------------------------------------------------
-template <typename T, int PMAX>
-static cudaError_t launch_pass_t(const PassParams& p, dim3 grid, cudaStream_t st) {
-  const int nchunks = (p.n - p.j + 31) / 32;
-  const int cps = p.chunks_per_split;
-  const int nch = cps < nchunks ? cps : nchunks;
-  int CW = 1;
-  while (CW * 2 <= PASS_WARPS && CW * 2 <= nch) CW *= 2;
-  const int WRS = PASS_WARPS / CW;
-  const size_t smem = (size_t)(PASS_TILE_G * RG) * (1 + PMAX) * sizeof(float) +
-                      (size_t)WRS * 2 * (32 * nch) * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_pass<T, PMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
-  k_pass<T, PMAX><<<grid, PASS_THREADS, smem, st>>>(p);
-  return cudaGetLastError();
-}
-
-template <typename T>
-static cudaError_t launch_pass_fmt(const PassParams& p, dim3 grid, cudaStream_t st) {
-  const int np = p.npend;
-  if (np <= 1) return launch_pass_t<T, 1>(p, grid, st);
-  if (np <= 2) return launch_pass_t<T, 2>(p, grid, st);
-  if (np <= 4) return launch_pass_t<T, 4>(p, grid, st);
-  if (np <= 8) return launch_pass_t<T, 8>(p, grid, st);
-  return launch_pass_t<T, 16>(p, grid, st);
-}
-
-cudaError_t launch_pass(int fmt, const PassParams& p, dim3 grid, cudaStream_t st) {
-  return fmt == 1 ? launch_pass_fmt<__half>(p, grid, st) : launch_pass_fmt<float>(p, grid, st);
-}
-
 cudaError_t launch_pass_reduce(const double* part, int gx, int n, int j, const double* xr,
                                int own_row, double* red, const DevScalars* sc, cudaStream_t st) {
   const int cols = n - j;

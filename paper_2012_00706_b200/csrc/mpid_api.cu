@@ -230,6 +230,7 @@ id_status id_create(id_handle* hp, const double* A_D, int64_t m_global, int64_t 
       row_offset + m_local > m_global || nranks < 1 || rank < 0 || rank >= nranks)
     return ID_ERR_DIM;
   if (nranks > 1 && !nccl_comm) return ID_ERR_ARG;
+  if (row_offset % 8) return ID_ERR_DIM;  // shards start on 8-row group boundaries
   if (((uintptr_t)workspace) & 255) return ID_ERR_ARG;
   mpid_ctx* h = new mpid_ctx();
   h->m_global = m_global;
@@ -435,9 +436,6 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
   CK(rec(h, h->ev[1]));
   CK(launch_init_pivot(h->norms, (int)n, h->perm, h->sc, h->st));
   h->kernel_launches += 1;
-  const int gx = gx_of(h->m_pad);
-  const int ntiles = (int)(h->m_pad / (PASS_TILE_G * RG));
-  const int tpc = (ntiles + gx - 1) / gx;
   const int own_lo = (int)std::min<int64_t>(h->row_offset, INT32_MAX);
   for (int j = 0; j < k_max; ++j) {
     const int j0 = j == 0 ? 0 : nb * ((j - 1) / nb);
@@ -447,33 +445,28 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     PassParams p{};
     p.S = h->S;
     p.ngroups = h->m_pad / 8;
+    const int64_t jl = (int64_t)j - h->row_offset;
+    p.g_lo = jl > 0 ? jl / 8 : 0;
     p.row_offset = h->row_offset;
     p.m_local = h->m_local;
+    p.m_pad = h->m_pad;
     p.n = (int)n;
     p.j = j;
     p.j0 = j0;
     p.npend = npend;
     p.store = store;
-    p.tiles_per_cta = tpc;
-    p.ntiles = ntiles;
-    const int nchunks = (int)((n - j + 31) / 32);
-    int gy = std::max(1, std::min(nchunks, (2 * num_sms() + gx - 1) / gx));
-    int cps = (nchunks + gy - 1) / gy;
-    cps = std::min(cps, 256);
-    gy = (nchunks + cps - 1) / cps;
-    p.chunks_per_split = cps;
     p.U = h->U;
     p.F = h->F;
     p.cvec = h->cvec;
     p.part = h->part;
     p.xr = h->xr;
     p.sc = h->sc;
-    p.m_pad = h->m_pad;
+    int gx_used = 0;
     if (profile) CK(rec(h, h->pass_ev[2 * j]));
-    CK(launch_pass(fmt, p, dim3(gx, gy), h->st));
+    CK(launch_pass_tma(fmt, p, num_sms(), &gx_used, h->st));
     if (profile) CK(rec(h, h->pass_ev[2 * j + 1]));
     const int own = (j >= own_lo && (int64_t)j < h->row_offset + h->m_local) ? 1 : 0;
-    CK(launch_pass_reduce(h->part, gx, (int)n, j, h->xr, own, h->red, h->sc, h->st));
+    CK(launch_pass_reduce(h->part, gx_used, (int)n, j, h->xr, own, h->red, h->sc, h->st));
     s = allreduce(h, h->red, (size_t)3 * n, NCCL_SUM);
     if (s) return s;
     CK(launch_reflector(h->red, (int)n, j, k_max, NSLOT, h->F, h->R, h->beta, h->cvec, h->tau, h->perm,

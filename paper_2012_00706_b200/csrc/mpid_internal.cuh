@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
+#include <algorithm>
 
 namespace mpid {
 
@@ -39,26 +40,30 @@ struct DevScalars {                   // device-resident per-call state
 };
 
 struct PassParams {
-  void* S;                 // T* stored matrix
+  void* S;                 // T* stored matrix (interleaved layout)
   int64_t ngroups;         // m_pad / 8
-  int64_t row_offset;      // global index of local row 0
+  int64_t g_lo;            // first 8-row group holding rows >= j
+  int64_t row_offset;      // global index of local row 0 (multiple of 8)
   int64_t m_local;         // real rows in this shard
+  int64_t m_pad;
   int n;
   int j;                   // step (global row/col index of the pivot position)
   int j0;                  // first pending step
   int npend;               // j - j0 pending reflectors
   int store;               // write back fl(A~) after forming
-  int tiles_per_cta;       // row tiles per blockIdx.x
-  int ntiles;              // total row tiles
-  int chunks_per_split;    // 32-column chunks per blockIdx.y
+  int chunks_per_split;    // 32-column chunks per blockIdx.y (set by the launcher)
+  int ncols_slot;          // columns per CTA (set by the launcher)
+  int gs;                  // row groups per pipeline stage (set by the launcher)
+  int nst;                 // pipeline depth (set by the launcher)
+  int gx_used;             // gridDim.x (set by the launcher)
   float* U;                // [NSLOT][m_pad] raw u vectors
   const float* F;          // [NSLOT][n]   f vectors (current column order)
   const double* cvec;      // [k_max] c_t = 1/(u_t - beta_t) per step
   double* part;            // [gridDim.x][2][n] partial (w, s)
   double* xr;              // [n] row j of A~ (owner rank writes)
   const DevScalars* sc;
-  int64_t m_pad;
 };
+constexpr int PASS_SMEM_MAX = 225 * 1024;
 
 // host-side launchers ---------------------------------------------------------
 cudaError_t launch_maxabs(const double* A, int64_t m, int64_t n, int64_t ld, double* part,
@@ -70,7 +75,7 @@ cudaError_t launch_round(int fmt, const double* A, int64_t m, int64_t m_pad, int
                          void* S, double* part, int gx, DevScalars* sc, cudaStream_t st);
 cudaError_t launch_init_pivot(const double* norms, int n, int* perm, DevScalars* sc,
                               cudaStream_t st);
-cudaError_t launch_pass(int fmt, const PassParams& p, dim3 grid, cudaStream_t st);
+cudaError_t launch_pass_tma(int fmt, PassParams p, int num_sms, int* gx_out, cudaStream_t st);
 cudaError_t launch_pass_reduce(const double* part, int gx, int n, int j, const double* xr,
                                int own_row, double* red, const DevScalars* sc, cudaStream_t st);
 cudaError_t launch_reflector(const double* red, int n, int j, int k_max, int nslot_f, float* F,
