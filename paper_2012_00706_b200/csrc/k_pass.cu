@@ -34,14 +34,20 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
+// bounded wait: a pipeline bug traps (an error the host sees) instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
+  uint32_t done = 0;
+  for (uint32_t spin = 0;; ++spin) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (spin > (1u << 26)) __trap();
+  }
 }
 __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -374,7 +380,8 @@ static cudaError_t launch_tma_fmt(PassParams p, int num_sms, int* gx_out, cudaSt
   const int ncols = std::min(n - j, 32 * cps);
   p.ncols_slot = ncols;
   const int cpw = (cps + NCW - 1) / NCW;
-  const int pmax = p.npend <= 1 ? 1 : p.npend <= 2 ? 2 : p.npend <= 4 ? 4 : 8;
+  const int pmax = p.npend <= 1 ? 1 : p.npend <= 2 ? 2 : p.npend <= 4 ? 4 : p.npend <= 8 ? 8 : 16;
+  if (p.npend > pmax || pmax > NB_MAX) return cudaErrorInvalidValue;
   // stage = GS row groups: aim at ~24 KB of matrix data, at most 32 groups (256 rows)
   const int rowbytes = ncols * 8 * esz;
   int GS = std::max(1, std::min(32, (24 * 1024) / rowbytes));
@@ -398,7 +405,8 @@ static cudaError_t launch_tma_fmt(PassParams p, int num_sms, int* gx_out, cudaSt
     case 1: return launch_tma_p<T, 1>(p, grid, smem, cpw, st);
     case 2: return launch_tma_p<T, 2>(p, grid, smem, cpw, st);
     case 4: return launch_tma_p<T, 4>(p, grid, smem, cpw, st);
-    default: return launch_tma_p<T, 8>(p, grid, smem, cpw, st);
+    case 8: return launch_tma_p<T, 8>(p, grid, smem, cpw, st);
+    default: return launch_tma_p<T, 16>(p, grid, smem, cpw, st);
   }
 }
 

@@ -76,10 +76,8 @@ int64_t m_pad_of(int64_t m_local) {
   const int64_t T = PASS_TILE_G * RG;
   return std::max<int64_t>(T, (m_local + T - 1) / T * T);
 }
-int gx_of(int64_t m_pad) {
-  const int64_t ntiles = m_pad / (PASS_TILE_G * RG);
-  return (int)std::min<int64_t>(ntiles, 2 * num_sms());
-}
+// rows of per-CTA partials the panel pass may write: its grid.x never exceeds the SM count
+int pass_gx_cap() { return num_sms(); }
 int round_gy(int64_t m_pad, int64_t n) {
   const int64_t gx = (n + 31) / 32;
   const int64_t ngroups = m_pad / 8;
@@ -105,7 +103,7 @@ Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
   L.U = take((size_t)NSLOT * mp * 4);
   L.F = take((size_t)NSLOT * n * 4);
   L.R = take((size_t)k * n * 4);
-  L.part = take((size_t)gx_of(mp) * 2 * n * 8);
+  L.part = take((size_t)pass_gx_cap() * 2 * n * 8);
   L.red = take((size_t)3 * n * 8);
   L.xr = take((size_t)n * 8);
   L.norms = take((size_t)(n + 2) * 8);
@@ -463,7 +461,9 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     p.sc = h->sc;
     int gx_used = 0;
     if (profile) CK(rec(h, h->pass_ev[2 * j]));
-    CK(launch_pass_tma(fmt, p, num_sms(), &gx_used, h->st));
+    CK(launch_pass_tma(fmt, p, pass_gx_cap(), &gx_used, h->st));
+    if (gx_used < 1 || gx_used > pass_gx_cap())
+      return fail(h, ID_ERR_STATE, "panel pass grid %d exceeds the partials buffer (%d)", gx_used, pass_gx_cap());
     if (profile) CK(rec(h, h->pass_ev[2 * j + 1]));
     const int own = (j >= own_lo && (int64_t)j < h->row_offset + h->m_local) ? 1 : 0;
     CK(launch_pass_reduce(h->part, gx_used, (int)n, j, h->xr, own, h->red, h->sc, h->st));
@@ -557,6 +557,8 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   CK(cudaStreamSynchronize(h->st));
   h->fmt = fmt;
   const DevScalars& sc = h->sc_host;
+  if (sc.k_out < 0 || sc.k_out > k_max)
+    return fail(h, ID_ERR_STATE, "internal: k_out=%d outside [0, %d]", sc.k_out, k_max);
   h->k_out = sc.k_out;
   h->qr_status = sc.status;
   *k_out = sc.k_out;
