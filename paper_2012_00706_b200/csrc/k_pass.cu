@@ -1,21 +1,26 @@
 // k_pass — the per-step panel pass of the low-precision pivoted Householder QR
-// (Algorithm 2 line 4, P:163; Eq. (6)-(7)), the dominant (HBM-bound) kernel.
+// (Algorithm 2 line 4, P:163; Eq. (6)-(7), P:115-128), the dominant (HBM-bound) kernel.
 //
-// What one launch computes for step j (DESIGN.md §Kernels, readings R4-R6):
+// What one launch computes for step j (DESIGN.md §5, readings R4-R6):
 //   A~ = S - sum_{pending l} v_l f_l^T   formed per element in fp32 (FMA, step order)
 //   [store steps] A~ <- fl_L(A~), written back to S (the storage rounding point)
 //   u = A~(:, j) (rows >= j), w = A~^T u and s_i = ||A~(j:m, i)||^2 with 8-row
 //   fp32 FMA chains added in fp64, and the row x = A~(j, :).
 //
-// B200 structure: one persistent CTA per SM; warp 0 is a TMA producer that streams
-// stages of GS consecutive 8-row groups (each row group of the CTA's column range
-// is contiguous in the interleaved layout) with cp.async.bulk into an NST-deep
-// shared-memory ring, together with the stage's pivot-column segment and the
-// pending u vectors; 8 consumer warps form, reduce and (on store steps) round in
-// place, after which the producer writes the stage back with cp.async.bulk
-// stores.  mbarrier full/empty pairs hand stages over; no register staging of
-// global loads, so the bytes in flight per SM are the ring (~150-190 KB).
-// Packed fp32x2 FMAs (FFMA2, sm_100) halve the formation / reduction issue count.
+// B200 structure: one persistent CTA per SM (18 warps, warp-specialised):
+//   warp 0      TMA producer: one elected lane streams stages of GS consecutive
+//               8-row groups (each row group of the CTA's column range is one
+//               contiguous range in the interleaved layout) with cp.async.bulk
+//               into an NST-deep shared-memory ring, plus the stage's pivot-column
+//               segment and the pending u rows; on store steps it writes the
+//               rounded stage back with bulk stores once the consumers free it.
+//   warp 1      prep: per stage, the pending -v rows (v_t = fl(u_t c_t), v_t(t) = 1)
+//               and u = A~(:, j) for the stage's rows (+ u to global for later steps).
+//   warps 2-17  consumers: lane owns columns (c, c + 32) of its warp's 64-column
+//               block, so every FFMA2 works on a natural (col0, col1) register
+//               pair: update x2 += (-v_r) * f2, then w2 += x2 * u_r, s2 += x2 * x2.
+// mbarriers: full (TMA tx) -> prep (32 arrivals) -> consumers -> empty (NCW arrivals).
+// Bound: HBM.  Per element: 1 cvt + npend/2 + 1 FFMA2-equivalents on the FMA pipe.
 #include "mpid_internal.cuh"
 
 namespace mpid {
@@ -69,42 +74,53 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-template <typename T> struct V8;
-template <> struct V8<__half> {
-  static constexpr int BYTES = 16;
-  __device__ static __forceinline__ void load(const __half* p, float2* x) {
-    const uint4 v = *reinterpret_cast<const uint4*>(p);
-    const __half2* h = reinterpret_cast<const __half2*>(&v);
+// 8 consecutive rows of one column (one 16 B / 32 B chunk of the interleaved layout)
+template <typename T> struct Chunk;
+template <> struct Chunk<__half> {
+  // a/b: the chunks of column 0 / column 1 -> x[q] = (col0 row q, col1 row q)
+  __device__ static __forceinline__ void load2(const __half* a, const __half* b, float2* x) {
+    const uint4 va = *reinterpret_cast<const uint4*>(a);
+    const uint4 vb = *reinterpret_cast<const uint4*>(b);
+    const __half* ha = reinterpret_cast<const __half*>(&va);
+    const __half* hb = reinterpret_cast<const __half*>(&vb);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) x[i] = __half22float2(h[i]);
+    for (int q = 0; q < 8; ++q) x[q] = make_float2(__half2float(ha[q]), __half2float(hb[q]));
   }
-  // round x to fp16 in place (RNE) and write back
-  __device__ static __forceinline__ void round_store(__half* p, float2* x) {
-    uint4 v;
-    __half2* h = reinterpret_cast<__half2*>(&v);
+  // round to fp16 (RNE), write back, and replace x by the rounded values
+  __device__ static __forceinline__ void round_store2(__half* a, __half* b, float2* x) {
+    uint4 va, vb;
+    __half2* ha = reinterpret_cast<__half2*>(&va);
+    __half2* hb = reinterpret_cast<__half2*>(&vb);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      h[i] = __float22half2_rn(x[i]);
-      x[i] = __half22float2(h[i]);
+    for (int q = 0; q < 4; ++q) {
+      ha[q] = __floats2half2_rn(x[2 * q].x, x[2 * q + 1].x);
+      hb[q] = __floats2half2_rn(x[2 * q].y, x[2 * q + 1].y);
+      const float2 a2 = __half22float2(ha[q]);
+      const float2 b2 = __half22float2(hb[q]);
+      x[2 * q] = make_float2(a2.x, b2.x);
+      x[2 * q + 1] = make_float2(a2.y, b2.y);
     }
-    *reinterpret_cast<uint4*>(p) = v;
+    *reinterpret_cast<uint4*>(a) = va;
+    *reinterpret_cast<uint4*>(b) = vb;
   }
   __device__ static __forceinline__ float get(const __half* p, int i) { return __half2float(p[i]); }
   __device__ static __forceinline__ float rnd(float a) { return __half2float(__float2half_rn(a)); }
 };
-template <> struct V8<float> {
-  static constexpr int BYTES = 32;
-  __device__ static __forceinline__ void load(const float* p, float2* x) {
-    const float4 a = reinterpret_cast<const float4*>(p)[0];
-    const float4 b = reinterpret_cast<const float4*>(p)[1];
-    x[0] = make_float2(a.x, a.y); x[1] = make_float2(a.z, a.w);
-    x[2] = make_float2(b.x, b.y); x[3] = make_float2(b.z, b.w);
+template <> struct Chunk<float> {
+  __device__ static __forceinline__ void load2(const float* a, const float* b, float2* x) {
+    const float4 a0 = reinterpret_cast<const float4*>(a)[0], a1 = reinterpret_cast<const float4*>(a)[1];
+    const float4 b0 = reinterpret_cast<const float4*>(b)[0], b1 = reinterpret_cast<const float4*>(b)[1];
+    x[0] = make_float2(a0.x, b0.x); x[1] = make_float2(a0.y, b0.y);
+    x[2] = make_float2(a0.z, b0.z); x[3] = make_float2(a0.w, b0.w);
+    x[4] = make_float2(a1.x, b1.x); x[5] = make_float2(a1.y, b1.y);
+    x[6] = make_float2(a1.z, b1.z); x[7] = make_float2(a1.w, b1.w);
   }
-  __device__ static __forceinline__ void round_store(float* p, float2* x) {
-    reinterpret_cast<float4*>(p)[0] = make_float4(x[0].x, x[0].y, x[1].x, x[1].y);
-    reinterpret_cast<float4*>(p)[1] = make_float4(x[2].x, x[2].y, x[3].x, x[3].y);
+  __device__ static __forceinline__ void round_store2(float* a, float* b, float2* x) {
+    reinterpret_cast<float4*>(a)[0] = make_float4(x[0].x, x[1].x, x[2].x, x[3].x);
+    reinterpret_cast<float4*>(a)[1] = make_float4(x[4].x, x[5].x, x[6].x, x[7].x);
+    reinterpret_cast<float4*>(b)[0] = make_float4(x[0].y, x[1].y, x[2].y, x[3].y);
+    reinterpret_cast<float4*>(b)[1] = make_float4(x[4].y, x[5].y, x[6].y, x[7].y);
   }
   __device__ static __forceinline__ float get(const float* p, int i) { return p[i]; }
   __device__ static __forceinline__ float rnd(float a) { return a; }
@@ -115,8 +131,9 @@ template <> struct V8<float> {
 struct SlotGeom {
   int data;   // GS * ncols * 8 * sizeof(T)
   int ucol;   // GS * 8 * sizeof(T)
-  int upend;  // PMAX * GS * 8 * 4
-  int uv;     // (1 + PMAX) * GS * 8 * 4
+  int upend;  // PMAX * GS * 8 * 4   (raw pending u rows, TMA)
+  int us;     // GS * 8 * 4          (u of this step)
+  int nv;     // PMAX * GS * 8 * 4   (-v rows)
   int total;
 };
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
@@ -125,27 +142,32 @@ __host__ __device__ inline SlotGeom slot_geom(int GS, int ncols, int esz, int pm
   g.data = 0;
   g.ucol = al16(GS * ncols * 8 * esz);
   g.upend = g.ucol + al16(GS * 8 * esz);
-  g.uv = g.upend + al16(pmax * GS * 8 * 4);
-  g.total = g.uv + al16((1 + pmax) * GS * 8 * 4);
+  g.us = g.upend + al16(pmax * GS * 8 * 4);
+  g.nv = g.us + al16(GS * 8 * 4);
+  g.total = g.nv + al16(pmax * GS * 8 * 4);
   return g;
 }
 
-constexpr int NCW = 8;  // consumer warps
+constexpr int NCW = 16;                      // consumer warps
+constexpr int PASS_BLOCK = 32 * (NCW + 2);   // + producer + prep
+constexpr int COLS_PER_WARP = 64;            // lane owns columns lane, lane + 32
+constexpr int RED_BYTES = 1024 * 2 * 8;      // cross-warp partials (WR * CW * 64 <= 1024 columns)
 
-template <typename T, int PMAX, int CPW>
-__global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassParams p) {
+template <typename T, int PMAX>
+__global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
   if (p.sc->done) return;
   extern __shared__ __align__(128) unsigned char smem[];
   const int n = p.n, j = p.j, npend = p.npend;
   const int GS = p.gs, NST = p.nst;
   T* __restrict__ S = reinterpret_cast<T*>(p.S);
-  // column range of this CTA
-  const int c_lo = j + 32 * p.chunks_per_split * blockIdx.y;
+  const int c_lo = j + 32 * p.chunks_per_split * blockIdx.y;   // CTA column range
   const int c_hi = min(n, c_lo + 32 * p.chunks_per_split);
-  const int ncols = c_hi - c_lo;                      // > 0 by construction (host)
+  const int ncols = c_hi - c_lo;                                  // > 0 (host)
   const SlotGeom geo = slot_geom(GS, p.ncols_slot, (int)sizeof(T), PMAX);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NST * geo.total);
-  uint64_t* empty = full + NST;
+  double* red = reinterpret_cast<double*>(smem + (size_t)NST * geo.total);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NST * geo.total + RED_BYTES);
+  uint64_t* prep = full + NST;
+  uint64_t* empty = prep + NST;
   // row groups of this CTA: active groups [g_lo, ngroups) split evenly over gridDim.x
   const int64_t g_lo = p.g_lo;
   const int64_t nact = p.ngroups - g_lo;
@@ -159,19 +181,19 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassParams p) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
+      mbar_init(&prep[s], 32);
       mbar_init(&empty[s], NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  int slot_l[PMAX];
-#pragma unroll
-  for (int l = 0; l < PMAX; ++l) slot_l[l] = (p.j0 + l) % NSLOT;
-
   if (warp == 0) {
     // ======================= TMA producer (one lane) =======================
     if (lane != 0) return;
+    int slot_l[PMAX];
+#pragma unroll
+    for (int l = 0; l < PMAX; ++l) slot_l[l] = (p.j0 + l) % NSLOT;
     auto issue_store = [&](int i) {
       const int slot = i % NST;
       const int64_t g0 = gb + (int64_t)i * GS;
@@ -222,197 +244,227 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1) k_pass_tma(PassParams p) {
     return;
   }
 
-  // ========================== consumers (8 warps) ==========================
-  const int cw = warp - 1;
-  const int ct = threadIdx.x - 32;                   // 0..255
-  const int slot_j = j % NSLOT;
-  float fj[PMAX];
-  double cl_[PMAX];
+  if (warp == 1) {
+    // ========================= prep warp ==========================
+    float fj[PMAX];
+    double cl_[PMAX];
+    int64_t tstep[PMAX];
+#pragma unroll
+    for (int l = 0; l < PMAX; ++l) {
+      const int sl = (p.j0 + l) % NSLOT;
+      fj[l] = (l < npend) ? p.F[(int64_t)sl * n + j] : 0.f;
+      cl_[l] = (l < npend) ? p.cvec[p.j0 + l] : 0.0;
+      tstep[l] = p.j0 + l;
+    }
+    float* __restrict__ Uj = p.U + (int64_t)(j % NSLOT) * p.m_pad;
+    for (int i = 0; i < nst; ++i) {
+      const int slot = i % NST;
+      const int64_t g0 = gb + (int64_t)i * GS;
+      const int gsz = (int)((ge - g0) < GS ? (ge - g0) : GS);
+      unsigned char* base = smem + (size_t)slot * geo.total;
+      const T* ucol = reinterpret_cast<const T*>(base + geo.ucol);
+      const float* upend = reinterpret_cast<const float*>(base + geo.upend);
+      float* us = reinterpret_cast<float*>(base + geo.us);
+      float* nv = reinterpret_cast<float*>(base + geo.nv);
+      mbar_wait(&full[slot], (i / NST) & 1);
+      for (int r = lane; r < gsz * 8; r += 32) {
+        const int64_t rl = g0 * 8 + r;
+        const int64_t rg = p.row_offset + rl;
+        const bool real = rl < p.m_local;
+        float a = Chunk<T>::get(ucol + (r >> 3) * 8, r & 7);
+#pragma unroll
+        for (int l = 0; l < PMAX; ++l) {
+          if (l < npend) {
+            float v;
+            if (!real || rg < tstep[l]) v = 0.f;
+            else if (rg == tstep[l]) v = 1.f;
+            else v = __double2float_rn((double)upend[l * GS * 8 + r] * cl_[l]);
+            nv[l * GS * 8 + r] = -v;
+            a = fmaf(-v, fj[l], a);
+          }
+        }
+        if (p.store) a = Chunk<T>::rnd(a);
+        const float u = (real && rg >= j) ? a : 0.f;
+        us[r] = u;
+        if (blockIdx.y == 0) Uj[rl] = u;
+      }
+      mbar_arrive(&prep[slot]);   // every lane arrives (count 32): its smem writes are released
+    }
+    return;
+  }
+
+  // ========================== consumers (16 warps) ==========================
+  const int cwarp = warp - 2;
+  const int CW = p.cw, WR = p.wr;
+  const int cw = cwarp % CW, rw = cwarp / CW;
+  const bool active = rw < WR;
+  const int col0 = cw * COLS_PER_WARP + lane;          // CTA-relative columns of this lane
+  const int col1 = col0 + 32;
+  const bool v0 = active && col0 < ncols, v1 = active && col1 < ncols;
+  const int slot0 = p.j0 % NSLOT;
+  float2 f2[PMAX];
 #pragma unroll
   for (int l = 0; l < PMAX; ++l) {
-    fj[l] = (l < npend) ? p.F[(int64_t)slot_l[l] * n + j] : 0.f;
-    cl_[l] = (l < npend) ? p.cvec[p.j0 + l] : 0.0;
+    const int sl = (slot0 + l) % NSLOT;
+    f2[l] = make_float2((l < npend && v0) ? p.F[(int64_t)sl * n + c_lo + col0] : 0.f,
+                        (l < npend && v1) ? p.F[(int64_t)sl * n + c_lo + col1] : 0.f);
   }
-  // this lane's columns: chunk q = cw + NCW * t
-  float fr[CPW][PMAX];
-  bool valid[CPW];
-  int col[CPW];
-#pragma unroll
-  for (int t = 0; t < CPW; ++t) {
-    col[t] = c_lo + 32 * (cw + NCW * t) + lane;
-    valid[t] = col[t] < c_hi;
-#pragma unroll
-    for (int l = 0; l < PMAX; ++l)
-      fr[t][l] = (valid[t] && l < npend) ? p.F[(int64_t)slot_l[l] * n + col[t]] : 0.f;
-  }
-  double accw[CPW], accs[CPW];
-#pragma unroll
-  for (int t = 0; t < CPW; ++t) accw[t] = accs[t] = 0.0;
+  double aw0 = 0.0, aw1 = 0.0, as0 = 0.0, as1 = 0.0;
   const int64_t jloc = (int64_t)j - p.row_offset;
-  const bool own_j = jloc >= 0 && jloc < p.m_local;
-  const int64_t gj = own_j ? (jloc >> 3) : -1;
+  const int64_t gj = (jloc >= 0 && jloc < p.m_local) ? (jloc >> 3) : -1;
+  const int jr = (int)(jloc & 7);
+  // clamp the column offsets of invalid lanes into the row (their results are discarded)
+  const int o0 = (v0 ? col0 : 0) * 8, o1 = (v1 ? col1 : 0) * 8;
 
   for (int i = 0; i < nst; ++i) {
     const int slot = i % NST;
     const int64_t g0 = gb + (int64_t)i * GS;
     const int gsz = (int)((ge - g0) < GS ? (ge - g0) : GS);
     unsigned char* base = smem + (size_t)slot * geo.total;
-    const T* data = reinterpret_cast<const T*>(base);
-    const T* ucol = reinterpret_cast<const T*>(base + geo.ucol);
-    const float* upend = reinterpret_cast<const float*>(base + geo.upend);
-    float* us = reinterpret_cast<float*>(base + geo.uv);
-    float* nv = us + GS * 8;                           // -v rows, [PMAX][GS*8]
-    mbar_wait(&full[slot], (i / NST) & 1);
-    // ---- prep: pending -v rows and u for the stage's rows -------------------
-    for (int r = ct; r < gsz * 8; r += 256) {
-      const int64_t rl = g0 * 8 + r;
-      const int64_t rg = p.row_offset + rl;
-      const bool real = rl < p.m_local;
-      float a = V8<T>::get(ucol + (r >> 3) * 8, r & 7);
-#pragma unroll
-      for (int l = 0; l < PMAX; ++l) {
-        if (l < npend) {
-          const int64_t tstep = p.j0 + l;
-          float v;
-          if (!real || rg < tstep) v = 0.f;
-          else if (rg == tstep) v = 1.f;
-          else v = __double2float_rn((double)upend[l * GS * 8 + r] * cl_[l]);
-          nv[l * GS * 8 + r] = -v;
-          a = fmaf(-v, fj[l], a);
-        }
-      }
-      if (p.store) a = V8<T>::rnd(a);
-      const float u = (real && rg >= j) ? a : 0.f;
-      us[r] = u;
-      if (blockIdx.y == 0) p.U[(int64_t)slot_j * p.m_pad + rl] = u;
-    }
-    consumer_bar();
-    // ---- main: form, (round+write back), reduce ------------------------------
-    for (int r = 0; r < gsz; ++r) {
-      const int64_t g = g0 + r;
-      float2 vv[PMAX][4];
-#pragma unroll
-      for (int l = 0; l < PMAX; ++l) {
-        if (l < npend) {
-          const float4 a = *reinterpret_cast<const float4*>(nv + l * GS * 8 + r * 8);
-          const float4 b = *reinterpret_cast<const float4*>(nv + l * GS * 8 + r * 8 + 4);
-          vv[l][0] = make_float2(a.x, a.y); vv[l][1] = make_float2(a.z, a.w);
-          vv[l][2] = make_float2(b.x, b.y); vv[l][3] = make_float2(b.z, b.w);
-        }
-      }
-      const float4 ua = *reinterpret_cast<const float4*>(us + r * 8);
-      const float4 ub = *reinterpret_cast<const float4*>(us + r * 8 + 4);
-      const float uu[8] = {ua.x, ua.y, ua.z, ua.w, ub.x, ub.y, ub.z, ub.w};
-      const bool gjrow = (g == gj);
-#pragma unroll
-      for (int t = 0; t < CPW; ++t) {
-        if (!valid[t]) continue;
-        T* xp = const_cast<T*>(data) + ((size_t)r * ncols + (col[t] - c_lo)) * 8;
-        float2 x[4];
-        V8<T>::load(xp, x);
+    T* data = reinterpret_cast<T*>(base);
+    const float* us = reinterpret_cast<const float*>(base + geo.us);
+    const float* nv = reinterpret_cast<const float*>(base + geo.nv);
+    mbar_wait(&prep[slot], (i / NST) & 1);
+    if (active && (v0 || v1)) {
+      for (int gl = rw; gl < gsz; gl += WR) {
+        T* d0 = data + (size_t)gl * ncols * 8 + o0;
+        T* d1 = data + (size_t)gl * ncols * 8 + o1;
+        float2 x[8];
+        Chunk<T>::load2(d0, d1, x);
 #pragma unroll
         for (int l = 0; l < PMAX; ++l) {
           if (l < npend) {
-            const float2 ff = make_float2(fr[t][l], fr[t][l]);
+            const float4 va = *reinterpret_cast<const float4*>(nv + l * GS * 8 + gl * 8);
+            const float4 vb = *reinterpret_cast<const float4*>(nv + l * GS * 8 + gl * 8 + 4);
+            const float vv[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) x[q] = __ffma2_rn(vv[l][q], ff, x[q]);
+            for (int q = 0; q < 8; ++q) x[q] = __ffma2_rn(make_float2(vv[q], vv[q]), f2[l], x[q]);
           }
         }
-        if (p.store) V8<T>::round_store(xp, x);
-        float xs[8] = {x[0].x, x[0].y, x[1].x, x[1].y, x[2].x, x[2].y, x[3].x, x[3].y};
-        if (gjrow) {
-          const int jr = (int)(jloc - g * 8);
+        if (p.store) Chunk<T>::round_store2(d0, d1, x);
+        const float4 ua = *reinterpret_cast<const float4*>(us + gl * 8);
+        const float4 ub = *reinterpret_cast<const float4*>(us + gl * 8 + 4);
+        const float uu[8] = {ua.x, ua.y, ua.z, ua.w, ub.x, ub.y, ub.z, ub.w};
+        if (g0 + gl == gj) {                              // the group holding row j (rare)
+          float2 xj = x[0];
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (q < jr) xs[q] = 0.f;
-          p.xr[col[t]] = xs[jr];
+          for (int q = 0; q < 8; ++q) {
+            if (q == jr) xj = x[q];
+            if (q < jr) x[q] = make_float2(0.f, 0.f);
+          }
+          if (v0) p.xr[c_lo + col0] = xj.x;
+          if (v1) p.xr[c_lo + col1] = xj.y;
         }
-        float2 acc = __fmul2_rn(make_float2(xs[0], xs[0]), make_float2(uu[0], xs[0]));
+        float2 pw = __fmul2_rn(x[0], make_float2(uu[0], uu[0]));
+        float2 ps = __fmul2_rn(x[0], x[0]);
 #pragma unroll
-        for (int q = 1; q < 8; ++q) acc = __ffma2_rn(make_float2(xs[q], xs[q]), make_float2(uu[q], xs[q]), acc);
-        accw[t] += (double)acc.x;
-        accs[t] += (double)acc.y;
+        for (int q = 1; q < 8; ++q) {
+          pw = __ffma2_rn(x[q], make_float2(uu[q], uu[q]), pw);
+          ps = __ffma2_rn(x[q], x[q], ps);
+        }
+        aw0 += (double)pw.x;
+        aw1 += (double)pw.y;
+        as0 += (double)ps.x;
+        as1 += (double)ps.y;
       }
     }
     if (p.store) fence_async_smem();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
   }
-#pragma unroll
-  for (int t = 0; t < CPW; ++t) {
-    if (valid[t]) {
-      p.part[((int64_t)blockIdx.x * 2 + 0) * n + col[t]] = accw[t];
-      p.part[((int64_t)blockIdx.x * 2 + 1) * n + col[t]] = accs[t];
+  // cross-warp (row-split) combine in fixed order rw = 0..WR-1, then one write per column
+  if (WR > 1) {
+    if (active) {
+      const int base_c = (rw * CW + cw) * COLS_PER_WARP;   // < WR*CW*64 <= 1024
+      red[(base_c + lane) * 2 + 0] = aw0;
+      red[(base_c + lane) * 2 + 1] = as0;
+      red[(base_c + lane + 32) * 2 + 0] = aw1;
+      red[(base_c + lane + 32) * 2 + 1] = as1;
     }
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * NCW) : "memory");
+    if (active && rw == 0) {
+      aw0 = as0 = aw1 = as1 = 0.0;
+      for (int r = 0; r < WR; ++r) {
+        const int base_c = (r * CW + cw) * COLS_PER_WARP;
+        aw0 += red[(base_c + lane) * 2 + 0];
+        as0 += red[(base_c + lane) * 2 + 1];
+        aw1 += red[(base_c + lane + 32) * 2 + 0];
+        as1 += red[(base_c + lane + 32) * 2 + 1];
+      }
+    }
+  }
+  if (active && rw == 0) {
+    double* pw = p.part + ((int64_t)blockIdx.x * 2 + 0) * n + c_lo;
+    double* ps = p.part + ((int64_t)blockIdx.x * 2 + 1) * n + c_lo;
+    if (v0) { pw[col0] = aw0; ps[col0] = as0; }
+    if (v1) { pw[col1] = aw1; ps[col1] = as1; }
   }
 }
 
 // ---------------------------------------------------------------------------
-template <typename T, int PMAX, int CPW>
-static cudaError_t launch_tma_t(const PassParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+template <typename T, int PMAX>
+static cudaError_t launch_ws_t(const PassParams& p, dim3 grid, size_t smem, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_pass_tma<T, PMAX, CPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         PASS_SMEM_MAX);
+    cudaError_t e = cudaFuncSetAttribute(k_pass_ws<T, PMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         PASS_SMEM_MAX);
+    if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_pass_tma<T, PMAX, CPW><<<grid, 32 * (NCW + 1), smem, st>>>(p);
+  k_pass_ws<T, PMAX><<<grid, PASS_BLOCK, smem, st>>>(p);
   return cudaGetLastError();
 }
 
-template <typename T, int PMAX>
-static cudaError_t launch_tma_p(const PassParams& p, dim3 grid, size_t smem, int cpw, cudaStream_t st) {
-  if (cpw <= 1) return launch_tma_t<T, PMAX, 1>(p, grid, smem, st);
-  if (cpw <= 2) return launch_tma_t<T, PMAX, 2>(p, grid, smem, st);
-  if (cpw <= 4) return launch_tma_t<T, PMAX, 4>(p, grid, smem, st);
-  return launch_tma_t<T, PMAX, 8>(p, grid, smem, st);
-}
-
 template <typename T>
-static cudaError_t launch_tma_fmt(PassParams p, int num_sms, int* gx_out, cudaStream_t st) {
+static cudaError_t launch_ws_fmt(PassParams p, int max_ctas, int* gx_out, cudaStream_t st) {
   const int n = p.n, j = p.j;
   const int esz = (int)sizeof(T);
   const int nchunks = (n - j + 31) / 32;
-  // column splits: at most NCW * 8 chunks (2048 columns) per CTA
-  const int gy = (nchunks + NCW * 8 - 1) / (NCW * 8);
+  // column splits: at most NCW * 64 = 1024 columns per CTA
+  const int max_chunks = NCW * COLS_PER_WARP / 32;
+  const int gy = (nchunks + max_chunks - 1) / max_chunks;
   const int cps = (nchunks + gy - 1) / gy;
   p.chunks_per_split = cps;
   const int ncols = std::min(n - j, 32 * cps);
   p.ncols_slot = ncols;
-  const int cpw = (cps + NCW - 1) / NCW;
+  const int CW = (ncols + COLS_PER_WARP - 1) / COLS_PER_WARP;   // column-warps (<= 16)
+  const int WR = NCW / CW;                                       // row-split warps
+  p.cw = CW;
+  p.wr = WR;
   const int pmax = p.npend <= 1 ? 1 : p.npend <= 2 ? 2 : p.npend <= 4 ? 4 : p.npend <= 8 ? 8 : 16;
   if (p.npend > pmax || pmax > NB_MAX) return cudaErrorInvalidValue;
-  // stage = GS row groups: aim at ~24 KB of matrix data, at most 32 groups (256 rows)
+  // stage = GS row groups: ~32 KB of matrix data, a multiple of WR, at most 64 groups
   const int rowbytes = ncols * 8 * esz;
-  int GS = std::max(1, std::min(32, (24 * 1024) / rowbytes));
+  int gpw = std::max(1, (32 * 1024) / (rowbytes * WR));
+  int GS = std::min(64, WR * gpw);
   SlotGeom g = slot_geom(GS, ncols, esz, pmax);
-  while (GS > 1 && 3 * (size_t)g.total + 64 > (size_t)PASS_SMEM_MAX) {
+  const size_t fixed = RED_BYTES + 3 * 8 * 8 + 64;
+  while (GS > 1 && 2 * (size_t)g.total + fixed > (size_t)PASS_SMEM_MAX) {
     GS = std::max(1, GS / 2);
     g = slot_geom(GS, ncols, esz, pmax);
   }
-  int nst = (int)std::min<size_t>(8, (PASS_SMEM_MAX - 256) / (size_t)g.total);
+  int nst = (int)std::min<size_t>(8, (PASS_SMEM_MAX - fixed) / (size_t)g.total);
   if (nst < 2) return cudaErrorInvalidConfiguration;
   p.gs = GS;
   p.nst = nst;
-  const size_t smem = (size_t)nst * g.total + 2 * nst * sizeof(uint64_t);
+  const size_t smem = (size_t)nst * g.total + RED_BYTES + 3 * nst * sizeof(uint64_t);
   const int64_t nact = p.ngroups - p.g_lo;
-  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms / std::max(1, gy) > 0 ? num_sms / gy : 1,
-                                                              (nact + GS - 1) / GS));
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, max_ctas / gy), (nact + GS - 1) / GS));
   dim3 grid(gx, gy);
   p.gx_used = gx;
   *gx_out = gx;
   switch (pmax) {
-    case 1: return launch_tma_p<T, 1>(p, grid, smem, cpw, st);
-    case 2: return launch_tma_p<T, 2>(p, grid, smem, cpw, st);
-    case 4: return launch_tma_p<T, 4>(p, grid, smem, cpw, st);
-    case 8: return launch_tma_p<T, 8>(p, grid, smem, cpw, st);
-    default: return launch_tma_p<T, 16>(p, grid, smem, cpw, st);
+    case 1: return launch_ws_t<T, 1>(p, grid, smem, st);
+    case 2: return launch_ws_t<T, 2>(p, grid, smem, st);
+    case 4: return launch_ws_t<T, 4>(p, grid, smem, st);
+    case 8: return launch_ws_t<T, 8>(p, grid, smem, st);
+    default: return launch_ws_t<T, 16>(p, grid, smem, st);
   }
 }
 
-cudaError_t launch_pass_tma(int fmt, PassParams p, int num_sms, int* gx_out, cudaStream_t st) {
-  return fmt == 1 ? launch_tma_fmt<__half>(p, num_sms, gx_out, st)
-                  : launch_tma_fmt<float>(p, num_sms, gx_out, st);
+cudaError_t launch_pass_tma(int fmt, PassParams p, int max_ctas, int* gx_out, cudaStream_t st) {
+  return fmt == 1 ? launch_ws_fmt<__half>(p, max_ctas, gx_out, st)
+                  : launch_ws_fmt<float>(p, max_ctas, gx_out, st);
 }
 
 }  // namespace mpid

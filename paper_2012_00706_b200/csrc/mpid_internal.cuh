@@ -56,6 +56,7 @@ struct PassParams {
   int gs;                  // row groups per pipeline stage (set by the launcher)
   int nst;                 // pipeline depth (set by the launcher)
   int gx_used;             // gridDim.x (set by the launcher)
+  int cw, wr;              // consumer warps: column-warps x row-split warps (launcher)
   float* U;                // [NSLOT][m_pad] raw u vectors
   const float* F;          // [NSLOT][n]   f vectors (current column order)
   const double* cvec;      // [k_max] c_t = 1/(u_t - beta_t) per step
