@@ -27,13 +27,21 @@ __global__ void k_gather_cols(const double* __restrict__ A, int64_t m, int64_t l
 }
 
 // ---------------------------------------------------------------------------
-// 64x64-tiled fp64 GEMM core, 256 threads, 4x4 outputs per thread, K tile 16,
-// double-buffered shared memory.  Thread layout inside a warp is 4 (M) x 8 (N)
-// so the shared-memory operand reads are broadcast-friendly.
+// fp64 tensor-core GEMM core (DMMA: mma.sync.aligned.m8n8k4.row.col.f64).
+// CTA tile 128 x 128, 8 warps as 2 (M) x 4 (N), warp tile 64 x 32 = 8 x 4 MMA
+// tiles, K staged 16 at a time through double-buffered shared memory
+// (register-staged 16 B global loads, coalesced along the contiguous dimension).
+//   GM_TN_PARTIAL: out[split][c][i] = sum_{r in split} X(r, i) Y(r, c)   (X m x M, Y m x N)
+//   GM_NN_ERROR:   out[block]       = sum (A(r, c) - sum_l X(r, l) B(l, c))^2
+//   GM_NN_UPDATE:  out(r, c)       -= sum_l X(r, l) B(l, c)               (TRSM update)
+// Fragments of m8n8k4 f64 (PTX ISA): A(g, t), B(t, g), C(g, 2t + {0,1}) with
+// g = lane >> 2, t = lane & 3.
 // ---------------------------------------------------------------------------
-constexpr int GT = 64, GK = 16;
+constexpr int GT = 128, GK = 16;
+constexpr int LDK = GK + 4;      // [mn][k] tiles: row stride 160 B -> conflict-free fragment reads
+constexpr int LDM = GT + 8;      // [k][mn] tile (NN A operand): 136 doubles -> conflict-free
 
-enum GemmMode { GM_TN_PARTIAL = 0, GM_NN_ERROR = 1, GM_NN_UPDATE = 2 };
+enum GemmMode { GM_TN_PARTIAL = 0, GM_NN_ERROR = 1, GM_NN_UPDATE = 2, GM_NN_STORE = 3 };
 
 struct GemmArgs {
   // TN: C(i, c) = sum_r X(r, i) Y(r, c), rows r in the split's range; X m x M, Y m x N
@@ -44,59 +52,122 @@ struct GemmArgs {
   int64_t ldy;
   int64_t M, N, K;   // TN: M = k1, N = n1, K = m (rows) ; NN: M = m, N = ncols, K = k
   int64_t k_per_split;
-  double* out;       // TN: partials [split][M][N] ; NN_ERROR: partial sums per block ; NN_UPDATE: C
+  double* out;       // TN: partials [split][N][M] ; NN_ERROR: partial sums per block ; NN_UPDATE: C
   int64_t ldo;
-  const double* A;   // NN_ERROR: A_D (m x N), lda
+  const double* A;   // NN_ERROR: A_D (m x n_all), lda; column c of the product is A's column cmap[c]
   int64_t lda;
+  const int* cmap;
+  int d_tma;         // NN_ERROR: 1 = the A_D tile may be prefetched with bulk copies (16 B aligned rows)
 };
+constexpr int DLD = GT + 4;      // NN_ERROR: smem A_D tile [c][r], 132 doubles per column
+
+__device__ __forceinline__ void dmma(double* c, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
 
 template <int MODE>
-__global__ void __launch_bounds__(256) k_gemm64(GemmArgs g) {
-  __shared__ __align__(16) double As[2][GK][GT];
-  __shared__ __align__(16) double Bs[2][GK][GT];
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int ti = (warp >> 1) * 4 + (lane >> 3);     // 0..15 (M)
-  const int tj = (warp & 1) * 8 + (lane & 7);       // 0..15 (N)
-  const int64_t m0 = (int64_t)blockIdx.x * GT;      // M tile
-  const int64_t n0 = (int64_t)blockIdx.y * GT;      // N tile
+__global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
+  // A tile: TN -> As[i][k] (LDK), NN -> As[k][r] (LDM); B tile: Bs[c][k] (LDK)
+  constexpr int A_ELEMS = (MODE == GM_TN_PARTIAL) ? GT * LDK : GK * LDM;
+  extern __shared__ __align__(16) double dsm[];
+  double (*As)[A_ELEMS] = reinterpret_cast<double (*)[A_ELEMS]>(dsm);
+  double (*Bs)[GT * LDK] = reinterpret_cast<double (*)[GT * LDK]>(dsm + 2 * A_ELEMS);
+  double* Ds = dsm + 2 * A_ELEMS + 2 * GT * LDK;                  // NN_ERROR: A_D tile [c][r]
+  __shared__ __align__(8) uint64_t dbar;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;           // 2 x 4 warps
+  const int64_t m0 = (int64_t)blockIdx.x * GT;
+  const int64_t n0 = (int64_t)blockIdx.y * GT;
   int64_t k_begin = 0, k_end = g.K;
   if (MODE == GM_TN_PARTIAL) {
     k_begin = (int64_t)blockIdx.z * g.k_per_split;
     k_end = min(g.K, k_begin + g.k_per_split);
   }
-  // loader mapping: column/row index along the 64-wide dim, 4 consecutive k
-  const int ld_mn = tid & 63;
-  const int ld_k = (tid >> 6) * 4;
-
-  double ra[4], rb[4];
+  const int64_t rows_here = (g.M - m0 < GT) ? g.M - m0 : (int64_t)GT;
+  const int64_t cols_here = (g.N - n0 < GT) ? g.N - n0 : (int64_t)GT;
+  const bool dpre = (MODE == GM_NN_ERROR) && g.d_tma && (rows_here % 2 == 0);
+  if (MODE == GM_NN_ERROR && dpre) {
+    // prefetch the A_D tile (the error epilogue's operand) with bulk copies, one per
+    // column, overlapping the HBM read with the DMMA main loop
+    if (tid == 0) {
+      mbar_init(&dbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&dbar, (uint32_t)(rows_here * cols_here * 8));
+      for (int c = 0; c < cols_here; ++c)
+        tma_load(Ds + c * DLD, g.A + (int64_t)g.cmap[n0 + c] * g.lda + m0, (uint32_t)(rows_here * 8), &dbar);
+    }
+  }
+  double2 ra[4], rb[4];
+  // loads: 128 (mn) x 16 (k) doubles per operand = 1024 double2, 4 per thread
   auto gload = [&](int64_t kb) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int64_t kk = kb + ld_k + q;
+      const int idx = tid + q * 256;                  // 0..1023
       if (MODE == GM_TN_PARTIAL) {
-        const int64_t i = m0 + ld_mn, c = n0 + ld_mn;
-        ra[q] = (kk < k_end && i < g.M) ? g.X[i * g.ldx + kk] : 0.0;
-        rb[q] = (kk < k_end && c < g.N) ? g.Y[c * g.ldy + kk] : 0.0;
+        const int mn = idx >> 3, kk = (idx & 7) * 2;  // 8 double2 per 16-long k segment
+        const int64_t r = kb + kk;
+        const int64_t i = m0 + mn, c = n0 + mn;
+        ra[q] = make_double2(0.0, 0.0);
+        rb[q] = make_double2(0.0, 0.0);
+        if (i < g.M) {
+          const double* p = g.X + i * g.ldx + r;
+          if (r + 1 < k_end && (((uintptr_t)p & 15) == 0)) ra[q] = *reinterpret_cast<const double2*>(p);
+          else { if (r < k_end) ra[q].x = p[0]; if (r + 1 < k_end) ra[q].y = p[1]; }
+        }
+        if (c < g.N) {
+          const double* p = g.Y + c * g.ldy + r;
+          if (r + 1 < k_end && (((uintptr_t)p & 15) == 0)) rb[q] = *reinterpret_cast<const double2*>(p);
+          else { if (r < k_end) rb[q].x = p[0]; if (r + 1 < k_end) rb[q].y = p[1]; }
+        }
       } else {
-        const int64_t r = m0 + ld_mn, c = n0 + ld_mn;
-        ra[q] = (kk < k_end && r < g.M) ? g.X[kk * g.ldx + r] : 0.0;
-        rb[q] = (kk < k_end && c < g.N) ? g.Y[c * g.ldy + kk] : 0.0;
+        // A = X (m x K col-major): element (r, l) at X[r + l ldx]; tile [l][r]
+        {
+          const int l = idx >> 6, rr = (idx & 63) * 2;  // 64 double2 per 128-long column
+          const int64_t kk = kb + l, r = m0 + rr;
+          ra[q] = make_double2(0.0, 0.0);
+          if (kk < k_end) {
+            const double* p = g.X + kk * g.ldx + r;
+            if (r + 1 < g.M && (((uintptr_t)p & 15) == 0)) ra[q] = *reinterpret_cast<const double2*>(p);
+            else { if (r < g.M) ra[q].x = p[0]; if (r + 1 < g.M) ra[q].y = p[1]; }
+          }
+        }
+        // B (K x N col-major): element (l, c) at Y[l + c ldy]; tile [c][l]
+        {
+          const int cc = idx >> 3, l = (idx & 7) * 2;
+          const int64_t c = n0 + cc, kk = kb + l;
+          rb[q] = make_double2(0.0, 0.0);
+          if (c < g.N) {
+            const double* p = g.Y + c * g.ldy + kk;
+            if (kk < k_end) rb[q].x = p[0];
+            if (kk + 1 < k_end) rb[q].y = p[1];
+          }
+        }
       }
     }
   };
   auto sstore = [&](int buf) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      As[buf][ld_k + q][ld_mn] = ra[q];
-      Bs[buf][ld_k + q][ld_mn] = rb[q];
+      const int idx = tid + q * 256;
+      if (MODE == GM_TN_PARTIAL) {
+        const int mn = idx >> 3, kk = (idx & 7) * 2;
+        *reinterpret_cast<double2*>(&As[buf][mn * LDK + kk]) = ra[q];
+      } else {
+        const int l = idx >> 6, rr = (idx & 63) * 2;
+        *reinterpret_cast<double2*>(&As[buf][l * LDM + rr]) = ra[q];
+      }
+      const int cc = idx >> 3, l = (idx & 7) * 2;
+      *reinterpret_cast<double2*>(&Bs[buf][cc * LDK + l]) = rb[q];
     }
   };
-  double acc[4][4];
+  double acc[8][4][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
   if (k_begin < k_end) {
     gload(k_begin);
@@ -107,17 +178,19 @@ __global__ void __launch_bounds__(256) k_gemm64(GemmArgs g) {
       const bool more = kb + GK < k_end;
       if (more) gload(kb + GK);
 #pragma unroll
-      for (int kk = 0; kk < GK; ++kk) {
-        const double2 a01 = *reinterpret_cast<const double2*>(&As[buf][kk][ti * 4]);
-        const double2 a23 = *reinterpret_cast<const double2*>(&As[buf][kk][ti * 4 + 2]);
-        const double2 b01 = *reinterpret_cast<const double2*>(&Bs[buf][kk][tj * 4]);
-        const double2 b23 = *reinterpret_cast<const double2*>(&Bs[buf][kk][tj * 4 + 2]);
-        const double av[4] = {a01.x, a01.y, a23.x, a23.y};
-        const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+      for (int ks = 0; ks < GK / 4; ++ks) {
+        double af[8], bf[4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int mt = 0; mt < 8; ++mt) {
+          const int mm = wm * 64 + mt * 8 + gq, kk = ks * 4 + tq;
+          af[mt] = (MODE == GM_TN_PARTIAL) ? As[buf][mm * LDK + kk] : As[buf][kk * LDM + mm];
+        }
 #pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+        for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[buf][(wn * 32 + nt * 8 + gq) * LDK + ks * 4 + tq];
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
       }
       if (more) {
         sstore(buf ^ 1);
@@ -130,38 +203,58 @@ __global__ void __launch_bounds__(256) k_gemm64(GemmArgs g) {
   if (MODE == GM_TN_PARTIAL) {
     double* o = g.out + (int64_t)blockIdx.z * g.M * g.N;
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int64_t i = m0 + ti * 4 + a;
+    for (int mt = 0; mt < 8; ++mt) {
+      const int64_t i = m0 + wm * 64 + mt * 8 + gq;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int64_t c = n0 + tj * 4 + b;
-        if (i < g.M && c < g.N) o[c * g.M + i] = acc[a][b];
-      }
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
+          if (i < g.M && c < g.N) o[c * g.M + i] = acc[mt][nt][h];
+        }
+    }
+  } else if (MODE == GM_NN_STORE) {
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      const int64_t r = m0 + wm * 64 + mt * 8 + gq;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
+          if (r < g.M && c < g.N) g.out[c * g.ldo + r] = acc[mt][nt][h];
+        }
     }
   } else if (MODE == GM_NN_UPDATE) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int64_t r = m0 + ti * 4 + a;
+    for (int mt = 0; mt < 8; ++mt) {
+      const int64_t r = m0 + wm * 64 + mt * 8 + gq;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int64_t c = n0 + tj * 4 + b;
-        if (r < g.M && c < g.N) g.out[c * g.ldo + r] -= acc[a][b];
-      }
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
+          if (r < g.M && c < g.N) g.out[c * g.ldo + r] -= acc[mt][nt][h];
+        }
     }
   } else {  // GM_NN_ERROR: sum (A_D - A_I P)^2 over the tile
+    if (dpre) mbar_wait(&dbar, 0);
     double e2 = 0.0;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int64_t c = n0 + tj * 4 + b;
+    for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int64_t r = m0 + ti * 4 + a;
-        if (r < g.M && c < g.N) {
-          const double e = g.A[c * g.lda + r] - acc[a][b];
-          e2 = fma(e, e, e2);
+      for (int h = 0; h < 2; ++h) {
+        const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          const int64_t r = m0 + wm * 64 + mt * 8 + gq;
+          if (r < g.M && c < g.N) {
+            const double a = dpre ? Ds[(c - n0) * DLD + (r - m0)] : __ldcs(g.A + (int64_t)g.cmap[c] * g.lda + r);
+            const double e = a - acc[mt][nt][h];
+            e2 = fma(e, e, e2);
+          }
         }
       }
-    }
     __shared__ double red[8];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) e2 += __shfl_xor_sync(0xffffffffu, e2, o);
@@ -174,6 +267,25 @@ __global__ void __launch_bounds__(256) k_gemm64(GemmArgs g) {
       g.out[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
   }
+}
+
+template <int MODE>
+static size_t dgemm_smem() {
+  const int a = (MODE == GM_TN_PARTIAL) ? GT * LDK : GK * LDM;
+  const int d = (MODE == GM_NN_ERROR) ? GT * DLD : 0;
+  return (size_t)(2 * (a + GT * LDK) + d) * sizeof(double);
+}
+template <int MODE>
+static cudaError_t dgemm_launch(const GemmArgs& g, dim3 grid, cudaStream_t st) {
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(k_dgemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)dgemm_smem<MODE>());
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  k_dgemm<MODE><<<grid, 256, dgemm_smem<MODE>(), st>>>(g);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -361,8 +473,7 @@ cudaError_t launch_tsmm(const double* X, int64_t ldx, int k1, const double* Y, i
   g.k_per_split = ((m + splits - 1) / splits + GK - 1) / GK * GK;
   g.out = part;
   dim3 grid((unsigned)((k1 + GT - 1) / GT), (unsigned)((n1 + GT - 1) / GT), (unsigned)splits);
-  k_gemm64<GM_TN_PARTIAL><<<grid, 256, 0, st>>>(g);
-  return cudaGetLastError();
+  return dgemm_launch<GM_TN_PARTIAL>(g, grid, st);
 }
 
 cudaError_t launch_cholesky(double* G, int k, int* info, cudaStream_t st) {
@@ -388,7 +499,7 @@ cudaError_t launch_trsm_right_upper(double* X, int64_t m, int64_t ldx, const dou
       g.M = m; g.N = nbk; g.K = c0;
       g.out = X + (int64_t)c0 * ldx; g.ldo = ldx;
       dim3 grid((unsigned)((m + GT - 1) / GT), (unsigned)((nbk + GT - 1) / GT), 1);
-      k_gemm64<GM_NN_UPDATE><<<grid, 256, 0, st>>>(g);
+      { cudaError_t e = dgemm_launch<GM_NN_UPDATE>(g, grid, st); if (e != cudaSuccess) return e; }
     }
     k_trsm_rows_block<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(X, m, ldx, Rm, k, c0, nbk);
   }
@@ -428,17 +539,39 @@ cudaError_t launch_assemble_P(const double* T, int64_t ldt, int k, int n, const 
   return cudaGetLastError();
 }
 
-cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int n, const double* X, int k,
-                         const double* P, int64_t ldp, double* part, int* nblk_out, cudaStream_t st) {
+cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, const int* cmap, const double* X,
+                         int k, const double* T, int64_t ldt, double* part, int* nblk_out, cudaStream_t st) {
   GemmArgs g{};
   g.X = X; g.ldx = m;
-  g.Y = P; g.ldy = ldp;
-  g.M = m; g.N = n; g.K = k;
+  g.Y = T; g.ldy = ldt;
+  g.M = m; g.N = ncols; g.K = k;
   g.out = part;
   g.A = A; g.lda = ld;
-  dim3 grid((unsigned)((m + GT - 1) / GT), (unsigned)((n + GT - 1) / GT), 1);
+  g.cmap = cmap;
+  g.d_tma = ((ld % 2) == 0 && (((uintptr_t)A) & 15) == 0) ? 1 : 0;
+  dim3 grid((unsigned)((m + GT - 1) / GT), (unsigned)((ncols + GT - 1) / GT), 1);
   *nblk_out = (int)(grid.x * grid.y);
-  k_gemm64<GM_NN_ERROR><<<grid, 256, 0, st>>>(g);
+  return dgemm_launch<GM_NN_ERROR>(g, grid, st);
+}
+
+cudaError_t launch_nn_store(const double* X, int64_t m, int64_t ldx, const double* B, int64_t ldb, int K,
+                            int N, double* out, int64_t ldo, cudaStream_t st) {
+  GemmArgs g{};
+  g.X = X; g.ldx = ldx;
+  g.Y = B; g.ldy = ldb;
+  g.M = m; g.N = N; g.K = K;
+  g.out = out; g.ldo = ldo;
+  dim3 grid((unsigned)((m + GT - 1) / GT), (unsigned)((N + GT - 1) / GT), 1);
+  return dgemm_launch<GM_NN_STORE>(g, grid, st);
+}
+
+__global__ void k_eye(double* I, int k) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < (int64_t)k * k) I[idx] = (idx % k == idx / k) ? 1.0 : 0.0;
+}
+cudaError_t launch_eye(double* I, int k, cudaStream_t st) {
+  const int64_t tot = (int64_t)k * k;
+  k_eye<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(I, k);
   return cudaGetLastError();
 }
 

@@ -25,15 +25,31 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// K0: per-block max |a_ij| (grid-stride over columns x rows)
+// K0: per-block max |a_ij|.  Work items = (column, 2048-row segment); a CTA takes
+// items blockIdx.x, blockIdx.x + gridDim.x, ...; 16 B streaming loads, 4 per thread
+// in flight per item.
 __global__ void __launch_bounds__(256) k_maxabs(const double* __restrict__ A, int64_t m, int64_t n,
                                                 int64_t ld, double* __restrict__ part) {
+  constexpr int SEG = 2048;
+  const int64_t segs = (m + SEG - 1) / SEG;
+  const int64_t items = segs * n;
+  const bool vec = ((ld & 1) == 0) && ((((uintptr_t)A) & 15) == 0);
   double mx = 0.0;
-  const int64_t total = m * n;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = idx / m, r = idx - c * m;
-    mx = fmax(mx, fabs(__ldg(A + c * ld + r)));
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t c = it / segs, sg = it - c * segs;
+    const double* col = A + c * ld;
+    const int64_t r0 = sg * SEG;
+    if (vec && r0 + SEG <= m) {
+      const double2* p = reinterpret_cast<const double2*>(col + r0);
+      double2 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = __ldcs(p + threadIdx.x + q * 256);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) mx = fmax(mx, fmax(fabs(v[q].x), fabs(v[q].y)));
+    } else {
+      const int64_t r1 = (r0 + SEG < m) ? r0 + SEG : m;
+      for (int64_t r = r0 + threadIdx.x; r < r1; r += 256) mx = fmax(mx, fabs(__ldcs(col + r)));
+    }
   }
   __shared__ double sh[8];
   mx = warp_max(mx);
@@ -99,23 +115,37 @@ __global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int
   const int64_t ntiles = ngroups / (TR / 8);
   const double s = sc->scale;
   double colsq[4] = {0.0, 0.0, 0.0, 0.0};
-  double adsq = 0.0;
+  double adq[4] = {0.0, 0.0, 0.0, 0.0};
   int inf = 0;
-  for (int64_t t = blockIdx.y; t < ntiles; t += gridDim.y) {
+  // register prefetch: the next tile's 32 loads are in flight while this tile is
+  // converted and written out
+  double a[4][TR / 32];
+  auto load_tile = [&](int64_t t) {
     const int64_t r0 = t * TR;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t c = c0 + warp * 4 + q;
+      const double* col = A + c * ld;
+#pragma unroll
+      for (int i = 0; i < TR / 32; ++i) {
+        const int64_t r = r0 + i * 32 + lane;
+        a[q][i] = (c < n && r < m) ? __ldcs(col + r) : 0.0;
+      }
+    }
+  };
+  int64_t t = blockIdx.y;
+  if (t < ntiles) load_tile(t);
+  for (; t < ntiles; t += gridDim.y) {
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int cl = warp * 4 + q;
-      const int64_t c = c0 + cl;
-      const double* col = A + c * ld;
 #pragma unroll
       for (int i = 0; i < TR / 32; ++i) {
         const int rr = i * 32 + lane;
-        const int64_t r = r0 + rr;
-        const double a = (c < n && r < m) ? __ldcs(col + r) : 0.0;
-        adsq = fma(a, a, adsq);
-        const double x = __dmul_rn(s, a);
+        const double av = a[q][i];
+        adq[q] = fma(av, av, adq[q]);
+        const double x = __dmul_rn(s, av);
         T v;
         double d;
         if (sizeof(T) == 2) {
@@ -133,6 +163,7 @@ __global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int
       }
     }
     __syncthreads();
+    if (t + gridDim.y < ntiles) load_tile(t + gridDim.y);
     // write: thread -> (column lane, row group warp + 8 j)
 #pragma unroll
     for (int jg = 0; jg < TR / 8 / 8; ++jg) {
@@ -150,6 +181,7 @@ __global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int
       }
     }
   }
+  const double adsq = (adq[0] + adq[1]) + (adq[2] + adq[3]);
   __shared__ double shc[32];
   __shared__ double sha[8];
   __shared__ int shi;
@@ -159,8 +191,8 @@ __global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int
     double v = warp_sum(colsq[q]);
     if (lane == 0) shc[warp * 4 + q] = v;
   }
-  double a = warp_sum(adsq);
-  if (lane == 0) sha[warp] = a;
+  double asum = warp_sum(adsq);
+  if (lane == 0) sha[warp] = asum;
   __syncthreads();
   if (inf) atomicOr(&shi, 1);
   if (warp == 0) {

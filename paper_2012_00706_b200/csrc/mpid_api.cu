@@ -57,7 +57,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t AD, S, U, F, R, part, red, xr, norms, perm, scal3, sc, maxpart, rpart;
-  size_t AI, Q1, G1, G2, W, tpart, Rd, T, Pw, epart, misc;
+  size_t AI, Q1, G1, G2, W, tpart, Rd, T, Pw, epart, Ik, Rinv, misc;
   size_t total;
 };
 
@@ -86,7 +86,7 @@ int round_gy(int64_t m_pad, int64_t n) {
   return (int)std::min<int64_t>(gy, 4096);
 }
 int tsmm_splits(int64_t k1, int64_t n1, int64_t m) {
-  const int64_t tiles = ((k1 + 63) / 64) * ((n1 + 63) / 64);
+  const int64_t tiles = ((k1 + 127) / 128) * ((n1 + 127) / 128);   // k_dgemm CTA tile 128 x 128
   int64_t s = std::max<int64_t>(1, (2 * num_sms() + tiles - 1) / tiles);
   s = std::min<int64_t>(s, std::max<int64_t>(1, m / 1024));
   return (int)std::min<int64_t>(s, 128);
@@ -123,7 +123,9 @@ Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
   L.Rd = take((size_t)k * n * 8);
   L.T = take((size_t)k * n * 8);
   L.Pw = take((size_t)k * n * 8);
-  L.epart = take((size_t)((m_local + 63) / 64) * ((n + 63) / 64) * 8);
+  L.epart = take((size_t)((m_local + 127) / 128) * ((n + 127) / 128) * 8);
+  L.Ik = take((size_t)k * k * 8);
+  L.Rinv = take((size_t)k * k * 8);
   L.misc = take(1024);
   L.total = off;
   return L;
@@ -153,7 +155,7 @@ struct mpid_ctx {
   int* perm = nullptr;
   DevScalars* sc = nullptr;
   double *AI = nullptr, *Q1 = nullptr, *G1 = nullptr, *G2 = nullptr, *W = nullptr, *tpart = nullptr,
-         *Rd = nullptr, *T = nullptr, *Pw = nullptr, *epart = nullptr;
+         *Rd = nullptr, *T = nullptr, *Pw = nullptr, *epart = nullptr, *Ik = nullptr, *Rinv = nullptr;
   int* info = nullptr;
   double* err2 = nullptr;
   // state
@@ -288,6 +290,8 @@ id_status id_create(id_handle* hp, const double* A_D, int64_t m_global, int64_t 
   h->T = (double*)(w + L.T);
   h->Pw = (double*)(w + L.Pw);
   h->epart = (double*)(w + L.epart);
+  h->Ik = (double*)(w + L.Ik);
+  h->Rinv = (double*)(w + L.Rinv);
   h->info = (int*)(w + L.misc);
   h->err2 = (double*)(w + L.misc + 64);
   for (auto& e : h->ev) {
@@ -622,10 +626,11 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
     id_status s = allreduce(h, h->G1, (size_t)k * k, NCCL_SUM);
     if (s) return s;
     CK(launch_cholesky(h->G1, k, h->info, h->st));
-    // Q1 = A_I R1^{-1}
-    CK(cudaMemcpyAsync(h->Q1, h->AI, (size_t)m * k * 8, cudaMemcpyDeviceToDevice, h->st));
-    CK(launch_trsm_right_upper(h->Q1, m, m, h->G1, k, h->st));
-    launches += 1 + 2 * ((k + 31) / 32);
+    // Q1 = A_I R1^{-1}: the k x k inverse by triangular solves on I_k, then one DMMA GEMM
+    CK(launch_eye(h->Ik, k, h->st));
+    CK(launch_trsm_left_upper(h->G1, nullptr, k, h->Ik, k, nullptr, k, h->Rinv, k, 0, h->st));
+    CK(launch_nn_store(h->AI, m, m, h->Rinv, k, k, k, h->Q1, m, h->st));
+    launches += 4;
     // G2 = Q1^T Q1
     CK(launch_tsmm(h->Q1, m, k, h->Q1, m, k, m, h->tpart, sp, h->st));
     CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G2, h->st));
@@ -670,8 +675,14 @@ id_status id_error(id_handle h, double* abs_fro, double* rel_fro) {
   const int k = h->k_out;
   CK(cudaEventRecord(h->ev[5], h->st));
   int nblk = 0;
-  CK(launch_error(h->AD, h->m_local, h->ld, (int)h->n, h->AI, k, h->Pw, k, h->epart, &nblk, h->st));
-  CK(launch_sum_scalar(h->epart, nblk, h->err2, h->st));
+  // skeleton columns contribute exactly 0 (P(:, I) = I_k): sum over J = perm[k:] only
+  const int nj = (int)h->n - k;
+  if (nj > 0) {
+    CK(launch_error(h->AD, h->m_local, h->ld, nj, h->perm + k, h->AI, k, h->T, k, h->epart, &nblk, h->st));
+    CK(launch_sum_scalar(h->epart, nblk, h->err2, h->st));
+  } else {
+    CK(cudaMemsetAsync(h->err2, 0, sizeof(double), h->st));
+  }
   id_status s = allreduce(h, h->err2, 1, NCCL_SUM);
   if (s) return s;
   CK(cudaEventRecord(h->ev[6], h->st));

@@ -66,6 +66,57 @@ struct PassParams {
 };
 constexpr int PASS_SMEM_MAX = 225 * 1024;
 
+// PTX helpers: mbarriers and bulk (TMA) copies, shared by the kernels --------
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+// bounded wait: a pipeline bug traps (an error the host sees) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t spin = 0;; ++spin) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (spin > (1u << 26)) __trap();
+  }
+}
+// global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0, 16 B aligned)
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(su32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // host-side launchers ---------------------------------------------------------
 cudaError_t launch_maxabs(const double* A, int64_t m, int64_t n, int64_t ld, double* part,
                           int nblk, cudaStream_t st);
@@ -104,8 +155,13 @@ cudaError_t launch_R_to_fp64(const float* R, int k, int n, double* Rd, cudaStrea
 cudaError_t launch_R_export(const float* R, int k, int n, float* out, int64_t ldr, cudaStream_t st);
 cudaError_t launch_assemble_P(const double* T, int64_t ldt, int k, int n, const int* perm, double* P,
                               int64_t ldp, cudaStream_t st);
-cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int n, const double* X, int k,
-                         const double* P, int64_t ldp, double* part, int* nblk_out, cudaStream_t st);
+// error over the columns J: sum_{r, c} (A(r, cmap[c]) - sum_l X(r, l) T(l, c))^2, c < ncols
+cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, const int* cmap, const double* X,
+                         int k, const double* T, int64_t ldt, double* part, int* nblk_out, cudaStream_t st);
+// out(m x N) = X(m x K) B(K x N), all col-major
+cudaError_t launch_nn_store(const double* X, int64_t m, int64_t ldx, const double* B, int64_t ldb, int K,
+                            int N, double* out, int64_t ldo, cudaStream_t st);
+cudaError_t launch_eye(double* I, int k, cudaStream_t st);
 cudaError_t launch_sum_scalar(const double* part, int nblk, double* out, cudaStream_t st);
 
 }  // namespace mpid
