@@ -84,6 +84,26 @@ def id_error(A_D: np.ndarray, I: np.ndarray, P: np.ndarray):
     return math.sqrt(abs2), math.sqrt(abs2) / math.sqrt(nrm2) if nrm2 > 0 else float("nan")
 
 
+def id_error_blocked(A_D: np.ndarray, I: np.ndarray, P: np.ndarray, cols: int = 64):
+    """id_error for large matrices: the same definition (Remark 2: residual formed
+    and squared in fp64), evaluated 64 columns at a time; each column's sum of
+    squares is numpy's fp64 pairwise sum and the column sums are added with
+    math.fsum.  Pinned against id_error (tests/test_oracle_id.py)."""
+    A_D = np.asarray(A_D)
+    I = np.asarray(I)
+    AI = np.ascontiguousarray(A_D[:, I])
+    n = A_D.shape[1]
+    parts, nrm = [], []
+    for c0 in range(0, n, cols):
+        c1 = min(n, c0 + cols)
+        blk = np.asarray(A_D[:, c0:c1], dtype=np.float64)
+        E = blk - AI @ P[:, c0:c1]
+        parts.extend(np.einsum("ij,ij->j", E, E).tolist())
+        nrm.extend(np.einsum("ij,ij->j", blk, blk).tolist())
+    abs2, nrm2 = math.fsum(parts), math.fsum(nrm)
+    return math.sqrt(abs2), math.sqrt(abs2) / math.sqrt(nrm2) if nrm2 > 0 else float("nan")
+
+
 def lemma_bound(k: int, n: int, sigma_k1: float):
     """Lemma 2.1: (sqrt(1 + k(n-k)), sqrt(1 + k(n-k)) sigma_{k+1})."""
     c = math.sqrt(1.0 + k * (n - k))

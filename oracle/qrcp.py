@@ -111,8 +111,18 @@ def chain8(X: np.ndarray, Y: np.ndarray, wdt) -> np.ndarray:
     return acc.astype(np.float64).sum(axis=0)
 
 
+class _Local:
+    """Single-process 'communicator': the sum over ranks of one rank is itself."""
+    rank, size = 0, 1
+
+    @staticmethod
+    def sum(x):
+        return np.asarray(x, dtype=np.float64)
+
+
 def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1,
-                     eps: float = 0.0, norms: str = "downdate", acc: str = "chain8") -> QRCPResult:
+                     eps: float = 0.0, norms: str = "downdate", acc: str = "chain8",
+                     row_offset: int = 0, comm=None) -> QRCPResult:
     """Householder QRCP of the already-rounded A_L, in the precision model above.
 
     Step j (0-based), following Eq. (6)-(7):
@@ -131,12 +141,24 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
       5. W(j:m, j:) <- fl(W - v f^T), one rounding per entry                     [update, R4b]
     The tolerance stop (reading R8) is tested before step j >= 1 on the exact
     norms of step 3: sqrt(sum_{i >= j} s_i) <= eps ||A_L||_F -> k = j.
+
+    Row sharding: A_L may be this rank's rows [row_offset,
+    row_offset + m_loc) of the global matrix (row_offset % 8 == 0, so 8-row groups
+    align).  Every column reduction (initial norms, s, w = W^T u) and the pivot
+    row x = W(j, j:) (owner rank only, zeros elsewhere) is then summed over ranks
+    with comm.sum (fp64) — the one exchange per step — and every decision (pivot,
+    beta, R, f, norms) is taken identically on all ranks from the summed values.
+    With comm=None the matrix is the whole A_L.
     """
     fmtL = fmt_of(fmt)
     wdt = _work_dtype(fmt)
+    comm = _Local if comm is None else comm
     A_L = np.asarray(A_L, dtype=np.float64)
-    m, n = A_L.shape
-    if not (1 <= k_max <= min(m, n)):
+    m, n = A_L.shape                                        # m = rows of this shard
+    if row_offset % 8:
+        raise ValueError("row_offset must be a multiple of 8")
+    m_glob = int(comm.sum(np.array([float(m)]))[0])
+    if not (1 <= k_max <= min(m_glob, n)):
         raise ValueError("k out of range (DimensionError)")
     m8 = (m + 7) // 8 * 8
     W = np.zeros((m8, n), dtype=wdt, order="F")
@@ -146,7 +168,7 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
     V = np.zeros((m, k_max), dtype=np.float64)
     tau = np.zeros(k_max)
     top2 = np.zeros((k_max, 2))
-    col2 = np.sum(A_L * A_L, axis=0)
+    col2 = comm.sum(np.sum(A_L * A_L, axis=0))
     normAL = math.sqrt(float(np.sum(col2)))
     maxnorm0 = math.sqrt(float(np.max(col2))) if n else 0.0
     vn = col2.copy()                                        # exact initial norms^2
@@ -154,16 +176,21 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
 
     def reduce(X, Y):
         if acc == "chain8":
-            return chain8(X, Y, wdt)
-        return np.sum(X.astype(np.float64) * Y.astype(np.float64), axis=0)
+            return comm.sum(chain8(X, Y, wdt))
+        return comm.sum(np.sum(X.astype(np.float64) * Y.astype(np.float64), axis=0))
+
+    def local(jg):
+        """first local row whose global index is >= jg, and the first row of its 8-row group"""
+        jl = min(max(jg - row_offset, 0), m8)
+        return jl, (jl // 8) * 8
 
     resid = []
     status, k_out = "ok", k_max
     for j in range(k_max):
-        g0 = (j // 8) * 8                                   # first row of j's 8-row group
+        jl, g0 = local(j)                                   # local row of j / of its 8-row group
         if norms == "recompute":
             Wj = W[g0:, j:].copy()
-            Wj[: j - g0] = 0
+            Wj[: jl - g0] = 0
             vn[j:] = reduce(Wj, Wj)
         cand = vn[j:]
         c_ = np.flatnonzero(cand == cand.max())             # step 1, tie -> lowest original index
@@ -177,9 +204,9 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
             perm[[j, p]] = perm[[p, j]]
             vn[[j, p]] = vn[[p, j]]
         if j > 0 and j % nb == 0 and fmtL is not DOUBLE:    # step 2, store point
-            W[j:, j:] = round_to(W[j:, j:].astype(np.float64), fmtL).reshape(m8 - j, n - j)
+            W[jl:, j:] = round_to(W[jl:, j:].astype(np.float64), fmtL).reshape(m8 - jl, n - j)
         Wj = W[g0:, j:].copy()                              # step 3 (rows < j masked to 0)
-        Wj[: j - g0] = 0
+        Wj[: jl - g0] = 0
         u = Wj[:, :1]
         s = reduce(Wj, Wj)
         resid.append(math.sqrt(float(np.sum(s))))           # exact remaining mass before step j
@@ -187,28 +214,30 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
             k_out = j                                       # tolerance stop (reading R8)
             break
         w = reduce(Wj, u)
+        owner = row_offset <= j < row_offset + m
+        x = comm.sum(W[j - row_offset, j:].astype(np.float64) if owner else np.zeros(n - j))
         sj = float(s[0])
         if not (sj >= tiny):
             status, k_out = "underflow", j
             break
-        u0 = float(W[j, j])                                 # step 4
+        u0 = float(x[0])                                    # step 4 (= W(j, j))
         beta = -math.copysign(math.sqrt(sj), u0)
         c = 1.0 / (u0 - beta)
-        uu = W[j:, j].astype(np.float64)
+        uu = W[jl:, j].astype(np.float64)
         v = (uu * c).astype(wdt)
-        v[0] = 1.0
+        if owner:
+            v[0] = 1.0
         tau[j] = (beta - u0) / beta
         Rraw = w / beta
-        x = W[j, j:].astype(np.float64)
         f = (x - Rraw).astype(wdt)
         R[j, j:] = (Rraw * math.copysign(1.0, beta)).astype(wdt)
         vn[j + 1:] = s[1:] - Rraw[1:] ** 2                  # one-step downdate (R6)
-        W[j:, j:] = _fma(-v[:, None], f[None, :], W[j:, j:], wdt)   # step 5
-        V[j:, j] = v[: m - j]
-    if status == "ok" and k_out == k_max and k_max < min(m, n):
-        g0 = (k_max // 8) * 8
+        W[jl:, j:] = _fma(-v[:, None], f[None, :], W[jl:, j:], wdt)   # step 5
+        V[jl:, j] = v[: max(m - jl, 0)]
+    if status == "ok" and k_out == k_max and k_max < min(m_glob, n):
+        jl, g0 = local(k_max)
         Wj = W[g0:, k_max:].copy()
-        Wj[: k_max - g0] = 0
+        Wj[: jl - g0] = 0
         resid.append(math.sqrt(float(np.sum(reduce(Wj, Wj)))))   # exact mass after k steps
     R = R[:k_out]
     return QRCPResult(perm, R, k_out, status, V[:, :k_out], tau[:k_out], top2[:k_out],

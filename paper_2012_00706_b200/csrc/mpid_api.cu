@@ -86,10 +86,11 @@ int round_gy(int64_t m_pad, int64_t n) {
   return (int)std::min<int64_t>(gy, 4096);
 }
 int tsmm_splits(int64_t k1, int64_t n1, int64_t m) {
-  const int64_t tiles = ((k1 + 127) / 128) * ((n1 + 127) / 128);   // k_dgemm CTA tile 128 x 128
+  // k_dgemm CTA tile 128 x 128, one CTA per SM: aim at two full waves of equal-work CTAs
+  const int64_t tiles = ((k1 + 127) / 128) * ((n1 + 127) / 128);
   int64_t s = std::max<int64_t>(1, (2 * num_sms() + tiles - 1) / tiles);
-  s = std::min<int64_t>(s, std::max<int64_t>(1, m / 1024));
-  return (int)std::min<int64_t>(s, 128);
+  s = std::min<int64_t>(s, std::max<int64_t>(1, m / 512));
+  return (int)std::min<int64_t>(s, 512);
 }
 
 Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {

@@ -103,3 +103,14 @@ def test_table3_ratios_and_generator_spectrum(t):
     s = np.linalg.svd(A, compute_uv=False)
     big = sigma > 1e-13
     assert np.allclose(s[big], sigma[big], rtol=1e-10, atol=1e-15)
+
+
+def test_blocked_error_equals_definition():
+    """id_error_blocked (used at full size) against the fsum definition id_error."""
+    from oracle.id import id_error_blocked
+    A = gen_config("C2", 0)[:, :300]
+    I = np.array([5, 17, 2, 250, 99, 64, 130])
+    P = coeffs_lsq(A, I)
+    a = id_error(A, I, P)
+    b = id_error_blocked(A, I, P, cols=37)
+    assert abs(a[0] - b[0]) <= 1e-13 * a[0] and abs(a[1] - b[1]) <= 1e-13 * a[1]
