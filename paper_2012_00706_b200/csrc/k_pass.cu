@@ -208,8 +208,9 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
       tstep[l] = p.j0 + l;
     }
     float* __restrict__ Uj = p.U + (int64_t)(j % NSLOT) * p.m_pad;
+    int slot = 0;
+    uint32_t phase = 0;
     for (int i = 0; i < nst; ++i) {
-      const int slot = i % NST;
       const int64_t g0 = gb + (int64_t)i * GS;
       const int gsz = (int)((ge - g0) < GS ? (ge - g0) : GS);
       unsigned char* base = smem + (size_t)slot * geo.total;
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
       const float* upend = reinterpret_cast<const float*>(base + geo.upend);
       float* us = reinterpret_cast<float*>(base + geo.us);
       float* nv = reinterpret_cast<float*>(base + geo.nv);
-      mbar_wait(&full[slot], (i / NST) & 1);
+      mbar_wait(&full[slot], phase);
       for (int r = lane; r < gsz * 8; r += 32) {
         const int64_t rl = g0 * 8 + r;
         const int64_t rg = p.row_offset + rl;
@@ -240,6 +241,7 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
         if (blockIdx.y == 0) Uj[rl] = u;
       }
       mbar_arrive(&prep[slot]);   // every lane arrives (count 32): its smem writes are released
+      if (++slot == NST) { slot = 0; phase ^= 1; }
     }
     return;
   }
@@ -267,15 +269,17 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
   // clamp the column offsets of invalid lanes into the row (their results are discarded)
   const int o0 = (v0 ? col0 : 0) * 8, o1 = (v1 ? col1 : 0) * 8;
 
+  int slot = 0;
+  uint32_t phase = 0;
   for (int i = 0; i < nst; ++i) {
-    const int slot = i % NST;
     const int64_t g0 = gb + (int64_t)i * GS;
     const int gsz = (int)((ge - g0) < GS ? (ge - g0) : GS);
+    const int gjs = (gj >= g0 && gj < g0 + gsz) ? (int)(gj - g0) : -1;   // stage group holding row j
     unsigned char* base = smem + (size_t)slot * geo.total;
     T* data = reinterpret_cast<T*>(base);
     const float* us = reinterpret_cast<const float*>(base + geo.us);
     const float* nv = reinterpret_cast<const float*>(base + geo.nv);
-    mbar_wait(&prep[slot], (i / NST) & 1);
+    mbar_wait(&prep[slot], phase);
     if (active && (v0 || v1)) {
       for (int gl = rw; gl < gsz; gl += WR) {
         T* d0 = data + (size_t)gl * ncols * 8 + o0;
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
         const float4 ua = *reinterpret_cast<const float4*>(us + gl * 8);
         const float4 ub = *reinterpret_cast<const float4*>(us + gl * 8 + 4);
         const float uu[8] = {ua.x, ua.y, ua.z, ua.w, ub.x, ub.y, ub.z, ub.w};
-        if (g0 + gl == gj) {                              // the group holding row j (rare)
+        if (gl == gjs) {                                  // the group holding row j (rare)
           float2 xj = x[0];
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -322,6 +326,7 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
     if (p.store) fence_async_smem();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
+    if (++slot == NST) { slot = 0; phase ^= 1; }
   }
   // cross-warp (row-split) combine in fixed order rw = 0..WR-1, then one write per column
   if (WR > 1) {
@@ -384,9 +389,9 @@ static cudaError_t launch_ws_fmt(PassParams p, int max_ctas, int* gx_out, cudaSt
   p.wr = WR;
   const int pmax = p.npend <= 1 ? 1 : p.npend <= 2 ? 2 : p.npend <= 4 ? 4 : p.npend <= 8 ? 8 : 16;
   if (p.npend > pmax || pmax > NB_MAX) return cudaErrorInvalidValue;
-  // stage = GS row groups: ~32 KB of matrix data, a multiple of WR, at most 64 groups
+  // stage = GS row groups: ~48 KB of matrix data, a multiple of WR, at most 64 groups
   const int rowbytes = ncols * 8 * esz;
-  int gpw = std::max(1, (32 * 1024) / (rowbytes * WR));
+  int gpw = std::max(1, (48 * 1024) / (rowbytes * WR));
   int GS = std::min(64, WR * gpw);
   SlotGeom g = slot_geom(GS, ncols, esz, pmax);
   const size_t fixed = RED_BYTES + 3 * 8 * 8 + 64;
