@@ -177,8 +177,11 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
     for (int64_t kb = k_begin; kb < k_end; kb += GK) {
       const bool more = kb + GK < k_end;
       if (more) gload(kb + GK);
+      const int64_t krem = (k_end - kb + 3) / 4;
+      const int ksteps = krem < GK / 4 ? (int)krem : GK / 4;              // skip all-zero k-steps
 #pragma unroll
       for (int ks = 0; ks < GK / 4; ++ks) {
+        if (ks >= ksteps) break;
         double af[8], bf[4];
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) {
@@ -266,6 +269,183 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
       for (int w = 0; w < 8; ++w) t += red[w];
       g.out[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused fp64 error, persistent: e^2 = sum_{r, c} (A_D(r, cmap[c]) - sum_l X(r, l) T(l, c))^2
+// (Remark 2: products in double; the residual is never stored).
+// One CTA per SM walks its 128 x 128 output tiles (row block major, so the tiles of
+// one row block share the A_I tile in L2) as ONE flattened (tile, k-stage) loop:
+// the next stage's loads — including the next tile's first stage — are in
+// flight while the current stage's DMMAs run, and each tile's A_D block is
+// prefetched into shared memory by bulk copies one tile ahead of its epilogue.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntiles, int ncb) {
+  extern __shared__ __align__(16) double dsm[];
+  double (*As)[GK * LDM] = reinterpret_cast<double (*)[GK * LDM]>(dsm);
+  double (*Bs)[GT * LDK] = reinterpret_cast<double (*)[GT * LDK]>(dsm + 2 * GK * LDM);
+  double* Ds = dsm + 2 * GK * LDM + 2 * GT * LDK;
+  __shared__ __align__(8) uint64_t dbar;
+  __shared__ double red[8];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int64_t K = g.K;
+  const int nks = (int)((K + GK - 1) / GK);
+  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = my_tiles * nks;
+  if (tid == 0) {
+    mbar_init(&dbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto tile_of = [&](int64_t lt, int64_t& m0, int64_t& n0) {
+    const int64_t t = blockIdx.x + lt * gridDim.x;
+    m0 = (t / ncb) * GT;
+    n0 = (t % ncb) * GT;
+  };
+  auto d_ok = [&](int64_t m0) {
+    const int64_t rows = (g.M - m0 < GT) ? g.M - m0 : (int64_t)GT;
+    return g.d_tma && (rows % 2 == 0);
+  };
+  auto issue_d = [&](int64_t m0, int64_t n0) {   // warp 0: each lane issues 4 of the 128 column copies
+    const int64_t rows = (g.M - m0 < GT) ? g.M - m0 : (int64_t)GT;
+    const int cols = (int)((g.N - n0 < GT) ? g.N - n0 : (int64_t)GT);
+    int src[GT / 32];
+#pragma unroll
+    for (int q = 0; q < GT / 32; ++q) {
+      const int c = lane + 32 * q;
+      src[q] = c < cols ? g.cmap[n0 + c] : 0;
+    }
+    if (lane == 0) mbar_expect_tx(&dbar, (uint32_t)(rows * cols * 8));
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < GT / 32; ++q) {
+      const int c = lane + 32 * q;
+      if (c < cols) tma_load(Ds + c * DLD, g.A + (int64_t)src[q] * g.lda + m0, (uint32_t)(rows * 8), &dbar);
+    }
+  };
+  double2 ra[4], rb[4];
+  auto gload = [&](int64_t m0, int64_t n0, int64_t kb) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid + q * 256;
+      {
+        const int l = idx >> 6, rr = (idx & 63) * 2;
+        const int64_t kk = kb + l, r = m0 + rr;
+        ra[q] = make_double2(0.0, 0.0);
+        if (kk < K) {
+          const double* p = g.X + kk * g.ldx + r;
+          if (r + 1 < g.M && (((uintptr_t)p & 15) == 0)) ra[q] = *reinterpret_cast<const double2*>(p);
+          else { if (r < g.M) ra[q].x = p[0]; if (r + 1 < g.M) ra[q].y = p[1]; }
+        }
+      }
+      {
+        const int cc = idx >> 3, l = (idx & 7) * 2;
+        const int64_t c = n0 + cc, kk = kb + l;
+        rb[q] = make_double2(0.0, 0.0);
+        if (c < g.N) {
+          const double* p = g.Y + c * g.ldy + kk;
+          if (kk < K) rb[q].x = p[0];
+          if (kk + 1 < K) rb[q].y = p[1];
+        }
+      }
+    }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid + q * 256;
+      const int l = idx >> 6, rr = (idx & 63) * 2;
+      *reinterpret_cast<double2*>(&As[buf][l * LDM + rr]) = ra[q];
+      const int cc = idx >> 3, l2 = (idx & 7) * 2;
+      *reinterpret_cast<double2*>(&Bs[buf][cc * LDK + l2]) = rb[q];
+    }
+  };
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  double e2 = 0.0;
+  uint32_t dphase = 0;
+  if (total > 0) {
+    int64_t m0, n0;
+    tile_of(0, m0, n0);
+    if (warp == 0 && d_ok(m0)) issue_d(m0, n0);
+    gload(m0, n0, 0);
+    sstore(0);
+    __syncthreads();
+  }
+  int buf = 0;
+  int64_t lt = 0, m0 = 0, n0 = 0, m1 = 0, n1 = 0;
+  int ks_i = 0;
+  if (total > 0) tile_of(0, m0, n0);
+  for (int64_t it = 0; it < total; ++it) {
+    const int64_t kb = (int64_t)ks_i * GK;
+    if (ks_i == 0 && it > 0 && warp == 0 && d_ok(m0)) issue_d(m0, n0);  // this tile's A_D block
+    const bool more = it + 1 < total;
+    const bool last_k = ks_i == nks - 1;
+    if (more) {
+      if (last_k) tile_of(lt + 1, m1, n1);
+      else { m1 = m0; n1 = n0; }
+      gload(m1, n1, last_k ? 0 : kb + GK);
+    }
+    const int64_t krem = (K - kb + 3) / 4;
+    const int ksteps = krem < GK / 4 ? (int)krem : GK / 4;
+#pragma unroll
+    for (int ks = 0; ks < GK / 4; ++ks) {
+      if (ks >= ksteps) break;
+      double af[8], bf[4];
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) af[mt] = As[buf][(ks * 4 + tq) * LDM + wm * 64 + mt * 8 + gq];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[buf][(wn * 32 + nt * 8 + gq) * LDK + ks * 4 + tq];
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
+    }
+    if (last_k) {                            // epilogue of tile lt
+      const bool dp = d_ok(m0);
+      if (dp) {
+        mbar_wait(&dbar, dphase);
+        dphase ^= 1;
+      }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt) {
+            const int64_t r = m0 + wm * 64 + mt * 8 + gq;
+            if (r < g.M && c < g.N) {
+              const double a = dp ? Ds[(c - n0) * DLD + (r - m0)] : __ldcs(g.A + (int64_t)g.cmap[c] * g.lda + r);
+              const double e = a - acc[mt][nt][h];
+              e2 = fma(e, e, e2);
+            }
+            acc[mt][nt][h] = 0.0;
+          }
+        }
+    }
+    if (more) {
+      sstore(buf ^ 1);
+      __syncthreads();                        // also: every thread is done with Ds before the next issue_d
+      buf ^= 1;
+    }
+    if (last_k) { ++lt; m0 = m1; n0 = n1; ks_i = 0; } else { ++ks_i; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+  if (lane == 0) red[warp] = e2;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w];
+    g.out[blockIdx.x] = t;
   }
 }
 
@@ -549,9 +729,22 @@ cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, cons
   g.A = A; g.lda = ld;
   g.cmap = cmap;
   g.d_tma = ((ld % 2) == 0 && (((uintptr_t)A) & 15) == 0) ? 1 : 0;
-  dim3 grid((unsigned)((m + GT - 1) / GT), (unsigned)((ncols + GT - 1) / GT), 1);
-  *nblk_out = (int)(grid.x * grid.y);
-  return dgemm_launch<GM_NN_ERROR>(g, grid, st);
+  const int64_t nrb = (m + GT - 1) / GT, ncb = (ncols + GT - 1) / GT;
+  const int64_t ntiles = nrb * ncb;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>(ntiles, sms);
+  const size_t smem = (size_t)(2 * GK * LDM + 2 * GT * LDK + GT * DLD) * sizeof(double);
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(k_err_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  *nblk_out = grid;
+  k_err_persist<<<grid, 256, smem, st>>>(g, ntiles, (int)ncb);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_nn_store(const double* X, int64_t m, int64_t ldx, const double* B, int64_t ldb, int K,
