@@ -70,14 +70,19 @@ typedef enum {
 
 /* Numerical-model knobs of the QRCP (readings R4-R6).  NULL = defaults. */
 typedef struct {
-  int32_t nb;        /* store interval: the trailing matrix is re-stored in the
-                        low format every nb steps (1 = SPEC's store-after-every-
-                        update); 0 = default (4).  1 <= nb <= 16. */
+  int32_t nb;        /* store interval = panel width: the trailing matrix is re-stored
+                        in the low format every nb steps (1 = SPEC's store-after-every-
+                        update); 0 = default (4 with FFMA formation, 16 with tcgen05).
+                        1 <= nb <= 32 (<= 16 with FFMA formation). */
   int32_t use_graph; /* 0 or 1 (default) = capture the k-step loop in a CUDA graph
                         and replay it; -1 = plain stream launches. */
   int32_t profile_pass; /* 1 = bracket every panel-pass launch with CUDA events
                            (id_stats.t_pass_ms); adds event nodes between kernels. */
-  int32_t reserved[5];
+  int32_t formation; /* how the pending update A~ = S - V F^T is formed each step:
+                        1 = CUDA-core FFMA in step order (bit-identical to the oracle's
+                        sequential model), 2 = tcgen05 tensor cores (3xTF32, TMEM;
+                        DESIGN.md R14), 0 = default (1: measured faster on C4). */
+  int32_t reserved[4];
 } id_qrcp_opts;
 
 /* Per-call statistics (device-event times of the last calls, in ms). */
@@ -96,7 +101,8 @@ typedef struct {
   int32_t k_out;
   int32_t nb;
   int32_t status_qrcp;
-  int32_t reserved[5];
+  int32_t formation;     /* formation used by the last QRCP (see id_qrcp_opts) */
+  int32_t reserved[4];
 } id_stats;
 
 /* Bytes of device workspace for a shard of m_local rows, n columns, rank <= k_max,

@@ -120,9 +120,26 @@ class _Local:
         return np.asarray(x, dtype=np.float64)
 
 
+def pair8(X: np.ndarray, Y: np.ndarray, wdt) -> np.ndarray:
+    """Column sums of X*Y in the tensor-core pass's order (reading R5b): within each
+    group of 8 consecutive rows two working-precision FMA chains, one over the even
+    rows (0, 2, 4, 6) and one over the odd rows (1, 3, 5, 7), started with a product;
+    the two chain values added in working precision; group partials added in fp64."""
+    G = X.shape[0] // 8
+    Xg = X.reshape(G, 8, -1)
+    Yg = Y.reshape(G, 8, -1)
+    ev = (Xg[:, 0].astype(np.float64) * Yg[:, 0].astype(np.float64)).astype(wdt)
+    od = (Xg[:, 1].astype(np.float64) * Yg[:, 1].astype(np.float64)).astype(wdt)
+    for i in (2, 4, 6):
+        ev = _fma(Xg[:, i], Yg[:, i], ev, wdt)
+        od = _fma(Xg[:, i + 1], Yg[:, i + 1], od, wdt)
+    tot = (ev.astype(np.float64) + od.astype(np.float64)).astype(wdt)
+    return tot.astype(np.float64).sum(axis=0)
+
+
 def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1,
-                     eps: float = 0.0, norms: str = "downdate", acc: str = "chain8",
-                     row_offset: int = 0, comm=None) -> QRCPResult:
+                     eps: float = 0.0, norms: str = "downdate", acc: str = "auto",
+                     row_offset: int = 0, comm=None, formation: str = "fma") -> QRCPResult:
     """Householder QRCP of the already-rounded A_L, in the precision model above.
 
     Step j (0-based), following Eq. (6)-(7):
@@ -134,7 +151,8 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
       2. every nb steps (j > 0, j % nb == 0): W(j:, j:) <- fl_L(W(j:, j:))      [store point, R4]
       3. s_i = ||W(j:m, i)||^2, w = W(j:m, j:)^T u with u = W(j:m, j), summed in
          the blocked order `acc` ("chain8": 8-row fp32 FMA chains + fp64, R5;
-         "fp64": exact products summed in fp64)                                 [reductions]
+         "pair8": even/odd-row chains, the tensor-core pass's order, R5b; "fp64":
+         exact products summed in fp64; "auto": pair8 for formation="tc", else chain8)
       4. beta = -sign(u_0) sqrt(s_j); c = 1/(u_0 - beta); v = fl(u c), v_0 = 1;
          tau = (beta - u_0)/beta; R(j, i) = w_i / beta (row sign-normalised so
          R_jj = |beta|); f = fl(x - w/beta) with x = W(j, j:) (= tau W^T v)
@@ -149,6 +167,15 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
     with comm.sum (fp64) — the one exchange per step — and every decision (pivot,
     beta, R, f, norms) is taken identically on all ranks from the summed values.
     With comm=None the matrix is the whole A_L.
+
+    formation="tc" (reading R14; the tensor-core pass): W is the
+    stored matrix S, updated only at store points, and each step forms the
+    trailing block as X = fl32(S - fl32(V_p F_p^T)) with the pending product
+    V_p F_p^T evaluated exactly (fp64; the GPU's 3xTF32 tcgen05 product is within
+    ~2^-21 of it) and rounded once to fp32 (the TMEM accumulator), then one fp32
+    subtraction.  The pivot column u = X(:, 0) (the GPU forms it in TMEM lane 127
+    of every CTA with the same operands), X(j, :) is the pivot row, and at a store
+    point fl_L(X) becomes the new S.
     """
     fmtL = fmt_of(fmt)
     wdt = _work_dtype(fmt)
@@ -174,9 +201,14 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
     vn = col2.copy()                                        # exact initial norms^2
     tiny = DOUBLE.min_normal if fmtL is DOUBLE else SINGLE.min_normal
 
+    if acc == "auto":
+        acc = "pair8" if formation == "tc" else "chain8"
+
     def reduce(X, Y):
         if acc == "chain8":
             return comm.sum(chain8(X, Y, wdt))
+        if acc == "pair8":
+            return comm.sum(pair8(X, Y, wdt))
         return comm.sum(np.sum(X.astype(np.float64) * Y.astype(np.float64), axis=0))
 
     def local(jg):
@@ -184,10 +216,25 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
         jl = min(max(jg - row_offset, 0), m8)
         return jl, (jl // 8) * 8
 
+    tc = formation == "tc"
+    if tc and fmtL is DOUBLE:
+        raise ValueError("formation='tc' models the low-precision tensor-core pass")
+    Vp = np.zeros((m8, 0))                                  # tc: pending v (full length) and f rows
+    Fp = np.zeros((0, n))
+
+    def form_tc(j):
+        """(X, u): the formed trailing block W(:, j:) and the pivot column u = X(:, 0)
+        (formation='tc')."""
+        D = (Vp @ Fp[:, j:]).astype(np.float32) if Fp.shape[0] else np.zeros((m8, n - j), np.float32)
+        X = (W[:, j:].astype(np.float64) - D.astype(np.float64)).astype(wdt)
+        return X, X[:, 0].copy()
+
     resid = []
     status, k_out = "ok", k_max
     for j in range(k_max):
         jl, g0 = local(j)                                   # local row of j / of its 8-row group
+        if tc and norms == "recompute":
+            raise ValueError("formation='tc' uses the downdated exact norms")
         if norms == "recompute":
             Wj = W[g0:, j:].copy()
             Wj[: jl - g0] = 0
@@ -203,11 +250,24 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
             R[:j, [j, p]] = R[:j, [p, j]]
             perm[[j, p]] = perm[[p, j]]
             vn[[j, p]] = vn[[p, j]]
-        if j > 0 and j % nb == 0 and fmtL is not DOUBLE:    # step 2, store point
-            W[jl:, j:] = round_to(W[jl:, j:].astype(np.float64), fmtL).reshape(m8 - jl, n - j)
-        Wj = W[g0:, j:].copy()                              # step 3 (rows < j masked to 0)
-        Wj[: jl - g0] = 0
-        u = Wj[:, :1]
+            Fp[:, [j, p]] = Fp[:, [p, j]]
+        if tc:
+            X, ucol = form_tc(j)
+            if j > 0 and j % nb == 0:                       # store point: S <- fl_L(X)
+                X = round_to(X.astype(np.float64), fmtL).reshape(m8, n - j).astype(wdt)
+                ucol = X[:, 0].copy()
+                W[:, j:] = X
+                Vp, Fp = np.zeros((m8, 0)), np.zeros((0, n))
+            Wj = X[g0:].copy()
+            Wj[: jl - g0] = 0
+            u = ucol[g0:].copy().reshape(-1, 1)
+            u[: jl - g0] = 0
+        else:
+            if j > 0 and j % nb == 0 and fmtL is not DOUBLE:    # step 2, store point
+                W[jl:, j:] = round_to(W[jl:, j:].astype(np.float64), fmtL).reshape(m8 - jl, n - j)
+            Wj = W[g0:, j:].copy()                              # step 3 (rows < j masked to 0)
+            Wj[: jl - g0] = 0
+            u = Wj[:, :1]
         s = reduce(Wj, Wj)
         resid.append(math.sqrt(float(np.sum(s))))           # exact remaining mass before step j
         if eps > 0.0 and j > 0 and resid[-1] <= eps * normAL:
@@ -215,7 +275,8 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
             break
         w = reduce(Wj, u)
         owner = row_offset <= j < row_offset + m
-        x = comm.sum(W[j - row_offset, j:].astype(np.float64) if owner else np.zeros(n - j))
+        xsrc = X[j - row_offset] if tc and owner else (W[j - row_offset, j:] if owner else None)
+        x = comm.sum(xsrc.astype(np.float64) if owner else np.zeros(n - j))
         sj = float(s[0])
         if not (sj >= tiny):
             status, k_out = "underflow", j
@@ -223,7 +284,7 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
         u0 = float(x[0])                                    # step 4 (= W(j, j))
         beta = -math.copysign(math.sqrt(sj), u0)
         c = 1.0 / (u0 - beta)
-        uu = W[jl:, j].astype(np.float64)
+        uu = (ucol[jl:] if tc else W[jl:, j]).astype(np.float64)
         v = (uu * c).astype(wdt)
         if owner:
             v[0] = 1.0
@@ -232,11 +293,19 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
         f = (x - Rraw).astype(wdt)
         R[j, j:] = (Rraw * math.copysign(1.0, beta)).astype(wdt)
         vn[j + 1:] = s[1:] - Rraw[1:] ** 2                  # one-step downdate (R6)
-        W[jl:, j:] = _fma(-v[:, None], f[None, :], W[jl:, j:], wdt)   # step 5
+        if tc:                                              # step 5 deferred: pending (v, f)
+            vfull = np.zeros(m8)
+            vfull[jl:] = v
+            frow = np.zeros(n)
+            frow[j:] = f
+            Vp = np.concatenate([Vp, vfull[:, None]], axis=1)
+            Fp = np.concatenate([Fp, frow[None, :]], axis=0)
+        else:
+            W[jl:, j:] = _fma(-v[:, None], f[None, :], W[jl:, j:], wdt)   # step 5
         V[jl:, j] = v[: max(m - jl, 0)]
     if status == "ok" and k_out == k_max and k_max < min(m_glob, n):
         jl, g0 = local(k_max)
-        Wj = W[g0:, k_max:].copy()
+        Wj = (form_tc(k_max)[0][g0:] if tc else W[g0:, k_max:]).copy()
         Wj[: jl - g0] = 0
         resid.append(math.sqrt(float(np.sum(reduce(Wj, Wj)))))   # exact mass after k steps
     R = R[:k_out]

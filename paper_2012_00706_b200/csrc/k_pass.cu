@@ -38,8 +38,9 @@ template <> struct Chunk<__half> {
 #pragma unroll
     for (int q = 0; q < 8; ++q) x[q] = make_float2(__half2float(ha[q]), __half2float(hb[q]));
   }
-  // round to fp16 (RNE), write back, and replace x by the rounded values
-  __device__ static __forceinline__ void round_store2(__half* a, __half* b, float2* x) {
+  // round to fp16 (RNE), write back the chunks of the valid columns (wa, wb), and
+  // replace x by the rounded values
+  __device__ static __forceinline__ void round_store2(__half* a, __half* b, float2* x, bool wa, bool wb) {
     uint4 va, vb;
     __half2* ha = reinterpret_cast<__half2*>(&va);
     __half2* hb = reinterpret_cast<__half2*>(&vb);
@@ -52,8 +53,8 @@ template <> struct Chunk<__half> {
       x[2 * q] = make_float2(a2.x, b2.x);
       x[2 * q + 1] = make_float2(a2.y, b2.y);
     }
-    *reinterpret_cast<uint4*>(a) = va;
-    *reinterpret_cast<uint4*>(b) = vb;
+    if (wa) *reinterpret_cast<uint4*>(a) = va;
+    if (wb) *reinterpret_cast<uint4*>(b) = vb;
   }
   __device__ static __forceinline__ float get(const __half* p, int i) { return __half2float(p[i]); }
   __device__ static __forceinline__ float rnd(float a) { return __half2float(__float2half_rn(a)); }
@@ -67,11 +68,15 @@ template <> struct Chunk<float> {
     x[4] = make_float2(a1.x, b1.x); x[5] = make_float2(a1.y, b1.y);
     x[6] = make_float2(a1.z, b1.z); x[7] = make_float2(a1.w, b1.w);
   }
-  __device__ static __forceinline__ void round_store2(float* a, float* b, float2* x) {
-    reinterpret_cast<float4*>(a)[0] = make_float4(x[0].x, x[1].x, x[2].x, x[3].x);
-    reinterpret_cast<float4*>(a)[1] = make_float4(x[4].x, x[5].x, x[6].x, x[7].x);
-    reinterpret_cast<float4*>(b)[0] = make_float4(x[0].y, x[1].y, x[2].y, x[3].y);
-    reinterpret_cast<float4*>(b)[1] = make_float4(x[4].y, x[5].y, x[6].y, x[7].y);
+  __device__ static __forceinline__ void round_store2(float* a, float* b, float2* x, bool wa, bool wb) {
+    if (wa) {
+      reinterpret_cast<float4*>(a)[0] = make_float4(x[0].x, x[1].x, x[2].x, x[3].x);
+      reinterpret_cast<float4*>(a)[1] = make_float4(x[4].x, x[5].x, x[6].x, x[7].x);
+    }
+    if (wb) {
+      reinterpret_cast<float4*>(b)[0] = make_float4(x[0].y, x[1].y, x[2].y, x[3].y);
+      reinterpret_cast<float4*>(b)[1] = make_float4(x[4].y, x[5].y, x[6].y, x[7].y);
+    }
   }
   __device__ static __forceinline__ float get(const float* p, int i) { return p[i]; }
   __device__ static __forceinline__ float rnd(float a) { return a; }
@@ -296,7 +301,8 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
             for (int q = 0; q < 8; ++q) x[q] = __ffma2_rn(make_float2(vv[q], vv[q]), f2[l], x[q]);
           }
         }
-        if (p.store) Chunk<T>::round_store2(d0, d1, x);
+        // invalid lanes alias column 0's chunk: they must not write it back
+        if (p.store) Chunk<T>::round_store2(d0, d1, x, v0, v1);
         const float4 ua = *reinterpret_cast<const float4*>(us + gl * 8);
         const float4 ub = *reinterpret_cast<const float4*>(us + gl * 8 + 4);
         const float uu[8] = {ua.x, ua.y, ua.z, ua.w, ub.x, ub.y, ub.z, ub.w};

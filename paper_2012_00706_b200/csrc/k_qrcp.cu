@@ -219,26 +219,31 @@ __global__ void __launch_bounds__(1024) k_init_pivot(const double* __restrict__ 
 template <typename T>
 __global__ void k_swap(T* __restrict__ S, int64_t ngroups, int n, int jn, int j0,
                        float* __restrict__ F, float* __restrict__ R, int* __restrict__ perm,
-                       const DevScalars* __restrict__ sc) {
+                       T* __restrict__ Sj, const DevScalars* __restrict__ sc) {
   if (sc->done) return;
   const int p = sc->pivot;
-  if (p == jn || p < 0) return;
+  if (p < 0) return;
+  const bool sw = p != jn;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g < ngroups) {
-    if (sizeof(T) == 2) {
-      uint4* a = reinterpret_cast<uint4*>(S + (g * n + jn) * RG);
-      uint4* b = reinterpret_cast<uint4*>(S + (g * n + p) * RG);
-      const uint4 ta = *a, tb = *b;
-      *a = tb;
-      *b = ta;
-    } else {
-      uint4* a = reinterpret_cast<uint4*>(S + (g * n + jn) * RG);
-      uint4* b = reinterpret_cast<uint4*>(S + (g * n + p) * RG);
-      const uint4 ta0 = a[0], ta1 = a[1], tb0 = b[0], tb1 = b[1];
-      a[0] = tb0; a[1] = tb1;
-      b[0] = ta0; b[1] = ta1;
+    // the new pivot column jn, also copied to the contiguous buffer Sj (tcgen05 pass)
+    constexpr int W = (int)sizeof(T) / 2;   // uint4 words per 8-row chunk
+    uint4* a = reinterpret_cast<uint4*>(S + (g * n + jn) * RG);
+    uint4* b = reinterpret_cast<uint4*>(S + (g * n + p) * RG);
+    uint4 ta[W], tb[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) { ta[w] = a[w]; tb[w] = sw ? b[w] : ta[w]; }
+    if (sw) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) { a[w] = tb[w]; b[w] = ta[w]; }
+    }
+    if (Sj) {
+      uint4* d = reinterpret_cast<uint4*>(Sj + g * RG);
+#pragma unroll
+      for (int w = 0; w < W; ++w) d[w] = tb[w];
     }
   }
+  if (!sw) return;
   if (blockIdx.x == 0) {
     for (int t = j0 + threadIdx.x; t < jn; t += blockDim.x) {
       float* f = F + (int64_t)(t % NSLOT) * n;
@@ -283,13 +288,13 @@ cudaError_t launch_init_pivot(const double* norms, int n, int* perm, DevScalars*
 }
 
 cudaError_t launch_swap(int fmt, void* S, int64_t ngroups, int n, int jn, int j0, int steps_done,
-                        float* F, float* R, int* perm, DevScalars* sc, cudaStream_t st) {
+                        float* F, float* R, int* perm, void* Sj, DevScalars* sc, cudaStream_t st) {
   (void)steps_done;
   const unsigned nb = (unsigned)((ngroups + 255) / 256);
   if (fmt == 1)
-    k_swap<__half><<<nb, 256, 0, st>>>((__half*)S, ngroups, n, jn, j0, F, R, perm, sc);
+    k_swap<__half><<<nb, 256, 0, st>>>((__half*)S, ngroups, n, jn, j0, F, R, perm, (__half*)Sj, sc);
   else
-    k_swap<float><<<nb, 256, 0, st>>>((float*)S, ngroups, n, jn, j0, F, R, perm, sc);
+    k_swap<float><<<nb, 256, 0, st>>>((float*)S, ngroups, n, jn, j0, F, R, perm, (float*)Sj, sc);
   return cudaGetLastError();
 }
 

@@ -56,7 +56,7 @@ constexpr int NCCL_SUM = 0, NCCL_MAX = 2;
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t AD, S, U, F, R, part, red, xr, norms, perm, scal3, sc, maxpart, rpart;
+  size_t AD, S, U, F, Vh, Vl, Sj, R, part, red, xr, norms, perm, scal3, sc, maxpart, rpart;
   size_t AI, Q1, G1, G2, W, tpart, Rd, T, Pw, epart, Ik, Rinv, misc;
   size_t total;
 };
@@ -103,6 +103,9 @@ Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
   (void)sbytes;
   L.U = take((size_t)NSLOT * mp * 4);
   L.F = take((size_t)NSLOT * n * 4);
+  L.Vh = take((size_t)(mp + 128) * NB_MAX * 4);   // tcgen05 pass: panel V operand (hi / lo)
+  L.Vl = take((size_t)(mp + 128) * NB_MAX * 4);
+  L.Sj = take((size_t)(mp + 128) * 4);             // the pivot column of S, contiguous
   L.R = take((size_t)k * n * 4);
   L.part = take((size_t)pass_gx_cap() * 2 * n * 8);
   L.red = take((size_t)3 * n * 8);
@@ -150,7 +153,10 @@ struct mpid_ctx {
   bool host_AD = false;
   // device pointers
   void* S = nullptr;
-  float *U = nullptr, *F = nullptr, *R = nullptr;
+  float *U = nullptr, *F = nullptr, *R = nullptr, *Vh = nullptr, *Vl = nullptr;
+  void* Sj = nullptr;
+  alignas(64) unsigned char tmapS[2][128];   // CUtensorMap of S for fp16 / fp32 (tcgen05 pass)
+  int tmap_ok[2] = {-1, -1};
   double *part = nullptr, *red = nullptr, *xr = nullptr, *norms = nullptr, *beta = nullptr,
          *cvec = nullptr, *tau = nullptr, *maxpart = nullptr, *rpart = nullptr;
   int* perm = nullptr;
@@ -269,6 +275,11 @@ id_status id_create(id_handle* hp, const double* A_D, int64_t m_global, int64_t 
   h->S = w + L.S;
   h->U = (float*)(w + L.U);
   h->F = (float*)(w + L.F);
+  h->Vh = (float*)(w + L.Vh);
+  h->Vl = (float*)(w + L.Vl);
+  h->Sj = w + L.Sj;
+  h->tmap_ok[0] = encode_tmap_S(h->tmapS[0], h->S, 1, h->m_pad / 8, (int)n);
+  h->tmap_ok[1] = encode_tmap_S(h->tmapS[1], h->S, 2, h->m_pad / 8, (int)n);
   h->R = (float*)(w + L.R);
   h->part = (double*)(w + L.part);
   h->red = (double*)(w + L.red);
@@ -321,6 +332,9 @@ id_status id_create(id_handle* hp, const double* A_D, int64_t m_global, int64_t 
   }
   // zero U (padding rows must stay 0); S is fully written by the rounding kernel
   cudaMemsetAsync(h->U, 0, (size_t)NSLOT * h->m_pad * 4, h->st);
+  // the V operand's unused K columns are multiplied by zero F entries: keep them finite
+  cudaMemsetAsync(h->Vh, 0, (size_t)(h->m_pad + 128) * NB_MAX * 4, h->st);
+  cudaMemsetAsync(h->Vl, 0, (size_t)(h->m_pad + 128) * NB_MAX * 4, h->st);
   *hp = h;
   return ID_OK;
 }
@@ -428,7 +442,7 @@ static id_status enqueue_round(mpid_ctx* h, int fmt, int scaling, double eps) {
 }
 
 static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, double eps, int nb,
-                              bool profile) {
+                              int formation, bool profile) {
   const int64_t n = h->n;
   h->kernel_launches = 0;
   h->pass_launches = 0;
@@ -444,7 +458,8 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     const int j0 = j == 0 ? 0 : nb * ((j - 1) / nb);
     const int npend = j - j0;
     const int store = (npend == nb) ? 1 : 0;
-    CK(launch_swap(fmt, h->S, h->m_pad / 8, (int)n, j, j0, j, h->F, h->R, h->perm, h->sc, h->st));
+    CK(launch_swap(fmt, h->S, h->m_pad / 8, (int)n, j, j0, j, h->F, h->R, h->perm,
+                   formation == 2 ? h->Sj : nullptr, h->sc, h->st));
     PassParams p{};
     p.S = h->S;
     p.ngroups = h->m_pad / 8;
@@ -466,7 +481,21 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     p.sc = h->sc;
     int gx_used = 0;
     if (profile) CK(rec(h, h->pass_ev[2 * j]));
-    CK(launch_pass_tma(fmt, p, pass_gx_cap(), &gx_used, h->st));
+    if (formation == 2) {
+      p.Vh = h->Vh;
+      p.Vl = h->Vl;
+      p.nbw = (nb + 7) & ~7;
+      if (npend > 0) {   // the newest pending reflector t = j - 1 joins the panel's V operand
+        CK(launch_vop(h->U, h->m_pad, h->m_local, h->row_offset, j - 1, j - 1 - j0, h->cvec, h->Vh, h->Vl,
+                      p.nbw, h->sc, h->st));
+        h->kernel_launches += 1;
+      }
+      p.Sj = h->Sj;
+      if (h->tmap_ok[fmt - 1] != 0)
+        return fail(h, ID_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", h->tmap_ok[fmt - 1]);
+      CK(launch_pass_tc(fmt, p, h->tmapS[fmt - 1], pass_gx_cap(), &gx_used, h->st));
+    }
+    else CK(launch_pass_tma(fmt, p, pass_gx_cap(), &gx_used, h->st));
     if (gx_used < 1 || gx_used > pass_gx_cap())
       return fail(h, ID_ERR_STATE, "panel pass grid %d exceeds the partials buffer (%d)", gx_used, pass_gx_cap());
     if (profile) CK(rec(h, h->pass_ev[2 * j + 1]));
@@ -514,8 +543,14 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
     return fail(h, ID_ERR_DIM, "k_max=%d outside [1, min(m, n)]", k_max);
   if (k_max > h->k_cap) return fail(h, ID_ERR_DIM, "workspace too small for k_max=%d (cap %lld)", k_max,
                                     (long long)h->k_cap);
-  int nb = opts && opts->nb > 0 ? opts->nb : 4;
-  if (nb > NB_MAX) return fail(h, ID_ERR_ARG, "nb=%d > %d", nb, NB_MAX);
+  // formation of the pending trailing update: 1 = CUDA-core FFMA pass (bit-identical to the
+  // oracle's sequential FMA model; the faster one on C4), 2 = tcgen05 pass
+  int formation = opts ? opts->formation : 0;
+  if (formation == 0) formation = 1;
+  if (formation != 1 && formation != 2) return fail(h, ID_ERR_ARG, "bad formation %d", formation);
+  int nb = opts && opts->nb > 0 ? opts->nb : (formation == 2 ? 16 : 4);
+  if (nb > NB_MAX || (formation == 1 && nb > 16))
+    return fail(h, ID_ERR_ARG, "nb=%d too large for formation %d", nb, formation);
   const bool use_graph = !(opts && opts->use_graph < 0);
   const bool profile = opts && opts->profile_pass;
   h->have_qr = h->have_coef = false;
@@ -527,13 +562,13 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   if (use_graph) {
     uint64_t eb;
     memcpy(&eb, &eps, 8);
-    auto key = std::make_tuple((int)fmt, (int)scaling, (int)k_max, nb, eb, profile ? 1 : 0);
+    auto key = std::make_tuple((int)fmt, (int)scaling, (int)k_max, nb * 4 + formation, eb, profile ? 1 : 0);
     auto it = h->graphs.find(key);
     if (it == h->graphs.end()) {
       cudaGraph_t g;
       h->st = h->cap;  // capture on the internal stream (the caller's may be the legacy stream)
       CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
-      id_status s = enqueue_qrcp(h, fmt, scaling, k_max, eps, nb, profile);
+      id_status s = enqueue_qrcp(h, fmt, scaling, k_max, eps, nb, formation, profile);
       cudaError_t e = cudaStreamEndCapture(h->cap, &g);
       h->st = h->user_st;
       if (s) return s;
@@ -552,7 +587,7 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
     CK(cudaStreamWaitEvent(h->user_st, h->join_ev, 0));
     h->stats.kernel_launches = h->graph_launches[key];
   } else {
-    id_status s = enqueue_qrcp(h, fmt, scaling, k_max, eps, nb, profile);
+    id_status s = enqueue_qrcp(h, fmt, scaling, k_max, eps, nb, formation, profile);
     if (s) return s;
     h->stats.kernel_launches = h->kernel_launches;
   }
@@ -589,6 +624,7 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   h->stats.resid_est = sqrt(std::max(0.0, sc.resid2));
   h->stats.k_out = sc.k_out;
   h->stats.nb = nb;
+  h->stats.formation = formation;
   h->stats.status_qrcp = sc.status;
   if (sc.overflow || sc.status == ID_ERR_OVERFLOW)
     return fail(h, ID_ERR_OVERFLOW, "A_L overflows the low format after scaling (S:53)");

@@ -17,7 +17,7 @@ namespace mpid {
 // one row group reads 512 B (fp16) / 1 KB (fp32) contiguous bytes.
 // ---------------------------------------------------------------------------
 constexpr int RG = 8;                  // rows per group
-constexpr int NB_MAX = 16;             // max store interval (pending reflectors)
+constexpr int NB_MAX = 32;             // max store interval (pending reflectors; 16 for the FFMA pass)
 constexpr int NSLOT = NB_MAX + 1;      // cyclic slots for u / f vectors
 constexpr int PASS_THREADS = 256;      // 8 warps
 constexpr int PASS_WARPS = PASS_THREADS / 32;
@@ -57,6 +57,10 @@ struct PassParams {
   int nst;                 // pipeline depth (set by the launcher)
   int gx_used;             // gridDim.x (set by the launcher)
   int cw, wr;              // consumer warps: column-warps x row-split warps (launcher)
+  const float* Vh;         // tcgen05 pass: the panel's V operand (hi / lo tf32), K-major
+  const float* Vl;         //   core-matrix layout, nbw columns, (m_pad + 128) rows
+  int nbw;                 // K width of the operand layouts (nb rounded up to 8)
+  const void* Sj;          // tcgen05 pass: the pivot column j of S, contiguous (m_pad rows)
   float* U;                // [NSLOT][m_pad] raw u vectors
   const float* F;          // [NSLOT][n]   f vectors (current column order)
   const double* cvec;      // [k_max] c_t = 1/(u_t - beta_t) per step
@@ -128,13 +132,18 @@ cudaError_t launch_round(int fmt, const double* A, int64_t m, int64_t m_pad, int
 cudaError_t launch_init_pivot(const double* norms, int n, int* perm, DevScalars* sc,
                               cudaStream_t st);
 cudaError_t launch_pass_tma(int fmt, PassParams p, int num_sms, int* gx_out, cudaStream_t st);
+cudaError_t launch_pass_tc(int fmt, PassParams p, const void* tmap, int max_ctas, int* gx_out, cudaStream_t st);
+// 3-D tensor map of the stored matrix S ([ngroups][n][8] elements) for the tcgen05 pass
+int encode_tmap_S(void* tmap_out, void* S, int fmt, int64_t ngroups, int n);
+cudaError_t launch_vop(const float* U, int64_t m_pad, int64_t m_local, int64_t row_offset, int t, int k,
+                       const double* cvec, float* Vh, float* Vl, int nbw, const DevScalars* sc, cudaStream_t st);
 cudaError_t launch_pass_reduce(const double* part, int gx, int n, int j, const double* xr,
                                int own_row, double* red, const DevScalars* sc, cudaStream_t st);
 cudaError_t launch_reflector(const double* red, int n, int j, int k_max, int nslot_f, float* F,
                              float* R, double* beta, double* cvec, double* tau, const int* perm,
                              DevScalars* sc, cudaStream_t st);
 cudaError_t launch_swap(int fmt, void* S, int64_t ngroups, int n, int jn, int j0, int steps_done,
-                        float* F, float* R, int* perm, DevScalars* sc, cudaStream_t st);
+                        float* F, float* R, int* perm, void* Sj, DevScalars* sc, cudaStream_t st);
 cudaError_t launch_export_S(int fmt, const void* S, int64_t m_local, int n, void* out, int64_t ld,
                             cudaStream_t st);
 

@@ -45,7 +45,7 @@ class IDError(RuntimeError):
 
 class QRCPOpts(C.Structure):
     _fields_ = [("nb", C.c_int32), ("use_graph", C.c_int32), ("profile_pass", C.c_int32),
-                ("reserved", C.c_int32 * 5)]
+                ("formation", C.c_int32), ("reserved", C.c_int32 * 4)]
 
 
 class Stats(C.Structure):
@@ -53,7 +53,8 @@ class Stats(C.Structure):
                 ("resid_est", C.c_double), ("t_round_ms", C.c_double), ("t_qrcp_ms", C.c_double),
                 ("t_coef_ms", C.c_double), ("t_err_ms", C.c_double), ("t_pass_ms", C.c_double),
                 ("pass_launches", C.c_int64), ("kernel_launches", C.c_int64), ("k_out", C.c_int32),
-                ("nb", C.c_int32), ("status_qrcp", C.c_int32), ("reserved", C.c_int32 * 5)]
+                ("nb", C.c_int32), ("status_qrcp", C.c_int32), ("formation", C.c_int32),
+                ("reserved", C.c_int32 * 4)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
@@ -235,8 +236,11 @@ class MPID:
         return rc
 
     def qrcp(self, fmt="fp16", scaling="pow2", k=None, eps=0.0, nb=0, use_graph=True,
-             profile=False, allow_underflow=False) -> QRCPOut:
-        o = QRCPOpts(nb=nb, use_graph=1 if use_graph else -1, profile_pass=1 if profile else 0)
+             profile=False, allow_underflow=False, formation=0) -> QRCPOut:
+        """formation: 0 auto, 1 / "ffma" CUDA-core FFMA, 2 / "tc" tcgen05 (include/mpid.h)."""
+        formation = {"auto": 0, "ffma": 1, "tc": 2}.get(formation, formation)
+        o = QRCPOpts(nb=nb, use_graph=1 if use_graph else -1, profile_pass=1 if profile else 0,
+                     formation=formation)
         k = self.k_max if k is None else k
         rc, kout, piv = id_qrcp_lowprec(self.h, FMT[fmt] if isinstance(fmt, str) else fmt,
                                         SCALING[scaling] if isinstance(scaling, str) else scaling,

@@ -8,12 +8,12 @@ from oracle.qrcp import QRCPResult, certified_steps, make_AL, qrcp_householder
 _ORACLE = {}
 
 
-def oracle_qrcp(key, A, fmt, scaling, k, nb, eps=0.0):
+def oracle_qrcp(key, A, fmt, scaling, k, nb, eps=0.0, formation="fma"):
     """Cached oracle QRCP of fl(s A).  A fixed-rank run's first k steps do not depend
     on k_max, so a cached longer run is truncated: the result's perm[:k], top2[:k],
     resid[:k+1] are exact; R/V are the first k rows/columns (R's trailing columns are
     in the longer run's order)."""
-    ck = (key, fmt, scaling, nb, eps)
+    ck = (key, fmt, scaling, nb, eps, formation)
     hit = _ORACLE.get(ck)
     if hit is not None and (hit.k_out == k or (eps == 0.0 and hit.k_out > k and hit.status == "ok")):
         if hit.k_out == k:
@@ -21,7 +21,7 @@ def oracle_qrcp(key, A, fmt, scaling, k, nb, eps=0.0):
         return QRCPResult(hit.perm.copy(), hit.R[:k], k, hit.status, hit.V[:, :k], hit.tau[:k],
                           hit.top2[:k], hit.maxnorm0, hit.normAL, hit.resid[:k + 1])
     AL, _ = make_AL(A, fmt, scaling)
-    r = qrcp_householder(AL, k, fmt, nb=nb, eps=eps)
+    r = qrcp_householder(AL, k, fmt, nb=nb, eps=eps, formation=formation)
     if hit is None or r.k_out > hit.k_out:
         _ORACLE[ck] = r
     return r
@@ -34,7 +34,8 @@ def to_dev(A: np.ndarray):
 
 
 def run_gpu(A: np.ndarray, fmt: str, scaling: str, k: int, nb: int = 4, eps: float = 0.0,
-            mode: str = "lsq", use_graph: bool = True, allow_underflow=False, host=False):
+            mode: str = "lsq", use_graph: bool = True, allow_underflow=False, host=False,
+            formation: str = "ffma"):
     from paper_2012_00706_b200.mpid import MPID
     import torch
     if host:
@@ -42,7 +43,8 @@ def run_gpu(A: np.ndarray, fmt: str, scaling: str, k: int, nb: int = 4, eps: flo
     else:
         At = to_dev(A)
     h = MPID(At, k_max=k)
-    q = h.qrcp(fmt, scaling, k=k, eps=eps, nb=nb, use_graph=use_graph, allow_underflow=allow_underflow)
+    q = h.qrcp(fmt, scaling, k=k, eps=eps, nb=nb, use_graph=use_graph, allow_underflow=allow_underflow,
+               formation=formation)
     out = {"k": q.k, "piv": q.piv, "status": q.status}
     if q.k > 0 and q.status == 0:
         out["R"] = h.get_R().cpu().numpy().astype(np.float64)

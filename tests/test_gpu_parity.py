@@ -91,10 +91,12 @@ def test_underflow_status():
     assert out["status"] == 4 and out["k"] == 0
 
 
-def _compare(A, fmt, scaling, k, nb, min_prefix_frac=0.0, eps=0.0, key=None):
-    out = run_gpu(A, fmt, scaling, k, nb=nb, eps=eps)
+def _compare(A, fmt, scaling, k, nb, min_prefix_frac=0.0, eps=0.0, key=None, formation="ffma"):
+    out = run_gpu(A, fmt, scaling, k, nb=nb, eps=eps, formation=formation)
     AL, s = make_AL(A, fmt, scaling)
-    r = oracle_qrcp(key, A, fmt, scaling, k, nb, eps) if key else qrcp_householder(AL, k, fmt, nb=nb, eps=eps)
+    oform = "tc" if formation == "tc" else "fma"
+    r = (oracle_qrcp(key, A, fmt, scaling, k, nb, eps, formation=oform) if key
+         else qrcp_householder(AL, k, fmt, nb=nb, eps=eps, formation=oform))
     agree, first_unc = prefix_match(out["piv"], r)
     assert out["piv"][0] == int(np.argmax(np.linalg.norm(AL, axis=0)))
     assert agree >= first_unc, (agree, first_unc, out["piv"][:10], r.perm[:10])
@@ -134,6 +136,53 @@ def test_planted_pivot_set(fmt, nb):
     out, r, agree, fu = _compare(A, fmt, "pow2" if fmt == "fp16" else "none", 64, nb)
     assert sorted(out["piv"]) == sorted(skel)
     assert np.array_equal(out["piv"], skel)
+
+
+# ---- the tcgen05 formation (R14): 3xTF32 tensor-core product in TMEM --------
+@pytest.mark.parametrize("fmt,scaling,nb", [("fp16", "pow2", 8), ("fp16", "pow2", 16), ("fp16", "pow2", 32),
+                                            ("fp32", "none", 8), ("fp16", "pow2", 1)])
+def test_C1_parity_tcgen05(fmt, scaling, nb):
+    out, r, agree, fu = _compare(cfg("C1"), fmt, scaling, 32, nb, formation="tc")
+    assert out["stats"]["formation"] == 2
+
+
+@pytest.mark.parametrize("k", [128, 64])
+def test_C2_parity_tcgen05(k):
+    _compare(cfg("C2"), "fp16", "maxabs", k, 16, key="C2tc", formation="tc")
+
+
+def test_planted_pivot_set_tcgen05():
+    A, skel, C = gen_planted(4096, 512, 64, rho=1.05, eta=1e-9, seed=3)
+    out, r, agree, fu = _compare(A, "fp16", "pow2", 64, 16, formation="tc")
+    assert np.array_equal(out["piv"], skel)
+
+
+def test_tcgen05_R_close_to_oracle():
+    """R rows agree with the oracle's tc model to the 3xTF32 product accuracy (~2^-21)."""
+    A = cfg("C1")
+    out = run_gpu(A, "fp16", "pow2", 32, nb=16, formation="tc")
+    AL, _ = make_AL(A, "fp16", "pow2")
+    r = qrcp_householder(AL, 32, "fp16", nb=16, formation="tc")
+    assert np.array_equal(out["piv"], r.perm[:32])
+    assert np.abs(out["R"][:, :32] - r.R[:, :32]).max() <= 1e-5 * r.maxnorm0
+
+
+@pytest.mark.parametrize("n,fmt,nb", [(1030, "fp32", 2), (1030, "fp16", 4), (2048, "fp32", 4)])
+def test_column_split_store_steps_bit_identical(n, fmt, nb):
+    """n > 1024: the pass splits the columns over two CTAs; on store steps no lane may
+    write another column's chunk (regression: invalid lanes aliased a CTA's first column)."""
+    rng = np.random.default_rng(5)
+    from synth.generators import haar
+    U = haar(rng, 4096, 300)
+    V = haar(rng, n, 300)
+    A = np.asfortranarray((U * np.exp(-np.arange(1, 301) / 30.0)) @ V.T)
+    sc = "pow2" if fmt == "fp16" else "none"
+    out = run_gpu(A, fmt, sc, 40, nb=nb)
+    AL, _ = make_AL(A, fmt, sc)
+    r = qrcp_householder(AL, 40, fmt, nb=nb)
+    assert np.array_equal(out["piv"], r.perm[:40])
+    assert np.array_equal(out["perm"], r.perm)
+    assert np.array_equal(out["R"], r.R)                 # same operation order: bit-identical
 
 
 def test_exact_rank_zero_error():
