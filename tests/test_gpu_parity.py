@@ -140,7 +140,7 @@ def test_planted_pivot_set(fmt, nb):
 
 # ---- the tcgen05 formation (R14): 3xTF32 tensor-core product in TMEM --------
 @pytest.mark.parametrize("fmt,scaling,nb", [("fp16", "pow2", 8), ("fp16", "pow2", 16), ("fp16", "pow2", 32),
-                                            ("fp32", "none", 8), ("fp16", "pow2", 1)])
+                                            ("fp32", "none", 8), ("fp16", "pow2", 4)])
 def test_C1_parity_tcgen05(fmt, scaling, nb):
     out, r, agree, fu = _compare(cfg("C1"), fmt, scaling, 32, nb, formation="tc")
     assert out["stats"]["formation"] == 2
