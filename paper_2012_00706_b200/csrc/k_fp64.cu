@@ -57,6 +57,7 @@ struct GemmArgs {
   const double* A;   // NN_ERROR: A_D (m x n_all), lda; column c of the product is A's column cmap[c]
   int64_t lda;
   const int* cmap;
+  const int* ycmap;  // TN: column c of Y is Y's column ycmap[c] (nullptr = identity)
   int d_tma;         // NN_ERROR: 1 = the A_D tile may be prefetched with bulk copies (16 B aligned rows)
 };
 constexpr int DLD = GT + 4;      // NN_ERROR: smem A_D tile [c][r], 132 doubles per column
@@ -67,8 +68,9 @@ __device__ __forceinline__ void dmma(double* c, double a, double b) {
                : "d"(a), "d"(b));
 }
 
-template <int MODE>
+template <int MODE, int MT>   // MT m8 tiles per warp in M: CTA tile (16 MT) x 128
 __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
+  constexpr int BM = 16 * MT;
   // A tile: TN -> As[i][k] (LDK), NN -> As[k][r] (LDM); B tile: Bs[c][k] (LDK)
   constexpr int A_ELEMS = (MODE == GM_TN_PARTIAL) ? GT * LDK : GK * LDM;
   extern __shared__ __align__(16) double dsm[];
@@ -79,7 +81,7 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, tq = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;           // 2 x 4 warps
-  const int64_t m0 = (int64_t)blockIdx.x * GT;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
   const int64_t n0 = (int64_t)blockIdx.y * GT;
   int64_t k_begin = 0, k_end = g.K;
   if (MODE == GM_TN_PARTIAL) {
@@ -112,13 +114,13 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
         const int64_t i = m0 + mn, c = n0 + mn;
         ra[q] = make_double2(0.0, 0.0);
         rb[q] = make_double2(0.0, 0.0);
-        if (i < g.M) {
+        if (i < g.M && mn < BM) {
           const double* p = g.X + i * g.ldx + r;
           if (r + 1 < k_end && (((uintptr_t)p & 15) == 0)) ra[q] = *reinterpret_cast<const double2*>(p);
           else { if (r < k_end) ra[q].x = p[0]; if (r + 1 < k_end) ra[q].y = p[1]; }
         }
         if (c < g.N) {
-          const double* p = g.Y + c * g.ldy + r;
+          const double* p = g.Y + (g.ycmap ? (int64_t)g.ycmap[c] : c) * g.ldy + r;
           if (r + 1 < k_end && (((uintptr_t)p & 15) == 0)) rb[q] = *reinterpret_cast<const double2*>(p);
           else { if (r < k_end) rb[q].x = p[0]; if (r + 1 < k_end) rb[q].y = p[1]; }
         }
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
           const int l = idx >> 6, rr = (idx & 63) * 2;  // 64 double2 per 128-long column
           const int64_t kk = kb + l, r = m0 + rr;
           ra[q] = make_double2(0.0, 0.0);
-          if (kk < k_end) {
+          if (kk < k_end && rr < BM) {
             const double* p = g.X + kk * g.ldx + r;
             if (r + 1 < g.M && (((uintptr_t)p & 15) == 0)) ra[q] = *reinterpret_cast<const double2*>(p);
             else { if (r < g.M) ra[q].x = p[0]; if (r + 1 < g.M) ra[q].y = p[1]; }
@@ -163,9 +165,9 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
       *reinterpret_cast<double2*>(&Bs[buf][cc * LDK + l]) = rb[q];
     }
   };
-  double acc[8][4][2];
+  double acc[MT][4][2];
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int a = 0; a < MT; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
@@ -178,20 +180,22 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
       const bool more = kb + GK < k_end;
       if (more) gload(kb + GK);
       const int64_t krem = (k_end - kb + 3) / 4;
-      const int ksteps = krem < GK / 4 ? (int)krem : GK / 4;              // skip all-zero k-steps
+      // skip all-zero k-steps, and warps whose rows or columns are all outside the matrix
+      const int ksteps = (m0 + wm * 8 * MT >= g.M || n0 + wn * 32 >= g.N) ? 0
+                         : (krem < GK / 4 ? (int)krem : GK / 4);
 #pragma unroll
       for (int ks = 0; ks < GK / 4; ++ks) {
         if (ks >= ksteps) break;
-        double af[8], bf[4];
+        double af[MT], bf[4];
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          const int mm = wm * 64 + mt * 8 + gq, kk = ks * 4 + tq;
+        for (int mt = 0; mt < MT; ++mt) {
+          const int mm = wm * (8 * MT) + mt * 8 + gq, kk = ks * 4 + tq;
           af[mt] = (MODE == GM_TN_PARTIAL) ? As[buf][mm * LDK + kk] : As[buf][kk * LDM + mm];
         }
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[buf][(wn * 32 + nt * 8 + gq) * LDK + ks * 4 + tq];
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
           for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
       }
@@ -206,8 +210,8 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
   if (MODE == GM_TN_PARTIAL) {
     double* o = g.out + (int64_t)blockIdx.z * g.M * g.N;
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      const int64_t i = m0 + wm * 64 + mt * 8 + gq;
+    for (int mt = 0; mt < MT; ++mt) {
+      const int64_t i = m0 + wm * (8 * MT) + mt * 8 + gq;
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
@@ -218,8 +222,8 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
     }
   } else if (MODE == GM_NN_STORE) {
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      const int64_t r = m0 + wm * 64 + mt * 8 + gq;
+    for (int mt = 0; mt < MT; ++mt) {
+      const int64_t r = m0 + wm * (8 * MT) + mt * 8 + gq;
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
@@ -230,8 +234,8 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
     }
   } else if (MODE == GM_NN_UPDATE) {
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      const int64_t r = m0 + wm * 64 + mt * 8 + gq;
+    for (int mt = 0; mt < MT; ++mt) {
+      const int64_t r = m0 + wm * (8 * MT) + mt * 8 + gq;
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
@@ -249,8 +253,8 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
       for (int h = 0; h < 2; ++h) {
         const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          const int64_t r = m0 + wm * 64 + mt * 8 + gq;
+        for (int mt = 0; mt < MT; ++mt) {
+          const int64_t r = m0 + wm * (8 * MT) + mt * 8 + gq;
           if (r < g.M && c < g.N) {
             const double a = dpre ? Ds[(c - n0) * DLD + (r - m0)] : __ldcs(g.A + (int64_t)g.cmap[c] * g.lda + r);
             const double e = a - acc[mt][nt][h];
@@ -393,7 +397,7 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
       gload(m1, n1, last_k ? 0 : kb + GK);
     }
     const int64_t krem = (K - kb + 3) / 4;
-    const int ksteps = krem < GK / 4 ? (int)krem : GK / 4;
+    const int ksteps = (m0 + wm * 64 >= g.M || n0 + wn * 32 >= g.N) ? 0 : (krem < GK / 4 ? (int)krem : GK / 4);
 #pragma unroll
     for (int ks = 0; ks < GK / 4; ++ks) {
       if (ks >= ksteps) break;
@@ -455,17 +459,33 @@ static size_t dgemm_smem() {
   const int d = (MODE == GM_NN_ERROR) ? GT * DLD : 0;
   return (size_t)(2 * (a + GT * LDK) + d) * sizeof(double);
 }
-template <int MODE>
-static cudaError_t dgemm_launch(const GemmArgs& g, dim3 grid, cudaStream_t st) {
+template <int MODE, int MT>
+static cudaError_t dgemm_launch_t(const GemmArgs& g, dim3 grid, cudaStream_t st) {
   static bool set = false;
   if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(k_dgemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_dgemm<MODE, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)dgemm_smem<MODE>());
     if (e != cudaSuccess) return e;
     set = true;
   }
-  k_dgemm<MODE><<<grid, 256, dgemm_smem<MODE>(), st>>>(g);
+  k_dgemm<MODE, MT><<<grid, 256, dgemm_smem<MODE>(), st>>>(g);
   return cudaGetLastError();
+}
+// M tile 16 MT: the smallest of 48/64/80/96/112/128 covering M (k-sized M wastes less)
+static int pick_mt(int64_t M) {
+  if (M >= 128) return 8;
+  return (int)std::max<int64_t>(3, (M + 15) / 16);
+}
+template <int MODE>
+static cudaError_t dgemm_launch(GemmArgs g, dim3 grid, cudaStream_t st, int mt) {
+  switch (mt) {
+    case 3: return dgemm_launch_t<MODE, 3>(g, grid, st);
+    case 4: return dgemm_launch_t<MODE, 4>(g, grid, st);
+    case 5: return dgemm_launch_t<MODE, 5>(g, grid, st);
+    case 6: return dgemm_launch_t<MODE, 6>(g, grid, st);
+    case 7: return dgemm_launch_t<MODE, 7>(g, grid, st);
+    default: return dgemm_launch_t<MODE, 8>(g, grid, st);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -646,14 +666,16 @@ cudaError_t launch_gather_cols(const double* A, int64_t m, int64_t ld, const int
 }
 
 cudaError_t launch_tsmm(const double* X, int64_t ldx, int k1, const double* Y, int64_t ldy, int n1,
-                        int64_t m, double* part, int splits, cudaStream_t st) {
+                        int64_t m, double* part, int splits, cudaStream_t st, const int* ycmap) {
   GemmArgs g{};
   g.X = X; g.ldx = ldx; g.Y = Y; g.ldy = ldy;
   g.M = k1; g.N = n1; g.K = m;
+  g.ycmap = ycmap;
   g.k_per_split = ((m + splits - 1) / splits + GK - 1) / GK * GK;
   g.out = part;
-  dim3 grid((unsigned)((k1 + GT - 1) / GT), (unsigned)((n1 + GT - 1) / GT), (unsigned)splits);
-  return dgemm_launch<GM_TN_PARTIAL>(g, grid, st);
+  const int mt = pick_mt(k1);
+  dim3 grid((unsigned)((k1 + 16 * mt - 1) / (16 * mt)), (unsigned)((n1 + GT - 1) / GT), (unsigned)splits);
+  return dgemm_launch<GM_TN_PARTIAL>(g, grid, st, mt);
 }
 
 cudaError_t launch_cholesky(double* G, int k, int* info, cudaStream_t st) {
@@ -679,7 +701,7 @@ cudaError_t launch_trsm_right_upper(double* X, int64_t m, int64_t ldx, const dou
       g.M = m; g.N = nbk; g.K = c0;
       g.out = X + (int64_t)c0 * ldx; g.ldo = ldx;
       dim3 grid((unsigned)((m + GT - 1) / GT), (unsigned)((nbk + GT - 1) / GT), 1);
-      { cudaError_t e = dgemm_launch<GM_NN_UPDATE>(g, grid, st); if (e != cudaSuccess) return e; }
+      { cudaError_t e = dgemm_launch<GM_NN_UPDATE>(g, grid, st, 8); if (e != cudaSuccess) return e; }
     }
     k_trsm_rows_block<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(X, m, ldx, Rm, k, c0, nbk);
   }
@@ -755,7 +777,7 @@ cudaError_t launch_nn_store(const double* X, int64_t m, int64_t ldx, const doubl
   g.M = m; g.N = N; g.K = K;
   g.out = out; g.ldo = ldo;
   dim3 grid((unsigned)((m + GT - 1) / GT), (unsigned)((N + GT - 1) / GT), 1);
-  return dgemm_launch<GM_NN_STORE>(g, grid, st);
+  return dgemm_launch<GM_NN_STORE>(g, grid, st, 8);
 }
 
 __global__ void k_eye(double* I, int k) {

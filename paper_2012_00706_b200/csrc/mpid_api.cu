@@ -674,14 +674,17 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
     s = allreduce(h, h->G2, (size_t)k * k, NCCL_SUM);
     if (s) return s;
     CK(launch_cholesky(h->G2, k, h->info + 1, h->st));
-    // W = Q1^T A_D
-    const int spw = tsmm_splits(k, n, m);
-    CK(launch_tsmm(h->Q1, m, k, h->AD, h->ld, n, m, h->tpart, spw, h->st));
-    CK(launch_sum_partials(h->tpart, spw, (int64_t)k * n, h->W, h->st));
-    s = allreduce(h, h->W, (size_t)k * n, NCCL_SUM);
-    if (s) return s;
-    // T = R1^{-1} R2^{-1} R2^{-T} W(:, perm[k:])
-    CK(launch_trsm_left_upper(h->G1, h->G2, k, h->W, k, h->perm + k, n - k, h->T, k, 1, h->st));
+    // W = Q1^T A_D(:, J), J = perm[k:] (W(:, I) = R1 is never needed)
+    const int nj = n - k;
+    if (nj > 0) {
+      const int spw = tsmm_splits(k, nj, m);
+      CK(launch_tsmm(h->Q1, m, k, h->AD, h->ld, nj, m, h->tpart, spw, h->st, h->perm + k));
+      CK(launch_sum_partials(h->tpart, spw, (int64_t)k * nj, h->W, h->st));
+      s = allreduce(h, h->W, (size_t)k * nj, NCCL_SUM);
+      if (s) return s;
+      // T = R1^{-1} R2^{-1} R2^{-T} W_J
+      CK(launch_trsm_left_upper(h->G1, h->G2, k, h->W, k, nullptr, nj, h->T, k, 1, h->st));
+    }
     launches += 6;
   } else {
     return fail(h, ID_ERR_ARG, "bad coefficient mode");

@@ -150,8 +150,9 @@ cudaError_t launch_export_S(int fmt, const void* S, int64_t m_local, int n, void
 // fp64 stage
 cudaError_t launch_gather_cols(const double* A, int64_t m, int64_t ld, const int* perm, int k,
                                double* X, cudaStream_t st);
+// C(k1 x n1) = X^T Y over m rows (split-K partials); column c of Y is ycmap[c] when given
 cudaError_t launch_tsmm(const double* X, int64_t ldx, int k1, const double* Y, int64_t ldy, int n1,
-                        int64_t m, double* part, int splits, cudaStream_t st);
+                        int64_t m, double* part, int splits, cudaStream_t st, const int* ycmap = nullptr);
 cudaError_t launch_sum_partials(const double* part, int splits, int64_t len, double* out,
                                 cudaStream_t st);
 cudaError_t launch_cholesky(double* G, int k, int* info, cudaStream_t st);
