@@ -313,21 +313,27 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
     const int64_t rows = (g.M - m0 < GT) ? g.M - m0 : (int64_t)GT;
     return g.d_tma && (rows % 2 == 0);
   };
-  auto issue_d = [&](int64_t m0, int64_t n0) {   // warp 0: each lane issues 4 of the 128 column copies
-    const int64_t rows = (g.M - m0 < GT) ? g.M - m0 : (int64_t)GT;
-    const int cols = (int)((g.N - n0 < GT) ? g.N - n0 : (int64_t)GT);
-    int src[GT / 32];
+  // warp 0 issues the A_D block copies of a tile: each lane 4 of the 128 column copies.
+  // The column map of the NEXT tile is loaded right after (src_next), so the copies
+  // never wait on a dependent global load at a tile boundary.
+  int src_next[GT / 32];
+  auto load_src = [&](int64_t n0) {
 #pragma unroll
     for (int q = 0; q < GT / 32; ++q) {
-      const int c = lane + 32 * q;
-      src[q] = c < cols ? g.cmap[n0 + c] : 0;
+      const int64_t c = n0 + lane + 32 * q;
+      src_next[q] = c < g.N ? g.cmap[c] : 0;
     }
+  };
+  auto issue_d = [&](int64_t m0, int64_t n0) {
+    const int64_t rows = (g.M - m0 < GT) ? g.M - m0 : (int64_t)GT;
+    const int cols = (int)((g.N - n0 < GT) ? g.N - n0 : (int64_t)GT);
     if (lane == 0) mbar_expect_tx(&dbar, (uint32_t)(rows * cols * 8));
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < GT / 32; ++q) {
       const int c = lane + 32 * q;
-      if (c < cols) tma_load(Ds + c * DLD, g.A + (int64_t)src[q] * g.lda + m0, (uint32_t)(rows * 8), &dbar);
+      if (c < cols)
+        tma_load(Ds + c * DLD, g.A + (int64_t)src_next[q] * g.lda + m0, (uint32_t)(rows * 8), &dbar);
     }
   };
   double2 ra[4], rb[4];
@@ -377,7 +383,15 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
   if (total > 0) {
     int64_t m0, n0;
     tile_of(0, m0, n0);
-    if (warp == 0 && d_ok(m0)) issue_d(m0, n0);
+    if (warp == 0) {
+      load_src(n0);
+      if (d_ok(m0)) issue_d(m0, n0);
+      if (my_tiles > 1) {
+        int64_t m1, n1;
+        tile_of(1, m1, n1);
+        load_src(n1);
+      }
+    }
     gload(m0, n0, 0);
     sstore(0);
     __syncthreads();
@@ -388,7 +402,14 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
   if (total > 0) tile_of(0, m0, n0);
   for (int64_t it = 0; it < total; ++it) {
     const int64_t kb = (int64_t)ks_i * GK;
-    if (ks_i == 0 && it > 0 && warp == 0 && d_ok(m0)) issue_d(m0, n0);  // this tile's A_D block
+    if (ks_i == 0 && it > 0 && warp == 0) {                // this tile's A_D block, next tile's map
+      if (d_ok(m0)) issue_d(m0, n0);
+      if (lt + 1 < my_tiles) {
+        int64_t m2, n2;
+        tile_of(lt + 1, m2, n2);
+        load_src(n2);
+      }
+    }
     const bool more = it + 1 < total;
     const bool last_k = ks_i == nks - 1;
     if (more) {
