@@ -28,12 +28,12 @@ __global__ void k_gather_cols(const double* __restrict__ A, int64_t m, int64_t l
 
 // ---------------------------------------------------------------------------
 // fp64 tensor-core GEMM core (DMMA: mma.sync.aligned.m8n8k4.row.col.f64).
-// CTA tile 128 x 128, 8 warps as 2 (M) x 4 (N), warp tile 64 x 32 = 8 x 4 MMA
-// tiles, K staged 16 at a time through double-buffered shared memory
+// CTA tile (16 MT) x 128, 8 warps as 2 (M) x 4 (N), warp tile 8 MT x 32 = MT x 4
+// MMA tiles, K staged 16 at a time through double-buffered shared memory
 // (register-staged 16 B global loads, coalesced along the contiguous dimension).
 //   GM_TN_PARTIAL: out[split][c][i] = sum_{r in split} X(r, i) Y(r, c)   (X m x M, Y m x N)
-//   GM_NN_ERROR:   out[block]       = sum (A(r, c) - sum_l X(r, l) B(l, c))^2
-//   GM_NN_UPDATE:  out(r, c)       -= sum_l X(r, l) B(l, c)               (TRSM update)
+//   GM_NN_STORE:   out(r, c)        = sum_l X(r, l) B(l, c)               (Q1 = A_I R1^-1)
+// The fused error is its own persistent kernel (k_err_persist, below).
 // Fragments of m8n8k4 f64 (PTX ISA): A(g, t), B(t, g), C(g, 2t + {0,1}) with
 // g = lane >> 2, t = lane & 3.
 // ---------------------------------------------------------------------------
@@ -41,7 +41,7 @@ constexpr int GT = 128, GK = 16;
 constexpr int LDK = GK + 4;      // [mn][k] tiles: row stride 160 B -> conflict-free fragment reads
 constexpr int LDM = GT + 8;      // [k][mn] tile (NN A operand): 136 doubles -> conflict-free
 
-enum GemmMode { GM_TN_PARTIAL = 0, GM_NN_ERROR = 1, GM_NN_UPDATE = 2, GM_NN_STORE = 3 };
+enum GemmMode { GM_TN_PARTIAL = 0, GM_NN_STORE = 1 };
 
 struct GemmArgs {
   // TN: C(i, c) = sum_r X(r, i) Y(r, c), rows r in the split's range; X m x M, Y m x N
@@ -76,8 +76,6 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
   extern __shared__ __align__(16) double dsm[];
   double (*As)[A_ELEMS] = reinterpret_cast<double (*)[A_ELEMS]>(dsm);
   double (*Bs)[GT * LDK] = reinterpret_cast<double (*)[GT * LDK]>(dsm + 2 * A_ELEMS);
-  double* Ds = dsm + 2 * A_ELEMS + 2 * GT * LDK;                  // NN_ERROR: A_D tile [c][r]
-  __shared__ __align__(8) uint64_t dbar;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, tq = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;           // 2 x 4 warps
@@ -87,20 +85,6 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
   if (MODE == GM_TN_PARTIAL) {
     k_begin = (int64_t)blockIdx.z * g.k_per_split;
     k_end = min(g.K, k_begin + g.k_per_split);
-  }
-  const int64_t rows_here = (g.M - m0 < GT) ? g.M - m0 : (int64_t)GT;
-  const int64_t cols_here = (g.N - n0 < GT) ? g.N - n0 : (int64_t)GT;
-  const bool dpre = (MODE == GM_NN_ERROR) && g.d_tma && (rows_here % 2 == 0);
-  if (MODE == GM_NN_ERROR && dpre) {
-    // prefetch the A_D tile (the error epilogue's operand) with bulk copies, one per
-    // column, overlapping the HBM read with the DMMA main loop
-    if (tid == 0) {
-      mbar_init(&dbar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      mbar_expect_tx(&dbar, (uint32_t)(rows_here * cols_here * 8));
-      for (int c = 0; c < cols_here; ++c)
-        tma_load(Ds + c * DLD, g.A + (int64_t)g.cmap[n0 + c] * g.lda + m0, (uint32_t)(rows_here * 8), &dbar);
-    }
   }
   double2 ra[4], rb[4];
   // loads: 128 (mn) x 16 (k) doubles per operand = 1024 double2, 4 per thread
@@ -231,47 +215,6 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
           const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
           if (r < g.M && c < g.N) g.out[c * g.ldo + r] = acc[mt][nt][h];
         }
-    }
-  } else if (MODE == GM_NN_UPDATE) {
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      const int64_t r = m0 + wm * (8 * MT) + mt * 8 + gq;
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
-          if (r < g.M && c < g.N) g.out[c * g.ldo + r] -= acc[mt][nt][h];
-        }
-    }
-  } else {  // GM_NN_ERROR: sum (A_D - A_I P)^2 over the tile
-    if (dpre) mbar_wait(&dbar, 0);
-    double e2 = 0.0;
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const int64_t r = m0 + wm * (8 * MT) + mt * 8 + gq;
-          if (r < g.M && c < g.N) {
-            const double a = dpre ? Ds[(c - n0) * DLD + (r - m0)] : __ldcs(g.A + (int64_t)g.cmap[c] * g.lda + r);
-            const double e = a - acc[mt][nt][h];
-            e2 = fma(e, e, e2);
-          }
-        }
-      }
-    __shared__ double red[8];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) e2 += __shfl_xor_sync(0xffffffffu, e2, o);
-    if (lane == 0) red[warp] = e2;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) t += red[w];
-      g.out[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
   }
 }
@@ -438,22 +381,39 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
         mbar_wait(&dbar, dphase);
         dphase ^= 1;
       }
+      const bool fullt = dp && m0 + GT <= g.M && n0 + GT <= g.N;
+      if (fullt) {                           // fast path: compile-time smem offsets, 4 chains
+        const double* dbase = Ds + (wn * 32 + tq * 2) * DLD + wm * 64 + gq;
+        double ea[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
+        for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
+          for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int mt = 0; mt < 8; ++mt) {
-            const int64_t r = m0 + wm * 64 + mt * 8 + gq;
-            if (r < g.M && c < g.N) {
-              const double a = dp ? Ds[(c - n0) * DLD + (r - m0)] : __ldcs(g.A + (int64_t)g.cmap[c] * g.lda + r);
-              const double e = a - acc[mt][nt][h];
-              e2 = fma(e, e, e2);
+            for (int mt = 0; mt < 8; ++mt) {
+              const double e = dbase[(nt * 8 + h) * DLD + mt * 8] - acc[mt][nt][h];
+              ea[mt & 3] = fma(e, e, ea[mt & 3]);
+              acc[mt][nt][h] = 0.0;
             }
-            acc[mt][nt][h] = 0.0;
+        e2 += (ea[0] + ea[1]) + (ea[2] + ea[3]);
+      } else {
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+              const int64_t r = m0 + wm * 64 + mt * 8 + gq;
+              if (r < g.M && c < g.N) {
+                const double a = dp ? Ds[(c - n0) * DLD + (r - m0)] : __ldcs(g.A + (int64_t)g.cmap[c] * g.lda + r);
+                const double e = a - acc[mt][nt][h];
+                e2 = fma(e, e, e2);
+              }
+              acc[mt][nt][h] = 0.0;
+            }
           }
-        }
+      }
     }
     if (more) {
       sstore(buf ^ 1);
@@ -477,8 +437,7 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
 template <int MODE>
 static size_t dgemm_smem() {
   const int a = (MODE == GM_TN_PARTIAL) ? GT * LDK : GK * LDM;
-  const int d = (MODE == GM_NN_ERROR) ? GT * DLD : 0;
-  return (size_t)(2 * (a + GT * LDK) + d) * sizeof(double);
+  return (size_t)(2 * (a + GT * LDK)) * sizeof(double);
 }
 template <int MODE, int MT>
 static cudaError_t dgemm_launch_t(const GemmArgs& g, dim3 grid, cudaStream_t st) {
@@ -551,38 +510,6 @@ __global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ G, int k
     if (c < r) G[r + (int64_t)c * k] = 0.0;
   }
   if (threadIdx.x == 0) *info = bad;
-}
-
-// ---------------------------------------------------------------------------
-// In-block part of the blocked right TRSM X <- X R^{-1} (R upper k x k):
-// columns [c0, c0 + nbk) of every row, after the GEMM update with the previous
-// blocks.  One thread per row, the nbk unknowns in registers.
-// ---------------------------------------------------------------------------
-constexpr int TRSM_NB = 32;
-__global__ void __launch_bounds__(128) k_trsm_rows_block(double* __restrict__ X, int64_t m,
-                                                         int64_t ldx, const double* __restrict__ R,
-                                                         int k, int c0, int nbk) {
-  __shared__ double Rb[TRSM_NB][TRSM_NB + 1];
-  for (int i = threadIdx.x; i < TRSM_NB * TRSM_NB; i += blockDim.x) {
-    const int a = i % TRSM_NB, b = i / TRSM_NB;
-    Rb[a][b] = (a < nbk && b < nbk) ? R[(c0 + a) + (int64_t)(c0 + b) * k] : (a == b ? 1.0 : 0.0);
-  }
-  __syncthreads();
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= m) return;
-  double q[TRSM_NB];
-#pragma unroll
-  for (int c = 0; c < TRSM_NB; ++c) q[c] = c < nbk ? X[(int64_t)(c0 + c) * ldx + r] : 0.0;
-#pragma unroll
-  for (int c = 0; c < TRSM_NB; ++c) {
-    double s = q[c];
-#pragma unroll
-    for (int l = 0; l < c; ++l) s = fma(-q[l], Rb[l][c], s);
-    q[c] = s / Rb[c][c];
-  }
-#pragma unroll
-  for (int c = 0; c < TRSM_NB; ++c)
-    if (c < nbk) X[(int64_t)(c0 + c) * ldx + r] = q[c];
 }
 
 // ---------------------------------------------------------------------------
@@ -708,24 +635,6 @@ cudaError_t launch_cholesky(double* G, int k, int* info, cudaStream_t st) {
     set = true;
   }
   k_cholesky<<<1, 1024, smem, st>>>(G, k, info);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_trsm_right_upper(double* X, int64_t m, int64_t ldx, const double* Rm, int k,
-                                    cudaStream_t st) {
-  for (int c0 = 0; c0 < k; c0 += TRSM_NB) {
-    const int nbk = k - c0 < TRSM_NB ? k - c0 : TRSM_NB;
-    if (c0 > 0) {  // X(:, c0:c0+nbk) -= X(:, 0:c0) R(0:c0, c0:c0+nbk)
-      GemmArgs g{};
-      g.X = X; g.ldx = ldx;
-      g.Y = Rm + (int64_t)c0 * k; g.ldy = k;
-      g.M = m; g.N = nbk; g.K = c0;
-      g.out = X + (int64_t)c0 * ldx; g.ldo = ldx;
-      dim3 grid((unsigned)((m + GT - 1) / GT), (unsigned)((nbk + GT - 1) / GT), 1);
-      { cudaError_t e = dgemm_launch<GM_NN_UPDATE>(g, grid, st, 8); if (e != cudaSuccess) return e; }
-    }
-    k_trsm_rows_block<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(X, m, ldx, Rm, k, c0, nbk);
-  }
   return cudaGetLastError();
 }
 

@@ -216,27 +216,6 @@ __global__ void k_sum_rows(const double* __restrict__ part, int rows, int64_t st
   out[c] = t;
 }
 
-// (unused helper kept for single-rank debugging) normAL2 = sum norms, normAD2 = sum aux
-__global__ void k_round_scalars(const double* __restrict__ norms, int64_t n,
-                                const double* __restrict__ aux, int naux, DevScalars* sc) {
-  __shared__ double sh[2][32];
-  double a = 0.0, b = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += norms[i];
-  for (int i = threadIdx.x; i < naux; i += blockDim.x) b += aux[i];
-  a = warp_sum(a);
-  b = warp_sum(b);
-  if ((threadIdx.x & 31) == 0) { sh[0][threadIdx.x >> 5] = a; sh[1][threadIdx.x >> 5] = b; }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int nw = blockDim.x >> 5;
-    double x = threadIdx.x < nw ? sh[0][threadIdx.x] : 0.0;
-    double y = threadIdx.x < nw ? sh[1][threadIdx.x] : 0.0;
-    x = warp_sum(x);
-    y = warp_sum(y);
-    if (threadIdx.x == 0) { sc->normAL2 = x; sc->normAD2 = y; }
-  }
-}
-
 // S (interleaved) -> column-major out (A_L export for bit-exact checks)
 template <typename T>
 __global__ void k_export(const T* __restrict__ S, int64_t m, int64_t n, T* __restrict__ out,

@@ -156,8 +156,6 @@ cudaError_t launch_tsmm(const double* X, int64_t ldx, int k1, const double* Y, i
 cudaError_t launch_sum_partials(const double* part, int splits, int64_t len, double* out,
                                 cudaStream_t st);
 cudaError_t launch_cholesky(double* G, int k, int* info, cudaStream_t st);
-cudaError_t launch_trsm_right_upper(double* X, int64_t m, int64_t ldx, const double* Rm, int k,
-                                    cudaStream_t st);
 cudaError_t launch_trsm_left_upper(const double* R1, const double* R2, int k, const double* B,
                                    int64_t ldb, const int* map, int ncols, double* T, int64_t ldt,
                                    int mode, cudaStream_t st);
