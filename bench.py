@@ -259,6 +259,15 @@ def main():
     fq, fc, fe = flops(m_glob, n, q.k, args.mode)
     value = (fq + fc + fe) / (ms_step * 1e-3) / 1e12
 
+    # ---- the paper's other metrics, outside the timed region ----
+    extra_err = {}
+    try:
+        extra_err["rel_fro_low_skeleton"] = h.error_ex("AL", "fro")[1]
+        extra_err["rel_2norm_mixed"] = h.error_ex("AD", 2, iters=40)[1]
+        extra_err["rel_2norm_low_skeleton"] = h.error_ex("AL", 2, iters=40)[1]
+    except Exception as ex:  # reported, never silently replaced
+        extra_err["error"] = str(ex)
+
     # ---- roofline of the dominant kernel (k_pass), per launch -----------------
     peak, peak_kind, peaks = load_peaks()
     pb = pass_bytes(m_loc, n, q.k, args.nb, s_bytes)
@@ -329,7 +338,7 @@ def main():
                           "pass_total": pass_avg_ms},
             "tflops_parts": {"qrcp": fq / (statistics.mean(qr_ms) * 1e-3) / 1e12,
                              "fp64": (fc + fe) / ((statistics.mean(coef_ms) + statistics.mean(err_ms)) * 1e-3) / 1e12},
-            "k_out": q.k, "rel_err_fro": e[1],
+            "k_out": q.k, "rel_err_fro": e[1], "errors_untimed": extra_err,
             "roofline": {"kernel": "k_pass (per-step panel pass)", "bound": "hbm", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "launches_per_step": q.k,

@@ -144,6 +144,19 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
  * identical on all ranks), using the P of the last id_coeffs_fp64. */
 id_status id_error(id_handle h, double* abs_fro, double* rel_fro);
 
+/* The paper's variants and metrics, using the P of the last
+ * id_coeffs_fp64:
+ *   skeleton 0 = A_D(:, I)            (mixed ID  Â_M = A_D(:, I) P)
+ *            1 = fl_L(s A_D(:, I))/s  (low-precision skeleton, Â_L)
+ *   norm     0 = Frobenius, exact fused fp64 reduction (as id_error)
+ *            2 = spectral norm ("relative accuracy in terms of the matrix 2-norm"):
+ *                power iteration x -> E^T E x on E = A_D - X P, never materialised,
+ *                `iters` iterations (0 = 40) from x0 = 1/sqrt(n); ||A_D||_2 by the same
+ *                iteration (cached per handle).  A lower estimate that converges from below.
+ * Outputs: host scalars, identical on all ranks.  Requires id_coeffs_fp64. */
+id_status id_error_ex(id_handle h, int32_t skeleton, int32_t norm, int32_t iters, double* abs_err,
+                      double* rel_err);
+
 /* R (k_out x n fp32, columns in pivoted order, R_jj >= 0) into DEVICE memory. */
 id_status id_get_R(id_handle h, float* R_out, int64_t ldr);
 

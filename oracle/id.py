@@ -104,6 +104,32 @@ def id_error_blocked(A_D: np.ndarray, I: np.ndarray, P: np.ndarray, cols: int = 
     return math.sqrt(abs2), math.sqrt(abs2) / math.sqrt(nrm2) if nrm2 > 0 else float("nan")
 
 
+def low_skeleton(A_D: np.ndarray, I: np.ndarray, fmt: str, s: float) -> np.ndarray:
+    """A_L(:, I) in A_D's units: fl_L(s A_D(:, I)) / s (P:196, the low-precision ID's
+    skeleton; Algorithm 2 line 8 with A_L instead of A_D)."""
+    from .rounding import round_to
+    AI = np.asarray(A_D, dtype=np.float64)[:, np.asarray(I)]
+    return round_to(AI * s, fmt).reshape(AI.shape) / s
+
+
+def id_error_skeleton(A_D: np.ndarray, X: np.ndarray, P: np.ndarray):
+    """(||A_D - X P||_F, same / ||A_D||_F) for an arbitrary skeleton X (m x k), fp64,
+    column sums of squares added with math.fsum (the Â_L variant of P:196)."""
+    A_D = np.asarray(A_D, dtype=np.float64)
+    E = A_D - X @ P
+    abs2 = math.fsum(math.fsum(col) for col in (E * E).T)
+    nrm2 = math.fsum(math.fsum(col) for col in (A_D * A_D).T)
+    return math.sqrt(abs2), math.sqrt(abs2) / math.sqrt(nrm2) if nrm2 > 0 else float("nan")
+
+
+def spectral_error(A_D: np.ndarray, X: np.ndarray, P: np.ndarray):
+    """(||A_D - X P||_2, same / ||A_D||_2) by LAPACK SVD — the paper's metric."""
+    A_D = np.asarray(A_D, dtype=np.float64)
+    e = float(np.linalg.norm(A_D - X @ P, 2))
+    a = float(np.linalg.norm(A_D, 2))
+    return e, e / a if a > 0 else float("nan")
+
+
 def lemma_bound(k: int, n: int, sigma_k1: float):
     """Lemma 2.1: (sqrt(1 + k(n-k)), sqrt(1 + k(n-k)) sigma_{k+1})."""
     c = math.sqrt(1.0 + k * (n - k))

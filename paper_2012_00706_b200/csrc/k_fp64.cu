@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
 #pragma unroll
     for (int q = 0; q < GT / 32; ++q) {
       const int64_t c = n0 + lane + 32 * q;
-      src_next[q] = c < g.N ? g.cmap[c] : 0;
+      src_next[q] = c < g.N ? (g.cmap ? g.cmap[c] : (int)c) : 0;
     }
   };
   auto issue_d = [&](int64_t m0, int64_t n0) {
@@ -406,7 +406,8 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
             for (int mt = 0; mt < 8; ++mt) {
               const int64_t r = m0 + wm * 64 + mt * 8 + gq;
               if (r < g.M && c < g.N) {
-                const double a = dp ? Ds[(c - n0) * DLD + (r - m0)] : __ldcs(g.A + (int64_t)g.cmap[c] * g.lda + r);
+                const double a = dp ? Ds[(c - n0) * DLD + (r - m0)]
+                                    : __ldcs(g.A + (g.cmap ? (int64_t)g.cmap[c] : c) * g.lda + r);
                 const double e = a - acc[mt][nt][h];
                 e2 = fma(e, e, e2);
               }

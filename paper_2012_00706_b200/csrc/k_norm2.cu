@@ -1,0 +1,208 @@
+// The paper's other ID variant and its error metric:
+//
+//  * the low-precision skeleton ("single precision ID"):
+//    Â_L = A_L(:, I) P with A_L = fl_L(s A_D), in A_D's units X = fl_L(s A_D(:, I)) / s;
+//  * the relative 2-norm error ("We report relative accuracy in terms of the
+//    matrix 2-norm"): ||E||_2 = sqrt(lambda_max(E^T E)) by power iteration on the
+//    never-materialised operator E = A_D - X P, x -> E^T (E x), each iteration two
+//    fp64 streaming passes over A_D (HBM-bound GEMVs) plus k-sized corrections.
+//
+// Kernels (fp64, bandwidth-bound):
+//   k_gemv_n   y(m) = A(:, 0:n) x            row-parallel, coalesced column sweeps
+//   k_gemv_t   part[b][c] = sum_{rows of b} A(r, c) y(r)   column dots, row splits
+//   k_small_*  k x n products with P and vector updates (one CTA)
+#include "mpid_internal.cuh"
+#include <math.h>
+
+namespace mpid {
+
+// X(:, l) = fl_L(s A(:, perm[l])) / s   (fmt 1 = fp16, 2 = fp32; one RNE rounding from fp64)
+__global__ void k_gather_lowp(const double* __restrict__ A, int64_t m, int64_t ld, const int* __restrict__ perm,
+                              int fmt, const DevScalars* __restrict__ sc, double* __restrict__ X) {
+  const int l = blockIdx.y;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  const double s = sc->scale;
+  const double x = __dmul_rn(s, A[(int64_t)perm[l] * ld + r]);
+  const double q = fmt == 1 ? (double)__half2float(__double2half(x)) : (double)__double2float_rn(x);
+  X[(int64_t)l * m + r] = q / s;
+}
+
+// y = A x  (+ y if accumulate < 0: y = y - A x); 2 rows per thread, x staged in shared memory
+__global__ void __launch_bounds__(256) k_gemv_n(const double* __restrict__ A, int64_t m, int64_t ld, int n,
+                                                const double* __restrict__ x, double* __restrict__ y,
+                                                int subtract) {
+  extern __shared__ double xs[];
+  for (int c = threadIdx.x; c < n; c += blockDim.x) xs[c] = x[c];
+  __syncthreads();
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (r >= m) return;
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+  const bool pair = r + 1 < m && ((ld & 1) == 0);
+  int c = 0;
+  if (pair) {
+    for (; c + 1 < n; c += 2) {
+      const double2 u = __ldcs(reinterpret_cast<const double2*>(A + (int64_t)c * ld + r));
+      const double2 v = __ldcs(reinterpret_cast<const double2*>(A + (int64_t)(c + 1) * ld + r));
+      a0 = fma(u.x, xs[c], a0);
+      a1 = fma(u.y, xs[c], a1);
+      b0 = fma(v.x, xs[c + 1], b0);
+      b1 = fma(v.y, xs[c + 1], b1);
+    }
+    for (; c < n; ++c) {
+      const double2 u = __ldcs(reinterpret_cast<const double2*>(A + (int64_t)c * ld + r));
+      a0 = fma(u.x, xs[c], a0);
+      a1 = fma(u.y, xs[c], a1);
+    }
+  } else {
+    for (; c < n; ++c) {
+      a0 = fma(A[(int64_t)c * ld + r], xs[c], a0);
+      if (r + 1 < m) a1 = fma(A[(int64_t)c * ld + r + 1], xs[c], a1);
+    }
+  }
+  const double y0 = a0 + b0, y1 = a1 + b1;
+  if (subtract) {
+    y[r] -= y0;
+    if (r + 1 < m) y[r + 1] -= y1;
+  } else {
+    y[r] = y0;
+    if (r + 1 < m) y[r + 1] = y1;
+  }
+}
+
+// part[b][c] = sum_{r in row block b} A(r, c) y(r); grid (n, nb), block 256
+__global__ void __launch_bounds__(256) k_gemv_t(const double* __restrict__ A, int64_t m, int64_t ld, int n,
+                                                const double* __restrict__ y, int64_t rows_per_block,
+                                                double* __restrict__ part) {
+  const int c = blockIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
+  const int64_t r1 = (r0 + rows_per_block < m) ? r0 + rows_per_block : m;
+  const double* col = A + (int64_t)c * ld;
+  double t0 = 0.0, t1 = 0.0;
+  int64_t r = r0 + threadIdx.x;
+  for (; r + 256 < r1; r += 512) {
+    t0 = fma(__ldcs(col + r), y[r], t0);
+    t1 = fma(__ldcs(col + r + 256), y[r + 256], t1);
+  }
+  for (; r < r1; r += 256) t0 = fma(__ldcs(col + r), y[r], t0);
+  double t = t0 + t1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  __shared__ double sh[8];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double u = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) u += sh[w];
+    part[(int64_t)blockIdx.y * n + c] = u;
+  }
+}
+
+// out[c] = sum_b part[b][c] (fixed order) - (sub ? sub[c] : 0)
+__global__ void k_sum_cols(const double* __restrict__ part, int nblk, int n, const double* __restrict__ sub,
+                           double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double t = 0.0;
+  for (int b = 0; b < nblk; ++b) t += part[(int64_t)b * n + c];
+  out[c] = sub ? t - sub[c] : t;
+}
+
+// w(k) = P(k x n, ld ldp) x(n)  — one CTA, warp per row group
+__global__ void k_p_times(const double* __restrict__ P, int64_t ldp, int k, int n, const double* __restrict__ x,
+                          double* __restrict__ w) {
+  for (int i = threadIdx.x >> 5; i < k; i += blockDim.x >> 5) {
+    double t = 0.0;
+    for (int c = threadIdx.x & 31; c < n; c += 32) t = fma(P[(int64_t)c * ldp + i], x[c], t);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((threadIdx.x & 31) == 0) w[i] = t;
+  }
+}
+
+// v(n) = P^T w  — thread per column
+__global__ void k_pt_times(const double* __restrict__ P, int64_t ldp, int k, int n, const double* __restrict__ w,
+                           double* __restrict__ v) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double t = 0.0;
+  for (int i = 0; i < k; ++i) t = fma(P[(int64_t)c * ldp + i], w[i], t);
+  v[c] = t;
+}
+
+// norm2 = ||z||, x = z / ||z||, est[it] = ||z|| (one CTA)
+__global__ void k_normalize(const double* __restrict__ z, int n, double* __restrict__ x, double* __restrict__ est,
+                            int it) {
+  __shared__ double sh[32];
+  double t = 0.0;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) t = fma(z[c], z[c], t);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (int)(blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) sh[0] = t;
+  }
+  __syncthreads();
+  const double nz = sqrt(sh[0]);
+  const double inv = nz > 0.0 ? 1.0 / nz : 0.0;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) x[c] = z[c] * inv;
+  if (threadIdx.x == 0) est[it] = nz;
+}
+
+// x0 = (1, 1, ..., 1) / sqrt(n) (deterministic start, no random numbers)
+__global__ void k_ones(double* __restrict__ x, int n) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n) x[c] = 1.0 / sqrt((double)n);
+}
+
+// ---------------------------------------------------------------------------
+cudaError_t launch_gather_lowp(const double* A, int64_t m, int64_t ld, const int* perm, int k, int fmt,
+                               const DevScalars* sc, double* X, cudaStream_t st) {
+  dim3 grid((unsigned)((m + 255) / 256), (unsigned)k);
+  k_gather_lowp<<<grid, 256, 0, st>>>(A, m, ld, perm, fmt, sc, X);
+  return cudaGetLastError();
+}
+cudaError_t launch_gemv_n(const double* A, int64_t m, int64_t ld, int n, const double* x, double* y, int subtract,
+                          cudaStream_t st) {
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(k_gemv_n, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    set = true;
+  }
+  if (n > 8192) return cudaErrorInvalidValue;
+  k_gemv_n<<<(unsigned)((m + 511) / 512), 256, (size_t)n * 8, st>>>(A, m, ld, n, x, y, subtract);
+  return cudaGetLastError();
+}
+cudaError_t launch_gemv_t(const double* A, int64_t m, int64_t ld, int n, const double* y, double* part, int nblk,
+                          cudaStream_t st) {
+  const int64_t rpb = (m + nblk - 1) / nblk;
+  k_gemv_t<<<dim3((unsigned)n, (unsigned)nblk), 256, 0, st>>>(A, m, ld, n, y, rpb, part);
+  return cudaGetLastError();
+}
+cudaError_t launch_sum_cols(const double* part, int nblk, int n, const double* sub, double* out, cudaStream_t st) {
+  k_sum_cols<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nblk, n, sub, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_p_times(const double* P, int64_t ldp, int k, int n, const double* x, double* w, cudaStream_t st) {
+  k_p_times<<<1, 1024, 0, st>>>(P, ldp, k, n, x, w);
+  return cudaGetLastError();
+}
+cudaError_t launch_pt_times(const double* P, int64_t ldp, int k, int n, const double* w, double* v, cudaStream_t st) {
+  k_pt_times<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(P, ldp, k, n, w, v);
+  return cudaGetLastError();
+}
+cudaError_t launch_normalize(const double* z, int n, double* x, double* est, int it, cudaStream_t st) {
+  k_normalize<<<1, 1024, 0, st>>>(z, n, x, est, it);
+  return cudaGetLastError();
+}
+cudaError_t launch_ones(double* x, int n, cudaStream_t st) {
+  k_ones<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, n);
+  return cudaGetLastError();
+}
+
+}  // namespace mpid

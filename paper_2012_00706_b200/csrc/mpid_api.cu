@@ -57,7 +57,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t AD, S, U, F, Vh, Vl, Sj, R, part, red, xr, norms, perm, scal3, sc, maxpart, rpart;
-  size_t AI, Q1, G1, G2, W, tpart, Rd, T, Pw, epart, Ik, Rinv, misc;
+  size_t AI, Q1, G1, G2, W, tpart, Rd, T, Pw, epart, Ik, Rinv, py, pvec, misc;
   size_t total;
 };
 
@@ -71,6 +71,8 @@ int num_sms() {
   }
   return sms;
 }
+
+constexpr int PW_NBLK = 64;   // row blocks of the transposed GEMV (power iteration)
 
 int64_t m_pad_of(int64_t m_local) {
   const int64_t T = PASS_TILE_G * RG;
@@ -130,6 +132,8 @@ Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
   L.epart = take((size_t)((m_local + 127) / 128) * ((n + 127) / 128) * 8);
   L.Ik = take((size_t)k * k * 8);
   L.Rinv = take((size_t)k * k * 8);
+  L.py = take((size_t)m_local * 8);                                  // power iteration: y = E x
+  L.pvec = take((size_t)(4 * n + 2 * k + 256 + PW_NBLK * n) * 8);    // x, z, v, w, u, est, partials
   L.misc = take(1024);
   L.total = off;
   return L;
@@ -162,7 +166,9 @@ struct mpid_ctx {
   int* perm = nullptr;
   DevScalars* sc = nullptr;
   double *AI = nullptr, *Q1 = nullptr, *G1 = nullptr, *G2 = nullptr, *W = nullptr, *tpart = nullptr,
-         *Rd = nullptr, *T = nullptr, *Pw = nullptr, *epart = nullptr, *Ik = nullptr, *Rinv = nullptr;
+         *Rd = nullptr, *T = nullptr, *Pw = nullptr, *epart = nullptr, *Ik = nullptr, *Rinv = nullptr,
+         *py = nullptr, *pvec = nullptr;
+  double normAD_spec = -1.0;   // cached ||A_D||_2 (power iteration), < 0 = not yet
   int* info = nullptr;
   double* err2 = nullptr;
   // state
@@ -304,6 +310,8 @@ id_status id_create(id_handle* hp, const double* A_D, int64_t m_global, int64_t 
   h->epart = (double*)(w + L.epart);
   h->Ik = (double*)(w + L.Ik);
   h->Rinv = (double*)(w + L.Rinv);
+  h->py = (double*)(w + L.py);
+  h->pvec = (double*)(w + L.pvec);
   h->info = (int*)(w + L.misc);
   h->err2 = (double*)(w + L.misc + 64);
   for (auto& e : h->ev) {
@@ -735,6 +743,88 @@ id_status id_error(id_handle h, double* abs_fro, double* rel_fro) {
   h->stats.kernel_launches += 2;
   *abs_fro = sqrt(e2);
   *rel_fro = h->sc_host.normAD2 > 0 ? sqrt(e2 / h->sc_host.normAD2) : NAN;
+  return ID_OK;
+}
+
+// power iteration for ||E||_2, E = A_D - X P (X = nullptr: E = A_D); returns the estimate
+static id_status power_norm2(mpid_ctx* h, const double* X, int k, int iters, double* out) {
+  const int n = (int)h->n;
+  const int64_t m = h->m_local;
+  double* x = h->pvec;
+  double* z = x + n;
+  double* v = z + n;
+  double* wk = v + n;
+  double* uk = wk + k;
+  double* est = uk + k;
+  double* part = est + 256;
+  CK(launch_ones(x, n, h->st));
+  for (int it = 0; it < iters; ++it) {
+    CK(launch_gemv_n(h->AD, m, h->ld, n, x, h->py, 0, h->st));           // y = A_D x
+    if (X) {
+      CK(launch_p_times(h->Pw, k, k, n, x, wk, h->st));                  // w = P x
+      CK(launch_gemv_n(X, m, m, k, wk, h->py, 1, h->st));                // y -= X w
+    }
+    CK(launch_gemv_t(h->AD, m, h->ld, n, h->py, part, PW_NBLK, h->st));  // A_D^T y (row-block partials)
+    if (X) {
+      CK(launch_gemv_t(X, m, m, k, h->py, part + (int64_t)PW_NBLK * n, PW_NBLK, h->st));
+      CK(launch_sum_cols(part + (int64_t)PW_NBLK * n, PW_NBLK, k, nullptr, uk, h->st));   // u = X^T y
+      id_status s = allreduce(h, uk, (size_t)k, NCCL_SUM);
+      if (s) return s;
+      CK(launch_pt_times(h->Pw, k, k, n, uk, v, h->st));                 // v = P^T u
+      CK(launch_sum_cols(part, PW_NBLK, n, v, z, h->st));                // z = A_D^T y - v
+    } else {
+      CK(launch_sum_cols(part, PW_NBLK, n, nullptr, z, h->st));
+    }
+    id_status s = allreduce(h, z, (size_t)n, NCCL_SUM);
+    if (s) return s;
+    CK(launch_normalize(z, n, x, est, it < 255 ? it : 255, h->st));      // est = ||E^T E x||, x = z / |z|
+  }
+  double e = 0.0;
+  CK(cudaMemcpyAsync(&e, est + (iters - 1 < 255 ? iters - 1 : 255), 8, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  *out = sqrt(e);
+  return ID_OK;
+}
+
+id_status id_error_ex(id_handle h, int32_t skeleton, int32_t norm, int32_t iters, double* abs_err,
+                      double* rel_err) {
+  if (!h || !abs_err || !rel_err) return ID_ERR_ARG;
+  cudaGetLastError();
+  if (!h->have_coef) return fail(h, ID_ERR_STATE, "id_error_ex needs id_coeffs_fp64 first");
+  if (skeleton != 0 && skeleton != 1) return fail(h, ID_ERR_ARG, "skeleton must be 0 (A_D) or 1 (A_L)");
+  if (norm != 0 && norm != 2) return fail(h, ID_ERR_ARG, "norm must be 0 (Frobenius) or 2 (spectral)");
+  if (iters < 0 || iters > 256) return fail(h, ID_ERR_ARG, "iters must be in [0, 256]");
+  if (iters == 0) iters = 40;
+  const int k = h->k_out;
+  const int n = (int)h->n;
+  const double* X = h->AI;                                     // A_D(:, I)
+  if (skeleton == 1) {                                         // fl_L(s A_D(:, I)) / s into Q1 (free after coeffs)
+    CK(launch_gather_lowp(h->AD, h->m_local, h->ld, h->perm, k, h->fmt, h->sc, h->Q1, h->st));
+    X = h->Q1;
+  }
+  if (norm == 0) {
+    if (skeleton == 0) return id_error(h, abs_err, rel_err);
+    int nblk = 0;   // all n columns: the low-precision skeleton columns are not reproduced exactly
+    CK(launch_error(h->AD, h->m_local, h->ld, n, nullptr, X, k, h->Pw, k, h->epart, &nblk, h->st));
+    CK(launch_sum_scalar(h->epart, nblk, h->err2, h->st));
+    id_status s = allreduce(h, h->err2, 1, NCCL_SUM);
+    if (s) return s;
+    double e2 = 0.0;
+    CK(cudaMemcpyAsync(&e2, h->err2, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    *abs_err = sqrt(e2);
+    *rel_err = h->sc_host.normAD2 > 0 ? sqrt(e2 / h->sc_host.normAD2) : NAN;
+    return ID_OK;
+  }
+  double e = 0.0;
+  id_status s = power_norm2(h, X, k, iters, &e);
+  if (s) return s;
+  if (h->normAD_spec < 0.0) {
+    s = power_norm2(h, nullptr, k, iters, &h->normAD_spec);
+    if (s) return s;
+  }
+  *abs_err = e;
+  *rel_err = h->normAD_spec > 0 ? e / h->normAD_spec : NAN;
   return ID_OK;
 }
 

@@ -170,6 +170,18 @@ cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, cons
 cudaError_t launch_nn_store(const double* X, int64_t m, int64_t ldx, const double* B, int64_t ldb, int K,
                             int N, double* out, int64_t ldo, cudaStream_t st);
 cudaError_t launch_eye(double* I, int k, cudaStream_t st);
+// NEXT-1 / NEXT-2 (k_norm2.cu): the low-precision skeleton and the 2-norm by power iteration
+cudaError_t launch_gather_lowp(const double* A, int64_t m, int64_t ld, const int* perm, int k, int fmt,
+                               const DevScalars* sc, double* X, cudaStream_t st);
+cudaError_t launch_gemv_n(const double* A, int64_t m, int64_t ld, int n, const double* x, double* y, int subtract,
+                          cudaStream_t st);
+cudaError_t launch_gemv_t(const double* A, int64_t m, int64_t ld, int n, const double* y, double* part, int nblk,
+                          cudaStream_t st);
+cudaError_t launch_sum_cols(const double* part, int nblk, int n, const double* sub, double* out, cudaStream_t st);
+cudaError_t launch_p_times(const double* P, int64_t ldp, int k, int n, const double* x, double* w, cudaStream_t st);
+cudaError_t launch_pt_times(const double* P, int64_t ldp, int k, int n, const double* w, double* v, cudaStream_t st);
+cudaError_t launch_normalize(const double* z, int n, double* x, double* est, int it, cudaStream_t st);
+cudaError_t launch_ones(double* x, int n, cudaStream_t st);
 cudaError_t launch_sum_scalar(const double* part, int nblk, double* out, cudaStream_t st);
 
 }  // namespace mpid

@@ -30,7 +30,7 @@ SCALING = {"none": ID_SCALE_NONE, "maxabs": ID_SCALE_MAXABS, "pow2": ID_SCALE_PO
 COEF = {"R": ID_COEF_R, "r": ID_COEF_R, "lsq": ID_COEF_LSQ, "LSQ": ID_COEF_LSQ}
 
 # every function declared in include/mpid.h
-EXPORTS = ["id_workspace_bytes", "id_create", "id_qrcp_lowprec", "id_coeffs_fp64", "id_error",
+EXPORTS = ["id_workspace_bytes", "id_create", "id_qrcp_lowprec", "id_coeffs_fp64", "id_error", "id_error_ex",
            "id_get_R", "id_get_perm", "id_get_AL", "id_round_only", "id_get_stats", "id_last_error", "id_destroy",
            "id_nccl_unique_id_bytes", "id_nccl_get_unique_id", "id_nccl_comm_init",
            "id_nccl_comm_destroy", "id_version"]
@@ -84,6 +84,8 @@ def lib():
     L.id_coeffs_fp64.argtypes = [vp, C.c_int, vp, i64]
     L.id_error.restype = C.c_int
     L.id_error.argtypes = [vp, C.POINTER(dbl), C.POINTER(dbl)]
+    L.id_error_ex.restype = C.c_int
+    L.id_error_ex.argtypes = [vp, i32, i32, i32, C.POINTER(dbl), C.POINTER(dbl)]
     L.id_get_R.restype = C.c_int
     L.id_get_R.argtypes = [vp, vp, i64]
     L.id_get_perm.restype = C.c_int
@@ -265,6 +267,15 @@ class MPID:
         rc, a, r = id_error(self.h)
         self._check(rc)
         return a, r
+
+    def error_ex(self, skeleton="AD", norm="fro", iters=0):
+        """Variant / metric of the paper (include/mpid.h id_error_ex): skeleton "AD" (mixed
+        ID) or "AL" (low-precision skeleton); norm "fro" or 2 (power iteration)."""
+        a, r = C.c_double(0), C.c_double(0)
+        sk = {"AD": 0, "AL": 1}[skeleton] if isinstance(skeleton, str) else int(skeleton)
+        nm = 0 if norm in ("fro", 0) else 2
+        self._check(lib().id_error_ex(self.h, sk, nm, iters, C.byref(a), C.byref(r)))
+        return a.value, r.value
 
     def get_R(self):
         import torch

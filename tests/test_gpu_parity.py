@@ -273,3 +273,34 @@ def test_host_buffer_path_equals_device_path():
     a = run_gpu(A, "fp16", "pow2", 32)
     b = run_gpu(A, "fp16", "pow2", 32, host=True)
     assert np.array_equal(a["piv"], b["piv"]) and np.array_equal(a["P"], b["P"])
+
+
+# ---- NEXT-1 / NEXT-2: the low-precision skeleton and the paper's 2-norm metric ----------
+@pytest.mark.parametrize("fmt,scaling", [("fp16", "pow2"), ("fp32", "none")])
+def test_error_variants_and_spectral_norm(fmt, scaling):
+    from oracle.id import id_error_skeleton, low_skeleton, spectral_error
+    from oracle.qrcp import scale_factor
+    from paper_2012_00706_b200.mpid import MPID
+    from tests.gpu_helpers import to_dev
+    A = np.asfortranarray(gen_config("C2", 0)[:, :400])
+    k = 24
+    h = MPID(to_dev(A), k_max=k)
+    q = h.qrcp(fmt, scaling, k=k)
+    I = q.piv
+    for mode in ("lsq", "R"):
+        P = h.coeffs(mode).cpu().numpy()
+        s = scale_factor(A, scaling)
+        XL = low_skeleton(A, I, fmt, s)
+        # Frobenius, both skeletons, against the oracle given the GPU's (I, P)
+        ef = h.error_ex("AD", "fro")
+        assert abs(ef[0] - id_error_skeleton(A, A[:, I], P)[0]) <= 1e-9 * ef[0]
+        el = h.error_ex("AL", "fro")
+        ref = id_error_skeleton(A, XL, P)
+        assert abs(el[0] - ref[0]) <= 1e-9 * ref[0] and abs(el[1] - ref[1]) <= 1e-9 * ref[1]
+        # 2-norm by power iteration: converges from below to LAPACK's value
+        for sk, X in (("AD", A[:, I]), ("AL", XL)):
+            e2 = h.error_ex(sk, 2, iters=200)
+            ex = spectral_error(A, X, P)
+            assert e2[0] <= ex[0] * (1 + 1e-9) and e2[0] >= ex[0] * (1 - 1e-3), (sk, e2, ex)
+            assert abs(e2[1] - ex[1]) <= 1e-3 * ex[1]
+    h.close()

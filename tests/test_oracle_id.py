@@ -114,3 +114,21 @@ def test_blocked_error_equals_definition():
     a = id_error(A, I, P)
     b = id_error_blocked(A, I, P, cols=37)
     assert abs(a[0] - b[0]) <= 1e-13 * a[0] and abs(a[1] - b[1]) <= 1e-13 * a[1]
+
+
+def test_low_skeleton_and_spectral_error_pins():
+    """Â_L skeleton = RNE rounding of the scaled columns (pinned by numpy's fp16/fp32
+    casts, which round once from fp64); the 2-norm error equals the largest singular
+    value of the residual and is >= the Eckart-Young 2-norm bound sigma_{k+1}."""
+    from oracle.id import id_error_skeleton, low_skeleton, spectral_error
+    A, sigma = gen_decay(2, 120, 80, seed=4)
+    I = np.array([0, 5, 9, 17, 33])
+    for fmt, dt in (("fp16", np.float16), ("fp32", np.float32)):
+        X = low_skeleton(A, I, fmt, 8.0)
+        assert np.array_equal(X, (A[:, I] * 8.0).astype(dt).astype(np.float64) / 8.0)
+    P = coeffs_lsq(A, I)
+    e2, r2 = spectral_error(A, A[:, I], P)
+    assert e2 >= sigma[len(I)] * (1 - 1e-12)
+    assert abs(r2 - e2 / sigma[0]) <= 1e-12 * r2
+    ef, _ = id_error_skeleton(A, A[:, I], P)
+    assert abs(ef - id_error(A, I, P)[0]) <= 1e-12 * ef and e2 <= ef * (1 + 1e-12)
