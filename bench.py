@@ -333,7 +333,7 @@ def main():
                        "rows_per_gpu": m_loc, "n": n, "k": k, "fmt": args.fmt, "nb": args.nb,
                        "coef": args.mode, "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (A_D 16 GiB, A_L 4 GiB per GPU); no flush"},
-            "stages_ms": {"round": statistics.mean(round_ms), "qrcp_incl_round": statistics.mean(qr_ms),
+            "stages_ms": {"round": statistics.mean(round_ms), "qrcp": statistics.mean(qr_ms),
                           "coef": statistics.mean(coef_ms), "error": statistics.mean(err_ms),
                           "pass_total": pass_avg_ms},
             "tflops_parts": {"qrcp": fq / (statistics.mean(qr_ms) * 1e-3) / 1e12,

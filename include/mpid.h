@@ -103,6 +103,8 @@ typedef struct {
   int32_t status_qrcp;
   int32_t formation;     /* formation used by the last QRCP (see id_qrcp_opts) */
   int32_t reserved[4];
+  double t_host_launch_ms; /* host time of the QRCP graph launch call */
+  double t_call_gpu_ms;    /* device time of the whole id_qrcp_lowprec call on the caller's stream */
 } id_stats;
 
 /* Bytes of device workspace for a shard of m_local rows, n columns, rank <= k_max,

@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <map>
 #include <string>
 #include <tuple>
@@ -588,9 +589,13 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
       h->graph_launches[key] = h->kernel_launches;
     }
     // fork: cap waits for the caller's prior work; join: the caller waits for the graph
+    CK(cudaEventRecord(h->ev[7], h->user_st));
     CK(cudaEventRecord(h->fork_ev, h->user_st));
     CK(cudaStreamWaitEvent(h->cap, h->fork_ev, 0));
+    const auto tl0 = std::chrono::steady_clock::now();
     CK(cudaGraphLaunch(it->second, h->cap));
+    h->stats.t_host_launch_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl0).count();
     CK(cudaEventRecord(h->join_ev, h->cap));
     CK(cudaStreamWaitEvent(h->user_st, h->join_ev, 0));
     h->stats.kernel_launches = h->graph_launches[key];
@@ -602,8 +607,14 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   h->perm_host.resize(h->n);
   CK(cudaMemcpyAsync(&h->sc_host, h->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, h->st));
   CK(cudaMemcpyAsync(h->perm_host.data(), h->perm, h->n * sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaEventRecord(h->ev[6], h->st));
   CK(cudaStreamSynchronize(h->st));
   h->fmt = fmt;
+  if (use_graph) {
+    float tc = 0.f;
+    cudaEventElapsedTime(&tc, h->ev[7], h->ev[6]);
+    h->stats.t_call_gpu_ms = tc;
+  }
   const DevScalars& sc = h->sc_host;
   if (sc.k_out < 0 || sc.k_out > k_max)
     return fail(h, ID_ERR_STATE, "internal: k_out=%d outside [0, %d]", sc.k_out, k_max);
