@@ -1,0 +1,90 @@
+"""Time the full ID (scale/round + QRCP + LSQ coefficients + fused error) through the C ABI
+on every BASELINE.json config that fits one GPU, plus the per-GPU workload of C5 at
+8 GPUs (one 2^21-row shard; the allreduces it would add are ~k x 10-30 us).
+
+    python tools/bench_configs.py > profiles/r01_configs.jsonl
+
+One JSON line per (config, fmt, k): device time per ID (median of reps after a warm-up),
+stage times, TFLOP/s of the algorithmic flops (bench.flops), the pass's HBM fraction
+and the relative Frobenius error.  Inputs are generated on the device (C4/C5) or on
+the host (C1-C3) — never timed.
+"""
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from bench import flops, load_peaks, pass_bytes  # noqa: E402
+from paper_2012_00706_b200 import mpid  # noqa: E402
+from synth import config_spec, fourier_params, gen_config, gen_fourier  # noqa: E402
+
+CASES = [("C1", "fp16", 32, 0.0), ("C1", "fp32", 32, 0.0),
+         ("C2", "fp32", 16, 0.0), ("C2", "fp32", 64, 0.0), ("C2", "fp32", 128, 0.0),
+         ("C2", "fp16", 16, 0.0), ("C2", "fp16", 64, 0.0), ("C2", "fp16", 128, 0.0),
+         ("C3", "fp16", 256, 0.0), ("C3", "fp16", 512, 1e-3),
+         ("C4", "fp16", 100, 0.0), ("C4", "fp32", 100, 0.0),
+         ("C5/8", "fp16", 512, 0.0)]
+
+
+def device_matrix(name):
+    if name in ("C4", "C5/8"):
+        spec = config_spec("C4" if name == "C4" else "C5")
+        fp = fourier_params(spec.extra["N"], spec.extra["L"], spec.n, 0)
+        rows = spec.m if name == "C4" else spec.m // 8
+        return gen_fourier(fp, 0, 0, rows, device="cuda"), spec
+    spec = config_spec(name)
+    A = gen_config(name, 0)
+    return torch.from_numpy(np.ascontiguousarray(A.T)).cuda(), spec
+
+
+def main():
+    peak, _, _ = load_peaks()
+    only = sys.argv[1:]
+    cache = {}
+    for name, fmt, k, eps in CASES:
+        if only and name not in only:
+            continue
+        if name not in cache:
+            cache.clear()
+            torch.cuda.empty_cache()
+            cache[name] = device_matrix(name)
+        At, spec = cache[name]
+        n, m = At.shape
+        scaling = spec.scaling.get(fmt, "pow2" if fmt == "fp16" else "none")
+        h = mpid.MPID(At, k_max=k, m_global=m)
+        reps = 5 if m * n < 1e9 else 3
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        times, st = [], None
+        for it in range(reps + 1):
+            torch.cuda.synchronize()
+            ev[0].record()
+            q = h.qrcp(fmt, scaling, k=k, eps=eps)
+            h.coeffs("lsq")
+            e = h.error()
+            ev[1].record()
+            torch.cuda.synchronize()
+            if it > 0:
+                times.append(ev[0].elapsed_time(ev[1]))
+                st = h.stats()
+        t = statistics.median(times)
+        fq, fc, fe = flops(m, n, q.k, "lsq")
+        nb = st["nb"]
+        pb = pass_bytes(m, n, q.k, nb, 2 if fmt == "fp16" else 4)
+        line = {"config": name, "m": m, "n": n, "fmt": fmt, "k": q.k, "eps": eps, "nb": nb,
+                "ms_per_id": t, "tflops": (fq + fc + fe) / (t * 1e-3) / 1e12,
+                "stages_ms": {"round": st["t_round_ms"], "qrcp": st["t_qrcp_ms"], "coef": st["t_coef_ms"],
+                              "error": st["t_err_ms"]},
+                "qrcp_hbm_frac_of_measured": pb / (st["t_qrcp_ms"] * 1e-3) / 1e9 / peak,
+                "rel_err_fro": e[1]}
+        print(json.dumps(line), flush=True)
+        h.close()
+
+
+if __name__ == "__main__":
+    main()
