@@ -89,11 +89,34 @@ int round_gy(int64_t m_pad, int64_t n) {
   return (int)std::min<int64_t>(gy, 4096);
 }
 int tsmm_splits(int64_t k1, int64_t n1, int64_t m) {
-  // k_dgemm CTA tile 128 x 128, one CTA per SM: aim at two full waves of equal-work CTAs
+  // k_dgemm CTA tile <= 128 x 128, one CTA per SM, equal-work CTAs: pick the split count
+  // in [2 waves, 6 waves] whose last wave is the fullest (ties -> fewer splits)
+  const int64_t sms = num_sms();
   const int64_t tiles = ((k1 + 127) / 128) * ((n1 + 127) / 128);
-  int64_t s = std::max<int64_t>(1, (2 * num_sms() + tiles - 1) / tiles);
-  s = std::min<int64_t>(s, std::max<int64_t>(1, m / 512));
-  return (int)std::min<int64_t>(s, 512);
+  const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(512, m / 512));
+  const int64_t s0 = std::min<int64_t>(cap, std::max<int64_t>(1, (2 * sms + tiles - 1) / tiles));
+  int64_t best = s0;
+  double best_eff = -1.0;
+  for (int64_t s = s0; s <= std::min<int64_t>(cap, 3 * s0); ++s) {
+    const int64_t ctas = tiles * s, waves = (ctas + sms - 1) / sms;
+    const double eff = (double)ctas / (double)(waves * sms);
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+  }
+  return (int)best;
+}
+
+// split-K partials buffer: covers every (k1 <= k, n1 <= n) product the coefficients use;
+// the call sites clamp the split count to it (splits_for)
+size_t tpart_doubles(int64_t m_local, int64_t n, int64_t k) {
+  size_t need = 0;
+  for (int64_t k1 : {k, std::min<int64_t>(k, 128)})
+    for (int64_t n1 : {k1, n, std::max<int64_t>(1, n - k1)})
+      need = std::max<size_t>(need, (size_t)tsmm_splits(k1, n1, m_local) * k1 * n1);
+  return std::min<size_t>(need, (size_t)1024 * 128 * 128);
+}
+int splits_for(int64_t k1, int64_t n1, int64_t m, size_t cap) {
+  const int64_t s = tsmm_splits(k1, n1, m);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(s, (int64_t)(cap / (size_t)(k1 * n1))));
 }
 
 Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
@@ -124,9 +147,7 @@ Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
   L.G1 = take((size_t)k * k * 8);
   L.G2 = take((size_t)k * k * 8);
   L.W = take((size_t)k * n * 8);
-  const size_t tp = std::max<size_t>((size_t)tsmm_splits(k, n, m_local) * k * n,
-                                     (size_t)tsmm_splits(k, k, m_local) * k * k);
-  L.tpart = take(tp * 8);
+  L.tpart = take(tpart_doubles(m_local, n, k) * 8);
   L.Rd = take((size_t)k * n * 8);
   L.T = take((size_t)k * n * 8);
   L.Pw = take((size_t)k * n * 8);
@@ -675,7 +696,8 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
     launches += 2;
   } else if (mode == ID_COEF_LSQ) {
     // G1 = A_I^T A_I
-    int sp = tsmm_splits(k, k, m);
+    const size_t tcap = tpart_doubles(m, n, h->k_cap);
+    int sp = splits_for(k, k, m, tcap);
     CK(launch_tsmm(h->AI, m, k, h->AI, m, k, m, h->tpart, sp, h->st));
     CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G1, h->st));
     launches += 2;
@@ -696,7 +718,7 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
     // W = Q1^T A_D(:, J), J = perm[k:] (W(:, I) = R1 is never needed)
     const int nj = n - k;
     if (nj > 0) {
-      const int spw = tsmm_splits(k, nj, m);
+      const int spw = splits_for(k, nj, m, tcap);
       CK(launch_tsmm(h->Q1, m, k, h->AD, h->ld, nj, m, h->tpart, spw, h->st, h->perm + k));
       CK(launch_sum_partials(h->tpart, spw, (int64_t)k * nj, h->W, h->st));
       s = allreduce(h, h->W, (size_t)k * nj, NCCL_SUM);
