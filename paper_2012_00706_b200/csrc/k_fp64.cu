@@ -514,6 +514,80 @@ __global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ G, int k
 }
 
 // ---------------------------------------------------------------------------
+// Cholesky for k > 143 (G does not fit shared memory): left-looking, panels of 16
+// columns.  Thread t owns row p0 + t of the panel: the update with the finished
+// columns streams L(:, l) from global (coalesced) against a 64 x 16 shared chunk
+// of L(p0:p0+16, l), then the panel is factored in shared memory and written back.
+// Same output convention as k_cholesky (R = L^T in the upper triangle, info).
+// ---------------------------------------------------------------------------
+constexpr int CH_NB = 16, CH_LC = 64;   // 16-column panels: 16 fp64 accumulators per thread at 1024 threads
+__global__ void __launch_bounds__(1024) k_cholesky_blocked(double* __restrict__ G, int k, int* __restrict__ info) {
+  extern __shared__ double pn[];                    // panel [k][CH_NB + 1]
+  __shared__ double lb[CH_LC][CH_NB];               // L(p0 + c, l0 + l)
+  __shared__ int bad;
+  const int t = threadIdx.x;
+  if (t == 0) bad = 0;
+  __syncthreads();
+  for (int p0 = 0; p0 < k; p0 += CH_NB) {
+    const int w = min(CH_NB, k - p0), rows = k - p0;
+    double acc[CH_NB];
+#pragma unroll
+    for (int c = 0; c < CH_NB; ++c) acc[c] = (t < rows && c < w) ? G[(int64_t)(p0 + t) + (int64_t)(p0 + c) * k] : 0.0;
+    for (int l0 = 0; l0 < p0; l0 += CH_LC) {
+      const int lw = min(CH_LC, p0 - l0);
+      __syncthreads();
+      for (int e = t; e < CH_LC * CH_NB; e += blockDim.x) {
+        const int l = e / CH_NB, c = e % CH_NB;
+        lb[l][c] = (l < lw && c < w) ? G[(int64_t)(p0 + c) + (int64_t)(l0 + l) * k] : 0.0;
+      }
+      __syncthreads();
+      if (t < rows) {
+        for (int l = 0; l < lw; ++l) {
+          const double a = G[(int64_t)(p0 + t) + (int64_t)(l0 + l) * k];
+#pragma unroll
+          for (int c = 0; c < CH_NB; ++c) acc[c] = fma(-a, lb[l][c], acc[c]);
+        }
+      }
+    }
+    if (t < rows) {
+#pragma unroll
+      for (int c = 0; c < CH_NB; ++c) pn[t * (CH_NB + 1) + c] = acc[c];
+    }
+    __syncthreads();
+    for (int c = 0; c < w; ++c) {                      // factor the panel
+      if (t == 0) {
+        const double d = pn[c * (CH_NB + 1) + c];
+        if (!(d > 0.0) && !bad) bad = p0 + c + 1;
+        pn[c * (CH_NB + 1) + c] = d > 0.0 ? sqrt(d) : 1.0;
+      }
+      __syncthreads();
+      const double djj = pn[c * (CH_NB + 1) + c];
+      if (t > c && t < rows) pn[t * (CH_NB + 1) + c] /= djj;
+      __syncthreads();
+      if (t > c && t < rows) {
+        const double lic = pn[t * (CH_NB + 1) + c];
+        for (int c2 = c + 1; c2 < w && c2 <= t; ++c2) pn[t * (CH_NB + 1) + c2] -= lic * pn[c2 * (CH_NB + 1) + c];
+      }
+      __syncthreads();
+    }
+    if (t < rows) {
+      for (int c = 0; c < w && c <= t; ++c) G[(int64_t)(p0 + t) + (int64_t)(p0 + c) * k] = pn[t * (CH_NB + 1) + c];
+    }
+    __syncthreads();
+  }
+  for (int64_t idx = t; idx < (int64_t)k * k; idx += blockDim.x) {
+    const int r = (int)(idx % k), c = (int)(idx / k);
+    if (c > r) G[r + (int64_t)c * k] = G[c + (int64_t)r * k];
+  }
+  __syncthreads();
+  for (int64_t idx = t; idx < (int64_t)k * k; idx += blockDim.x) {
+    const int r = (int)(idx % k), c = (int)(idx / k);
+    if (c < r) G[r + (int64_t)c * k] = 0.0;
+  }
+  if (t == 0) *info = bad;
+}
+
+// ---------------------------------------------------------------------------
 // Small left triangular solves on a block of 32 right-hand sides held in
 // shared memory (the fp64 triangular solve for P).  For column i of the block,
 // b = B(:, map[i]) (map = perm + k for W(:, J), or identity + k for R12):
@@ -629,13 +703,19 @@ cudaError_t launch_tsmm(const double* X, int64_t ldx, int k1, const double* Y, i
 
 cudaError_t launch_cholesky(double* G, int k, int* info, cudaStream_t st) {
   const size_t sm = (size_t)k * k * sizeof(double);
-  const size_t smem = sm <= 160 * 1024 ? sm : 0;
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(k_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_cholesky_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     set = true;
   }
-  k_cholesky<<<1, 1024, smem, st>>>(G, k, info);
+  if (sm <= 160 * 1024) {
+    k_cholesky<<<1, 1024, sm, st>>>(G, k, info);
+  } else if (k <= 1024 && (size_t)k * (CH_NB + 1) * 8 <= 200 * 1024 - sizeof(double) * CH_LC * CH_NB) {
+    k_cholesky_blocked<<<1, 1024, (size_t)k * (CH_NB + 1) * 8, st>>>(G, k, info);
+  } else {
+    k_cholesky<<<1, 1024, 0, st>>>(G, k, info);      // global-memory fallback (k > 700)
+  }
   return cudaGetLastError();
 }
 

@@ -304,3 +304,14 @@ def test_error_variants_and_spectral_norm(fmt, scaling):
             assert e2[0] <= ex[0] * (1 + 1e-9) and e2[0] >= ex[0] * (1 - 1e-3), (sk, e2, ex)
             assert abs(e2[1] - ex[1]) <= 1e-3 * ex[1]
     h.close()
+
+
+@pytest.mark.parametrize("m,n,k", [(8192, 700, 300), (4096, 300, 140)])
+def test_lsq_large_k_blocked_cholesky(m, n, k):
+    """k > 143: the Gram matrix no longer fits shared memory and the blocked
+    left-looking Cholesky runs; P must still match the oracle's Householder LSQ."""
+    rng = np.random.default_rng(m + k)
+    A = np.asfortranarray(rng.standard_normal((m, n)) @ np.diag(np.exp(-np.arange(n) / 200.0)))
+    out = run_gpu(A, "fp32", "none", k)
+    P_ref = coeffs_lsq(A, out["piv"])
+    assert np.linalg.norm(out["P"] - P_ref) <= 1e-10 * np.linalg.norm(P_ref)
