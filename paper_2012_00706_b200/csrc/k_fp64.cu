@@ -435,6 +435,134 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
   }
 }
 
+// ---------------------------------------------------------------------------
+// TN split-K GEMM with a TC_NS-stage cp.async pipeline (the A_I^T A_I, Q1^T Q1 and
+// Q1^T A_D(:, J) products of the LSQ refit): the copy engine moves 16-byte chunks
+// straight into shared memory TN_S - 1 stages ahead, so the DMMA loop never waits on
+// a register round trip.  Requires 16-byte aligned columns (even ld, aligned bases);
+// other shapes use k_dgemm.
+// ---------------------------------------------------------------------------
+constexpr int TN_S = 4;
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(dst)), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int MT>
+__global__ void __launch_bounds__(256, 1) k_dgemm_tn_async(GemmArgs g) {
+  constexpr int BM = 16 * MT;
+  extern __shared__ __align__(16) double dsm[];
+  double* As = dsm;                                  // [TN_S][BM][LDK]
+  double* Bs = dsm + TN_S * BM * LDK;                // [TN_S][GT][LDK]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int64_t n0 = (int64_t)blockIdx.y * GT;
+  const int64_t k_begin = (int64_t)blockIdx.z * g.k_per_split;
+  const int64_t k_end = min(g.K, k_begin + g.k_per_split);
+  const int nst = k_begin < k_end ? (int)((k_end - k_begin + GK - 1) / GK) : 0;
+  // B column pointers of this thread's 4 chunks (fixed over the K loop)
+  const double* bsrc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int idx = tid + q * 256, mn = idx >> 3;
+    const int64_t c = n0 + mn;
+    bsrc[q] = c < g.N ? g.Y + (g.ycmap ? (int64_t)g.ycmap[c] : c) * g.ldy : nullptr;
+  }
+  auto issue = [&](int st) {
+    const int buf = st % TN_S;
+    const int64_t kb = k_begin + (int64_t)st * GK;
+    for (int idx = tid; idx < BM * 8; idx += 256) {
+      const int mn = idx >> 3, kk = (idx & 7) * 2;
+      const int64_t i = m0 + mn, r = kb + kk;
+      const bool v = i < g.M && r < k_end;           // k_end even: pairs never straddle it
+      cp_async16(&As[(buf * BM + mn) * LDK + kk], v ? g.X + i * g.ldx + r : g.X, v);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid + q * 256, mn = idx >> 3, kk = (idx & 7) * 2;
+      const int64_t r = kb + kk;
+      const bool v = bsrc[q] != nullptr && r < k_end;
+      cp_async16(&Bs[(buf * GT + mn) * LDK + kk], v ? bsrc[q] + r : g.Y, v);
+    }
+  };
+  double acc[MT][4][2];
+#pragma unroll
+  for (int a = 0; a < MT; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll
+  for (int st = 0; st < TN_S - 1; ++st) {
+    if (st < nst) issue(st);
+    cp_async_commit();
+  }
+  const bool idle = m0 + wm * 8 * MT >= g.M || n0 + wn * 32 >= g.N;
+  for (int it = 0; it < nst; ++it) {
+    cp_async_wait<TN_S - 2>();
+    __syncthreads();
+    if (it + TN_S - 1 < nst) issue(it + TN_S - 1);
+    cp_async_commit();
+    const int buf = it % TN_S;
+    const int64_t krem = (k_end - (k_begin + (int64_t)it * GK) + 3) / 4;
+    const int ksteps = idle ? 0 : (krem < GK / 4 ? (int)krem : GK / 4);
+    const double* Ab = As + (size_t)buf * BM * LDK;
+    const double* Bb = Bs + (size_t)buf * GT * LDK;
+#pragma unroll
+    for (int ks = 0; ks < GK / 4; ++ks) {
+      if (ks >= ksteps) break;
+      double af[MT], bf[4];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) af[mt] = Ab[(wm * (8 * MT) + mt * 8 + gq) * LDK + ks * 4 + tq];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bf[nt] = Bb[(wn * 32 + nt * 8 + gq) * LDK + ks * 4 + tq];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
+    }
+  }
+  cp_async_wait<0>();
+  double* o = g.out + (int64_t)blockIdx.z * g.M * g.N;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int64_t i = m0 + wm * (8 * MT) + mt * 8 + gq;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
+        if (i < g.M && c < g.N) o[c * g.M + i] = acc[mt][nt][h];
+      }
+  }
+}
+
+template <int MT>
+static cudaError_t tn_async_launch_t(const GemmArgs& g, dim3 grid, cudaStream_t st) {
+  const size_t smem = (size_t)TN_S * (16 * MT + GT) * LDK * sizeof(double);
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(k_dgemm_tn_async<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  k_dgemm_tn_async<MT><<<grid, 256, smem, st>>>(g);
+  return cudaGetLastError();
+}
+static cudaError_t tn_async_launch(const GemmArgs& g, dim3 grid, cudaStream_t st, int mt) {
+  switch (mt) {
+    case 3: return tn_async_launch_t<3>(g, grid, st);
+    case 4: return tn_async_launch_t<4>(g, grid, st);
+    case 5: return tn_async_launch_t<5>(g, grid, st);
+    case 6: return tn_async_launch_t<6>(g, grid, st);
+    case 7: return tn_async_launch_t<7>(g, grid, st);
+    default: return tn_async_launch_t<8>(g, grid, st);
+  }
+}
+
 template <int MODE>
 static size_t dgemm_smem() {
   const int a = (MODE == GM_TN_PARTIAL) ? GT * LDK : GK * LDM;
@@ -698,6 +826,11 @@ cudaError_t launch_tsmm(const double* X, int64_t ldx, int k1, const double* Y, i
   g.out = part;
   const int mt = pick_mt(k1);
   dim3 grid((unsigned)((k1 + 16 * mt - 1) / (16 * mt)), (unsigned)((n1 + GT - 1) / GT), (unsigned)splits);
+  // the cp.async pipeline needs every 16-byte chunk aligned: even leading dimensions,
+  // aligned bases, and split boundaries on even rows (k_per_split is a multiple of 16)
+  const bool aligned = (ldx % 2 == 0) && (ldy % 2 == 0) && ((((uintptr_t)X) | ((uintptr_t)Y)) & 15) == 0 &&
+                       (m % 2 == 0);
+  if (aligned) return tn_async_launch(g, grid, st, mt);
   return dgemm_launch<GM_TN_PARTIAL>(g, grid, st, mt);
 }
 
