@@ -42,8 +42,11 @@ extern "C" {
 typedef struct mpid_ctx* id_handle;
 
 /* Low-precision storage formats, Table 1.  Arithmetic is fp32 in both
- * ("simulated half"). */
-typedef enum { ID_FP16 = 1, ID_FP32 = 2 } id_format;
+ * ("simulated half").  ID_FP64 is the paper's double ID (Algorithm 1,
+ * P:143-155; Â_D of P:196): fp64 storage and arithmetic, every product-then-add
+ * rounded twice (DMUL, DADD; reading R16); it needs a workspace sized
+ * with fmt = ID_FP64, the FFMA formation, and nb <= 8. */
+typedef enum { ID_FP16 = 1, ID_FP32 = 2, ID_FP64 = 3 } id_format;
 
 /* Range scaling before rounding (BASELINE.json configs[1]; reading R7):
  * NONE: s = 1; MAXABS: s = 1/max|a_ij|; POW2: s = 2^-ceil(log2 max|a_ij|). */
@@ -109,7 +112,11 @@ typedef struct {
 
 /* Bytes of device workspace for a shard of m_local rows, n columns, rank <= k_max,
  * store interval nb (0 = default), storage format fmt.  host_AD != 0 reserves room
- * for a device copy of a host-resident A_D. */
+ * for a device copy of a host-resident A_D.  ID_FP16 and ID_FP32 share one layout;
+ * ID_FP64 sizes the larger fp64 layout.  The handle carves its workspace for the
+ * format of the current call (id_qrcp_lowprec / id_round_only); switching between a
+ * low format and ID_FP64 re-carves it, which drops the cached CUDA graphs and the
+ * previous results, and fails with ID_ERR_DIM if k_max no longer fits. */
 size_t id_workspace_bytes(int64_t m_local, int64_t n, int32_t k_max, int32_t nb,
                           id_format fmt, int32_t host_AD);
 
@@ -159,8 +166,12 @@ id_status id_error(id_handle h, double* abs_fro, double* rel_fro);
 id_status id_error_ex(id_handle h, int32_t skeleton, int32_t norm, int32_t iters, double* abs_err,
                       double* rel_err);
 
-/* R (k_out x n fp32, columns in pivoted order, R_jj >= 0) into DEVICE memory. */
+/* R (k_out x n fp32, columns in pivoted order, R_jj >= 0, column-major, ldr >= k_out)
+ * into DEVICE memory (an ID_FP64 R is rounded to fp32). */
 id_status id_get_R(id_handle h, float* R_out, int64_t ldr);
+
+/* The same R in fp64 (exact for every format) into DEVICE memory. */
+id_status id_get_R_fp64(id_handle h, double* R_out, int64_t ldr);
 
 /* The full column permutation Z (host, n entries, 0-based original indices in
  * pivoted order; perm_out[0:k_out] = I, the rest is the order R's trailing
@@ -168,7 +179,7 @@ id_status id_get_R(id_handle h, float* R_out, int64_t ldr);
 id_status id_get_perm(id_handle h, int32_t* perm_out);
 
 /* A_L of this shard (m_local x n, column-major, ld >= m_local) into DEVICE memory:
- * uint16 fp16 bit patterns for ID_FP16, float for ID_FP32.  Valid after
+ * uint16 fp16 bit patterns for ID_FP16, float for ID_FP32, double for ID_FP64.  Valid after
  * id_qrcp_lowprec with the same fmt and before any later re-store (i.e. it is
  * the rounded input only when called right after id_round_only). */
 id_status id_get_AL(id_handle h, void* out, int64_t ld);

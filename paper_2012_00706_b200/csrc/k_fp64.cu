@@ -763,20 +763,22 @@ __global__ void __launch_bounds__(1024) k_trsm_left_block(const double* __restri
     for (int r = rg; r < k; r += 32) T[(int64_t)col * ldt + r] = sb[r * 33 + c];
 }
 
-// R (k x n fp32, row-major, pivoted order) -> fp64 col-major k x n
-__global__ void k_R_to_fp64(const float* __restrict__ R, int k, int n, double* __restrict__ Rd) {
+// R (k x n, fp32 or fp64, row-major, pivoted order) -> fp64 col-major k x n
+template <typename RT>
+__global__ void k_R_to_fp64(const RT* __restrict__ R, int k, int n, double* __restrict__ Rd) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)k * n) return;
   const int i = (int)(idx % k), c = (int)(idx / k);
   Rd[idx] = (double)R[(int64_t)i * n + c];
 }
 
-// R (k x n fp32 row-major) -> fp32 col-major k x n with leading dimension ldr
-__global__ void k_R_export(const float* __restrict__ R, int k, int n, float* __restrict__ out, int64_t ldr) {
+// R (k x n row-major) -> col-major k x n with leading dimension ldr (fp64 -> fp32 rounds)
+template <typename RT, typename OT>
+__global__ void k_R_export(const RT* __restrict__ R, int k, int n, OT* __restrict__ out, int64_t ldr) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)k * n) return;
   const int i = (int)(idx % k), c = (int)(idx / k);
-  out[(int64_t)c * ldr + i] = R[(int64_t)i * n + c];
+  out[(int64_t)c * ldr + i] = (OT)R[(int64_t)i * n + c];
 }
 
 // P(:, perm[j]) = e_j (j < k), P(:, perm[k + i]) = T(:, i); col-major k x n, ldp
@@ -867,15 +869,22 @@ cudaError_t launch_trsm_left_upper(const double* R1, const double* R2, int k, co
   return cudaGetLastError();
 }
 
-cudaError_t launch_R_to_fp64(const float* R, int k, int n, double* Rd, cudaStream_t st) {
+cudaError_t launch_R_to_fp64(int r64, const void* R, int k, int n, double* Rd, cudaStream_t st) {
   const int64_t tot = (int64_t)k * n;
-  k_R_to_fp64<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(R, k, n, Rd);
+  const unsigned nb = (unsigned)((tot + 255) / 256);
+  if (r64) k_R_to_fp64<double><<<nb, 256, 0, st>>>((const double*)R, k, n, Rd);
+  else k_R_to_fp64<float><<<nb, 256, 0, st>>>((const float*)R, k, n, Rd);
   return cudaGetLastError();
 }
 
-cudaError_t launch_R_export(const float* R, int k, int n, float* out, int64_t ldr, cudaStream_t st) {
+cudaError_t launch_R_export(int r64, const void* R, int k, int n, void* out, int o64, int64_t ldr,
+                            cudaStream_t st) {
   const int64_t tot = (int64_t)k * n;
-  k_R_export<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(R, k, n, out, ldr);
+  const unsigned nb = (unsigned)((tot + 255) / 256);
+  if (r64 && o64) k_R_export<double, double><<<nb, 256, 0, st>>>((const double*)R, k, n, (double*)out, ldr);
+  else if (r64) k_R_export<double, float><<<nb, 256, 0, st>>>((const double*)R, k, n, (float*)out, ldr);
+  else if (o64) k_R_export<float, double><<<nb, 256, 0, st>>>((const float*)R, k, n, (double*)out, ldr);
+  else k_R_export<float, float><<<nb, 256, 0, st>>>((const float*)R, k, n, (float*)out, ldr);
   return cudaGetLastError();
 }
 

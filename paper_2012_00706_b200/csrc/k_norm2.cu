@@ -16,7 +16,7 @@
 
 namespace mpid {
 
-// X(:, l) = fl_L(s A(:, perm[l])) / s   (fmt 1 = fp16, 2 = fp32; one RNE rounding from fp64)
+// X(:, l) = fl_L(s A(:, perm[l])) / s   (fmt 1 = fp16, 2 = fp32, 3 = fp64; one RNE rounding from fp64)
 __global__ void k_gather_lowp(const double* __restrict__ A, int64_t m, int64_t ld, const int* __restrict__ perm,
                               int fmt, const DevScalars* __restrict__ sc, double* __restrict__ X) {
   const int l = blockIdx.y;
@@ -24,7 +24,7 @@ __global__ void k_gather_lowp(const double* __restrict__ A, int64_t m, int64_t l
   if (r >= m) return;
   const double s = sc->scale;
   const double x = __dmul_rn(s, A[(int64_t)perm[l] * ld + r]);
-  const double q = fmt == 1 ? (double)__half2float(__double2half(x)) : (double)__double2float_rn(x);
+  const double q = fmt == 1 ? (double)__half2float(__double2half(x)) : fmt == 2 ? (double)__double2float_rn(x) : x;
   X[(int64_t)l * m + r] = q / s;
 }
 

@@ -21,6 +21,11 @@
 //               pair: update x2 += (-v_r) * f2, then w2 += x2 * u_r, s2 += x2 * x2.
 // mbarriers: full (TMA tx) -> prep (32 arrivals) -> consumers -> empty (NCW arrivals).
 // Bound: HBM.  Per element: 1 cvt + npend/2 + 1 FFMA2-equivalents on the FMA pipe.
+//
+// The same kernel runs the double ID's fp64 QRCP (Â_D of P:196; Algorithm 1):
+// T = double, every working quantity (u, v, f, the formed A~) in fp64, and each
+// product-then-add as a separately rounded DMUL + DADD (the oracle's fp64 model, reading
+// R16); the interleaved layout and the pipeline are unchanged, with 4x the bytes.
 #include "mpid_internal.cuh"
 
 namespace mpid {
@@ -81,26 +86,84 @@ template <> struct Chunk<float> {
   __device__ static __forceinline__ float get(const float* p, int i) { return p[i]; }
   __device__ static __forceinline__ float rnd(float a) { return a; }
 };
+template <> struct Chunk<double> {
+  __device__ static __forceinline__ void load2(const double* a, const double* b, double2* x) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 va = reinterpret_cast<const double2*>(a)[q], vb = reinterpret_cast<const double2*>(b)[q];
+      x[2 * q] = make_double2(va.x, vb.x);
+      x[2 * q + 1] = make_double2(va.y, vb.y);
+    }
+  }
+  __device__ static __forceinline__ void round_store2(double* a, double* b, double2* x, bool wa, bool wb) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (wa) reinterpret_cast<double2*>(a)[q] = make_double2(x[2 * q].x, x[2 * q + 1].x);
+      if (wb) reinterpret_cast<double2*>(b)[q] = make_double2(x[2 * q].y, x[2 * q + 1].y);
+    }
+  }
+  __device__ static __forceinline__ double get(const double* p, int i) { return p[i]; }
+  __device__ static __forceinline__ double rnd(double a) { return a; }
+};
+
+// working precision of a storage format: fp32 for fp16/fp32 storage, fp64 for fp64
+template <typename T> struct Work { using W = float; using W2 = float2; };
+template <> struct Work<double> { using W = double; using W2 = double2; };
+
+__device__ __forceinline__ float2 splat2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ double2 splat2(double v) { return make_double2(v, v); }
+// x + nv * f, one rounding (FFMA2) in fp32; DMUL then DADD in fp64 (reading R16)
+__device__ __forceinline__ float2 upd2(float nv, float2 f, float2 x) { return __ffma2_rn(splat2(nv), f, x); }
+__device__ __forceinline__ double2 upd2(double nv, double2 f, double2 x) {
+  return make_double2(__dadd_rn(__dmul_rn(nv, f.x), x.x), __dadd_rn(__dmul_rn(nv, f.y), x.y));
+}
+__device__ __forceinline__ float upd1(float nv, float f, float a) { return fmaf(nv, f, a); }
+__device__ __forceinline__ double upd1(double nv, double f, double a) { return __dadd_rn(__dmul_rn(nv, f), a); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ double2 mul2(double2 a, double2 b) {
+  return make_double2(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y));
+}
+__device__ __forceinline__ float2 mac2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ double2 mac2(double2 a, double2 b, double2 c) {
+  return make_double2(__dadd_rn(__dmul_rn(a.x, b.x), c.x), __dadd_rn(__dmul_rn(a.y, b.y), c.y));
+}
+// one rounding of an fp64 value to the working precision
+template <typename W> __device__ __forceinline__ W to_work(double x);
+template <> __device__ __forceinline__ float to_work<float>(double x) { return __double2float_rn(x); }
+template <> __device__ __forceinline__ double to_work<double>(double x) { return x; }
+// 8 consecutive working-precision values from shared memory (16 B aligned)
+__device__ __forceinline__ void load8(const float* p, float* v) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load8(const double* p, double* v) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double2 a = reinterpret_cast<const double2*>(p)[q];
+    v[2 * q] = a.x;
+    v[2 * q + 1] = a.y;
+  }
+}
 }  // namespace
 
 // shared-memory slot layout (per stage), all offsets 16-byte aligned
 struct SlotGeom {
   int data;   // GS * ncols * 8 * sizeof(T)
   int ucol;   // GS * 8 * sizeof(T)
-  int upend;  // PMAX * GS * 8 * 4   (raw pending u rows, TMA)
-  int us;     // GS * 8 * 4          (u of this step)
-  int nv;     // PMAX * GS * 8 * 4   (-v rows)
+  int upend;  // PMAX * GS * 8 * wsz   (raw pending u rows, TMA; wsz = sizeof(W))
+  int us;     // GS * 8 * wsz          (u of this step)
+  int nv;     // PMAX * GS * 8 * wsz   (-v rows)
   int total;
 };
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
-__host__ __device__ inline SlotGeom slot_geom(int GS, int ncols, int esz, int pmax) {
+__host__ __device__ inline SlotGeom slot_geom(int GS, int ncols, int esz, int pmax, int wsz) {
   SlotGeom g;
   g.data = 0;
   g.ucol = al16(GS * ncols * 8 * esz);
   g.upend = g.ucol + al16(GS * 8 * esz);
-  g.us = g.upend + al16(pmax * GS * 8 * 4);
-  g.nv = g.us + al16(GS * 8 * 4);
-  g.total = g.nv + al16(pmax * GS * 8 * 4);
+  g.us = g.upend + al16(pmax * GS * 8 * wsz);
+  g.nv = g.us + al16(GS * 8 * wsz);
+  g.total = g.nv + al16(pmax * GS * 8 * wsz);
   return g;
 }
 
@@ -112,6 +175,11 @@ constexpr int RED_BYTES = 1024 * 2 * 8;      // cross-warp partials (WR * CW * 6
 template <typename T, int PMAX>
 __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
   if (p.sc->done) return;
+  using W = typename Work<T>::W;
+  using W2 = typename Work<T>::W2;
+  constexpr int WSZ = (int)sizeof(W);
+  W* __restrict__ Ubuf = reinterpret_cast<W*>(p.U);
+  const W* __restrict__ Fbuf = reinterpret_cast<const W*>(p.F);
   extern __shared__ __align__(128) unsigned char smem[];
   const int n = p.n, j = p.j, npend = p.npend;
   const int GS = p.gs, NST = p.nst;
@@ -119,7 +187,7 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
   const int c_lo = j + 32 * p.chunks_per_split * blockIdx.y;   // CTA column range
   const int c_hi = min(n, c_lo + 32 * p.chunks_per_split);
   const int ncols = c_hi - c_lo;                                  // > 0 (host)
-  const SlotGeom geo = slot_geom(GS, p.ncols_slot, (int)sizeof(T), PMAX);
+  const SlotGeom geo = slot_geom(GS, p.ncols_slot, (int)sizeof(T), PMAX, WSZ);
   double* red = reinterpret_cast<double*>(smem + (size_t)NST * geo.total);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NST * geo.total + RED_BYTES);
   uint64_t* prep = full + NST;
@@ -176,7 +244,7 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
       const int64_t g0 = gb + (int64_t)i * GS;
       const int gsz = (int)((ge - g0) < GS ? (ge - g0) : GS);
       unsigned char* base = smem + (size_t)slot * geo.total;
-      const uint32_t bytes = (uint32_t)(gsz * rowbytes + gsz * 8 * sizeof(T) + npend * gsz * 8 * 4);
+      const uint32_t bytes = (uint32_t)(gsz * rowbytes + gsz * 8 * sizeof(T) + npend * gsz * 8 * WSZ);
       mbar_expect_tx(&full[slot], bytes);
       for (int r = 0; r < gsz; ++r) {
         tma_load(base + r * rowbytes, S + ((g0 + r) * n + c_lo) * RG, rowbytes, &full[slot]);
@@ -186,8 +254,8 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
 #pragma unroll
       for (int l = 0; l < PMAX; ++l)
         if (l < npend)
-          tma_load(base + geo.upend + l * GS * 8 * 4, p.U + (int64_t)slot_l[l] * p.m_pad + g0 * 8,
-                   gsz * 8 * 4, &full[slot]);
+          tma_load(base + geo.upend + l * GS * 8 * WSZ, Ubuf + (int64_t)slot_l[l] * p.m_pad + g0 * 8,
+                   gsz * 8 * WSZ, &full[slot]);
     }
     if (p.store) {
       for (int i = max(0, nst - NST); i < nst; ++i) {
@@ -202,17 +270,17 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
 
   if (warp == 1) {
     // ========================= prep warp ==========================
-    float fj[PMAX];
+    W fj[PMAX];
     double cl_[PMAX];
     int64_t tstep[PMAX];
 #pragma unroll
     for (int l = 0; l < PMAX; ++l) {
       const int sl = (p.j0 + l) % NSLOT;
-      fj[l] = (l < npend) ? p.F[(int64_t)sl * n + j] : 0.f;
+      fj[l] = (l < npend) ? Fbuf[(int64_t)sl * n + j] : W(0);
       cl_[l] = (l < npend) ? p.cvec[p.j0 + l] : 0.0;
       tstep[l] = p.j0 + l;
     }
-    float* __restrict__ Uj = p.U + (int64_t)(j % NSLOT) * p.m_pad;
+    W* __restrict__ Uj = Ubuf + (int64_t)(j % NSLOT) * p.m_pad;
     int slot = 0;
     uint32_t phase = 0;
     for (int i = 0; i < nst; ++i) {
@@ -220,28 +288,28 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
       const int gsz = (int)((ge - g0) < GS ? (ge - g0) : GS);
       unsigned char* base = smem + (size_t)slot * geo.total;
       const T* ucol = reinterpret_cast<const T*>(base + geo.ucol);
-      const float* upend = reinterpret_cast<const float*>(base + geo.upend);
-      float* us = reinterpret_cast<float*>(base + geo.us);
-      float* nv = reinterpret_cast<float*>(base + geo.nv);
+      const W* upend = reinterpret_cast<const W*>(base + geo.upend);
+      W* us = reinterpret_cast<W*>(base + geo.us);
+      W* nv = reinterpret_cast<W*>(base + geo.nv);
       mbar_wait(&full[slot], phase);
       for (int r = lane; r < gsz * 8; r += 32) {
         const int64_t rl = g0 * 8 + r;
         const int64_t rg = p.row_offset + rl;
         const bool real = rl < p.m_local;
-        float a = Chunk<T>::get(ucol + (r >> 3) * 8, r & 7);
+        W a = Chunk<T>::get(ucol + (r >> 3) * 8, r & 7);
 #pragma unroll
         for (int l = 0; l < PMAX; ++l) {
           if (l < npend) {
-            float v;
-            if (!real || rg < tstep[l]) v = 0.f;
-            else if (rg == tstep[l]) v = 1.f;
-            else v = __double2float_rn((double)upend[l * GS * 8 + r] * cl_[l]);
+            W v;
+            if (!real || rg < tstep[l]) v = W(0);
+            else if (rg == tstep[l]) v = W(1);
+            else v = to_work<W>((double)upend[l * GS * 8 + r] * cl_[l]);
             nv[l * GS * 8 + r] = -v;
-            a = fmaf(-v, fj[l], a);
+            a = upd1(-v, fj[l], a);
           }
         }
         if (p.store) a = Chunk<T>::rnd(a);
-        const float u = (real && rg >= j) ? a : 0.f;
+        const W u = (real && rg >= j) ? a : W(0);
         us[r] = u;
         if (blockIdx.y == 0) Uj[rl] = u;
       }
@@ -260,12 +328,12 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
   const int col1 = col0 + 32;
   const bool v0 = active && col0 < ncols, v1 = active && col1 < ncols;
   const int slot0 = p.j0 % NSLOT;
-  float2 f2[PMAX];
+  W2 f2[PMAX];
 #pragma unroll
   for (int l = 0; l < PMAX; ++l) {
     const int sl = (slot0 + l) % NSLOT;
-    f2[l] = make_float2((l < npend && v0) ? p.F[(int64_t)sl * n + c_lo + col0] : 0.f,
-                        (l < npend && v1) ? p.F[(int64_t)sl * n + c_lo + col1] : 0.f);
+    f2[l].x = (l < npend && v0) ? Fbuf[(int64_t)sl * n + c_lo + col0] : W(0);
+    f2[l].y = (l < npend && v1) ? Fbuf[(int64_t)sl * n + c_lo + col1] : W(0);
   }
   double aw0 = 0.0, aw1 = 0.0, as0 = 0.0, as1 = 0.0;
   const int64_t jloc = (int64_t)j - p.row_offset;
@@ -282,46 +350,44 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
     const int gjs = (gj >= g0 && gj < g0 + gsz) ? (int)(gj - g0) : -1;   // stage group holding row j
     unsigned char* base = smem + (size_t)slot * geo.total;
     T* data = reinterpret_cast<T*>(base);
-    const float* us = reinterpret_cast<const float*>(base + geo.us);
-    const float* nv = reinterpret_cast<const float*>(base + geo.nv);
+    const W* us = reinterpret_cast<const W*>(base + geo.us);
+    const W* nv = reinterpret_cast<const W*>(base + geo.nv);
     mbar_wait(&prep[slot], phase);
     if (active && (v0 || v1)) {
       for (int gl = rw; gl < gsz; gl += WR) {
         T* d0 = data + (size_t)gl * ncols * 8 + o0;
         T* d1 = data + (size_t)gl * ncols * 8 + o1;
-        float2 x[8];
+        W2 x[8];
         Chunk<T>::load2(d0, d1, x);
 #pragma unroll
         for (int l = 0; l < PMAX; ++l) {
           if (l < npend) {
-            const float4 va = *reinterpret_cast<const float4*>(nv + l * GS * 8 + gl * 8);
-            const float4 vb = *reinterpret_cast<const float4*>(nv + l * GS * 8 + gl * 8 + 4);
-            const float vv[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+            W vv[8];
+            load8(nv + l * GS * 8 + gl * 8, vv);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) x[q] = __ffma2_rn(make_float2(vv[q], vv[q]), f2[l], x[q]);
+            for (int q = 0; q < 8; ++q) x[q] = upd2(vv[q], f2[l], x[q]);
           }
         }
         // invalid lanes alias column 0's chunk: they must not write it back
         if (p.store) Chunk<T>::round_store2(d0, d1, x, v0, v1);
-        const float4 ua = *reinterpret_cast<const float4*>(us + gl * 8);
-        const float4 ub = *reinterpret_cast<const float4*>(us + gl * 8 + 4);
-        const float uu[8] = {ua.x, ua.y, ua.z, ua.w, ub.x, ub.y, ub.z, ub.w};
+        W uu[8];
+        load8(us + gl * 8, uu);
         if (gl == gjs) {                                  // the group holding row j (rare)
-          float2 xj = x[0];
+          W2 xj = x[0];
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             if (q == jr) xj = x[q];
-            if (q < jr) x[q] = make_float2(0.f, 0.f);
+            if (q < jr) x[q] = splat2(W(0));
           }
           if (v0) p.xr[c_lo + col0] = xj.x;
           if (v1) p.xr[c_lo + col1] = xj.y;
         }
-        float2 pw = __fmul2_rn(x[0], make_float2(uu[0], uu[0]));
-        float2 ps = __fmul2_rn(x[0], x[0]);
+        W2 pw = mul2(x[0], splat2(uu[0]));
+        W2 ps = mul2(x[0], x[0]);
 #pragma unroll
         for (int q = 1; q < 8; ++q) {
-          pw = __ffma2_rn(x[q], make_float2(uu[q], uu[q]), pw);
-          ps = __ffma2_rn(x[q], x[q], ps);
+          pw = mac2(x[q], splat2(uu[q]), pw);
+          ps = mac2(x[q], x[q], ps);
         }
         aw0 += (double)pw.x;
         aw1 += (double)pw.y;
@@ -381,6 +447,7 @@ template <typename T>
 static cudaError_t launch_ws_fmt(PassParams p, int max_ctas, int* gx_out, cudaStream_t st) {
   const int n = p.n, j = p.j;
   const int esz = (int)sizeof(T);
+  const int wsz = (int)sizeof(typename Work<T>::W);
   const int nchunks = (n - j + 31) / 32;
   // column splits: at most NCW * 64 = 1024 columns per CTA
   const int max_chunks = NCW * COLS_PER_WARP / 32;
@@ -394,16 +461,16 @@ static cudaError_t launch_ws_fmt(PassParams p, int max_ctas, int* gx_out, cudaSt
   p.cw = CW;
   p.wr = WR;
   const int pmax = p.npend <= 1 ? 1 : p.npend <= 2 ? 2 : p.npend <= 4 ? 4 : p.npend <= 8 ? 8 : 16;
-  if (p.npend > pmax || pmax > NB_MAX) return cudaErrorInvalidValue;
+  if (p.npend > pmax || pmax > NB_MAX || (wsz == 8 && pmax > 8)) return cudaErrorInvalidValue;
   // stage = GS row groups: ~48 KB of matrix data, a multiple of WR, at most 64 groups
   const int rowbytes = ncols * 8 * esz;
   int gpw = std::max(1, (48 * 1024) / (rowbytes * WR));
   int GS = std::min(64, WR * gpw);
-  SlotGeom g = slot_geom(GS, ncols, esz, pmax);
+  SlotGeom g = slot_geom(GS, ncols, esz, pmax, wsz);
   const size_t fixed = RED_BYTES + 3 * 8 * 8 + 64;
   while (GS > 1 && 2 * (size_t)g.total + fixed > (size_t)PASS_SMEM_MAX) {
     GS = std::max(1, GS / 2);
-    g = slot_geom(GS, ncols, esz, pmax);
+    g = slot_geom(GS, ncols, esz, pmax, wsz);
   }
   int nst = (int)std::min<size_t>(8, (PASS_SMEM_MAX - fixed) / (size_t)g.total);
   if (nst < 2) return cudaErrorInvalidConfiguration;
@@ -420,13 +487,17 @@ static cudaError_t launch_ws_fmt(PassParams p, int max_ctas, int* gx_out, cudaSt
     case 2: return launch_ws_t<T, 2>(p, grid, smem, st);
     case 4: return launch_ws_t<T, 4>(p, grid, smem, st);
     case 8: return launch_ws_t<T, 8>(p, grid, smem, st);
-    default: return launch_ws_t<T, 16>(p, grid, smem, st);
+    default:
+      if constexpr (sizeof(T) < 8) return launch_ws_t<T, 16>(p, grid, smem, st);   // fp64: nb <= 8
+      return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_pass_tma(int fmt, PassParams p, int max_ctas, int* gx_out, cudaStream_t st) {
-  return fmt == 1 ? launch_ws_fmt<__half>(p, max_ctas, gx_out, st)
-                  : launch_ws_fmt<float>(p, max_ctas, gx_out, st);
+  if (fmt == 1) return launch_ws_fmt<__half>(p, max_ctas, gx_out, st);
+  if (fmt == 2) return launch_ws_fmt<float>(p, max_ctas, gx_out, st);
+  if (fmt == 3) return launch_ws_fmt<double>(p, max_ctas, gx_out, st);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace mpid

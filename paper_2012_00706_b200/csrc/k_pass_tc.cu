@@ -229,8 +229,8 @@ __global__ void __launch_bounds__(TC_BLOCK, 1) k_pass_tc(PassParams p, const __g
       const int ci = (i >> 5) * 31 + (i & 31) - 1;
       float f = 0.f;
       if (l < npend) {
-        if ((i & 31) == 0) f = p.F[(int64_t)((p.j0 + l) % NSLOT) * n + j];
-        else if (ci < ncols) f = p.F[(int64_t)((p.j0 + l) % NSLOT) * n + c_lo + ci];
+        if ((i & 31) == 0) f = reinterpret_cast<const float*>(p.F)[(int64_t)((p.j0 + l) % NSLOT) * n + j];
+        else if (ci < ncols) f = reinterpret_cast<const float*>(p.F)[(int64_t)((p.j0 + l) % NSLOT) * n + c_lo + ci];
       }
       float hi, lo;
       split_tf32(f, hi, lo);
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1) k_pass_tc(PassParams p, const __g
     const int64_t jloc = (int64_t)j - p.row_offset;
     const int64_t gj = (jloc >= 0 && jloc < p.m_local) ? (jloc >> 3) : -1;
     const int jr = (int)(jloc & 7);
-    float* __restrict__ Uj = p.U + (int64_t)(j % NSLOT) * p.m_pad;
+    float* __restrict__ Uj = reinterpret_cast<float*>(p.U) + (int64_t)(j % NSLOT) * p.m_pad;
     double aw = 0.0, as = 0.0;
     int slot = 0, acc = 0;
     uint32_t phase = 0, aphase = 0;

@@ -122,9 +122,15 @@ __device__ double block_sum(double v) {
   return r;
 }
 
+// W = working precision of F and R: fp32, or fp64 for the double QRCP (fmt 3)
+template <typename W> __device__ __forceinline__ W to_w(double x);
+template <> __device__ __forceinline__ float to_w<float>(double x) { return __double2float_rn(x); }
+template <> __device__ __forceinline__ double to_w<double>(double x) { return x; }
+
+template <typename W>
 __global__ void __launch_bounds__(1024) k_reflector(const double* __restrict__ red, int n, int j,
-                                                    int k_max, float* __restrict__ F,
-                                                    float* __restrict__ R, double* __restrict__ beta_out,
+                                                    int k_max, W* __restrict__ F,
+                                                    W* __restrict__ R, double* __restrict__ beta_out,
                                                     double* __restrict__ cvec, double* __restrict__ tau,
                                                     const int* __restrict__ perm,
                                                     DevScalars* __restrict__ sc) {
@@ -145,7 +151,8 @@ __global__ void __launch_bounds__(1024) k_reflector(const double* __restrict__ r
   }
   const double sj = red[n + j];
   const double uj = red[2 * n + j];
-  if (!(sj >= (double)FLT_MIN)) {                    // pivot norm^2 underflows fp32
+  const double tiny = sizeof(W) == 8 ? DBL_MIN : (double)FLT_MIN;
+  if (!(sj >= tiny)) {                               // pivot norm^2 underflows
     __syncthreads();
     if (threadIdx.x == 0) {
       sc->status = 4;  // ID_ERR_UNDERFLOW
@@ -167,12 +174,12 @@ __global__ void __launch_bounds__(1024) k_reflector(const double* __restrict__ r
   double rest = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     if (i < j) {
-      R[(int64_t)j * n + i] = 0.f;
+      R[(int64_t)j * n + i] = W(0);
       continue;
     }
     const double rraw = red[i] / beta;
-    R[(int64_t)j * n + i] = __double2float_rn(rraw * sgn);
-    F[(int64_t)slot * n + i] = __double2float_rn(red[2 * n + i] - rraw);
+    R[(int64_t)j * n + i] = to_w<W>(rraw * sgn);
+    F[(int64_t)slot * n + i] = to_w<W>(red[2 * n + i] - rraw);
     if (i > j) {
       const double vn = red[n + i] - rraw * rraw;      // one-step downdate from exact s_i
       rest += fmax(vn, 0.0);
@@ -216,9 +223,9 @@ __global__ void __launch_bounds__(1024) k_init_pivot(const double* __restrict__ 
 
 // swap columns jn <-> p (p = sc->pivot) in S (all row groups), in the pending
 // f vectors of steps [j0, jn), in R rows [0, jn), and in perm.
-template <typename T>
+template <typename T, typename W>
 __global__ void k_swap(T* __restrict__ S, int64_t ngroups, int n, int jn, int j0,
-                       float* __restrict__ F, float* __restrict__ R, int* __restrict__ perm,
+                       W* __restrict__ F, W* __restrict__ R, int* __restrict__ perm,
                        T* __restrict__ Sj, const DevScalars* __restrict__ sc) {
   if (sc->done) return;
   const int p = sc->pivot;
@@ -227,33 +234,33 @@ __global__ void k_swap(T* __restrict__ S, int64_t ngroups, int n, int jn, int j0
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g < ngroups) {
     // the new pivot column jn, also copied to the contiguous buffer Sj (tcgen05 pass)
-    constexpr int W = (int)sizeof(T) / 2;   // uint4 words per 8-row chunk
+    constexpr int NW = (int)sizeof(T) / 2;   // uint4 words per 8-row chunk
     uint4* a = reinterpret_cast<uint4*>(S + (g * n + jn) * RG);
     uint4* b = reinterpret_cast<uint4*>(S + (g * n + p) * RG);
-    uint4 ta[W], tb[W];
+    uint4 ta[NW], tb[NW];
 #pragma unroll
-    for (int w = 0; w < W; ++w) { ta[w] = a[w]; tb[w] = sw ? b[w] : ta[w]; }
+    for (int w = 0; w < NW; ++w) { ta[w] = a[w]; tb[w] = sw ? b[w] : ta[w]; }
     if (sw) {
 #pragma unroll
-      for (int w = 0; w < W; ++w) { a[w] = tb[w]; b[w] = ta[w]; }
+      for (int w = 0; w < NW; ++w) { a[w] = tb[w]; b[w] = ta[w]; }
     }
     if (Sj) {
       uint4* d = reinterpret_cast<uint4*>(Sj + g * RG);
 #pragma unroll
-      for (int w = 0; w < W; ++w) d[w] = tb[w];
+      for (int w = 0; w < NW; ++w) d[w] = tb[w];
     }
   }
   if (!sw) return;
   if (blockIdx.x == 0) {
     for (int t = j0 + threadIdx.x; t < jn; t += blockDim.x) {
-      float* f = F + (int64_t)(t % NSLOT) * n;
-      const float x = f[jn];
+      W* f = F + (int64_t)(t % NSLOT) * n;
+      const W x = f[jn];
       f[jn] = f[p];
       f[p] = x;
     }
     for (int t = threadIdx.x; t < jn; t += blockDim.x) {
-      float* r = R + (int64_t)t * n;
-      const float x = r[jn];
+      W* r = R + (int64_t)t * n;
+      const W x = r[jn];
       r[jn] = r[p];
       r[p] = x;
     }
@@ -273,11 +280,13 @@ cudaError_t launch_pass_reduce(const double* part, int gx, int n, int j, const d
   return cudaGetLastError();
 }
 
-cudaError_t launch_reflector(const double* red, int n, int j, int k_max, int nslot_f, float* F,
-                             float* R, double* beta, double* cvec, double* tau, const int* perm,
-                             DevScalars* sc, cudaStream_t st) {
-  (void)nslot_f;
-  k_reflector<<<1, 1024, 0, st>>>(red, n, j, k_max, F, R, beta, cvec, tau, perm, sc);
+cudaError_t launch_reflector(int fmt, const double* red, int n, int j, int k_max, void* F, void* R,
+                             double* beta, double* cvec, double* tau, const int* perm, DevScalars* sc,
+                             cudaStream_t st) {
+  if (fmt == 3)
+    k_reflector<double><<<1, 1024, 0, st>>>(red, n, j, k_max, (double*)F, (double*)R, beta, cvec, tau, perm, sc);
+  else
+    k_reflector<float><<<1, 1024, 0, st>>>(red, n, j, k_max, (float*)F, (float*)R, beta, cvec, tau, perm, sc);
   return cudaGetLastError();
 }
 
@@ -288,13 +297,18 @@ cudaError_t launch_init_pivot(const double* norms, int n, int* perm, DevScalars*
 }
 
 cudaError_t launch_swap(int fmt, void* S, int64_t ngroups, int n, int jn, int j0, int steps_done,
-                        float* F, float* R, int* perm, void* Sj, DevScalars* sc, cudaStream_t st) {
+                        void* F, void* R, int* perm, void* Sj, DevScalars* sc, cudaStream_t st) {
   (void)steps_done;
   const unsigned nb = (unsigned)((ngroups + 255) / 256);
   if (fmt == 1)
-    k_swap<__half><<<nb, 256, 0, st>>>((__half*)S, ngroups, n, jn, j0, F, R, perm, (__half*)Sj, sc);
+    k_swap<__half, float><<<nb, 256, 0, st>>>((__half*)S, ngroups, n, jn, j0, (float*)F, (float*)R, perm,
+                                               (__half*)Sj, sc);
+  else if (fmt == 2)
+    k_swap<float, float><<<nb, 256, 0, st>>>((float*)S, ngroups, n, jn, j0, (float*)F, (float*)R, perm,
+                                              (float*)Sj, sc);
   else
-    k_swap<float><<<nb, 256, 0, st>>>((float*)S, ngroups, n, jn, j0, F, R, perm, (float*)Sj, sc);
+    k_swap<double, double><<<nb, 256, 0, st>>>((double*)S, ngroups, n, jn, j0, (double*)F, (double*)R, perm,
+                                                (double*)Sj, sc);
   return cudaGetLastError();
 }
 

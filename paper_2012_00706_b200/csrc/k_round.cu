@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int
                                                T* __restrict__ S, double* __restrict__ part,
                                                double* __restrict__ aux,
                                                DevScalars* __restrict__ sc) {
-  constexpr int TR = 256;                          // rows per tile
+  constexpr int TR = sizeof(T) == 8 ? 128 : 256;   // rows per tile (fp64: the tile fits 48 KB)
   constexpr int PAD = 16 / sizeof(T);              // keep 16 B alignment, spread banks
   __shared__ __align__(16) T tile[32][TR + PAD];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -148,14 +148,17 @@ __global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int
         const double x = __dmul_rn(s, av);
         T v;
         double d;
-        if (sizeof(T) == 2) {
+        if constexpr (sizeof(T) == 2) {
           const __half hv = __double2half(x);          // cvt.rn.f16.f64: single RNE rounding
           d = (double)__half2float(hv);
           v = *reinterpret_cast<const T*>(&hv);
-        } else {
+        } else if constexpr (sizeof(T) == 4) {
           const float fv = __double2float_rn(x);       // cvt.rn.f32.f64
           d = (double)fv;
           v = *reinterpret_cast<const T*>(&fv);
+        } else {
+          d = x;                                       // fp64: A_L = s A_D (one rounding of the product)
+          v = x;
         }
         inf |= isinf(d) ? 1 : 0;
         colsq[q] = fma(d, d, colsq[q]);
@@ -172,12 +175,8 @@ __global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int
       if (c < n) {
         const uint4* src = reinterpret_cast<const uint4*>(&tile[lane][g * 8]);
         uint4* dst = reinterpret_cast<uint4*>(S + ((t * (TR / 8) + g) * n + c) * 8);
-        if (sizeof(T) == 2) {
-          __stcs(dst, src[0]);
-        } else {
-          __stcs(dst, src[0]);
-          __stcs(dst + 1, src[1]);
-        }
+#pragma unroll
+        for (int w = 0; w < (int)sizeof(T) / 2; ++w) __stcs(dst + w, src[w]);
       }
     }
   }
@@ -247,8 +246,10 @@ cudaError_t launch_round(int fmt, const double* A, int64_t m, int64_t m_pad, int
   double* aux = part + (int64_t)gy * n;
   if (fmt == 1)
     k_round<__half><<<grid, 256, 0, st>>>(A, m, m_pad / 8, n, ld, (__half*)S, part, aux, sc);
-  else
+  else if (fmt == 2)
     k_round<float><<<grid, 256, 0, st>>>(A, m, m_pad / 8, n, ld, (float*)S, part, aux, sc);
+  else
+    k_round<double><<<grid, 256, 0, st>>>(A, m, m_pad / 8, n, ld, (double*)S, part, aux, sc);
   return cudaGetLastError();
 }
 cudaError_t launch_sum_partials(const double* part, int splits, int64_t len, double* out,
@@ -262,8 +263,10 @@ cudaError_t launch_export_S(int fmt, const void* S, int64_t m_local, int n, void
   const unsigned nb = (unsigned)((tot + 255) / 256);
   if (fmt == 1)
     k_export<__half><<<nb, 256, 0, st>>>((const __half*)S, m_local, n, (__half*)out, ld);
-  else
+  else if (fmt == 2)
     k_export<float><<<nb, 256, 0, st>>>((const float*)S, m_local, n, (float*)out, ld);
+  else
+    k_export<double><<<nb, 256, 0, st>>>((const double*)S, m_local, n, (double*)out, ld);
   return cudaGetLastError();
 }
 

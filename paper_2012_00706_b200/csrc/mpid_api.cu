@@ -119,20 +119,20 @@ int splits_for(int64_t k1, int64_t n1, int64_t m, size_t cap) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(s, (int64_t)(cap / (size_t)(k1 * n1))));
 }
 
+// sbytes: 4 = room for fp16/fp32 storage with fp32 working vectors; 8 = also the fp64 QRCP
 Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
   Layout L{};
   const int64_t mp = m_pad_of(m_local);
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
   L.AD = take(host_AD ? (size_t)m_local * n * 8 : 0);
-  L.S = take((size_t)mp * n * 4);  // room for fp32 storage (fp16 uses half)
-  (void)sbytes;
-  L.U = take((size_t)NSLOT * mp * 4);
-  L.F = take((size_t)NSLOT * n * 4);
+  L.S = take((size_t)mp * n * sbytes);
+  L.U = take((size_t)NSLOT * mp * sbytes);
+  L.F = take((size_t)NSLOT * n * sbytes);
   L.Vh = take((size_t)(mp + 128) * NB_MAX * 4);   // tcgen05 pass: panel V operand (hi / lo)
   L.Vl = take((size_t)(mp + 128) * NB_MAX * 4);
   L.Sj = take((size_t)(mp + 128) * 4);             // the pivot column of S, contiguous
-  L.R = take((size_t)k * n * 4);
+  L.R = take((size_t)k * n * sbytes);
   L.part = take((size_t)pass_gx_cap() * 2 * n * 8);
   L.red = take((size_t)3 * n * 8);
   L.xr = take((size_t)n * 8);
@@ -177,9 +177,11 @@ struct mpid_ctx {
   Layout L{};
   int64_t k_cap = 0;
   bool host_AD = false;
-  // device pointers
+  int sbytes = 4;                 // workspace layout: 8 = sized for the fp64 QRCP too
+  // device pointers (U, F, R in the working precision: fp32, fp64 for ID_FP64)
   void* S = nullptr;
-  float *U = nullptr, *F = nullptr, *R = nullptr, *Vh = nullptr, *Vl = nullptr;
+  void *U = nullptr, *F = nullptr, *R = nullptr;
+  float *Vh = nullptr, *Vl = nullptr;
   void* Sj = nullptr;
   alignas(64) unsigned char tmapS[2][128];   // CUtensorMap of S for fp16 / fp32 (tcgen05 pass)
   int tmap_ok[2] = {-1, -1};
@@ -245,6 +247,79 @@ static id_status allreduce(mpid_ctx* h, double* buf, size_t count, int op) {
   return ID_OK;
 }
 
+// (Re)carve the workspace for working precision sbytes (4: fp16/fp32 QRCP, 8: also the
+// fp64 QRCP) at the largest k it holds.  A_D's copy (offset 0) and S's offset are the
+// same in both layouts; every pointer after them moves, so captured graphs are dropped.
+static id_status relayout(mpid_ctx* h, int sbytes) {
+  const int64_t m_local = h->m_local, n = h->n;
+  int64_t lo = 0, hi = std::min<int64_t>(n, h->m_global);  // largest k with layout(k) <= ws_bytes
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) / 2;
+    if (layout(m_local, n, mid, h->host_AD, sbytes).total <= h->ws_bytes) lo = mid;
+    else hi = mid - 1;
+  }
+  if (lo <= 0) return fail(h, ID_ERR_DIM, "workspace too small for %s", sbytes == 8 ? "ID_FP64" : "k = 1");
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+  h->graphs.clear();
+  h->graph_launches.clear();
+  h->have_qr = h->have_coef = false;
+  h->sbytes = sbytes;
+  const int64_t kmax = lo;
+  h->k_cap = kmax;
+  h->L = layout(m_local, n, kmax, h->host_AD, sbytes);
+  const Layout& L = h->L;
+  char* w = h->ws;
+  h->S = w + L.S;
+  h->U = w + L.U;
+  h->F = w + L.F;
+  h->Vh = (float*)(w + L.Vh);
+  h->Vl = (float*)(w + L.Vl);
+  h->Sj = w + L.Sj;
+  h->tmap_ok[0] = encode_tmap_S(h->tmapS[0], h->S, 1, h->m_pad / 8, (int)n);
+  h->tmap_ok[1] = encode_tmap_S(h->tmapS[1], h->S, 2, h->m_pad / 8, (int)n);
+  h->R = w + L.R;
+  h->part = (double*)(w + L.part);
+  h->red = (double*)(w + L.red);
+  h->xr = (double*)(w + L.xr);
+  h->norms = (double*)(w + L.norms);
+  h->perm = (int*)(w + L.perm);
+  h->beta = (double*)(w + L.scal3);
+  h->cvec = h->beta + kmax;
+  h->tau = h->cvec + kmax;
+  h->sc = (DevScalars*)(w + L.sc);
+  h->maxpart = (double*)(w + L.maxpart);
+  h->rpart = (double*)(w + L.rpart);
+  h->AI = (double*)(w + L.AI);
+  h->Q1 = (double*)(w + L.Q1);
+  h->G1 = (double*)(w + L.G1);
+  h->G2 = (double*)(w + L.G2);
+  h->W = (double*)(w + L.W);
+  h->tpart = (double*)(w + L.tpart);
+  h->Rd = (double*)(w + L.Rd);
+  h->T = (double*)(w + L.T);
+  h->Pw = (double*)(w + L.Pw);
+  h->epart = (double*)(w + L.epart);
+  h->Ik = (double*)(w + L.Ik);
+  h->Rinv = (double*)(w + L.Rinv);
+  h->py = (double*)(w + L.py);
+  h->pvec = (double*)(w + L.pvec);
+  h->info = (int*)(w + L.misc);
+  h->err2 = (double*)(w + L.misc + 64);
+  h->normAD_spec = -1.0;
+  // zero U (padding rows must stay 0); S is fully written by the rounding kernel
+  if (cudaMemsetAsync(h->U, 0, (size_t)NSLOT * h->m_pad * sbytes, h->st) != cudaSuccess ||
+      // the V operand's unused K columns are multiplied by zero F entries: keep them finite
+      cudaMemsetAsync(h->Vh, 0, (size_t)(h->m_pad + 128) * NB_MAX * 4, h->st) != cudaSuccess ||
+      cudaMemsetAsync(h->Vl, 0, (size_t)(h->m_pad + 128) * NB_MAX * 4, h->st) != cudaSuccess)
+    return fail(h, ID_ERR_CUDA, "workspace memset failed");
+  return ID_OK;
+}
+// the layout a call in format fmt needs
+static id_status ensure_layout(mpid_ctx* h, int fmt) {
+  const int sb = fmt == ID_FP64 ? 8 : 4;
+  return h->sbytes == sb ? ID_OK : relayout(h, sb);
+}
+
 extern "C" {
 
 const char* id_version(void) { return "mpid 0.1 (sm_100a; arXiv 2012.00706 mixed-precision ID)"; }
@@ -253,7 +328,7 @@ size_t id_workspace_bytes(int64_t m_local, int64_t n, int32_t k_max, int32_t nb,
                           int32_t host_AD) {
   (void)nb;
   if (m_local <= 0 || n <= 0 || k_max <= 0) return 0;
-  return layout(m_local, n, k_max, host_AD, fmt == ID_FP16 ? 2 : 4).total;
+  return layout(m_local, n, k_max, host_AD, fmt == ID_FP64 ? 8 : 4).total;
 }
 
 id_status id_create(id_handle* hp, const double* A_D, int64_t m_global, int64_t m_local,
@@ -284,58 +359,10 @@ id_status id_create(id_handle* hp, const double* A_D, int64_t m_global, int64_t 
   cudaError_t pe = cudaPointerGetAttributes(&pa, A_D);
   if (pe != cudaSuccess) cudaGetLastError();
   h->host_AD = (pe != cudaSuccess) || pa.type == cudaMemoryTypeHost || pa.type == cudaMemoryTypeUnregistered;
-  // the largest k this workspace supports
-  int64_t lo = 0, hi = std::min<int64_t>(n, m_global);  // largest k with layout(k) <= ws_bytes
-  while (lo < hi) {
-    const int64_t mid = (lo + hi + 1) / 2;
-    if (layout(m_local, n, mid, h->host_AD, 4).total <= ws_bytes) lo = mid;
-    else hi = mid - 1;
-  }
-  const int64_t kmax = lo;
-  if (kmax <= 0) {
+  if (relayout(h, 4) != ID_OK) {
     delete h;
     return ID_ERR_DIM;
   }
-  h->k_cap = kmax;
-  h->L = layout(m_local, n, kmax, h->host_AD, 4);
-  const Layout& L = h->L;
-  char* w = h->ws;
-  h->S = w + L.S;
-  h->U = (float*)(w + L.U);
-  h->F = (float*)(w + L.F);
-  h->Vh = (float*)(w + L.Vh);
-  h->Vl = (float*)(w + L.Vl);
-  h->Sj = w + L.Sj;
-  h->tmap_ok[0] = encode_tmap_S(h->tmapS[0], h->S, 1, h->m_pad / 8, (int)n);
-  h->tmap_ok[1] = encode_tmap_S(h->tmapS[1], h->S, 2, h->m_pad / 8, (int)n);
-  h->R = (float*)(w + L.R);
-  h->part = (double*)(w + L.part);
-  h->red = (double*)(w + L.red);
-  h->xr = (double*)(w + L.xr);
-  h->norms = (double*)(w + L.norms);
-  h->perm = (int*)(w + L.perm);
-  h->beta = (double*)(w + L.scal3);
-  h->cvec = h->beta + kmax;
-  h->tau = h->cvec + kmax;
-  h->sc = (DevScalars*)(w + L.sc);
-  h->maxpart = (double*)(w + L.maxpart);
-  h->rpart = (double*)(w + L.rpart);
-  h->AI = (double*)(w + L.AI);
-  h->Q1 = (double*)(w + L.Q1);
-  h->G1 = (double*)(w + L.G1);
-  h->G2 = (double*)(w + L.G2);
-  h->W = (double*)(w + L.W);
-  h->tpart = (double*)(w + L.tpart);
-  h->Rd = (double*)(w + L.Rd);
-  h->T = (double*)(w + L.T);
-  h->Pw = (double*)(w + L.Pw);
-  h->epart = (double*)(w + L.epart);
-  h->Ik = (double*)(w + L.Ik);
-  h->Rinv = (double*)(w + L.Rinv);
-  h->py = (double*)(w + L.py);
-  h->pvec = (double*)(w + L.pvec);
-  h->info = (int*)(w + L.misc);
-  h->err2 = (double*)(w + L.misc + 64);
   for (auto& e : h->ev) {
     if (cudaEventCreate(&e) != cudaSuccess) { delete h; return ID_ERR_CUDA; }
   }
@@ -346,7 +373,7 @@ id_status id_create(id_handle* hp, const double* A_D, int64_t m_global, int64_t 
     return ID_ERR_CUDA;
   }
   if (h->host_AD) {
-    double* dst = (double*)(w + L.AD);
+    double* dst = (double*)(h->ws + h->L.AD);
     cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)m_local * 8, A_D, (size_t)ld * 8, (size_t)m_local * 8,
                                       (size_t)n, cudaMemcpyHostToDevice, h->st);
     if (e != cudaSuccess) {
@@ -360,11 +387,6 @@ id_status id_create(id_handle* hp, const double* A_D, int64_t m_global, int64_t 
     h->AD = A_D;
     h->ld = ld;
   }
-  // zero U (padding rows must stay 0); S is fully written by the rounding kernel
-  cudaMemsetAsync(h->U, 0, (size_t)NSLOT * h->m_pad * 4, h->st);
-  // the V operand's unused K columns are multiplied by zero F entries: keep them finite
-  cudaMemsetAsync(h->Vh, 0, (size_t)(h->m_pad + 128) * NB_MAX * 4, h->st);
-  cudaMemsetAsync(h->Vl, 0, (size_t)(h->m_pad + 128) * NB_MAX * 4, h->st);
   *hp = h;
   return ID_OK;
 }
@@ -516,7 +538,7 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
       p.Vl = h->Vl;
       p.nbw = (nb + 7) & ~7;
       if (npend > 0) {   // the newest pending reflector t = j - 1 joins the panel's V operand
-        CK(launch_vop(h->U, h->m_pad, h->m_local, h->row_offset, j - 1, j - 1 - j0, h->cvec, h->Vh, h->Vl,
+        CK(launch_vop((const float*)h->U, h->m_pad, h->m_local, h->row_offset, j - 1, j - 1 - j0, h->cvec, h->Vh, h->Vl,
                       p.nbw, h->sc, h->st));
         h->kernel_launches += 1;
       }
@@ -533,7 +555,7 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     CK(launch_pass_reduce(h->part, gx_used, (int)n, j, h->xr, own, h->red, h->sc, h->st));
     s = allreduce(h, h->red, (size_t)3 * n, NCCL_SUM);
     if (s) return s;
-    CK(launch_reflector(h->red, (int)n, j, k_max, NSLOT, h->F, h->R, h->beta, h->cvec, h->tau, h->perm,
+    CK(launch_reflector(fmt, h->red, (int)n, j, k_max, h->F, h->R, h->beta, h->cvec, h->tau, h->perm,
                         h->sc, h->st));
     h->kernel_launches += 4;
     h->pass_launches += 1;
@@ -547,9 +569,11 @@ extern "C" {
 id_status id_round_only(id_handle h, id_format fmt, id_scaling scaling) {
   if (!h) return ID_ERR_ARG;
   cudaGetLastError();
-  if (fmt != ID_FP16 && fmt != ID_FP32) return fail(h, ID_ERR_ARG, "bad format");
+  if (fmt != ID_FP16 && fmt != ID_FP32 && fmt != ID_FP64) return fail(h, ID_ERR_ARG, "bad format");
   if (scaling < 0 || scaling > 2) return fail(h, ID_ERR_ARG, "bad scaling");
-  id_status s = enqueue_round(h, fmt, scaling, 0.0);
+  id_status s = ensure_layout(h, fmt);
+  if (s) return s;
+  s = enqueue_round(h, fmt, scaling, 0.0);
   if (s) return s;
   CK(cudaMemcpyAsync(&h->sc_host, h->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
@@ -566,8 +590,12 @@ id_status id_round_only(id_handle h, id_format fmt, id_scaling scaling) {
 id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_t k_max, double eps,
                           const id_qrcp_opts* opts, int32_t* k_out, int32_t* piv_out) {
   if (!h || !k_out || !piv_out) return ID_ERR_ARG;
-  if (fmt != ID_FP16 && fmt != ID_FP32) return fail(h, ID_ERR_ARG, "bad format %d", (int)fmt);
+  if (fmt != ID_FP16 && fmt != ID_FP32 && fmt != ID_FP64) return fail(h, ID_ERR_ARG, "bad format %d", (int)fmt);
   if (scaling < 0 || scaling > 2) return fail(h, ID_ERR_ARG, "bad scaling %d", (int)scaling);
+  {
+    const id_status ls = ensure_layout(h, fmt);
+    if (ls) return ls;
+  }
   if (!(eps >= 0.0 && eps < 1.0)) return fail(h, ID_ERR_DOMAIN, "eps must be in [0, 1)");
   if (k_max < 1 || k_max > std::min<int64_t>(h->n, h->m_global))
     return fail(h, ID_ERR_DIM, "k_max=%d outside [1, min(m, n)]", k_max);
@@ -578,9 +606,11 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   int formation = opts ? opts->formation : 0;
   if (formation == 0) formation = 1;
   if (formation != 1 && formation != 2) return fail(h, ID_ERR_ARG, "bad formation %d", formation);
+  if (formation == 2 && fmt == ID_FP64)
+    return fail(h, ID_ERR_ARG, "the tcgen05 formation models the low-precision pass (fp16 / fp32 only)");
   int nb = opts && opts->nb > 0 ? opts->nb : (formation == 2 ? 16 : 4);
-  if (nb > NB_MAX || (formation == 1 && nb > 16))
-    return fail(h, ID_ERR_ARG, "nb=%d too large for formation %d", nb, formation);
+  if (nb > NB_MAX || (formation == 1 && nb > 16) || (fmt == ID_FP64 && nb > 8))
+    return fail(h, ID_ERR_ARG, "nb=%d too large for formation %d / format %d", nb, formation, (int)fmt);
   const bool use_graph = !(opts && opts->use_graph < 0);
   const bool profile = opts && opts->profile_pass;
   h->have_qr = h->have_coef = false;
@@ -690,7 +720,7 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
   CK(launch_gather_cols(h->AD, m, h->ld, h->perm, k, h->AI, h->st));
   launches++;
   if (mode == ID_COEF_R) {
-    CK(launch_R_to_fp64(h->R, k, n, h->Rd, h->st));
+    CK(launch_R_to_fp64(h->fmt == ID_FP64, h->R, k, n, h->Rd, h->st));
     CK(launch_trsm_left_upper(h->Rd, nullptr, k, h->Rd + (int64_t)k * k, k, nullptr, n - k, h->T, k, 0,
                               h->st));
     launches += 2;
@@ -865,8 +895,17 @@ id_status id_get_R(id_handle h, float* R_out, int64_t ldr) {
   if (!h || !R_out) return ID_ERR_ARG;
   if (!h->have_qr) return fail(h, ID_ERR_STATE, "no QRCP result");
   if (ldr < h->k_out) return ID_ERR_ARG;
-  // R is stored row-major k x n; output column-major k x n
-  CK(launch_R_export(h->R, h->k_out, (int)h->n, R_out, ldr, h->st));
+  // R is stored row-major k x n; output column-major k x n (the fp64 R is rounded to fp32)
+  CK(launch_R_export(h->fmt == ID_FP64, h->R, h->k_out, (int)h->n, R_out, 0, ldr, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return ID_OK;
+}
+
+id_status id_get_R_fp64(id_handle h, double* R_out, int64_t ldr) {
+  if (!h || !R_out) return ID_ERR_ARG;
+  if (!h->have_qr) return fail(h, ID_ERR_STATE, "no QRCP result");
+  if (ldr < h->k_out) return ID_ERR_ARG;
+  CK(launch_R_export(h->fmt == ID_FP64, h->R, h->k_out, (int)h->n, R_out, 1, ldr, h->st));
   CK(cudaStreamSynchronize(h->st));
   return ID_OK;
 }

@@ -61,8 +61,8 @@ struct PassParams {
   const float* Vl;         //   core-matrix layout, nbw columns, (m_pad + 128) rows
   int nbw;                 // K width of the operand layouts (nb rounded up to 8)
   const void* Sj;          // tcgen05 pass: the pivot column j of S, contiguous (m_pad rows)
-  float* U;                // [NSLOT][m_pad] raw u vectors
-  const float* F;          // [NSLOT][n]   f vectors (current column order)
+  void* U;                 // [NSLOT][m_pad] raw u vectors (working precision: fp32, fp64 for fmt 3)
+  const void* F;           // [NSLOT][n]   f vectors (current column order, working precision)
   const double* cvec;      // [k_max] c_t = 1/(u_t - beta_t) per step
   double* part;            // [gridDim.x][2][n] partial (w, s)
   double* xr;              // [n] row j of A~ (owner rank writes)
@@ -139,11 +139,12 @@ cudaError_t launch_vop(const float* U, int64_t m_pad, int64_t m_local, int64_t r
                        const double* cvec, float* Vh, float* Vl, int nbw, const DevScalars* sc, cudaStream_t st);
 cudaError_t launch_pass_reduce(const double* part, int gx, int n, int j, const double* xr,
                                int own_row, double* red, const DevScalars* sc, cudaStream_t st);
-cudaError_t launch_reflector(const double* red, int n, int j, int k_max, int nslot_f, float* F,
-                             float* R, double* beta, double* cvec, double* tau, const int* perm,
-                             DevScalars* sc, cudaStream_t st);
+// F, R in the working precision: fp32 (fmt 1, 2) or fp64 (fmt 3)
+cudaError_t launch_reflector(int fmt, const double* red, int n, int j, int k_max, void* F, void* R,
+                             double* beta, double* cvec, double* tau, const int* perm, DevScalars* sc,
+                             cudaStream_t st);
 cudaError_t launch_swap(int fmt, void* S, int64_t ngroups, int n, int jn, int j0, int steps_done,
-                        float* F, float* R, int* perm, void* Sj, DevScalars* sc, cudaStream_t st);
+                        void* F, void* R, int* perm, void* Sj, DevScalars* sc, cudaStream_t st);
 cudaError_t launch_export_S(int fmt, const void* S, int64_t m_local, int n, void* out, int64_t ld,
                             cudaStream_t st);
 
@@ -159,8 +160,9 @@ cudaError_t launch_cholesky(double* G, int k, int* info, cudaStream_t st);
 cudaError_t launch_trsm_left_upper(const double* R1, const double* R2, int k, const double* B,
                                    int64_t ldb, const int* map, int ncols, double* T, int64_t ldt,
                                    int mode, cudaStream_t st);
-cudaError_t launch_R_to_fp64(const float* R, int k, int n, double* Rd, cudaStream_t st);
-cudaError_t launch_R_export(const float* R, int k, int n, float* out, int64_t ldr, cudaStream_t st);
+// R (k x n row-major, fp32 or fp64 when r64) -> fp64 col-major / exported col-major (fp32 or fp64 when o64)
+cudaError_t launch_R_to_fp64(int r64, const void* R, int k, int n, double* Rd, cudaStream_t st);
+cudaError_t launch_R_export(int r64, const void* R, int k, int n, void* out, int o64, int64_t ldr, cudaStream_t st);
 cudaError_t launch_assemble_P(const double* T, int64_t ldt, int k, int n, const int* perm, double* P,
                               int64_t ldp, cudaStream_t st);
 // error over the columns J: sum_{r, c} (A(r, cmap[c]) - sum_l X(r, l) T(l, c))^2, c < ncols

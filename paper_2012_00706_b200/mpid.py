@@ -20,18 +20,18 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmpid.so")
 
-ID_FP16, ID_FP32 = 1, 2
+ID_FP16, ID_FP32, ID_FP64 = 1, 2, 3
 ID_SCALE_NONE, ID_SCALE_MAXABS, ID_SCALE_POW2 = 0, 1, 2
 ID_COEF_R, ID_COEF_LSQ = 0, 1
 STATUS = {0: "OK", 1: "ARG", 2: "DIM", 3: "OVERFLOW", 4: "UNDERFLOW", 5: "DEGENERATE",
           6: "DOMAIN", 7: "CUDA", 8: "NCCL", 9: "OOM", 10: "STATE"}
-FMT = {"fp16": ID_FP16, "fp32": ID_FP32}
+FMT = {"fp16": ID_FP16, "fp32": ID_FP32, "fp64": ID_FP64}
 SCALING = {"none": ID_SCALE_NONE, "maxabs": ID_SCALE_MAXABS, "pow2": ID_SCALE_POW2}
 COEF = {"R": ID_COEF_R, "r": ID_COEF_R, "lsq": ID_COEF_LSQ, "LSQ": ID_COEF_LSQ}
 
 # every function declared in include/mpid.h
 EXPORTS = ["id_workspace_bytes", "id_create", "id_qrcp_lowprec", "id_coeffs_fp64", "id_error", "id_error_ex",
-           "id_get_R", "id_get_perm", "id_get_AL", "id_round_only", "id_get_stats", "id_last_error", "id_destroy",
+           "id_get_R", "id_get_R_fp64", "id_get_perm", "id_get_AL", "id_round_only", "id_get_stats", "id_last_error", "id_destroy",
            "id_nccl_unique_id_bytes", "id_nccl_get_unique_id", "id_nccl_comm_init",
            "id_nccl_comm_destroy", "id_version"]
 
@@ -88,6 +88,8 @@ def lib():
     L.id_error_ex.argtypes = [vp, i32, i32, i32, C.POINTER(dbl), C.POINTER(dbl)]
     L.id_get_R.restype = C.c_int
     L.id_get_R.argtypes = [vp, vp, i64]
+    L.id_get_R_fp64.restype = C.c_int
+    L.id_get_R_fp64.argtypes = [vp, vp, i64]
     L.id_get_perm.restype = C.c_int
     L.id_get_perm.argtypes = [vp, C.POINTER(i32)]
     L.id_get_AL.restype = C.c_int
@@ -198,7 +200,8 @@ class MPID:
 
     def __init__(self, A_D, k_max: int, m_global: int | None = None, row_offset: int = 0,
                  comm: int | None = None, rank: int = 0, nranks: int = 1, stream=None,
-                 device=None):
+                 device=None, fp64: bool = False):
+        """fp64=True sizes the workspace for the double ID too (fmt "fp64")."""
         import torch
         assert A_D.dtype == torch.float64 and A_D.dim() == 2 and A_D.is_contiguous()
         n, m_local = A_D.shape
@@ -209,7 +212,8 @@ class MPID:
             A_D.device if A_D.is_cuda else torch.device("cuda", torch.cuda.current_device()))
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         host = 0 if A_D.is_cuda else 1
-        self.ws_bytes = id_workspace_bytes(self.m_local, self.n, self.k_max, 0, ID_FP32, host)
+        self.ws_bytes = id_workspace_bytes(self.m_local, self.n, self.k_max, 0, ID_FP64 if fp64 else ID_FP32,
+                                           host)
         self.ws = torch.empty(self.ws_bytes + 256, dtype=torch.uint8, device=self.device)
         base = self.ws.data_ptr()
         self.ws_ptr = (base + 255) // 256 * 256
@@ -283,6 +287,12 @@ class MPID:
         self._check(lib().id_get_R(self.h, C.c_void_p(Rt.data_ptr()), self.k))
         return Rt.t()
 
+    def get_R64(self):
+        import torch
+        Rt = torch.empty((self.n, self.k), dtype=torch.float64, device=self.device)
+        self._check(lib().id_get_R_fp64(self.h, C.c_void_p(Rt.data_ptr()), self.k))
+        return Rt.t()
+
     def get_perm(self) -> np.ndarray:
         buf = (C.c_int32 * self.n)()
         self._check(lib().id_get_perm(self.h, buf))
@@ -290,7 +300,7 @@ class MPID:
 
     def get_AL(self):
         import torch
-        dt = torch.float16 if self.fmt == "fp16" else torch.float32
+        dt = {"fp16": torch.float16, "fp32": torch.float32, "fp64": torch.float64}[self.fmt]
         out = torch.empty((self.n, self.m_local), dtype=dt, device=self.device)
         self._check(lib().id_get_AL(self.h, C.c_void_p(out.data_ptr()), self.m_local))
         return out.t()

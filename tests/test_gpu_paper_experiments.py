@@ -53,7 +53,7 @@ def _double_id(name, A, kmax=51):
 def _gpu_mixed(A, fmt, scaling, k):
     from paper_2012_00706_b200.mpid import IDError, MPID
     from tests.gpu_helpers import to_dev
-    h = MPID(to_dev(A), k_max=k)
+    h = MPID(to_dev(A), k_max=k, fp64=fmt == "fp64")
     try:
         q = h.qrcp(fmt, scaling, k=k, allow_underflow=True)
         out = {"k_out": q.k, "status": q.status, "I": q.piv[:q.k]}
@@ -90,6 +90,10 @@ def test_rank_sweep_single(name):
         below_u += dist < 6e-8
         assert g["rel2"] <= env, (name, k, g["rel2"], env)
         assert abs(g["rel2"] - rel2_D) <= 1e-6, (name, k, g["rel2"], rel2_D)
+        # the GPU's own double ID (ID_FP64) is the oracle's to rounding
+        gd = _gpu_mixed(A, "fp64", "none", k)
+        dist_D, _ = _dist_to_double(A, gd, dres, k)
+        assert dist_D <= 1e-12, (name, k, dist_D)
         if name == "slow":
             assert dist < 1e-5, (k, dist)
     for r in rows:

@@ -28,7 +28,8 @@ CASES = [("C1", "fp16", 32, 0.0), ("C1", "fp32", 32, 0.0),
          ("C2", "fp32", 16, 0.0), ("C2", "fp32", 64, 0.0), ("C2", "fp32", 128, 0.0),
          ("C2", "fp16", 16, 0.0), ("C2", "fp16", 64, 0.0), ("C2", "fp16", 128, 0.0),
          ("C3", "fp16", 256, 0.0), ("C3", "fp16", 512, 1e-3),
-         ("C4", "fp16", 100, 0.0), ("C4", "fp32", 100, 0.0),
+         ("C3", "fp64", 256, 0.0),
+         ("C4", "fp16", 100, 0.0), ("C4", "fp32", 100, 0.0), ("C4", "fp64", 100, 0.0),
          ("C5/8", "fp16", 512, 0.0)]
 
 
@@ -56,8 +57,8 @@ def main():
             cache[name] = device_matrix(name)
         At, spec = cache[name]
         n, m = At.shape
-        scaling = spec.scaling.get(fmt, "pow2" if fmt == "fp16" else "none")
-        h = mpid.MPID(At, k_max=k, m_global=m)
+        scaling = spec.scaling.get(fmt, "pow2" if fmt == "fp16" else "none") if fmt != "fp64" else "none"
+        h = mpid.MPID(At, k_max=k, m_global=m, fp64=fmt == "fp64")
         reps = 5 if m * n < 1e9 else 3
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         times, st = [], None
@@ -75,7 +76,7 @@ def main():
         t = statistics.median(times)
         fq, fc, fe = flops(m, n, q.k, "lsq")
         nb = st["nb"]
-        pb = pass_bytes(m, n, q.k, nb, 2 if fmt == "fp16" else 4)
+        pb = pass_bytes(m, n, q.k, nb, {"fp16": 2, "fp32": 4, "fp64": 8}[fmt])
         line = {"config": name, "m": m, "n": n, "fmt": fmt, "k": q.k, "eps": eps, "nb": nb,
                 "ms_per_id": t, "tflops": (fq + fc + fe) / (t * 1e-3) / 1e12,
                 "stages_ms": {"round": st["t_round_ms"], "qrcp": st["t_qrcp_ms"], "coef": st["t_coef_ms"],
