@@ -84,7 +84,14 @@ typedef struct {
   int32_t formation; /* how the pending update A~ = S - V F^T is formed each step:
                         1 = CUDA-core FFMA in step order (bit-identical to the oracle's
                         sequential model), 2 = tcgen05 tensor cores (3xTF32, TMEM;
-                        DESIGN.md R14), 0 = default (1: measured faster on C4). */
+                        DESIGN.md R14), 0 = default (1: measured faster on C4).
+                        3 = Gram pivoting (the paper's "sketching"
+                        future work P:402; R17): no k-step panel passes;
+                        G = A_L^T A_L on tcgen05 (kind::f16, fp32 accumulation drained
+                        into fp64 every 2048 rows), then a pivoted Cholesky of G in
+                        fp64 gives the pivots and R (fp16 only; nb ignored).  Squares
+                        the condition number: pivots agree with the Householder QRCP
+                        while the residual norms stay above ~sqrt(2048 u32) max||a||. */
   int32_t reserved[4];
 } id_qrcp_opts;
 
@@ -172,6 +179,11 @@ id_status id_get_R(id_handle h, float* R_out, int64_t ldr);
 
 /* The same R in fp64 (exact for every format) into DEVICE memory. */
 id_status id_get_R_fp64(id_handle h, double* R_out, int64_t ldr);
+
+/* Diagnostics of the Gram pivoting (formation 3): G = A_L^T A_L (n x n, fp64, column-major,
+ * ldg >= n; the global G for row-sharded A) into DEVICE memory.  Valid after an
+ * id_qrcp_lowprec with formation 3. */
+id_status id_get_gram(id_handle h, double* G_out, int64_t ldg);
 
 /* The full column permutation Z (host, n entries, 0-based original indices in
  * pivoted order; perm_out[0:k_out] = I, the rest is the order R's trailing

@@ -1,0 +1,450 @@
+// Gram-based pivoting (the paper's future work "matrix sketching",
+// P:402): the k pivots and R of the low-precision QRCP from G = A_L^T A_L instead of k
+// streaming Householder passes (reading R17, oracle/gram.py).
+//
+//   k_gram_tc   G's upper block triangle on the 5th-generation tensor cores:
+//               tcgen05.mma kind::f16 (fp16 A_L, fp32 accumulation in TMEM), 128 x 128
+//               output tiles, split-K.  The interleaved layout of S is already the
+//               K-major core-matrix layout the MMA reads: one 8-row group of 8
+//               consecutive columns is a contiguous 128 B core matrix (8 columns x 16 B
+//               = 8 fp16 rows), so a 2-D tensor-map box {128 columns, 8 row groups}
+//               lands in shared memory as the operand tile (LBO = 2048 B along K, SBO =
+//               128 B along M/N) with no re-layout.  The fp32 accumulator is drained
+//               every KC = 2048 rows into fp64 registers (double-buffered TMEM), so the
+//               fp32 accumulation error is that of a 2048-term sum.
+//   k_gram_reduce  G = sum of the split-K partials (fixed order), symmetric fill.
+//   k_pchol     outer-product pivoted Cholesky of G for k steps, one CTA: pivot = argmax
+//               of the residual diagonal d (ties: lowest original index), R(j, :) =
+//               (G(p_j, :) - R(:j, j)^T R(:j, :)) / sqrt(d_j), d -= R(j, :)^2 — the
+//               QRCP's pivots and R (R_jj > 0) in exact arithmetic.
+//
+// Roofline: k_gram_tc is tensor-bound, 2 m n^2 / 2 flops (upper triangle incl. the
+// diagonal tiles) at kind::f16; A_L is read once per tile column from L2 (concurrent
+// CTAs work on the same K range).
+#include "mpid_internal.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cfloat>
+#include <math.h>
+
+namespace mpid {
+
+namespace {
+constexpr int GT = 128;              // output tile: 128 x 128 (MMA M = N = 128)
+constexpr int GSG = 8;               // row groups per pipeline stage (64 rows)
+constexpr int GNST = 6;              // pipeline depth
+constexpr int GCH = 32;              // stages per TMEM drain (KC = 2048 rows)
+constexpr int G_EPI = 16;            // epilogue warps
+constexpr int G_BLOCK = 32 * (2 + G_EPI);
+constexpr int G_OPB = GSG * GT * 16; // bytes of one operand stage (16 KB)
+constexpr int G_SMEM = GNST * 2 * G_OPB + 1024;
+
+__device__ __forceinline__ uint64_t gdesc(uint32_t saddr) {
+  // K-major, no swizzle: LBO = 2048 B (next 8 rows of K = next row group), SBO = 128 B
+  // (next 8 columns), sm_100 descriptor version bit 46
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((2048 >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((128 >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+// kind::f16: fp16 A and B (formats 0), fp32 accumulator (bit 4), K-major both, N = M = 128
+__device__ __forceinline__ uint32_t idesc_f16() {
+  return (1u << 4) | ((uint32_t)(GT >> 3) << 17) | ((uint32_t)(GT >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(idesc_f16()), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_g(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32_g(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_g(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          su32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
+
+struct GramWork {   // split-K work items: item i -> split s = i / ntiles, tile t = i % ntiles
+  int nbk, ntiles, splits;
+  int64_t gper;     // row groups per split (multiple of GSG * GCH)
+};
+__host__ __device__ inline void tile_of(int t, int nbk, int& bi, int& bj) {
+  // upper block triangle, row by row: (0,0) (0,1) .. (0,nbk-1) (1,1) ..
+  int b = 0, rem = t;
+  while (rem >= nbk - b) { rem -= nbk - b; ++b; }
+  bi = b;
+  bj = b + rem;
+}
+}  // namespace
+
+GramWork gram_work(int64_t ngroups, int n, int num_sms) {
+  GramWork w;
+  w.nbk = (n + GT - 1) / GT;
+  w.ntiles = w.nbk * (w.nbk + 1) / 2;
+  const int64_t unit = (int64_t)GSG * GCH;                       // 256 groups = 2048 rows
+  const int64_t units = (ngroups + unit - 1) / unit;
+  int64_t s = std::max<int64_t>(1, (2 * num_sms + w.ntiles - 1) / w.ntiles);
+  s = std::min<int64_t>(s, std::max<int64_t>(1, 512 / w.ntiles));
+  s = std::min<int64_t>(s, units);
+  w.gper = (units + s - 1) / s * unit;
+  w.splits = (int)((ngroups + w.gper - 1) / w.gper);
+  return w;
+}
+
+size_t gram_part_doubles(int64_t ngroups, int n, int num_sms) {
+  const GramWork w = gram_work(ngroups, n, num_sms);
+  return (size_t)w.ntiles * w.splits * GT * GT;
+}
+
+__global__ void __launch_bounds__(G_BLOCK, 1) k_gram_tc(const __grid_constant__ CUtensorMap tmS, int64_t ngroups,
+                                                       GramWork w, double* __restrict__ part,
+                                                       const DevScalars* __restrict__ sc) {
+  if (sc->done) return;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + GNST * 2 * G_OPB);
+  uint64_t* empty = full + GNST;
+  uint64_t* tfull = empty + GNST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int items = w.ntiles * w.splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < GNST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], G_EPI);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(2 * GT));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  auto range = [&](int item, int& bi, int& bj, int64_t& g0, int& nstages) {
+    const int s = item / w.ntiles, t = item - s * w.ntiles;
+    tile_of(t, w.nbk, bi, bj);
+    g0 = (int64_t)s * w.gper;
+    const int64_t g1 = (g0 + w.gper < ngroups) ? g0 + w.gper : ngroups;
+    nstages = (int)((g1 - g0 + GSG - 1) / GSG);
+  };
+
+  if (warp == 0) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        int bi, bj, nstages;
+        int64_t g0;
+        range(item, bi, bj, g0, nstages);
+        const bool diag = bi == bj;
+        for (int st = 0; st < nstages; ++st) {
+          mbar_wait(&empty[slot], phase ^ 1);
+          unsigned char* a = smem + (size_t)slot * 2 * G_OPB;
+          mbar_expect_tx(&full[slot], diag ? G_OPB : 2 * G_OPB);
+          const int gg = (int)(g0 + (int64_t)st * GSG);
+          tma_load_2d_g(a, &tmS, bi * GT * 2, gg, &full[slot]);
+          if (!diag) tma_load_2d_g(a + G_OPB, &tmS, bj * GT * 2, gg, &full[slot]);
+          if (++slot == GNST) { slot = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer (one thread) =======================
+    if (lane == 0) {
+      int slot = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        int bi, bj, nstages;
+        int64_t g0;
+        range(item, bi, bj, g0, nstages);
+        const bool diag = bi == bj;
+        for (int st = 0; st < nstages; ++st) {
+          if (st % GCH == 0) {
+            mbar_wait(&tempty[acc], aphase ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          }
+          mbar_wait(&full[slot], phase);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a = su32(smem + (size_t)slot * 2 * G_OPB);
+          const uint32_t b = diag ? a : a + G_OPB;
+          const uint32_t d = tmem + (uint32_t)(acc * GT);
+#pragma unroll
+          for (int q = 0; q < GSG / 2; ++q)   // K = 16 rows = 2 row groups per MMA
+            mma_f16(d, gdesc(a + q * 2 * 2048), gdesc(b + q * 2 * 2048), (st % GCH == 0 && q == 0) ? 0u : 1u);
+          mma_commit_g(&empty[slot]);          // the stage is free once these MMAs have read it
+          if (st % GCH == GCH - 1 || st == nstages - 1) {
+            mma_commit_g(&tfull[acc]);
+            if (++acc == 2) { acc = 0; aphase ^= 1; }
+          }
+          if (++slot == GNST) { slot = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ======================= epilogue (16 warps) =======================
+    // warp: TMEM lane quarter (warp % 4) = G rows 32 q .. 32 q + 31 of the tile, column
+    // block cb = (warp - 2) / 4 = G columns 32 cb .. 32 cb + 31
+    const int quarter = warp & 3, cb = (warp - 2) >> 2;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+      int bi, bj, nstages;
+      int64_t g0;
+      range(item, bi, bj, g0, nstages);
+      double a[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) a[i] = 0.0;
+      const int nch = (nstages + GCH - 1) / GCH;
+      for (int c = 0; c < nch; ++c) {
+        mbar_wait(&tfull[acc], aphase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        uint32_t r[32];
+        tmem_ld32_g(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * GT + cb * 32), r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) a[i] += (double)__uint_as_float(r[i]);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+      const int s = item / w.ntiles, t = item - s * w.ntiles;
+      double* out = part + ((int64_t)t * w.splits + s) * GT * GT + (int64_t)(quarter * 32 + lane) * GT + cb * 32;
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) *reinterpret_cast<double2*>(out + i) = make_double2(a[i], a[i + 1]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * GT));
+}
+
+// G (n x n col-major, symmetric) = sum over splits of the tile partials, fixed order
+__global__ void k_gram_reduce(const double* __restrict__ part, GramWork w, int n, double* __restrict__ G,
+                              const DevScalars* __restrict__ sc) {
+  if (sc->done) return;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * n) return;
+  int c1 = (int)(idx % n), c2 = (int)(idx / n);
+  int b1 = c1 / GT, b2 = c2 / GT;
+  int r = c1 - b1 * GT, c = c2 - b2 * GT;
+  if (b1 > b2) { const int tb = b1; b1 = b2; b2 = tb; const int tr = r; r = c; c = tr; }
+  const int t = b1 * w.nbk - b1 * (b1 - 1) / 2 + (b2 - b1);
+  double s = 0.0;
+  for (int sp = 0; sp < w.splits; ++sp) s += part[((int64_t)t * w.splits + sp) * GT * GT + (int64_t)r * GT + c];
+  G[idx] = s;
+}
+
+// ---------------------------------------------------------------------------
+// pivoted Cholesky, one CTA of 1024 threads for all k steps
+struct AM {
+  double v;
+  int orig, pos;
+};
+__device__ __forceinline__ bool am_gt(const AM& a, const AM& b) {
+  return a.v > b.v || (a.v == b.v && a.orig < b.orig);
+}
+__device__ AM block_argmax_g(AM a, AM* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    AM b;
+    b.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+    b.orig = __shfl_xor_sync(0xffffffffu, a.orig, o);
+    b.pos = __shfl_xor_sync(0xffffffffu, a.pos, o);
+    if (am_gt(b, a)) a = b;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) sh[warp] = a;
+  __syncthreads();
+  if (warp == 0) {
+    a = lane < (int)(blockDim.x >> 5) ? sh[lane] : AM{-INFINITY, 0x7fffffff, -1};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      AM b;
+      b.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+      b.orig = __shfl_xor_sync(0xffffffffu, a.orig, o);
+      b.pos = __shfl_xor_sync(0xffffffffu, a.pos, o);
+      if (am_gt(b, a)) a = b;
+    }
+    if (lane == 0) sh[0] = a;
+  }
+  __syncthreads();
+  const AM r = sh[0];
+  __syncthreads();
+  return r;
+}
+__device__ double block_sum_g(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[0] = v;
+  }
+  __syncthreads();
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) k_pchol(const double* __restrict__ G, int n, int k_max,
+                                                double* __restrict__ d, int* __restrict__ perm,
+                                                double* __restrict__ R64, float* __restrict__ R,
+                                                DevScalars* __restrict__ sc) {
+  if (sc->done) return;
+  __shared__ AM sha[32];
+  __shared__ double shs[32];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    perm[i] = i;
+    d[i] = G[(int64_t)i * n + i];                      // residual norms^2 start at diag(G)
+  }
+  __syncthreads();
+  int k_out = k_max, status = 0;
+  for (int j = 0; j < k_max; ++j) {
+    if (j > 0 && sc->eps2normAL2 > 0.0) {            // tolerance stop (reading R8 on d)
+      double t = 0.0;
+      for (int i = j + threadIdx.x; i < n; i += blockDim.x) t += d[i];
+      t = block_sum_g(t, shs);
+      if (t <= sc->eps2normAL2) { k_out = j; break; }
+    }
+    AM best{-INFINITY, 0x7fffffff, -1};
+    for (int i = j + threadIdx.x; i < n; i += blockDim.x) {
+      const AM c{d[i], perm[i], i};
+      if (am_gt(c, best)) best = c;
+    }
+    best = block_argmax_g(best, sha);
+    const int p = best.pos;
+    if (p != j) {                                      // swap positions j <-> p
+      for (int l = threadIdx.x; l < j; l += blockDim.x) {
+        const double x = R64[(int64_t)l * n + j];
+        R64[(int64_t)l * n + j] = R64[(int64_t)l * n + p];
+        R64[(int64_t)l * n + p] = x;
+        const float y = R[(int64_t)l * n + j];
+        R[(int64_t)l * n + j] = R[(int64_t)l * n + p];
+        R[(int64_t)l * n + p] = y;
+      }
+      if (threadIdx.x == 0) {
+        const int q = perm[j];
+        perm[j] = perm[p];
+        perm[p] = q;
+        const double x = d[j];
+        d[j] = d[p];
+        d[p] = x;
+      }
+    }
+    __syncthreads();
+    const double dj = d[j];
+    if (!(dj > 0.0)) { k_out = j; status = 4; break; }   // the Gram's resolution is exhausted
+    const double rjj = sqrt(dj);
+    const int pj = perm[j];
+    const double* gcol = G + (int64_t)pj * n;             // G(:, p_j) = G(p_j, :)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double r;
+      if (i < j) r = 0.0;
+      else if (i == j) r = rjj;
+      else {
+        double s = gcol[perm[i]];
+        for (int l = 0; l < j; ++l) s = fma(-R64[(int64_t)l * n + j], R64[(int64_t)l * n + i], s);
+        r = s / rjj;
+        d[i] -= r * r;
+      }
+      R64[(int64_t)j * n + i] = r;
+      R[(int64_t)j * n + i] = __double2float_rn(r);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) d[j] = 0.0;
+    __syncthreads();
+  }
+  double rest = 0.0;
+  for (int i = k_out + threadIdx.x; i < n; i += blockDim.x) rest += fmax(d[i], 0.0);
+  rest = block_sum_g(rest, shs);
+  if (threadIdx.x == 0) {
+    sc->k_out = k_out;
+    sc->status = status;
+    sc->resid2 = rest;
+    sc->done = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+int encode_tmap_gram(void* tmap_out, void* S, int64_t ngroups, int n) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return -1;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  // fp16 S as [ngroups][n * 2] 8-byte units; box = 128 columns (256 units) x 8 row groups
+  const cuuint64_t dims[2] = {(cuuint64_t)n * 2, (cuuint64_t)ngroups};
+  const cuuint64_t strides[1] = {(cuuint64_t)n * 16};
+  const cuuint32_t box[2] = {(cuuint32_t)(GT * 2), (cuuint32_t)GSG};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(reinterpret_cast<CUtensorMap*>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, S, dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return (int)r;
+}
+
+cudaError_t launch_gram(const void* tmap, int64_t ngroups, int n, int num_sms, double* part, double* G,
+                        const DevScalars* sc, cudaStream_t st) {
+  const GramWork w = gram_work(ngroups, n, num_sms);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM + 64);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int items = w.ntiles * w.splits;
+  const int grid = std::min(items, num_sms);
+  k_gram_tc<<<grid, G_BLOCK, G_SMEM + 64, st>>>(*reinterpret_cast<const CUtensorMap*>(tmap), ngroups, w, part, sc);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t tot = (int64_t)n * n;
+  k_gram_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(part, w, n, G, sc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pchol(const double* G, int n, int k_max, double* d, int* perm, double* R64, float* R,
+                         DevScalars* sc, cudaStream_t st) {
+  k_pchol<<<1, 1024, 0, st>>>(G, n, k_max, d, perm, R64, R, sc);
+  return cudaGetLastError();
+}
+
+}  // namespace mpid

@@ -58,7 +58,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t AD, S, U, F, Vh, Vl, Sj, R, part, red, xr, norms, perm, scal3, sc, maxpart, rpart;
-  size_t AI, Q1, G1, G2, W, tpart, Rd, T, Pw, epart, Ik, Rinv, py, pvec, misc;
+  size_t AI, Q1, G1, G2, W, tpart, Rd, T, Pw, epart, Ik, Rinv, py, pvec, gpart, G, misc;
   size_t total;
 };
 
@@ -156,6 +156,8 @@ Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
   L.Rinv = take((size_t)k * k * 8);
   L.py = take((size_t)m_local * 8);                                  // power iteration: y = E x
   L.pvec = take((size_t)(4 * n + 2 * k + 256 + PW_NBLK * n) * 8);    // x, z, v, w, u, est, partials
+  L.gpart = take(gram_part_doubles(mp / 8, (int)n, num_sms()) * 8);  // Gram pivoting: tile partials
+  L.G = take((size_t)n * n * 8);                                      //   and G = A_L^T A_L
   L.misc = take(1024);
   L.total = off;
   return L;
@@ -185,6 +187,9 @@ struct mpid_ctx {
   void* Sj = nullptr;
   alignas(64) unsigned char tmapS[2][128];   // CUtensorMap of S for fp16 / fp32 (tcgen05 pass)
   int tmap_ok[2] = {-1, -1};
+  alignas(64) unsigned char tmapG[128];      // CUtensorMap of fp16 S for the Gram kernel
+  int tmapG_ok = -1;
+  double *gpart = nullptr, *G = nullptr;
   double *part = nullptr, *red = nullptr, *xr = nullptr, *norms = nullptr, *beta = nullptr,
          *cvec = nullptr, *tau = nullptr, *maxpart = nullptr, *rpart = nullptr;
   int* perm = nullptr;
@@ -199,7 +204,7 @@ struct mpid_ctx {
   int fmt = 0;
   int k_out = 0;
   int qr_status = 0;
-  bool have_qr = false, have_coef = false;
+  bool have_qr = false, have_coef = false, have_gram = false;
   std::vector<int> perm_host;
   DevScalars sc_host{};
   std::string err;
@@ -277,6 +282,9 @@ static id_status relayout(mpid_ctx* h, int sbytes) {
   h->Sj = w + L.Sj;
   h->tmap_ok[0] = encode_tmap_S(h->tmapS[0], h->S, 1, h->m_pad / 8, (int)n);
   h->tmap_ok[1] = encode_tmap_S(h->tmapS[1], h->S, 2, h->m_pad / 8, (int)n);
+  h->tmapG_ok = encode_tmap_gram(h->tmapG, h->S, h->m_pad / 8, (int)n);
+  h->gpart = (double*)(w + L.gpart);
+  h->G = (double*)(w + L.G);
   h->R = w + L.R;
   h->part = (double*)(w + L.part);
   h->red = (double*)(w + L.red);
@@ -503,6 +511,18 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
   id_status s = enqueue_round(h, fmt, scaling, eps);
   if (s) return s;
   CK(rec(h, h->ev[1]));
+  if (formation == 3) {
+    // NEXT-4: G = A_L^T A_L on tcgen05, then the pivoted Cholesky (all k steps, one launch)
+    if (h->tmapG_ok != 0) return fail(h, ID_ERR_CUDA, "cuTensorMapEncodeTiled (Gram) failed (%d)", h->tmapG_ok);
+    CK(launch_gram(h->tmapG, h->m_pad / 8, (int)n, num_sms(), h->gpart, h->G, h->sc, h->st));
+    s = allreduce(h, h->G, (size_t)n * n, NCCL_SUM);
+    if (s) return s;
+    CK(launch_pchol(h->G, (int)n, k_max, h->red, h->perm, h->W, (float*)h->R, h->sc, h->st));
+    h->kernel_launches += 3;
+    h->pass_launches = 0;
+    CK(rec(h, h->ev[2]));
+    return ID_OK;
+  }
   CK(launch_init_pivot(h->norms, (int)n, h->perm, h->sc, h->st));
   h->kernel_launches += 1;
   const int own_lo = (int)std::min<int64_t>(h->row_offset, INT32_MAX);
@@ -605,7 +625,9 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   // oracle's sequential FMA model; the faster one on C4), 2 = tcgen05 pass
   int formation = opts ? opts->formation : 0;
   if (formation == 0) formation = 1;
-  if (formation != 1 && formation != 2) return fail(h, ID_ERR_ARG, "bad formation %d", formation);
+  if (formation < 1 || formation > 3) return fail(h, ID_ERR_ARG, "bad formation %d", formation);
+  if (formation == 3 && fmt != ID_FP16)
+    return fail(h, ID_ERR_ARG, "Gram pivoting (formation 3) runs on fp16 A_L (tcgen05 kind::f16)");
   if (formation == 2 && fmt == ID_FP64)
     return fail(h, ID_ERR_ARG, "the tcgen05 formation models the low-precision pass (fp16 / fp32 only)");
   int nb = opts && opts->nb > 0 ? opts->nb : (formation == 2 ? 16 : 4);
@@ -613,7 +635,7 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
     return fail(h, ID_ERR_ARG, "nb=%d too large for formation %d / format %d", nb, formation, (int)fmt);
   const bool use_graph = !(opts && opts->use_graph < 0);
   const bool profile = opts && opts->profile_pass;
-  h->have_qr = h->have_coef = false;
+  h->have_qr = h->have_coef = h->have_gram = false;
   if (profile && (int)h->pass_ev.size() < 2 * k_max) {
     const size_t old = h->pass_ev.size();
     h->pass_ev.resize(2 * k_max);
@@ -700,9 +722,11 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
     return fail(h, ID_ERR_OVERFLOW, "A_L overflows the low format after scaling (S:53)");
   if (sc.status == ID_ERR_UNDERFLOW) {
     h->have_qr = sc.k_out > 0;
+    h->have_gram = formation == 3;
     return fail(h, ID_ERR_UNDERFLOW, "pivot norm underflow at step %d (P:266)", sc.k_out);
   }
   h->have_qr = true;
+  h->have_gram = formation == 3;
   return ID_OK;
 }
 
@@ -906,6 +930,15 @@ id_status id_get_R_fp64(id_handle h, double* R_out, int64_t ldr) {
   if (!h->have_qr) return fail(h, ID_ERR_STATE, "no QRCP result");
   if (ldr < h->k_out) return ID_ERR_ARG;
   CK(launch_R_export(h->fmt == ID_FP64, h->R, h->k_out, (int)h->n, R_out, 1, ldr, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return ID_OK;
+}
+
+id_status id_get_gram(id_handle h, double* G_out, int64_t ldg) {
+  if (!h || !G_out || ldg < h->n) return ID_ERR_ARG;
+  if (!h->have_gram) return fail(h, ID_ERR_STATE, "no Gram matrix (run id_qrcp_lowprec with formation 3)");
+  CK(cudaMemcpy2DAsync(G_out, (size_t)ldg * 8, h->G, (size_t)h->n * 8, (size_t)h->n * 8, (size_t)h->n,
+                       cudaMemcpyDeviceToDevice, h->st));
   CK(cudaStreamSynchronize(h->st));
   return ID_OK;
 }

@@ -185,5 +185,12 @@ cudaError_t launch_pt_times(const double* P, int64_t ldp, int k, int n, const do
 cudaError_t launch_normalize(const double* z, int n, double* x, double* est, int it, cudaStream_t st);
 cudaError_t launch_ones(double* x, int n, cudaStream_t st);
 cudaError_t launch_sum_scalar(const double* part, int nblk, double* out, cudaStream_t st);
+// NEXT-4 (k_gram.cu): Gram-based pivoting — G = A_L^T A_L on tcgen05 (fp16 S), pivoted Cholesky
+size_t gram_part_doubles(int64_t ngroups, int n, int num_sms);
+int encode_tmap_gram(void* tmap_out, void* S, int64_t ngroups, int n);
+cudaError_t launch_gram(const void* tmap, int64_t ngroups, int n, int num_sms, double* part, double* G,
+                        const DevScalars* sc, cudaStream_t st);
+cudaError_t launch_pchol(const double* G, int n, int k_max, double* d, int* perm, double* R64, float* R,
+                         DevScalars* sc, cudaStream_t st);
 
 }  // namespace mpid

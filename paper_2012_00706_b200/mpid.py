@@ -31,7 +31,7 @@ COEF = {"R": ID_COEF_R, "r": ID_COEF_R, "lsq": ID_COEF_LSQ, "LSQ": ID_COEF_LSQ}
 
 # every function declared in include/mpid.h
 EXPORTS = ["id_workspace_bytes", "id_create", "id_qrcp_lowprec", "id_coeffs_fp64", "id_error", "id_error_ex",
-           "id_get_R", "id_get_R_fp64", "id_get_perm", "id_get_AL", "id_round_only", "id_get_stats", "id_last_error", "id_destroy",
+           "id_get_R", "id_get_R_fp64", "id_get_gram", "id_get_perm", "id_get_AL", "id_round_only", "id_get_stats", "id_last_error", "id_destroy",
            "id_nccl_unique_id_bytes", "id_nccl_get_unique_id", "id_nccl_comm_init",
            "id_nccl_comm_destroy", "id_version"]
 
@@ -90,6 +90,8 @@ def lib():
     L.id_get_R.argtypes = [vp, vp, i64]
     L.id_get_R_fp64.restype = C.c_int
     L.id_get_R_fp64.argtypes = [vp, vp, i64]
+    L.id_get_gram.restype = C.c_int
+    L.id_get_gram.argtypes = [vp, vp, i64]
     L.id_get_perm.restype = C.c_int
     L.id_get_perm.argtypes = [vp, C.POINTER(i32)]
     L.id_get_AL.restype = C.c_int
@@ -243,8 +245,8 @@ class MPID:
 
     def qrcp(self, fmt="fp16", scaling="pow2", k=None, eps=0.0, nb=0, use_graph=True,
              profile=False, allow_underflow=False, formation=0) -> QRCPOut:
-        """formation: 0 auto, 1 / "ffma" CUDA-core FFMA, 2 / "tc" tcgen05 (include/mpid.h)."""
-        formation = {"auto": 0, "ffma": 1, "tc": 2}.get(formation, formation)
+        """formation: 0 auto, 1 / "ffma" CUDA-core FFMA, 2 / "tc" tcgen05, 3 / "gram" Gram pivoting (include/mpid.h)."""
+        formation = {"auto": 0, "ffma": 1, "tc": 2, "gram": 3}.get(formation, formation)
         o = QRCPOpts(nb=nb, use_graph=1 if use_graph else -1, profile_pass=1 if profile else 0,
                      formation=formation)
         k = self.k_max if k is None else k
@@ -286,6 +288,12 @@ class MPID:
         Rt = torch.empty((self.n, self.k), dtype=torch.float32, device=self.device)
         self._check(lib().id_get_R(self.h, C.c_void_p(Rt.data_ptr()), self.k))
         return Rt.t()
+
+    def get_gram(self):
+        import torch
+        G = torch.empty((self.n, self.n), dtype=torch.float64, device=self.device)
+        self._check(lib().id_get_gram(self.h, C.c_void_p(G.data_ptr()), self.n))
+        return G.t()
 
     def get_R64(self):
         import torch

@@ -30,7 +30,9 @@ CASES = [("C1", "fp16", 32, 0.0), ("C1", "fp32", 32, 0.0),
          ("C3", "fp16", 256, 0.0), ("C3", "fp16", 512, 1e-3),
          ("C3", "fp64", 256, 0.0),
          ("C4", "fp16", 100, 0.0), ("C4", "fp32", 100, 0.0), ("C4", "fp64", 100, 0.0),
-         ("C5/8", "fp16", 512, 0.0)]
+         ("C5/8", "fp16", 512, 0.0),
+         # NEXT-4: Gram pivoting (formation 3)
+         ("C3", "fp16", 256, 0.0, "gram"), ("C4", "fp16", 100, 0.0, "gram"), ("C5/8", "fp16", 512, 0.0, "gram")]
 
 
 def device_matrix(name):
@@ -48,8 +50,12 @@ def main():
     peak, _, _ = load_peaks()
     only = sys.argv[1:]
     cache = {}
-    for name, fmt, k, eps in CASES:
-        if only and name not in only:
+    for case in CASES:
+        name, fmt, k, eps = case[:4]
+        formation = case[4] if len(case) > 4 else "auto"
+        names = [a for a in only if a.startswith("C")]
+        forms = [a for a in only if not a.startswith("C")]
+        if (names and name not in names) or (forms and formation not in forms):
             continue
         if name not in cache:
             cache.clear()
@@ -65,7 +71,7 @@ def main():
         for it in range(reps + 1):
             torch.cuda.synchronize()
             ev[0].record()
-            q = h.qrcp(fmt, scaling, k=k, eps=eps)
+            q = h.qrcp(fmt, scaling, k=k, eps=eps, formation=formation, allow_underflow=True)
             h.coeffs("lsq")
             e = h.error()
             ev[1].record()
@@ -77,11 +83,12 @@ def main():
         fq, fc, fe = flops(m, n, q.k, "lsq")
         nb = st["nb"]
         pb = pass_bytes(m, n, q.k, nb, {"fp16": 2, "fp32": 4, "fp64": 8}[fmt])
-        line = {"config": name, "m": m, "n": n, "fmt": fmt, "k": q.k, "eps": eps, "nb": nb,
+        line = {"config": name, "m": m, "n": n, "fmt": fmt, "formation": formation, "k": q.k, "eps": eps, "nb": nb,
                 "ms_per_id": t, "tflops": (fq + fc + fe) / (t * 1e-3) / 1e12,
                 "stages_ms": {"round": st["t_round_ms"], "qrcp": st["t_qrcp_ms"], "coef": st["t_coef_ms"],
                               "error": st["t_err_ms"]},
-                "qrcp_hbm_frac_of_measured": pb / (st["t_qrcp_ms"] * 1e-3) / 1e9 / peak,
+                "qrcp_hbm_frac_of_measured": pb / (st["t_qrcp_ms"] * 1e-3) / 1e9 / peak if formation != "gram" else None,
+                "gram_tflops": (m * n * n) / (st["t_qrcp_ms"] * 1e-3) / 1e12 if formation == "gram" else None,
                 "rel_err_fro": e[1]}
         print(json.dumps(line), flush=True)
         h.close()
