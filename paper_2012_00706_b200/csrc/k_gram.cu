@@ -322,20 +322,28 @@ __device__ double block_sum_g(double v, double* sh) {
   return r;
 }
 
-__global__ void __launch_bounds__(1024) k_pchol(const double* __restrict__ G, int n, int k_max,
-                                                double* __restrict__ d, int* __restrict__ perm,
-                                                double* __restrict__ R64, float* __restrict__ R,
-                                                DevScalars* __restrict__ sc) {
+// Blocked (left-looking within a panel, right-looking across panels) pivoted Cholesky:
+// Gc = the Schur complement of G after the previous panels (original column indexing);
+// step j of the panel [j0, j1): pivot = argmax of d over positions >= j (ties: lowest
+// original index), swap positions, R(j, i) = (Gc(p_j, p_i) - sum_{l=j0}^{j-1} R(l, j) R(l, i))
+// / sqrt(d_j), d_i -= R(j, i)^2.  k_schur then subtracts the panel's rows from Gc's
+// trailing block.  One CTA per panel (the per-step work is O(b n)); state in global memory.
+__global__ void __launch_bounds__(1024) k_pchol_panel(const double* __restrict__ Gc, int n, int j0, int j1,
+                                                      int k_max, double* __restrict__ d, int* __restrict__ perm,
+                                                      double* __restrict__ R64, float* __restrict__ R,
+                                                      DevScalars* __restrict__ sc) {
   if (sc->done) return;
   __shared__ AM sha[32];
   __shared__ double shs[32];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    perm[i] = i;
-    d[i] = G[(int64_t)i * n + i];                      // residual norms^2 start at diag(G)
+  if (j0 == 0) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      perm[i] = i;
+      d[i] = Gc[(int64_t)i * n + i];                   // residual norms^2 start at diag(G)
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  int k_out = k_max, status = 0;
-  for (int j = 0; j < k_max; ++j) {
+  int k_out = -1, status = 0;
+  for (int j = j0; j < j1; ++j) {
     if (j > 0 && sc->eps2normAL2 > 0.0) {            // tolerance stop (reading R8 on d)
       double t = 0.0;
       for (int i = j + threadIdx.x; i < n; i += blockDim.x) t += d[i];
@@ -371,15 +379,14 @@ __global__ void __launch_bounds__(1024) k_pchol(const double* __restrict__ G, in
     const double dj = d[j];
     if (!(dj > 0.0)) { k_out = j; status = 4; break; }   // the Gram's resolution is exhausted
     const double rjj = sqrt(dj);
-    const int pj = perm[j];
-    const double* gcol = G + (int64_t)pj * n;             // G(:, p_j) = G(p_j, :)
+    const double* gcol = Gc + (int64_t)perm[j] * n;       // Gc(:, p_j) = Gc(p_j, :)
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       double r;
       if (i < j) r = 0.0;
       else if (i == j) r = rjj;
       else {
         double s = gcol[perm[i]];
-        for (int l = 0; l < j; ++l) s = fma(-R64[(int64_t)l * n + j], R64[(int64_t)l * n + i], s);
+        for (int l = j0; l < j; ++l) s = fma(-R64[(int64_t)l * n + j], R64[(int64_t)l * n + i], s);
         r = s / rjj;
         d[i] -= r * r;
       }
@@ -390,6 +397,8 @@ __global__ void __launch_bounds__(1024) k_pchol(const double* __restrict__ G, in
     if (threadIdx.x == 0) d[j] = 0.0;
     __syncthreads();
   }
+  if (k_out < 0 && j1 < k_max) return;                  // panel done, more to come
+  if (k_out < 0) k_out = k_max;
   double rest = 0.0;
   for (int i = k_out + threadIdx.x; i < n; i += blockDim.x) rest += fmax(d[i], 0.0);
   rest = block_sum_g(rest, shs);
@@ -399,6 +408,29 @@ __global__ void __launch_bounds__(1024) k_pchol(const double* __restrict__ G, in
     sc->resid2 = rest;
     sc->done = 1;
   }
+}
+
+// Gc(p_a, p_b) -= sum_{l=j0}^{j1-1} R(l, a) R(l, b) for trailing positions a, b >= j1;
+// 32 x 32 position tiles, the panel rows staged in shared memory
+__global__ void __launch_bounds__(1024) k_schur(double* __restrict__ Gc, int n, int j0, int j1,
+                                                const int* __restrict__ perm, const double* __restrict__ R64,
+                                                const DevScalars* __restrict__ sc) {
+  if (sc->done) return;
+  __shared__ double ra[32][33], rb[32][33];
+  const int a0 = j1 + blockIdx.x * 32, b0 = j1 + blockIdx.y * 32;
+  if (a0 >= n || b0 >= n) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int nl = j1 - j0;
+  // ty = panel row l, tx = position offset
+  ra[ty][tx] = (ty < nl && a0 + tx < n) ? R64[(int64_t)(j0 + ty) * n + a0 + tx] : 0.0;
+  rb[ty][tx] = (ty < nl && b0 + tx < n) ? R64[(int64_t)(j0 + ty) * n + b0 + tx] : 0.0;
+  __syncthreads();
+  const int a = a0 + ty, b = b0 + tx;
+  if (a >= n || b >= n) return;
+  double s = 0.0;
+  for (int l = 0; l < nl; ++l) s = fma(ra[l][ty], rb[l][tx], s);
+  double* g = Gc + (int64_t)perm[b] * n + perm[a];
+  *g -= s;
 }
 
 // ---------------------------------------------------------------------------
@@ -441,10 +473,22 @@ cudaError_t launch_gram(const void* tmap, int64_t ngroups, int n, int num_sms, d
   return cudaGetLastError();
 }
 
-cudaError_t launch_pchol(const double* G, int n, int k_max, double* d, int* perm, double* R64, float* R,
+cudaError_t launch_pchol(const double* G, double* Gc, int n, int k_max, double* d, int* perm, double* R64, float* R,
                          DevScalars* sc, cudaStream_t st) {
-  k_pchol<<<1, 1024, 0, st>>>(G, n, k_max, d, perm, R64, R, sc);
-  return cudaGetLastError();
+  cudaError_t e = cudaMemcpyAsync(Gc, G, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return e;
+  constexpr int PB = 32;                                  // panel width (<= 32: one smem row per warp)
+  for (int j0 = 0; j0 < k_max; j0 += PB) {
+    const int j1 = std::min(k_max, j0 + PB);
+    k_pchol_panel<<<1, 1024, 0, st>>>(Gc, n, j0, j1, k_max, d, perm, R64, R, sc);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (j1 < k_max && j1 < n) {
+      const unsigned t = (unsigned)((n - j1 + 31) / 32);
+      k_schur<<<dim3(t, t), 1024, 0, st>>>(Gc, n, j0, j1, perm, R64, sc);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+  }
+  return cudaSuccess;
 }
 
 }  // namespace mpid

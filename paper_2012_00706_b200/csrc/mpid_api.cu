@@ -58,7 +58,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t AD, S, U, F, Vh, Vl, Sj, R, part, red, xr, norms, perm, scal3, sc, maxpart, rpart;
-  size_t AI, Q1, G1, G2, W, tpart, Rd, T, Pw, epart, Ik, Rinv, py, pvec, gpart, G, misc;
+  size_t AI, Q1, G1, G2, W, tpart, Rd, T, Pw, epart, Ik, Rinv, py, pvec, gpart, G, Gc, misc;
   size_t total;
 };
 
@@ -158,6 +158,7 @@ Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
   L.pvec = take((size_t)(4 * n + 2 * k + 256 + PW_NBLK * n) * 8);    // x, z, v, w, u, est, partials
   L.gpart = take(gram_part_doubles(mp / 8, (int)n, num_sms()) * 8);  // Gram pivoting: tile partials
   L.G = take((size_t)n * n * 8);                                      //   and G = A_L^T A_L
+  L.Gc = take((size_t)n * n * 8);                                     //   Schur-complement working copy
   L.misc = take(1024);
   L.total = off;
   return L;
@@ -189,7 +190,7 @@ struct mpid_ctx {
   int tmap_ok[2] = {-1, -1};
   alignas(64) unsigned char tmapG[128];      // CUtensorMap of fp16 S for the Gram kernel
   int tmapG_ok = -1;
-  double *gpart = nullptr, *G = nullptr;
+  double *gpart = nullptr, *G = nullptr, *Gc = nullptr;
   double *part = nullptr, *red = nullptr, *xr = nullptr, *norms = nullptr, *beta = nullptr,
          *cvec = nullptr, *tau = nullptr, *maxpart = nullptr, *rpart = nullptr;
   int* perm = nullptr;
@@ -285,6 +286,7 @@ static id_status relayout(mpid_ctx* h, int sbytes) {
   h->tmapG_ok = encode_tmap_gram(h->tmapG, h->S, h->m_pad / 8, (int)n);
   h->gpart = (double*)(w + L.gpart);
   h->G = (double*)(w + L.G);
+  h->Gc = (double*)(w + L.Gc);
   h->R = w + L.R;
   h->part = (double*)(w + L.part);
   h->red = (double*)(w + L.red);
@@ -517,8 +519,8 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     CK(launch_gram(h->tmapG, h->m_pad / 8, (int)n, num_sms(), h->gpart, h->G, h->sc, h->st));
     s = allreduce(h, h->G, (size_t)n * n, NCCL_SUM);
     if (s) return s;
-    CK(launch_pchol(h->G, (int)n, k_max, h->red, h->perm, h->W, (float*)h->R, h->sc, h->st));
-    h->kernel_launches += 3;
+    CK(launch_pchol(h->G, h->Gc, (int)n, k_max, h->red, h->perm, h->W, (float*)h->R, h->sc, h->st));
+    h->kernel_launches += 2 + 2 * ((k_max + 31) / 32);
     h->pass_launches = 0;
     CK(rec(h, h->ev[2]));
     return ID_OK;

@@ -190,7 +190,8 @@ size_t gram_part_doubles(int64_t ngroups, int n, int num_sms);
 int encode_tmap_gram(void* tmap_out, void* S, int64_t ngroups, int n);
 cudaError_t launch_gram(const void* tmap, int64_t ngroups, int n, int num_sms, double* part, double* G,
                         const DevScalars* sc, cudaStream_t st);
-cudaError_t launch_pchol(const double* G, int n, int k_max, double* d, int* perm, double* R64, float* R,
+// pivoted Cholesky of G (kept) on the working copy Gc, in panels of 32 steps + Schur updates
+cudaError_t launch_pchol(const double* G, double* Gc, int n, int k_max, double* d, int* perm, double* R64, float* R,
                          DevScalars* sc, cudaStream_t st);
 
 }  // namespace mpid
