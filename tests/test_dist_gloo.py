@@ -99,3 +99,53 @@ def test_gloo_two_ranks_sharded_qrcp_matches_unsharded():
     assert np.array_equal(a["perm"][:fu], ref.perm[:fu])
     # the only difference is the fp64 order of the cross-rank partial sums
     assert np.allclose(a["R"][:fu], ref.R[:fu], rtol=0, atol=1e-5 * ref.maxnorm0)
+
+
+def _gram_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2012_00706_b200.dist import sum_over_ranks
+        from oracle.gram import gram, pivoted_cholesky
+        from oracle.qrcp import make_AL
+        from synth import gen_config
+        A = gen_config("C2", 0)[:, :200]
+        AL, _ = make_AL(A, "fp16", "pow2")
+        row0, m_loc = shard_rows(A.shape[0], world, rank)
+        # Gram pivoting at N > 1: each rank's G_r = A_r^T A_r, ONE allreduce
+        # of the n x n Gram, then the pivoted Cholesky replicated on every rank
+        G = sum_over_ranks(gram(AL[row0:row0 + m_loc]))
+        r = pivoted_cholesky(np.asarray(G), 40)
+        q.put((rank, {"perm": r.perm.copy(), "R": r.R.copy()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_gram_pivoting_matches_unsharded():
+    import torch.multiprocessing as mp
+    from oracle.gram import certified_gram_steps, gram, pivoted_cholesky
+    from oracle.qrcp import make_AL
+    from synth import gen_config
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gram_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a, b = res[0], res[1]
+    assert np.array_equal(a["perm"], b["perm"]) and np.array_equal(a["R"], b["R"])
+    A = gen_config("C2", 0)[:, :200]
+    AL, _ = make_AL(A, "fp16", "pow2")
+    ref = pivoted_cholesky(gram(AL), 40)
+    cert = certified_gram_steps(ref, gamma=1e-13)
+    fu = int(np.argmin(cert)) if not cert.all() else 40
+    assert fu > 10
+    assert np.array_equal(a["perm"][:fu], ref.perm[:fu])
+    assert np.allclose(a["R"][:fu, :fu], ref.R[:fu, :fu], rtol=0, atol=1e-10 * np.sqrt(ref.d0max))
