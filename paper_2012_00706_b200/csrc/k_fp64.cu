@@ -39,7 +39,8 @@ __global__ void k_gather_cols(const double* __restrict__ A, int64_t m, int64_t l
 // ---------------------------------------------------------------------------
 constexpr int GT = 128, GK = 16;
 constexpr int LDK = GK + 4;      // [mn][k] tiles: row stride 160 B -> conflict-free fragment reads
-constexpr int LDM = GT + 8;      // [k][mn] tile (NN A operand): 136 doubles -> conflict-free
+constexpr int LDM = GT + 4;      // [k][mn] tile (NN A operand): 132 doubles: rows tq = 0..3 of a fragment
+                                 // read land in bank octets 0, 8, 16, 24 -> conflict-free
 
 enum GemmMode { GM_TN_PARTIAL = 0, GM_NN_STORE = 1 };
 
@@ -60,7 +61,8 @@ struct GemmArgs {
   const int* ycmap;  // TN: column c of Y is Y's column ycmap[c] (nullptr = identity)
   int d_tma;         // NN_ERROR: 1 = the A_D tile may be prefetched with bulk copies (16 B aligned rows)
 };
-constexpr int DLD = GT + 4;      // NN_ERROR: smem A_D tile [c][r], 132 doubles per column
+constexpr int DLD = GT + 2;      // NN_ERROR: smem A_D tile [c][r], 130 doubles per column (16 B aligned,
+                                 // epilogue columns 2 tq land in distinct bank octets)
 
 __device__ __forceinline__ void dmma(double* c, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -228,16 +230,20 @@ __global__ void __launch_bounds__(256, 1) k_dgemm(GemmArgs g) {
 // flight while the current stage's DMMAs run, and each tile's A_D block is
 // prefetched into shared memory by bulk copies one tile ahead of its epilogue.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntiles, int ncb) {
+// 16 warps (4 x 4), warp tile 32 x 32: twice the DMMA streams per SM sub-partition of an
+// 8-warp layout (the kernel is latency-bound on DMMA issue at 8 warps), 1024 double2 per
+// operand stage = 2 per thread
+constexpr int ERR_THREADS = 512, ERR_LD = 1024 / ERR_THREADS, ERR_WM = 32, ERR_MT = ERR_WM / 8;
+__global__ void __launch_bounds__(ERR_THREADS, 1) k_err_persist(GemmArgs g, int64_t ntiles, int ncb) {
   extern __shared__ __align__(16) double dsm[];
   double (*As)[GK * LDM] = reinterpret_cast<double (*)[GK * LDM]>(dsm);
   double (*Bs)[GT * LDK] = reinterpret_cast<double (*)[GT * LDK]>(dsm + 2 * GK * LDM);
   double* Ds = dsm + 2 * GK * LDM + 2 * GT * LDK;
   __shared__ __align__(8) uint64_t dbar;
-  __shared__ double red[8];
+  __shared__ double red[ERR_THREADS / 32];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, tq = lane & 3;
-  const int wm = warp >> 2, wn = warp & 3;
+  const int wm = warp >> 2, wn = warp & 3;           // 4 x 4 warps, warp tile 32 x 32
   const int64_t K = g.K;
   const int nks = (int)((K + GK - 1) / GK);
   const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -279,11 +285,11 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
         tma_load(Ds + c * DLD, g.A + (int64_t)src_next[q] * g.lda + m0, (uint32_t)(rows * 8), &dbar);
     }
   };
-  double2 ra[4], rb[4];
+  double2 ra[ERR_LD], rb[ERR_LD];
   auto gload = [&](int64_t m0, int64_t n0, int64_t kb) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int idx = tid + q * 256;
+    for (int q = 0; q < ERR_LD; ++q) {
+      const int idx = tid + q * ERR_THREADS;
       {
         const int l = idx >> 6, rr = (idx & 63) * 2;
         const int64_t kk = kb + l, r = m0 + rr;
@@ -308,17 +314,17 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
   };
   auto sstore = [&](int buf) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int idx = tid + q * 256;
+    for (int q = 0; q < ERR_LD; ++q) {
+      const int idx = tid + q * ERR_THREADS;
       const int l = idx >> 6, rr = (idx & 63) * 2;
       *reinterpret_cast<double2*>(&As[buf][l * LDM + rr]) = ra[q];
       const int cc = idx >> 3, l2 = (idx & 7) * 2;
       *reinterpret_cast<double2*>(&Bs[buf][cc * LDK + l2]) = rb[q];
     }
   };
-  double acc[8][4][2];
+  double acc[ERR_MT][4][2];
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int a = 0; a < ERR_MT; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   double e2 = 0.0;
@@ -361,17 +367,17 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
       gload(m1, n1, last_k ? 0 : kb + GK);
     }
     const int64_t krem = (K - kb + 3) / 4;
-    const int ksteps = (m0 + wm * 64 >= g.M || n0 + wn * 32 >= g.N) ? 0 : (krem < GK / 4 ? (int)krem : GK / 4);
+    const int ksteps = (m0 + wm * ERR_WM >= g.M || n0 + wn * 32 >= g.N) ? 0 : (krem < GK / 4 ? (int)krem : GK / 4);
 #pragma unroll
     for (int ks = 0; ks < GK / 4; ++ks) {
       if (ks >= ksteps) break;
-      double af[8], bf[4];
+      double af[ERR_MT], bf[4];
 #pragma unroll
-      for (int mt = 0; mt < 8; ++mt) af[mt] = As[buf][(ks * 4 + tq) * LDM + wm * 64 + mt * 8 + gq];
+      for (int mt = 0; mt < ERR_MT; ++mt) af[mt] = As[buf][(ks * 4 + tq) * LDM + wm * ERR_WM + mt * 8 + gq];
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[buf][(wn * 32 + nt * 8 + gq) * LDK + ks * 4 + tq];
 #pragma unroll
-      for (int mt = 0; mt < 8; ++mt)
+      for (int mt = 0; mt < ERR_MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
     }
@@ -383,16 +389,16 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
       }
       const bool fullt = dp && m0 + GT <= g.M && n0 + GT <= g.N;
       if (fullt) {                           // fast path: compile-time smem offsets, 4 chains
-        const double* dbase = Ds + (wn * 32 + tq * 2) * DLD + wm * 64 + gq;
+        const double* dbase = Ds + (wn * 32 + tq * 2) * DLD + wm * ERR_WM + gq;
         double ea[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int mt = 0; mt < 8; ++mt) {
+            for (int mt = 0; mt < ERR_MT; ++mt) {
               const double e = dbase[(nt * 8 + h) * DLD + mt * 8] - acc[mt][nt][h];
-              ea[mt & 3] = fma(e, e, ea[mt & 3]);
+              ea[(mt + 2 * h) & 3] = fma(e, e, ea[(mt + 2 * h) & 3]);
               acc[mt][nt][h] = 0.0;
             }
         e2 += (ea[0] + ea[1]) + (ea[2] + ea[3]);
@@ -403,8 +409,8 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
           for (int h = 0; h < 2; ++h) {
             const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
 #pragma unroll
-            for (int mt = 0; mt < 8; ++mt) {
-              const int64_t r = m0 + wm * 64 + mt * 8 + gq;
+            for (int mt = 0; mt < ERR_MT; ++mt) {
+              const int64_t r = m0 + wm * ERR_WM + mt * 8 + gq;
               if (r < g.M && c < g.N) {
                 const double a = dp ? Ds[(c - n0) * DLD + (r - m0)]
                                     : __ldcs(g.A + (g.cmap ? (int64_t)g.cmap[c] : c) * g.lda + r);
@@ -430,7 +436,7 @@ __global__ void __launch_bounds__(256, 1) k_err_persist(GemmArgs g, int64_t ntil
   if (tid == 0) {
     double t = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) t += red[w];
+    for (int w = 0; w < ERR_THREADS / 32; ++w) t += red[w];
     g.out[blockIdx.x] = t;
   }
 }
@@ -910,6 +916,7 @@ cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, cons
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<int64_t>(ntiles, sms);
+  *nblk_out = grid;
   const size_t smem = (size_t)(2 * GK * LDM + 2 * GT * LDK + GT * DLD) * sizeof(double);
   static bool set = false;
   if (!set) {
@@ -918,7 +925,7 @@ cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, cons
     set = true;
   }
   *nblk_out = grid;
-  k_err_persist<<<grid, 256, smem, st>>>(g, ntiles, (int)ncb);
+  k_err_persist<<<grid, ERR_THREADS, smem, st>>>(g, ntiles, (int)ncb);
   return cudaGetLastError();
 }
 
