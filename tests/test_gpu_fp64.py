@@ -128,3 +128,16 @@ def test_fp64_nb_and_tolerance():
     g = run64(A, 200, eps=eps)
     res = qrcp_householder(A, 200, "fp64", nb=4, eps=eps)
     assert abs(g["k"] - res.k_out) <= 1, (g["k"], res.k_out)
+
+
+def test_fp64_column_split_matches_oracle():
+    """n > 1024: the fp64 pass splits the columns over two CTA columns (and re-stores)."""
+    rng = np.random.default_rng(11)
+    m, n, k = 1536, 1100, 20
+    A = np.asfortranarray(rng.standard_normal((m, n)) * np.exp(-np.arange(n) / 300.0))
+    g = run64(A, k, nb=4)
+    res = qrcp_householder(A, k, "fp64", nb=4)
+    agree, first_unc = _prefix(g["piv"], res)
+    assert agree >= first_unc, (agree, first_unc)
+    if agree == k:
+        assert np.max(np.abs(g["R"] - res.R)) <= 1e-12 * res.maxnorm0

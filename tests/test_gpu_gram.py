@@ -122,3 +122,21 @@ def test_gram_tolerance_and_rank_exhaustion():
     g = run_gram(np.asfortranarray(B), 60)
     assert g["k"] >= 20
     assert g["k"] == 60 or g["status"] == 4
+
+
+def test_gram_wide_matrix():
+    """n > 1024 (more than 8 tile columns, ragged last tile) against the exact Gram."""
+    rng = np.random.default_rng(5)
+    A = np.asfortranarray(rng.standard_normal((4096, 1100)) * np.exp(-np.arange(1100) / 200.0))
+    g = run_gram(A, 40)
+    AL, _ = make_AL(A, "fp16", "pow2")
+    G = gram(AL)
+    absG = np.abs(AL).T @ np.abs(AL)
+    assert np.all(np.abs(g["G"] - G) <= GAMMA_GPU * absG + 1e-300)
+    res = pivoted_cholesky(g["G"], 40)
+    cert = certified_gram_steps(res, gamma=1e-13)
+    first = int(np.argmin(cert)) if not cert.all() else 40
+    agree = 0
+    while agree < 40 and g["piv"][agree] == res.perm[agree]:
+        agree += 1
+    assert agree >= first
