@@ -7,5 +7,5 @@ BASELINE.json's five configs.  See DESIGN.md "Input recipe".
 """
 from .generators import (  # noqa: F401
     CONFIGS, ConfigSpec, config_spec, gen_config, gen_decay, gen_planted,
-    gen_exact_rank, gen_fourier, fourier_params, haar, counter_normal,
+    gen_exact_rank, gen_fourier, fourier_params, haar, counter_normal, counter_sign, SKETCH_STREAM,
 )

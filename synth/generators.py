@@ -97,6 +97,23 @@ def counter_normal(seed: int, stream: int, rows, cols, device=None):
     return torch.sqrt(-2.0 * torch.log(u1)) * torch.cos(2.0 * math.pi * u2)
 
 
+def counter_sign(seed: int, stream: int, rows, cols) -> np.ndarray:
+    """Rademacher signs +-1 (int8) for global row indices `rows` and column indices
+    `cols`: the top bit of SplitMix64(base + ((r << 13) | c)) selects -1.  Shape
+    (len(cols), len(rows)).  The GPU's sketch kernel implements the same counter-based
+    generator (random numbers the method draws are reproduced, not shared)."""
+    base = _stream_base(seed, stream)
+    r = np.asarray(rows, dtype=np.uint64)[None, :]
+    c = np.asarray(cols, dtype=np.uint64)[:, None]
+    ctr = (r << np.uint64(13)) | c
+    with np.errstate(over="ignore"):
+        z = _splitmix_np(np.uint64(base) + ctr)
+    return np.where((z >> np.uint64(63)) != 0, -1, 1).astype(np.int8)
+
+
+SKETCH_STREAM = 7
+
+
 # ----------------------------------------------------------------------------
 # Haar factors, decay matrices
 # ----------------------------------------------------------------------------
