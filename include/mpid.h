@@ -91,8 +91,15 @@ typedef struct {
                         into fp64 every 2048 rows), then a pivoted Cholesky of G in
                         fp64 gives the pivots and R (fp16 only; nb ignored).  Squares
                         the condition number: pivots agree with the Householder QRCP
-                        while the residual norms stay above ~sqrt(2048 u32) max||a||. */
-  int32_t reserved[4];
+                        while the residual norms stay above ~sqrt(2048 u32) max||a||.
+                        4 = sketched pivoting (NEXT-4, second option; R18):
+                        Y = Omega A_L with a Rademacher Omega of l = k_max + p rows
+                        (p = sketch_oversample, default 10; seed = sketch_seed) on tcgen05,
+                        then an fp64 Householder QRCP of Y; fp16 only; needs
+                        l rounded up to 128 <= n.  R is the sketch's R factor. */
+  int32_t sketch_oversample; /* formation 4: l = k_max + sketch_oversample (0 = 10) */
+  int32_t sketch_seed;       /* formation 4: seed of the Rademacher sketch */
+  int32_t reserved[2];
 } id_qrcp_opts;
 
 /* Per-call statistics (device-event times of the last calls, in ms). */
@@ -184,6 +191,12 @@ id_status id_get_R_fp64(id_handle h, double* R_out, int64_t ldr);
  * ldg >= n; the global G for row-sharded A) into DEVICE memory.  Valid after an
  * id_qrcp_lowprec with formation 3. */
 id_status id_get_gram(id_handle h, double* G_out, int64_t ldg);
+
+/* Diagnostics of the sketched pivoting (formation 4): Y = Omega A_L (l x n, fp64,
+ * column-major, ldy >= l; the global sketch for row-sharded A) into DEVICE memory, and
+ * l.  Omega(i, r) = +1 or -1 from the counter-based generator of synth.counter_sign
+ * (stream 7, global row r).  Valid after an id_qrcp_lowprec with formation 4. */
+id_status id_get_sketch(id_handle h, double* Y_out, int64_t ldy, int32_t* l_out);
 
 /* The full column permutation Z (host, n entries, 0-based original indices in
  * pivoted order; perm_out[0:k_out] = I, the rest is the order R's trailing

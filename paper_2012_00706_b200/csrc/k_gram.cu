@@ -87,6 +87,8 @@ __device__ __forceinline__ void tma_load_2d_g(void* dst, const CUtensorMap* tm, 
 struct GramWork {   // split-K work items: item i -> split s = i / ntiles, tile t = i % ntiles
   int nbk, ntiles, splits;
   int64_t gper;     // row groups per split (multiple of GSG * GCH)
+  int sym;          // 1: G = S^T S, upper block triangle; 0: Y = Omega S, nbm x nbk tiles
+  int nbm;          // tile rows of the A operand (sym: = nbk)
 };
 __host__ __device__ inline void tile_of(int t, int nbk, int& bi, int& bj) {
   // upper block triangle, row by row: (0,0) (0,1) .. (0,nbk-1) (1,1) ..
@@ -97,15 +99,18 @@ __host__ __device__ inline void tile_of(int t, int nbk, int& bi, int& bj) {
 }
 }  // namespace
 
-GramWork gram_work(int64_t ngroups, int n, int num_sms) {
+GramWork gram_work(int64_t ngroups, int n, int num_sms, int lw = 0, int64_t cap_items = 0) {
   GramWork w;
   w.nbk = (n + GT - 1) / GT;
-  w.ntiles = w.nbk * (w.nbk + 1) / 2;
+  w.sym = lw == 0;
+  w.nbm = w.sym ? w.nbk : (lw + GT - 1) / GT;
+  w.ntiles = w.sym ? w.nbk * (w.nbk + 1) / 2 : w.nbm * w.nbk;
   const int64_t unit = (int64_t)GSG * GCH;                       // 256 groups = 2048 rows
   const int64_t units = (ngroups + unit - 1) / unit;
   int64_t s = std::max<int64_t>(1, (2 * num_sms + w.ntiles - 1) / w.ntiles);
   s = std::min<int64_t>(s, std::max<int64_t>(1, 512 / w.ntiles));
   s = std::min<int64_t>(s, units);
+  if (cap_items > 0) s = std::max<int64_t>(1, std::min<int64_t>(s, cap_items / w.ntiles));
   w.gper = (units + s - 1) / s * unit;
   w.splits = (int)((ngroups + w.gper - 1) / w.gper);
   return w;
@@ -116,7 +121,10 @@ size_t gram_part_doubles(int64_t ngroups, int n, int num_sms) {
   return (size_t)w.ntiles * w.splits * GT * GT;
 }
 
-__global__ void __launch_bounds__(G_BLOCK, 1) k_gram_tc(const __grid_constant__ CUtensorMap tmS, int64_t ngroups,
+// tmA: the A operand (M = rows of the result): S itself for the Gram, Omega^T for the
+// sketch (the same interleaved layout, lw columns); tmS: the B operand, S
+__global__ void __launch_bounds__(G_BLOCK, 1) k_gram_tc(const __grid_constant__ CUtensorMap tmA,
+                                                       const __grid_constant__ CUtensorMap tmS, int64_t ngroups,
                                                        GramWork w, double* __restrict__ part,
                                                        const DevScalars* __restrict__ sc) {
   if (sc->done) return;
@@ -153,7 +161,8 @@ __global__ void __launch_bounds__(G_BLOCK, 1) k_gram_tc(const __grid_constant__ 
 
   auto range = [&](int item, int& bi, int& bj, int64_t& g0, int& nstages) {
     const int s = item / w.ntiles, t = item - s * w.ntiles;
-    tile_of(t, w.nbk, bi, bj);
+    if (w.sym) tile_of(t, w.nbk, bi, bj);
+    else { bi = t / w.nbk; bj = t - bi * w.nbk; }
     g0 = (int64_t)s * w.gper;
     const int64_t g1 = (g0 + w.gper < ngroups) ? g0 + w.gper : ngroups;
     nstages = (int)((g1 - g0 + GSG - 1) / GSG);
@@ -168,13 +177,13 @@ __global__ void __launch_bounds__(G_BLOCK, 1) k_gram_tc(const __grid_constant__ 
         int bi, bj, nstages;
         int64_t g0;
         range(item, bi, bj, g0, nstages);
-        const bool diag = bi == bj;
+        const bool diag = w.sym && bi == bj;
         for (int st = 0; st < nstages; ++st) {
           mbar_wait(&empty[slot], phase ^ 1);
           unsigned char* a = smem + (size_t)slot * 2 * G_OPB;
           mbar_expect_tx(&full[slot], diag ? G_OPB : 2 * G_OPB);
           const int gg = (int)(g0 + (int64_t)st * GSG);
-          tma_load_2d_g(a, &tmS, bi * GT * 2, gg, &full[slot]);
+          tma_load_2d_g(a, &tmA, bi * GT * 2, gg, &full[slot]);
           if (!diag) tma_load_2d_g(a + G_OPB, &tmS, bj * GT * 2, gg, &full[slot]);
           if (++slot == GNST) { slot = 0; phase ^= 1; }
         }
@@ -189,7 +198,7 @@ __global__ void __launch_bounds__(G_BLOCK, 1) k_gram_tc(const __grid_constant__ 
         int bi, bj, nstages;
         int64_t g0;
         range(item, bi, bj, g0, nstages);
-        const bool diag = bi == bj;
+        const bool diag = w.sym && bi == bj;
         for (int st = 0; st < nstages; ++st) {
           if (st % GCH == 0) {
             mbar_wait(&tempty[acc], aphase ^ 1);
@@ -434,6 +443,183 @@ __global__ void __launch_bounds__(1024) k_schur(double* __restrict__ Gc, int n, 
 }
 
 // ---------------------------------------------------------------------------
+// Sketched pivoting (NEXT-4, second option; R18, oracle/sketch.py):
+//   k_omega         Omega^T (m_pad x lw, +-1 fp16) in the interleaved layout of S, from the
+//                   counter-based generator synth.counter_sign implements (SplitMix64 of
+//                   base + ((global row << 13) | column), top bit -> -1); columns >= l and
+//                   padding rows are 0
+//   k_gram_tc       (sym = 0) Y = Omega A_L on tcgen05, split-K partials
+//   k_sketch_reduce Y (lw x n, col-major fp64) = sum of the partials, fixed order
+//   k_small_qrcp    fp64 Householder QRCP of Y on one CTA, exact norms every step
+__device__ __forceinline__ uint64_t splitmix64_d(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void k_omega(__half* __restrict__ Om, int64_t ngroups, int lw, int l, int64_t m_local,
+                        int64_t row_offset, uint64_t base, const DevScalars* __restrict__ sc) {
+  if (sc->done) return;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // (group, column)
+  if (idx >= ngroups * lw) return;
+  const int64_t g = idx / lw;
+  const int c = (int)(idx - g * lw);
+  uint4 out;
+  __half* h = reinterpret_cast<__half*>(&out);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int64_t r = g * 8 + q;
+    float v = 0.f;
+    if (c < l && r < m_local) {
+      const uint64_t ctr = ((uint64_t)(row_offset + r) << 13) | (uint64_t)c;
+      v = (splitmix64_d(base + ctr) >> 63) ? -1.f : 1.f;
+    }
+    h[q] = __float2half_rn(v);
+  }
+  reinterpret_cast<uint4*>(Om)[idx] = out;
+}
+
+__global__ void k_sketch_reduce(const double* __restrict__ part, GramWork w, int lw, int n, double* __restrict__ Y,
+                                const DevScalars* __restrict__ sc) {
+  if (sc->done) return;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)lw * n) return;
+  const int i = (int)(idx % lw), c = (int)(idx / lw);
+  const int bi = i / GT, bj = c / GT;
+  const int t = bi * w.nbk + bj;
+  double s = 0.0;
+  for (int sp = 0; sp < w.splits; ++sp)
+    s += part[((int64_t)t * w.splits + sp) * GT * GT + (int64_t)(i - bi * GT) * GT + (c - bj * GT)];
+  Y[idx] = s;
+}
+
+// one CTA of 1024 threads (32 warps); warp-per-column reductions over the rows >= j
+__global__ void __launch_bounds__(1024) k_small_qrcp(double* __restrict__ Y, int ly, int n, int k_max,
+                                                     double* __restrict__ snorm, int* __restrict__ perm,
+                                                     double* __restrict__ R64, float* __restrict__ R,
+                                                     DevScalars* __restrict__ sc) {
+  if (sc->done) return;
+  extern __shared__ double vsh[];                     // v (ly doubles)
+  __shared__ AM sha[32];
+  __shared__ double shs[32];
+  __shared__ double sbeta, sc_, su0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = i;
+  // ||Y||_F^2 for the tolerance test (reading R8 on the sketch)
+  double tot0 = 0.0;
+  for (int c = warp; c < n; c += nw) {
+    double t = 0.0;
+    for (int r = lane; r < ly; r += 32) t = fma(Y[(int64_t)c * ly + r], Y[(int64_t)c * ly + r], t);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) tot0 += t;
+  }
+  tot0 = block_sum_g(tot0, shs);
+  int k_out = k_max, status = 0;
+  for (int j = 0; j < k_max; ++j) {
+    // exact residual norms of the trailing columns (rows >= j)
+    for (int c = j + warp; c < n; c += nw) {
+      double t = 0.0;
+      for (int r = j + lane; r < ly; r += 32) t = fma(Y[(int64_t)c * ly + r], Y[(int64_t)c * ly + r], t);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) snorm[c] = t;
+    }
+    __syncthreads();
+    if (j > 0 && sc->eps2normAL2 > 0.0) {
+      double t = 0.0;
+      for (int c = j + threadIdx.x; c < n; c += blockDim.x) t += snorm[c];
+      t = block_sum_g(t, shs);
+      // eps2normAL2 = eps^2 ||A_L||_F^2; the sketch's own mass replaces ||A_L||_F^2
+      if (t <= sc->eps2normAL2 / sc->normAL2 * tot0) { k_out = j; break; }
+    }
+    AM best{-INFINITY, 0x7fffffff, -1};
+    for (int c = j + threadIdx.x; c < n; c += blockDim.x) {
+      const AM a{snorm[c], perm[c], c};
+      if (am_gt(a, best)) best = a;
+    }
+    best = block_argmax_g(best, sha);
+    const int p = best.pos;
+    if (p != j) {
+      for (int r = threadIdx.x; r < ly; r += blockDim.x) {
+        const double x = Y[(int64_t)j * ly + r];
+        Y[(int64_t)j * ly + r] = Y[(int64_t)p * ly + r];
+        Y[(int64_t)p * ly + r] = x;
+      }
+      for (int l = threadIdx.x; l < j; l += blockDim.x) {
+        const double x = R64[(int64_t)l * n + j];
+        R64[(int64_t)l * n + j] = R64[(int64_t)l * n + p];
+        R64[(int64_t)l * n + p] = x;
+        const float y = R[(int64_t)l * n + j];
+        R[(int64_t)l * n + j] = R[(int64_t)l * n + p];
+        R[(int64_t)l * n + p] = y;
+      }
+      if (threadIdx.x == 0) {
+        const int q = perm[j];
+        perm[j] = perm[p];
+        perm[p] = q;
+        const double x = snorm[j];
+        snorm[j] = snorm[p];
+        snorm[p] = x;
+      }
+    }
+    __syncthreads();
+    const double sj = snorm[j];
+    if (!(sj >= DBL_MIN)) { k_out = j; status = 4; break; }
+    if (threadIdx.x == 0) {
+      const double u0 = Y[(int64_t)j * ly + j];
+      const double beta = -copysign(sqrt(sj), u0);
+      sbeta = beta;
+      sc_ = 1.0 / (u0 - beta);
+      su0 = u0;
+    }
+    __syncthreads();
+    const double beta = sbeta, cc = sc_;
+    const double sgn = beta < 0.0 ? -1.0 : 1.0;
+    for (int r = threadIdx.x; r < ly; r += blockDim.x)
+      vsh[r] = r < j ? 0.0 : (r == j ? 1.0 : __dmul_rn(Y[(int64_t)j * ly + r], cc));
+    __syncthreads();
+    // w_c = Y(j:, c)^T u, R(j, c) = w_c / beta, f_c = Y(j, c) - w_c / beta, Y(j:, c) -= v f_c
+    for (int c = j + warp; c < n; c += nw) {
+      double t = 0.0;
+      for (int r = j + lane; r < ly; r += 32) t = fma(Y[(int64_t)c * ly + r], Y[(int64_t)j * ly + r], t);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      const double rraw = t / beta;
+      const double f = Y[(int64_t)c * ly + j] - rraw;
+      __syncwarp();
+      if (c != j) {
+        for (int r = j + lane; r < ly; r += 32)
+          Y[(int64_t)c * ly + r] = __dadd_rn(__dmul_rn(-vsh[r], f), Y[(int64_t)c * ly + r]);
+      }
+      if (lane == 0) {
+        R64[(int64_t)j * n + c] = rraw * sgn;
+        R[(int64_t)j * n + c] = __double2float_rn(rraw * sgn);
+      }
+    }
+    __syncthreads();
+    // column j last (the others read its rows as u): Y(j:, j) -= v f_j
+    {
+      const double f = Y[(int64_t)j * ly + j] - R64[(int64_t)j * n + j] * sgn;
+      __syncthreads();
+      for (int r = j + threadIdx.x; r < ly; r += blockDim.x)
+        Y[(int64_t)j * ly + r] = __dadd_rn(__dmul_rn(-vsh[r], f), Y[(int64_t)j * ly + r]);
+    }
+    for (int i = threadIdx.x; i < j; i += blockDim.x) {
+      R64[(int64_t)j * n + i] = 0.0;
+      R[(int64_t)j * n + i] = 0.f;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    sc->k_out = k_out;
+    sc->status = status;
+    sc->resid2 = 0.0;
+    sc->done = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
 int encode_tmap_gram(void* tmap_out, void* S, int64_t ngroups, int n) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
@@ -456,6 +642,7 @@ int encode_tmap_gram(void* tmap_out, void* S, int64_t ngroups, int n) {
 
 cudaError_t launch_gram(const void* tmap, int64_t ngroups, int n, int num_sms, double* part, double* G,
                         const DevScalars* sc, cudaStream_t st) {
+  const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(tmap);
   const GramWork w = gram_work(ngroups, n, num_sms);
   static bool attr = false;
   if (!attr) {
@@ -465,11 +652,48 @@ cudaError_t launch_gram(const void* tmap, int64_t ngroups, int n, int num_sms, d
   }
   const int items = w.ntiles * w.splits;
   const int grid = std::min(items, num_sms);
-  k_gram_tc<<<grid, G_BLOCK, G_SMEM + 64, st>>>(*reinterpret_cast<const CUtensorMap*>(tmap), ngroups, w, part, sc);
+  k_gram_tc<<<grid, G_BLOCK, G_SMEM + 64, st>>>(*tm, *tm, ngroups, w, part, sc);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t tot = (int64_t)n * n;
   k_gram_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(part, w, n, G, sc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sketch(const void* tmapO, const void* tmapS, void* Om, int64_t ngroups, int n, int l, int lw,
+                          int64_t m_local, int64_t row_offset, uint64_t base, int num_sms, double* part,
+                          size_t part_doubles, double* Y, const DevScalars* sc, cudaStream_t st) {
+  const int64_t tot = ngroups * lw;
+  k_omega<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>((__half*)Om, ngroups, lw, l, m_local, row_offset, base, sc);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const GramWork w = gram_work(ngroups, n, num_sms, lw, (int64_t)(part_doubles / (GT * GT)));
+  if ((size_t)w.ntiles * w.splits * GT * GT > part_doubles) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM + 64);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int items = w.ntiles * w.splits;
+  k_gram_tc<<<std::min(items, num_sms), G_BLOCK, G_SMEM + 64, st>>>(
+      *reinterpret_cast<const CUtensorMap*>(tmapO), *reinterpret_cast<const CUtensorMap*>(tmapS), ngroups, w, part, sc);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int64_t ty = (int64_t)lw * n;
+  k_sketch_reduce<<<(unsigned)((ty + 255) / 256), 256, 0, st>>>(part, w, lw, n, Y, sc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_small_qrcp(double* Y, int ly, int n, int k_max, double* snorm, int* perm, double* R64, float* R,
+                              DevScalars* sc, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_small_qrcp, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if ((size_t)ly * 8 > 64 * 1024) return cudaErrorInvalidValue;
+  k_small_qrcp<<<1, 1024, (size_t)ly * 8, st>>>(Y, ly, n, k_max, snorm, perm, R64, R, sc);
   return cudaGetLastError();
 }
 

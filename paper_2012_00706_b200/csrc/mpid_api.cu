@@ -205,13 +205,18 @@ struct mpid_ctx {
   int fmt = 0;
   int k_out = 0;
   int qr_status = 0;
-  bool have_qr = false, have_coef = false, have_gram = false;
+  bool have_qr = false, have_coef = false, have_gram = false, have_sketch = false;
   std::vector<int> perm_host;
   DevScalars sc_host{};
   std::string err;
   // graphs keyed by (fmt, scaling, k_max, nb, eps bits, profile)
-  std::map<std::tuple<int, int, int, int, uint64_t, int>, cudaGraphExec_t> graphs;
-  std::map<std::tuple<int, int, int, int, uint64_t, int>, int64_t> graph_launches;
+  // graphs keyed by (fmt, scaling, k_max, nb * 4 + formation, eps bits, profile, sketch l << 32 | seed)
+  std::map<std::tuple<int, int, int, int, uint64_t, int, uint64_t>, cudaGraphExec_t> graphs;
+  std::map<std::tuple<int, int, int, int, uint64_t, int, uint64_t>, int64_t> graph_launches;
+  // sketched pivoting (formation 4): sketch rows l (lw rounded to 128), seed, Omega^T's tensor map
+  int sk_l = 0, sk_lw = 0;
+  uint32_t sk_seed = 0;
+  alignas(64) unsigned char tmapO[128];
   cudaEvent_t ev[8]{};
   std::vector<cudaEvent_t> pass_ev;
   int64_t pass_launches = 0, kernel_launches = 0;
@@ -251,6 +256,16 @@ static id_status allreduce(mpid_ctx* h, double* buf, size_t count, int op) {
   if (r != 0)
     return fail(h, ID_ERR_NCCL, "ncclAllReduce: %s", api.GetErrorString ? api.GetErrorString(r) : "?");
   return ID_OK;
+}
+
+// the counter-based sign generator's stream base (synth.counter_sign, stream 7): SplitMix64
+// of seed * 1000003 + 7 * 7919 + 12345 — generator plumbing, no arithmetic of the method
+static uint64_t sketch_base(uint32_t seed) {
+  uint64_t z = (uint64_t)seed * 1000003ull + 7ull * 7919ull + 12345ull;
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
 }
 
 // (Re)carve the workspace for working precision sbytes (4: fp16/fp32 QRCP, 8: also the
@@ -513,6 +528,21 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
   id_status s = enqueue_round(h, fmt, scaling, eps);
   if (s) return s;
   CK(rec(h, h->ev[1]));
+  if (formation == 4) {
+    // NEXT-4, second option: Y = Omega A_L (Rademacher sketch, tcgen05), fp64 QRCP of Y
+    CK(launch_sketch(h->tmapO, h->tmapG, (char*)h->S + (size_t)h->m_pad * n * 2, h->m_pad / 8, (int)n, h->sk_l,
+                     h->sk_lw, h->m_local, h->row_offset, sketch_base(h->sk_seed), num_sms(), h->gpart,
+                     gram_part_doubles(h->m_pad / 8, (int)n, num_sms()), h->G, h->sc, h->st));
+    s = allreduce(h, h->G, (size_t)h->sk_lw * n, NCCL_SUM);
+    if (s) return s;
+    // the QRCP works on a copy (Gc) so Y stays available to id_get_sketch
+    CK(cudaMemcpyAsync(h->Gc, h->G, (size_t)h->sk_lw * n * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    CK(launch_small_qrcp(h->Gc, h->sk_lw, (int)n, k_max, h->red, h->perm, h->W, (float*)h->R, h->sc, h->st));
+    h->kernel_launches += 4;
+    h->pass_launches = 0;
+    CK(rec(h, h->ev[2]));
+    return ID_OK;
+  }
   if (formation == 3) {
     // NEXT-4: G = A_L^T A_L on tcgen05, then the pivoted Cholesky (all k steps, one launch)
     if (h->tmapG_ok != 0) return fail(h, ID_ERR_CUDA, "cuTensorMapEncodeTiled (Gram) failed (%d)", h->tmapG_ok);
@@ -627,9 +657,19 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   // oracle's sequential FMA model; the faster one on C4), 2 = tcgen05 pass
   int formation = opts ? opts->formation : 0;
   if (formation == 0) formation = 1;
-  if (formation < 1 || formation > 3) return fail(h, ID_ERR_ARG, "bad formation %d", formation);
-  if (formation == 3 && fmt != ID_FP16)
-    return fail(h, ID_ERR_ARG, "Gram pivoting (formation 3) runs on fp16 A_L (tcgen05 kind::f16)");
+  if (formation < 1 || formation > 4) return fail(h, ID_ERR_ARG, "bad formation %d", formation);
+  if (formation >= 3 && fmt != ID_FP16)
+    return fail(h, ID_ERR_ARG, "Gram / sketched pivoting (formation 3, 4) run on fp16 A_L (tcgen05 kind::f16)");
+  if (formation == 4) {
+    const int over = opts && opts->sketch_oversample > 0 ? opts->sketch_oversample : 10;
+    h->sk_l = k_max + over;
+    h->sk_lw = (h->sk_l + 127) / 128 * 128;
+    h->sk_seed = opts ? (uint32_t)opts->sketch_seed : 0u;
+    if (h->sk_lw > h->n || h->sk_l > 8192)
+      return fail(h, ID_ERR_DIM, "sketch of %d rows (padded %d) exceeds n = %lld", h->sk_l, h->sk_lw, (long long)h->n);
+    const int r = encode_tmap_gram(h->tmapO, (char*)h->S + (size_t)h->m_pad * h->n * 2, h->m_pad / 8, h->sk_lw);
+    if (r != 0) return fail(h, ID_ERR_CUDA, "cuTensorMapEncodeTiled (sketch) failed (%d)", r);
+  }
   if (formation == 2 && fmt == ID_FP64)
     return fail(h, ID_ERR_ARG, "the tcgen05 formation models the low-precision pass (fp16 / fp32 only)");
   int nb = opts && opts->nb > 0 ? opts->nb : (formation == 2 ? 16 : 4);
@@ -637,7 +677,7 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
     return fail(h, ID_ERR_ARG, "nb=%d too large for formation %d / format %d", nb, formation, (int)fmt);
   const bool use_graph = !(opts && opts->use_graph < 0);
   const bool profile = opts && opts->profile_pass;
-  h->have_qr = h->have_coef = h->have_gram = false;
+  h->have_qr = h->have_coef = h->have_gram = h->have_sketch = false;
   if (profile && (int)h->pass_ev.size() < 2 * k_max) {
     const size_t old = h->pass_ev.size();
     h->pass_ev.resize(2 * k_max);
@@ -646,7 +686,8 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   if (use_graph) {
     uint64_t eb;
     memcpy(&eb, &eps, 8);
-    auto key = std::make_tuple((int)fmt, (int)scaling, (int)k_max, nb * 4 + formation, eb, profile ? 1 : 0);
+    const uint64_t skey = formation == 4 ? ((uint64_t)h->sk_l << 32 | h->sk_seed) : 0;
+    auto key = std::make_tuple((int)fmt, (int)scaling, (int)k_max, nb * 4 + formation, eb, profile ? 1 : 0, skey);
     auto it = h->graphs.find(key);
     if (it == h->graphs.end()) {
       cudaGraph_t g;
@@ -725,10 +766,12 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   if (sc.status == ID_ERR_UNDERFLOW) {
     h->have_qr = sc.k_out > 0;
     h->have_gram = formation == 3;
+    h->have_sketch = formation == 4;
     return fail(h, ID_ERR_UNDERFLOW, "pivot norm underflow at step %d (P:266)", sc.k_out);
   }
   h->have_qr = true;
   h->have_gram = formation == 3;
+  h->have_sketch = formation == 4;
   return ID_OK;
 }
 
@@ -942,6 +985,17 @@ id_status id_get_gram(id_handle h, double* G_out, int64_t ldg) {
   CK(cudaMemcpy2DAsync(G_out, (size_t)ldg * 8, h->G, (size_t)h->n * 8, (size_t)h->n * 8, (size_t)h->n,
                        cudaMemcpyDeviceToDevice, h->st));
   CK(cudaStreamSynchronize(h->st));
+  return ID_OK;
+}
+
+id_status id_get_sketch(id_handle h, double* Y_out, int64_t ldy, int32_t* l_out) {
+  if (!h || !Y_out || !l_out) return ID_ERR_ARG;
+  if (!h->have_sketch) return fail(h, ID_ERR_STATE, "no sketch (run id_qrcp_lowprec with formation 4)");
+  if (ldy < h->sk_l) return ID_ERR_ARG;
+  CK(cudaMemcpy2DAsync(Y_out, (size_t)ldy * 8, h->G, (size_t)h->sk_lw * 8, (size_t)h->sk_l * 8, (size_t)h->n,
+                       cudaMemcpyDeviceToDevice, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  *l_out = h->sk_l;
   return ID_OK;
 }
 

@@ -190,6 +190,13 @@ size_t gram_part_doubles(int64_t ngroups, int n, int num_sms);
 int encode_tmap_gram(void* tmap_out, void* S, int64_t ngroups, int n);
 cudaError_t launch_gram(const void* tmap, int64_t ngroups, int n, int num_sms, double* part, double* G,
                         const DevScalars* sc, cudaStream_t st);
+// NEXT-4 second option: Omega^T (+-1 fp16, interleaved, lw columns), Y = Omega A_L (lw x n fp64),
+// then the fp64 QRCP of Y on one CTA (ly = lw rows, zero rows beyond l)
+cudaError_t launch_sketch(const void* tmapO, const void* tmapS, void* Om, int64_t ngroups, int n, int l, int lw,
+                          int64_t m_local, int64_t row_offset, uint64_t base, int num_sms, double* part,
+                          size_t part_doubles, double* Y, const DevScalars* sc, cudaStream_t st);
+cudaError_t launch_small_qrcp(double* Y, int ly, int n, int k_max, double* snorm, int* perm, double* R64, float* R,
+                              DevScalars* sc, cudaStream_t st);
 // pivoted Cholesky of G (kept) on the working copy Gc, in panels of 32 steps + Schur updates
 cudaError_t launch_pchol(const double* G, double* Gc, int n, int k_max, double* d, int* perm, double* R64, float* R,
                          DevScalars* sc, cudaStream_t st);

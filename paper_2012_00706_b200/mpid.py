@@ -31,7 +31,7 @@ COEF = {"R": ID_COEF_R, "r": ID_COEF_R, "lsq": ID_COEF_LSQ, "LSQ": ID_COEF_LSQ}
 
 # every function declared in include/mpid.h
 EXPORTS = ["id_workspace_bytes", "id_create", "id_qrcp_lowprec", "id_coeffs_fp64", "id_error", "id_error_ex",
-           "id_get_R", "id_get_R_fp64", "id_get_gram", "id_get_perm", "id_get_AL", "id_round_only", "id_get_stats", "id_last_error", "id_destroy",
+           "id_get_R", "id_get_R_fp64", "id_get_gram", "id_get_sketch", "id_get_perm", "id_get_AL", "id_round_only", "id_get_stats", "id_last_error", "id_destroy",
            "id_nccl_unique_id_bytes", "id_nccl_get_unique_id", "id_nccl_comm_init",
            "id_nccl_comm_destroy", "id_version"]
 
@@ -45,7 +45,8 @@ class IDError(RuntimeError):
 
 class QRCPOpts(C.Structure):
     _fields_ = [("nb", C.c_int32), ("use_graph", C.c_int32), ("profile_pass", C.c_int32),
-                ("formation", C.c_int32), ("reserved", C.c_int32 * 4)]
+                ("formation", C.c_int32), ("sketch_oversample", C.c_int32), ("sketch_seed", C.c_int32),
+                ("reserved", C.c_int32 * 2)]
 
 
 class Stats(C.Structure):
@@ -92,6 +93,8 @@ def lib():
     L.id_get_R_fp64.argtypes = [vp, vp, i64]
     L.id_get_gram.restype = C.c_int
     L.id_get_gram.argtypes = [vp, vp, i64]
+    L.id_get_sketch.restype = C.c_int
+    L.id_get_sketch.argtypes = [vp, vp, i64, C.POINTER(i32)]
     L.id_get_perm.restype = C.c_int
     L.id_get_perm.argtypes = [vp, C.POINTER(i32)]
     L.id_get_AL.restype = C.c_int
@@ -244,11 +247,11 @@ class MPID:
         return rc
 
     def qrcp(self, fmt="fp16", scaling="pow2", k=None, eps=0.0, nb=0, use_graph=True,
-             profile=False, allow_underflow=False, formation=0) -> QRCPOut:
+             profile=False, allow_underflow=False, formation=0, oversample=0, seed=0) -> QRCPOut:
         """formation: 0 auto, 1 / "ffma" CUDA-core FFMA, 2 / "tc" tcgen05, 3 / "gram" Gram pivoting (include/mpid.h)."""
-        formation = {"auto": 0, "ffma": 1, "tc": 2, "gram": 3}.get(formation, formation)
+        formation = {"auto": 0, "ffma": 1, "tc": 2, "gram": 3, "sketch": 4}.get(formation, formation)
         o = QRCPOpts(nb=nb, use_graph=1 if use_graph else -1, profile_pass=1 if profile else 0,
-                     formation=formation)
+                     formation=formation, sketch_oversample=oversample, sketch_seed=seed)
         k = self.k_max if k is None else k
         rc, kout, piv = id_qrcp_lowprec(self.h, FMT[fmt] if isinstance(fmt, str) else fmt,
                                         SCALING[scaling] if isinstance(scaling, str) else scaling,
@@ -294,6 +297,15 @@ class MPID:
         G = torch.empty((self.n, self.n), dtype=torch.float64, device=self.device)
         self._check(lib().id_get_gram(self.h, C.c_void_p(G.data_ptr()), self.n))
         return G.t()
+
+    def get_sketch(self):
+        """(Y, l): the sketch Omega A_L as an l x n fp64 torch view of column-major storage."""
+        import torch
+        ld = self.k_max + 4096
+        Yt = torch.empty((self.n, ld), dtype=torch.float64, device=self.device)
+        lo = C.c_int32(0)
+        self._check(lib().id_get_sketch(self.h, C.c_void_p(Yt.data_ptr()), ld, C.byref(lo)))
+        return Yt[:, :lo.value].t(), lo.value
 
     def get_R64(self):
         import torch

@@ -32,7 +32,9 @@ CASES = [("C1", "fp16", 32, 0.0), ("C1", "fp32", 32, 0.0),
          ("C4", "fp16", 100, 0.0), ("C4", "fp32", 100, 0.0), ("C4", "fp64", 100, 0.0),
          ("C5/8", "fp16", 512, 0.0),
          # NEXT-4: Gram pivoting (formation 3)
-         ("C3", "fp16", 256, 0.0, "gram"), ("C4", "fp16", 100, 0.0, "gram"), ("C5/8", "fp16", 512, 0.0, "gram")]
+         ("C3", "fp16", 256, 0.0, "gram"), ("C4", "fp16", 100, 0.0, "gram"), ("C5/8", "fp16", 512, 0.0, "gram"),
+         # NEXT-4 second option: sketched pivoting (formation 4)
+         ("C3", "fp16", 256, 0.0, "sketch"), ("C4", "fp16", 100, 0.0, "sketch"), ("C5/8", "fp16", 512, 0.0, "sketch")]
 
 
 def device_matrix(name):
@@ -87,8 +89,10 @@ def main():
                 "ms_per_id": t, "tflops": (fq + fc + fe) / (t * 1e-3) / 1e12,
                 "stages_ms": {"round": st["t_round_ms"], "qrcp": st["t_qrcp_ms"], "coef": st["t_coef_ms"],
                               "error": st["t_err_ms"]},
-                "qrcp_hbm_frac_of_measured": pb / (st["t_qrcp_ms"] * 1e-3) / 1e9 / peak if formation != "gram" else None,
+                "qrcp_hbm_frac_of_measured": (pb / (st["t_qrcp_ms"] * 1e-3) / 1e9 / peak
+                                              if formation not in ("gram", "sketch") else None),
                 "gram_tflops": (m * n * n) / (st["t_qrcp_ms"] * 1e-3) / 1e12 if formation == "gram" else None,
+                "pivot_ms": st["t_qrcp_ms"],
                 "rel_err_fro": e[1]}
         print(json.dumps(line), flush=True)
         h.close()
