@@ -268,32 +268,31 @@ def main():
     except Exception as ex:  # reported, never silently replaced
         extra_err["error"] = str(ex)
 
-    # ---- NEXT-4 variant, timed separately (not the headline): Gram pivoting --------
+    # ---- NEXT-4 variants, timed separately (not the headline): Gram / sketched pivoting ----
     variants = {}
     if args.fmt == "fp16" and world == 1:
-        try:
-            for i in range(4):
-                torch.cuda.synchronize()
-                g0 = torch.cuda.Event(enable_timing=True)
-                g1 = torch.cuda.Event(enable_timing=True)
-                g0.record(stream)
-                qg = h.qrcp("fp16", scaling, k=k, formation="gram", allow_underflow=True)
-                h.coeffs(args.mode)
-                eg = h.error()
-                g1.record(stream)
-                torch.cuda.synchronize()
-                if i == 0:
-                    continue
-                sg = h.stats()
-                variants.setdefault("_t", []).append((g0.elapsed_time(g1), sg["t_qrcp_ms"]))
-            ts = variants.pop("_t")
-            variants["gram_pivoting"] = {
-                "ms_per_step": statistics.mean(t for t, _ in ts), "pivot_ms": statistics.mean(p for _, p in ts),
-                "k_out": qg.k, "rel_err_fro": eg[1],
-                "same_skeleton_as_householder": bool(sorted(qg.piv.tolist()) == sorted(q.piv.tolist())),
-                "note": "formation 3 (tcgen05 Gram + pivoted Cholesky), 3 timed steps, CUDA events"}
-        except Exception as ex:  # reported, never silently replaced
-            variants["gram_pivoting"] = {"error": str(ex)}
+        for name, form in (("gram_pivoting", "gram"), ("sketched_pivoting", "sketch")):
+            try:
+                ts = []
+                for i in range(4):
+                    torch.cuda.synchronize()
+                    g0 = torch.cuda.Event(enable_timing=True)
+                    g1 = torch.cuda.Event(enable_timing=True)
+                    g0.record(stream)
+                    qg = h.qrcp("fp16", scaling, k=k, formation=form, allow_underflow=True)
+                    h.coeffs(args.mode)
+                    eg = h.error()
+                    g1.record(stream)
+                    torch.cuda.synchronize()
+                    if i > 0:
+                        ts.append((g0.elapsed_time(g1), h.stats()["t_qrcp_ms"]))
+                variants[name] = {
+                    "ms_per_step": statistics.mean(t for t, _ in ts), "pivot_ms": statistics.mean(p for _, p in ts),
+                    "k_out": qg.k, "rel_err_fro": eg[1],
+                    "same_skeleton_as_householder": bool(sorted(qg.piv.tolist()) == sorted(q.piv.tolist())),
+                    "note": f"formation {form} (DESIGN.md NEXT-4), 3 timed steps, CUDA events"}
+            except Exception as ex:  # reported, never silently replaced
+                variants[name] = {"error": str(ex)}
         # the headline handle state (last QRCP) is restored for the checks below
         q = h.qrcp(args.fmt, scaling, k=k, nb=args.nb)
 
