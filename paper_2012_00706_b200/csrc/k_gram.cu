@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(1024) k_schur(double* __restrict__ Gc, int n, 
 //                   padding rows are 0
 //   k_gram_tc       (sym = 0) Y = Omega A_L on tcgen05, split-K partials
 //   k_sketch_reduce Y (lw x n, col-major fp64) = sum of the partials, fixed order
-//   k_small_qrcp    fp64 Householder QRCP of Y on one CTA, exact norms every step
+//   k_sq_*          fp64 Householder QRCP of Y, exact norms every step (3 kernels per step)
 __device__ __forceinline__ uint64_t splitmix64_d(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -493,130 +493,161 @@ __global__ void k_sketch_reduce(const double* __restrict__ part, GramWork w, int
   Y[idx] = s;
 }
 
-// one CTA of 1024 threads (32 warps); warp-per-column reductions over the rows >= j
-__global__ void __launch_bounds__(1024) k_small_qrcp(double* __restrict__ Y, int ly, int n, int k_max,
-                                                     double* __restrict__ snorm, int* __restrict__ perm,
-                                                     double* __restrict__ R64, float* __restrict__ R,
-                                                     DevScalars* __restrict__ sc) {
+// fp64 Householder QRCP of Y (ly x n, col-major), exact trailing norms every step, as
+// three kernels per step (graph-captured): the column work spreads over the GPU, the
+// step's scalar work runs on one CTA.  Scratch: snorm[n], v[ly], scal[4] = (beta, tot0).
+//   k_sq_norms0  snorm_c = ||Y(:, c)||^2, scal[1] = ||Y||_F^2          (warp per column)
+//   k_sq_pivot   tolerance test, argmax (ties: lowest original index), swap, beta, v
+//   k_sq_update  w_c = Y(j:, c)^T u, R(j, c), Y(j:, c) -= v f_c, snorm_c over rows > j
+__global__ void __launch_bounds__(1024) k_sq_norms0(const double* __restrict__ Y, int ly, int n,
+                                                    double* __restrict__ snorm, int* __restrict__ perm,
+                                                    const DevScalars* __restrict__ sc) {
   if (sc->done) return;
-  extern __shared__ double vsh[];                     // v (ly doubles)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 32 + warp;
+  if (c >= n) return;
+  double t = 0.0;
+  for (int r = lane; r < ly; r += 32) t = fma(Y[(int64_t)c * ly + r], Y[(int64_t)c * ly + r], t);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) {
+    snorm[c] = t;
+    perm[c] = c;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_sq_pivot(double* __restrict__ Y, int ly, int n, int j, int k_max,
+                                                   double* __restrict__ snorm, double* __restrict__ v,
+                                                   double* __restrict__ scal, int* __restrict__ perm,
+                                                   double* __restrict__ R64, float* __restrict__ R,
+                                                   DevScalars* __restrict__ sc) {
+  if (sc->done) return;
   __shared__ AM sha[32];
   __shared__ double shs[32];
-  __shared__ double sbeta, sc_, su0;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = i;
-  // ||Y||_F^2 for the tolerance test (reading R8 on the sketch)
-  double tot0 = 0.0;
-  for (int c = warp; c < n; c += nw) {
+  if (j == 0) {                                       // ||Y||_F^2 for the tolerance test
     double t = 0.0;
-    for (int r = lane; r < ly; r += 32) t = fma(Y[(int64_t)c * ly + r], Y[(int64_t)c * ly + r], t);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0) tot0 += t;
+    for (int c = threadIdx.x; c < n; c += blockDim.x) t += snorm[c];
+    t = block_sum_g(t, shs);
+    if (threadIdx.x == 0) scal[1] = t;
   }
-  tot0 = block_sum_g(tot0, shs);
-  int k_out = k_max, status = 0;
-  for (int j = 0; j < k_max; ++j) {
-    // exact residual norms of the trailing columns (rows >= j)
-    for (int c = j + warp; c < n; c += nw) {
-      double t = 0.0;
-      for (int r = j + lane; r < ly; r += 32) t = fma(Y[(int64_t)c * ly + r], Y[(int64_t)c * ly + r], t);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      if (lane == 0) snorm[c] = t;
+  if (j > 0 && sc->eps2normAL2 > 0.0) {               // reading R8 on the sketch's mass
+    double t = 0.0;
+    for (int c = j + threadIdx.x; c < n; c += blockDim.x) t += snorm[c];
+    t = block_sum_g(t, shs);
+    if (t <= sc->eps2normAL2 / sc->normAL2 * scal[1]) {
+      if (threadIdx.x == 0) { sc->k_out = j; sc->status = 0; sc->resid2 = 0.0; sc->done = 1; }
+      return;
     }
-    __syncthreads();
-    if (j > 0 && sc->eps2normAL2 > 0.0) {
-      double t = 0.0;
-      for (int c = j + threadIdx.x; c < n; c += blockDim.x) t += snorm[c];
-      t = block_sum_g(t, shs);
-      // eps2normAL2 = eps^2 ||A_L||_F^2; the sketch's own mass replaces ||A_L||_F^2
-      if (t <= sc->eps2normAL2 / sc->normAL2 * tot0) { k_out = j; break; }
+  }
+  AM best{-INFINITY, 0x7fffffff, -1};
+  for (int c = j + threadIdx.x; c < n; c += blockDim.x) {
+    const AM a{snorm[c], perm[c], c};
+    if (am_gt(a, best)) best = a;
+  }
+  best = block_argmax_g(best, sha);
+  const int p = best.pos;
+  if (p != j) {
+    for (int r = threadIdx.x; r < ly; r += blockDim.x) {
+      const double x = Y[(int64_t)j * ly + r];
+      Y[(int64_t)j * ly + r] = Y[(int64_t)p * ly + r];
+      Y[(int64_t)p * ly + r] = x;
     }
-    AM best{-INFINITY, 0x7fffffff, -1};
-    for (int c = j + threadIdx.x; c < n; c += blockDim.x) {
-      const AM a{snorm[c], perm[c], c};
-      if (am_gt(a, best)) best = a;
+    for (int l = threadIdx.x; l < j; l += blockDim.x) {
+      const double x = R64[(int64_t)l * n + j];
+      R64[(int64_t)l * n + j] = R64[(int64_t)l * n + p];
+      R64[(int64_t)l * n + p] = x;
+      const float y = R[(int64_t)l * n + j];
+      R[(int64_t)l * n + j] = R[(int64_t)l * n + p];
+      R[(int64_t)l * n + p] = y;
     }
-    best = block_argmax_g(best, sha);
-    const int p = best.pos;
-    if (p != j) {
-      for (int r = threadIdx.x; r < ly; r += blockDim.x) {
-        const double x = Y[(int64_t)j * ly + r];
-        Y[(int64_t)j * ly + r] = Y[(int64_t)p * ly + r];
-        Y[(int64_t)p * ly + r] = x;
-      }
-      for (int l = threadIdx.x; l < j; l += blockDim.x) {
-        const double x = R64[(int64_t)l * n + j];
-        R64[(int64_t)l * n + j] = R64[(int64_t)l * n + p];
-        R64[(int64_t)l * n + p] = x;
-        const float y = R[(int64_t)l * n + j];
-        R[(int64_t)l * n + j] = R[(int64_t)l * n + p];
-        R[(int64_t)l * n + p] = y;
-      }
-      if (threadIdx.x == 0) {
-        const int q = perm[j];
-        perm[j] = perm[p];
-        perm[p] = q;
-        const double x = snorm[j];
-        snorm[j] = snorm[p];
-        snorm[p] = x;
-      }
-    }
-    __syncthreads();
-    const double sj = snorm[j];
-    if (!(sj >= DBL_MIN)) { k_out = j; status = 4; break; }
     if (threadIdx.x == 0) {
-      const double u0 = Y[(int64_t)j * ly + j];
-      const double beta = -copysign(sqrt(sj), u0);
-      sbeta = beta;
-      sc_ = 1.0 / (u0 - beta);
-      su0 = u0;
+      const int q = perm[j];
+      perm[j] = perm[p];
+      perm[p] = q;
+      const double x = snorm[j];
+      snorm[j] = snorm[p];
+      snorm[p] = x;
     }
-    __syncthreads();
-    const double beta = sbeta, cc = sc_;
-    const double sgn = beta < 0.0 ? -1.0 : 1.0;
-    for (int r = threadIdx.x; r < ly; r += blockDim.x)
-      vsh[r] = r < j ? 0.0 : (r == j ? 1.0 : __dmul_rn(Y[(int64_t)j * ly + r], cc));
-    __syncthreads();
-    // w_c = Y(j:, c)^T u, R(j, c) = w_c / beta, f_c = Y(j, c) - w_c / beta, Y(j:, c) -= v f_c
-    for (int c = j + warp; c < n; c += nw) {
-      double t = 0.0;
-      for (int r = j + lane; r < ly; r += 32) t = fma(Y[(int64_t)c * ly + r], Y[(int64_t)j * ly + r], t);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      const double rraw = t / beta;
-      const double f = Y[(int64_t)c * ly + j] - rraw;
-      __syncwarp();
-      if (c != j) {
-        for (int r = j + lane; r < ly; r += 32)
-          Y[(int64_t)c * ly + r] = __dadd_rn(__dmul_rn(-vsh[r], f), Y[(int64_t)c * ly + r]);
-      }
-      if (lane == 0) {
-        R64[(int64_t)j * n + c] = rraw * sgn;
-        R[(int64_t)j * n + c] = __double2float_rn(rraw * sgn);
-      }
-    }
-    __syncthreads();
-    // column j last (the others read its rows as u): Y(j:, j) -= v f_j
-    {
-      const double f = Y[(int64_t)j * ly + j] - R64[(int64_t)j * n + j] * sgn;
-      __syncthreads();
-      for (int r = j + threadIdx.x; r < ly; r += blockDim.x)
-        Y[(int64_t)j * ly + r] = __dadd_rn(__dmul_rn(-vsh[r], f), Y[(int64_t)j * ly + r]);
-    }
-    for (int i = threadIdx.x; i < j; i += blockDim.x) {
-      R64[(int64_t)j * n + i] = 0.0;
-      R[(int64_t)j * n + i] = 0.f;
-    }
-    __syncthreads();
+  }
+  __syncthreads();
+  const double sj = snorm[j];
+  if (!(sj >= DBL_MIN)) {
+    if (threadIdx.x == 0) { sc->k_out = j; sc->status = 4; sc->resid2 = 0.0; sc->done = 1; }
+    return;
+  }
+  const double u0 = Y[(int64_t)j * ly + j];
+  const double beta = -copysign(sqrt(sj), u0);
+  const double cc = 1.0 / (u0 - beta);
+  for (int r = threadIdx.x; r < ly; r += blockDim.x)
+    v[r] = r < j ? 0.0 : (r == j ? 1.0 : __dmul_rn(Y[(int64_t)j * ly + r], cc));
+  for (int i = threadIdx.x; i < j; i += blockDim.x) {
+    R64[(int64_t)j * n + i] = 0.0;
+    R[(int64_t)j * n + i] = 0.f;
   }
   if (threadIdx.x == 0) {
-    sc->k_out = k_out;
-    sc->status = status;
-    sc->resid2 = 0.0;
-    sc->done = 1;
+    scal[0] = beta;
+    sc->k_out = j + 1;
+    if (j + 1 >= k_max) { sc->status = 0; sc->resid2 = 0.0; }
   }
+}
+
+// warp per column c >= j: w_c = Y(j:, c)^T u with u = Y(j:, j), R(j, c) = w_c / beta (sign-
+// normalised), f_c = Y(j, c) - w_c / beta, Y(j:, c) -= v f_c and the new norm over rows > j.
+// Column j is only read here (every warp's u); k_sq_colj updates it afterwards.
+__global__ void __launch_bounds__(1024) k_sq_update(double* __restrict__ Y, int ly, int n, int j, int k_max,
+                                                    double* __restrict__ snorm, const double* __restrict__ v,
+                                                    const double* __restrict__ scal, double* __restrict__ R64,
+                                                    float* __restrict__ R, DevScalars* __restrict__ sc) {
+  if (sc->done) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = j + blockIdx.x * 32 + warp;
+  if (c < n) {
+    const double beta = scal[0];
+    const double sgn = beta < 0.0 ? -1.0 : 1.0;
+    double t = 0.0;
+    for (int r = j + lane; r < ly; r += 32) t = fma(Y[(int64_t)c * ly + r], Y[(int64_t)j * ly + r], t);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    const double rraw = t / beta;
+    const double f = Y[(int64_t)c * ly + j] - rraw;
+    if (lane == 0) {
+      R64[(int64_t)j * n + c] = rraw * sgn;
+      R[(int64_t)j * n + c] = __double2float_rn(rraw * sgn);
+    }
+    if (c != j) {
+      double s2 = 0.0;
+      for (int r = j + lane; r < ly; r += 32) {
+        const double y = __dadd_rn(__dmul_rn(-v[r], f), Y[(int64_t)c * ly + r]);
+        Y[(int64_t)c * ly + r] = y;
+        if (r > j) s2 = fma(y, y, s2);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      if (lane == 0) snorm[c] = s2;
+    }
+  }
+  (void)k_max;
+}
+
+// column j's own update, after every column's dot product with u = Y(j:, j)
+__global__ void k_sq_colj(double* __restrict__ Y, int ly, int n, int j, const double* __restrict__ v,
+                          const double* __restrict__ scal, const double* __restrict__ R64,
+                          const DevScalars* __restrict__ sc) {
+  if (sc->done) return;
+  const double beta = scal[0];
+  const double sgn = beta < 0.0 ? -1.0 : 1.0;
+  const double f = Y[(int64_t)j * ly + j] - R64[(int64_t)j * n + j] * sgn;
+  __syncthreads();
+  for (int r = j + threadIdx.x; r < ly; r += blockDim.x)
+    Y[(int64_t)j * ly + r] = __dadd_rn(__dmul_rn(-v[r], f), Y[(int64_t)j * ly + r]);
+}
+
+__global__ void k_sq_finish(int k_max, DevScalars* __restrict__ sc) {
+  if (sc->done) return;
+  sc->k_out = k_max;
+  sc->status = 0;
+  sc->resid2 = 0.0;
+  sc->done = 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -684,16 +715,23 @@ cudaError_t launch_sketch(const void* tmapO, const void* tmapS, void* Om, int64_
   return cudaGetLastError();
 }
 
-cudaError_t launch_small_qrcp(double* Y, int ly, int n, int k_max, double* snorm, int* perm, double* R64, float* R,
+cudaError_t launch_small_qrcp(double* Y, int ly, int n, int k_max, double* scratch, int* perm, double* R64, float* R,
                               DevScalars* sc, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_small_qrcp, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
+  double* snorm = scratch;                 // n
+  double* v = scratch + n;                 // ly <= n
+  double* scal = scratch + 2 * (size_t)n;  // 4
+  if (ly > n) return cudaErrorInvalidValue;
+  const unsigned cb = (unsigned)((n + 31) / 32);
+  k_sq_norms0<<<cb, 1024, 0, st>>>(Y, ly, n, snorm, perm, sc);
+  cudaError_t e = cudaGetLastError();
+  for (int j = 0; j < k_max && e == cudaSuccess; ++j) {
+    k_sq_pivot<<<1, 1024, 0, st>>>(Y, ly, n, j, k_max, snorm, v, scal, perm, R64, R, sc);
+    k_sq_update<<<(unsigned)((n - j + 31) / 32), 1024, 0, st>>>(Y, ly, n, j, k_max, snorm, v, scal, R64, R, sc);
+    k_sq_colj<<<1, 256, 0, st>>>(Y, ly, n, j, v, scal, R64, sc);
+    e = cudaGetLastError();
   }
-  if ((size_t)ly * 8 > 64 * 1024) return cudaErrorInvalidValue;
-  k_small_qrcp<<<1, 1024, (size_t)ly * 8, st>>>(Y, ly, n, k_max, snorm, perm, R64, R, sc);
+  if (e != cudaSuccess) return e;
+  k_sq_finish<<<1, 1, 0, st>>>(k_max, sc);
   return cudaGetLastError();
 }
 

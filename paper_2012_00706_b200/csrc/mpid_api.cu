@@ -538,7 +538,7 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     // the QRCP works on a copy (Gc) so Y stays available to id_get_sketch
     CK(cudaMemcpyAsync(h->Gc, h->G, (size_t)h->sk_lw * n * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
     CK(launch_small_qrcp(h->Gc, h->sk_lw, (int)n, k_max, h->red, h->perm, h->W, (float*)h->R, h->sc, h->st));
-    h->kernel_launches += 4;
+    h->kernel_launches += 3 + 2 + 3 * k_max;
     h->pass_launches = 0;
     CK(rec(h, h->ev[2]));
     return ID_OK;
