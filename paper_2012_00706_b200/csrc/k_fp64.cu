@@ -549,12 +549,8 @@ __global__ void __launch_bounds__(256, 1) k_dgemm_tn_async(GemmArgs g) {
 template <int MT>
 static cudaError_t tn_async_launch_t(const GemmArgs& g, dim3 grid, cudaStream_t st) {
   const size_t smem = (size_t)TN_S * (16 * MT + GT) * LDK * sizeof(double);
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(k_dgemm_tn_async<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  cudaError_t e = smem_attr((const void*)k_dgemm_tn_async<MT>, (int)smem);
+  if (e != cudaSuccess) return e;
   k_dgemm_tn_async<MT><<<grid, 256, smem, st>>>(g);
   return cudaGetLastError();
 }
@@ -576,13 +572,8 @@ static size_t dgemm_smem() {
 }
 template <int MODE, int MT>
 static cudaError_t dgemm_launch_t(const GemmArgs& g, dim3 grid, cudaStream_t st) {
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(k_dgemm<MODE, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)dgemm_smem<MODE>());
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  cudaError_t e = smem_attr((const void*)k_dgemm<MODE, MT>, (int)dgemm_smem<MODE>());
+  if (e != cudaSuccess) return e;
   k_dgemm<MODE, MT><<<grid, 256, dgemm_smem<MODE>(), st>>>(g);
   return cudaGetLastError();
 }
@@ -844,12 +835,9 @@ cudaError_t launch_tsmm(const double* X, int64_t ldx, int k1, const double* Y, i
 
 cudaError_t launch_cholesky(double* G, int k, int* info, cudaStream_t st) {
   const size_t sm = (size_t)k * k * sizeof(double);
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(k_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(k_cholesky_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    set = true;
-  }
+  cudaError_t e = smem_attr((const void*)k_cholesky, 160 * 1024);
+  if (e == cudaSuccess) e = smem_attr((const void*)k_cholesky_blocked, 200 * 1024);
+  if (e != cudaSuccess) return e;
   if (sm <= 160 * 1024) {
     k_cholesky<<<1, 1024, sm, st>>>(G, k, info);
   } else if (k <= 1024 && (size_t)k * (CH_NB + 1) * 8 <= 200 * 1024 - sizeof(double) * CH_LC * CH_NB) {
@@ -865,11 +853,8 @@ cudaError_t launch_trsm_left_upper(const double* R1, const double* R2, int k, co
                                    int mode, cudaStream_t st) {
   if (ncols <= 0) return cudaSuccess;
   const size_t smem = (size_t)k * 33 * sizeof(double);
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(k_trsm_left_block, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    set = true;
-  }
+  cudaError_t e = smem_attr((const void*)k_trsm_left_block, 200 * 1024);
+  if (e != cudaSuccess) return e;
   k_trsm_left_block<<<(unsigned)((ncols + 31) / 32), 1024, smem, st>>>(R1, R2, k, B, ldb, map, ncols,
                                                                         T, ldt, mode);
   return cudaGetLastError();
@@ -918,12 +903,8 @@ cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, cons
   const int grid = (int)std::min<int64_t>(ntiles, sms);
   *nblk_out = grid;
   const size_t smem = (size_t)(2 * GK * LDM + 2 * GT * LDK + GT * DLD) * sizeof(double);
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(k_err_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  cudaError_t e = smem_attr((const void*)k_err_persist, (int)smem);
+  if (e != cudaSuccess) return e;
   *nblk_out = grid;
   k_err_persist<<<grid, ERR_THREADS, smem, st>>>(g, ntiles, (int)ncb);
   return cudaGetLastError();

@@ -675,16 +675,12 @@ cudaError_t launch_gram(const void* tmap, int64_t ngroups, int n, int num_sms, d
                         const DevScalars* sc, cudaStream_t st) {
   const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(tmap);
   const GramWork w = gram_work(ngroups, n, num_sms);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM + 64);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = smem_attr((const void*)k_gram_tc, G_SMEM + 64);
+  if (e != cudaSuccess) return e;
   const int items = w.ntiles * w.splits;
   const int grid = std::min(items, num_sms);
   k_gram_tc<<<grid, G_BLOCK, G_SMEM + 64, st>>>(*tm, *tm, ngroups, w, part, sc);
-  cudaError_t e = cudaGetLastError();
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t tot = (int64_t)n * n;
   k_gram_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(part, w, n, G, sc);
@@ -700,12 +696,7 @@ cudaError_t launch_sketch(const void* tmapO, const void* tmapS, void* Om, int64_
   if (e != cudaSuccess) return e;
   const GramWork w = gram_work(ngroups, n, num_sms, lw, (int64_t)(part_doubles / (GT * GT)));
   if ((size_t)w.ntiles * w.splits * GT * GT > part_doubles) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM + 64);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if ((e = smem_attr((const void*)k_gram_tc, G_SMEM + 64)) != cudaSuccess) return e;
   const int items = w.ntiles * w.splits;
   k_gram_tc<<<std::min(items, num_sms), G_BLOCK, G_SMEM + 64, st>>>(
       *reinterpret_cast<const CUtensorMap*>(tmapO), *reinterpret_cast<const CUtensorMap*>(tmapS), ngroups, w, part, sc);

@@ -169,11 +169,8 @@ cudaError_t launch_gather_lowp(const double* A, int64_t m, int64_t ld, const int
 }
 cudaError_t launch_gemv_n(const double* A, int64_t m, int64_t ld, int n, const double* x, double* y, int subtract,
                           cudaStream_t st) {
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(k_gemv_n, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    set = true;
-  }
+  cudaError_t e = smem_attr((const void*)k_gemv_n, 64 * 1024);
+  if (e != cudaSuccess) return e;
   if (n > 8192) return cudaErrorInvalidValue;
   k_gemv_n<<<(unsigned)((m + 511) / 512), 256, (size_t)n * 8, st>>>(A, m, ld, n, x, y, subtract);
   return cudaGetLastError();

@@ -432,13 +432,8 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
 // ---------------------------------------------------------------------------
 template <typename T, int PMAX>
 static cudaError_t launch_ws_t(const PassParams& p, dim3 grid, size_t smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_pass_ws<T, PMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         PASS_SMEM_MAX);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = smem_attr((const void*)k_pass_ws<T, PMAX>, PASS_SMEM_MAX);
+  if (e != cudaSuccess) return e;
   k_pass_ws<T, PMAX><<<grid, PASS_BLOCK, smem, st>>>(p);
   return cudaGetLastError();
 }

@@ -512,12 +512,8 @@ static cudaError_t launch_tc_t(PassParams p, const void* tmap, int max_ctas, int
   const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, max_ctas / gy), (nact + TC_RG - 1) / TC_RG));
   p.gx_used = gx;
   *gx_out = gx;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_pass_tc<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, PASS_SMEM_MAX);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = smem_attr((const void*)k_pass_tc<T>, PASS_SMEM_MAX);
+  if (e != cudaSuccess) return e;
   k_pass_tc<T><<<dim3(gx, gy), TC_BLOCK, g.total, st>>>(p, *reinterpret_cast<const CUtensorMap*>(tmap));
   return cudaGetLastError();
 }

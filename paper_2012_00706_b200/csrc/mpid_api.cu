@@ -18,6 +18,21 @@
 
 using namespace mpid;
 
+#include <mutex>
+cudaError_t mpid::smem_attr(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[{func, dev}];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
 // ----------------------------------------------------------------------------
 // NCCL through dlopen (the process's libnccl.so.2, e.g. PyTorch's)
 // ----------------------------------------------------------------------------
@@ -62,15 +77,17 @@ struct Layout {
   size_t total;
 };
 
-int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+int num_sms() {   // of the current device (cached per device ordinal)
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+    cache[dev] = sms > 0 ? sms : 148;
   }
-  return sms;
+  return cache[dev];
 }
 
 constexpr int PW_NBLK = 64;   // row blocks of the transposed GEMV (power iteration)

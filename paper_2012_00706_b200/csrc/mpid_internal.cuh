@@ -122,6 +122,9 @@ __device__ __forceinline__ void fence_async_smem() {
 }
 
 // host-side launchers ---------------------------------------------------------
+// cudaFuncAttributeMaxDynamicSharedMemorySize of `func` raised to >= bytes on the current
+// device (the attribute is per device; set once per (kernel, device), thread-safe)
+cudaError_t smem_attr(const void* func, int bytes);
 cudaError_t launch_maxabs(const double* A, int64_t m, int64_t n, int64_t ld, double* part,
                           int nblk, cudaStream_t st);
 cudaError_t launch_maxabs_finish(const double* part, int nblk, DevScalars* sc, int scaling,
