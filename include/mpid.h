@@ -119,7 +119,9 @@ typedef struct {
   int32_t nb;
   int32_t status_qrcp;
   int32_t formation;     /* formation used by the last QRCP (see id_qrcp_opts) */
-  int32_t reserved[4];
+  int32_t lsq_path;      /* last id_coeffs_fp64: 0 R mode, 1 LSQ preconditioned by the QRCP's R11
+                            (one Cholesky QR pass), 2 LSQ by CholeskyQR2 (fallback) */
+  int32_t reserved[3];
   double t_host_launch_ms; /* host time of the QRCP graph launch call */
   double t_call_gpu_ms;    /* device time of the whole id_qrcp_lowprec call on the caller's stream */
 } id_stats;

@@ -931,6 +931,33 @@ cudaError_t launch_eye(double* I, int k, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+__global__ void k_diag_ratio(const double* __restrict__ R, int k, double* __restrict__ out) {
+  __shared__ double mx[32], mn[32];
+  double a = 0.0, b = INFINITY;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const double d = fabs(R[i + (int64_t)i * k]);
+    a = fmax(a, d);
+    b = fmin(b, d);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    b = fmin(b, __shfl_xor_sync(0xffffffffu, b, o));
+  }
+  if ((threadIdx.x & 31) == 0) { mx[threadIdx.x >> 5] = a; mn[threadIdx.x >> 5] = b; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { a = fmax(a, mx[w]); b = fmin(b, mn[w]); }
+    a = fmax(a, mx[0]);
+    b = fmin(b, mn[0]);
+    *out = b > 0.0 ? a / b : INFINITY;
+  }
+}
+cudaError_t launch_diag_ratio(const double* R, int k, double* out, cudaStream_t st) {
+  k_diag_ratio<<<1, 256, 0, st>>>(R, k, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sum_scalar(const double* part, int nblk, double* out, cudaStream_t st) {
   k_sum_scalar<<<1, 1024, 0, st>>>(part, nblk, out);
   return cudaGetLastError();

@@ -806,43 +806,74 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
   CK(launch_gather_cols(h->AD, m, h->ld, h->perm, k, h->AI, h->st));
   launches++;
   if (mode == ID_COEF_R) {
+    h->stats.lsq_path = 0;
     CK(launch_R_to_fp64(h->fmt == ID_FP64, h->R, k, n, h->Rd, h->st));
     CK(launch_trsm_left_upper(h->Rd, nullptr, k, h->Rd + (int64_t)k * k, k, nullptr, n - k, h->T, k, 0,
                               h->st));
     launches += 2;
   } else if (mode == ID_COEF_LSQ) {
-    // G1 = A_I^T A_I
+    // P(:, J) = argmin ||A_I X - A_J|| by a preconditioned Cholesky QR in fp64:
+    //   Q1 = A_I R1^{-1},  G2 = Q1^T Q1 = R2^T R2,  W = Q1^T A_J,  T = R1^{-1} R2^{-1} R2^{-T} W
+    // with R1 = the QRCP's own low-precision R11 ("computed from the R matrix and
+    // pivot indices ... via a least-squares problem"; A_I R11^{-1} is already close to
+    // orthonormal, so one Cholesky pass suffices), or, when that Q1 is too ill-conditioned
+    // (R2's diagonal spread > 1e3 or a breakdown), R1 = chol(A_I^T A_I): CholeskyQR2.
     const size_t tcap = tpart_doubles(m, n, h->k_cap);
-    int sp = splits_for(k, k, m, tcap);
-    CK(launch_tsmm(h->AI, m, k, h->AI, m, k, m, h->tpart, sp, h->st));
-    CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G1, h->st));
-    launches += 2;
-    id_status s = allreduce(h, h->G1, (size_t)k * k, NCCL_SUM);
-    if (s) return s;
-    CK(launch_cholesky(h->G1, k, h->info, h->st));
-    // Q1 = A_I R1^{-1}: the k x k inverse by triangular solves on I_k, then one DMMA GEMM
-    CK(launch_eye(h->Ik, k, h->st));
-    CK(launch_trsm_left_upper(h->G1, nullptr, k, h->Ik, k, nullptr, k, h->Rinv, k, 0, h->st));
-    CK(launch_nn_store(h->AI, m, m, h->Rinv, k, k, k, h->Q1, m, h->st));
-    launches += 4;
-    // G2 = Q1^T Q1
-    CK(launch_tsmm(h->Q1, m, k, h->Q1, m, k, m, h->tpart, sp, h->st));
-    CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G2, h->st));
-    s = allreduce(h, h->G2, (size_t)k * k, NCCL_SUM);
-    if (s) return s;
-    CK(launch_cholesky(h->G2, k, h->info + 1, h->st));
-    // W = Q1^T A_D(:, J), J = perm[k:] (W(:, I) = R1 is never needed)
-    const int nj = n - k;
-    if (nj > 0) {
-      const int spw = splits_for(k, nj, m, tcap);
-      CK(launch_tsmm(h->Q1, m, k, h->AD, h->ld, nj, m, h->tpart, spw, h->st, h->perm + k));
-      CK(launch_sum_partials(h->tpart, spw, (int64_t)k * nj, h->W, h->st));
-      s = allreduce(h, h->W, (size_t)k * nj, NCCL_SUM);
+    const int sp = splits_for(k, k, m, tcap);
+    auto lsq = [&](bool precond) -> id_status {
+      const double* R1;
+      if (precond) {
+        CK(launch_R_to_fp64(h->fmt == ID_FP64, h->R, k, n, h->Rd, h->st));   // leading k x k block = R11
+        CK(cudaMemsetAsync(h->info, 0, sizeof(int), h->st));
+        R1 = h->Rd;
+        launches += 1;
+      } else {
+        CK(launch_tsmm(h->AI, m, k, h->AI, m, k, m, h->tpart, sp, h->st));     // G1 = A_I^T A_I
+        CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G1, h->st));
+        id_status s = allreduce(h, h->G1, (size_t)k * k, NCCL_SUM);
+        if (s) return s;
+        CK(launch_cholesky(h->G1, k, h->info, h->st));
+        R1 = h->G1;
+        launches += 3;
+      }
+      // Q1 = A_I R1^{-1}: the k x k inverse by triangular solves on I_k, then one DMMA GEMM
+      CK(launch_eye(h->Ik, k, h->st));
+      CK(launch_trsm_left_upper(R1, nullptr, k, h->Ik, k, nullptr, k, h->Rinv, k, 0, h->st));
+      CK(launch_nn_store(h->AI, m, m, h->Rinv, k, k, k, h->Q1, m, h->st));
+      // G2 = Q1^T Q1
+      CK(launch_tsmm(h->Q1, m, k, h->Q1, m, k, m, h->tpart, sp, h->st));
+      CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G2, h->st));
+      id_status s = allreduce(h, h->G2, (size_t)k * k, NCCL_SUM);
       if (s) return s;
-      // T = R1^{-1} R2^{-1} R2^{-T} W_J
-      CK(launch_trsm_left_upper(h->G1, h->G2, k, h->W, k, nullptr, nj, h->T, k, 1, h->st));
+      CK(launch_cholesky(h->G2, k, h->info + 1, h->st));
+      CK(launch_diag_ratio(h->G2, k, h->err2 + 1, h->st));
+      launches += 7;
+      // W = Q1^T A_D(:, J), J = perm[k:] (W(:, I) is never needed)
+      const int nj = n - k;
+      if (nj > 0) {
+        const int spw = splits_for(k, nj, m, tcap);
+        CK(launch_tsmm(h->Q1, m, k, h->AD, h->ld, nj, m, h->tpart, spw, h->st, h->perm + k));
+        CK(launch_sum_partials(h->tpart, spw, (int64_t)k * nj, h->W, h->st));
+        s = allreduce(h, h->W, (size_t)k * nj, NCCL_SUM);
+        if (s) return s;
+        CK(launch_trsm_left_upper(R1, h->G2, k, h->W, k, nullptr, nj, h->T, k, 1, h->st));
+        launches += 3;
+      }
+      return ID_OK;
+    };
+    id_status s = lsq(true);
+    if (s) return s;
+    int inf[2] = {0, 0};
+    double ratio = 0.0;
+    CK(cudaMemcpyAsync(inf, h->info, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(&ratio, h->err2 + 1, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    h->stats.lsq_path = 1;
+    if (inf[1] != 0 || !(ratio <= 1e3)) {                 // identical decision on every rank
+      s = lsq(false);
+      if (s) return s;
+      h->stats.lsq_path = 2;
     }
-    launches += 6;
   } else {
     return fail(h, ID_ERR_ARG, "bad coefficient mode");
   }

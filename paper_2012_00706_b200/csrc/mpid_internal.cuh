@@ -160,6 +160,8 @@ cudaError_t launch_tsmm(const double* X, int64_t ldx, int k1, const double* Y, i
 cudaError_t launch_sum_partials(const double* part, int splits, int64_t len, double* out,
                                 cudaStream_t st);
 cudaError_t launch_cholesky(double* G, int k, int* info, cudaStream_t st);
+// out = max_i |R_ii| / min_i |R_ii| of an upper col-major k x k R (inf if a zero diagonal)
+cudaError_t launch_diag_ratio(const double* R, int k, double* out, cudaStream_t st);
 cudaError_t launch_trsm_left_upper(const double* R1, const double* R2, int k, const double* B,
                                    int64_t ldb, const int* map, int ncols, double* T, int64_t ldt,
                                    int mode, cudaStream_t st);

@@ -55,7 +55,8 @@ class Stats(C.Structure):
                 ("t_coef_ms", C.c_double), ("t_err_ms", C.c_double), ("t_pass_ms", C.c_double),
                 ("pass_launches", C.c_int64), ("kernel_launches", C.c_int64), ("k_out", C.c_int32),
                 ("nb", C.c_int32), ("status_qrcp", C.c_int32), ("formation", C.c_int32),
-                ("reserved", C.c_int32 * 4), ("t_host_launch_ms", C.c_double), ("t_call_gpu_ms", C.c_double)]
+                ("lsq_path", C.c_int32), ("reserved", C.c_int32 * 3), ("t_host_launch_ms", C.c_double),
+                ("t_call_gpu_ms", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
