@@ -315,3 +315,28 @@ def test_lsq_large_k_blocked_cholesky(m, n, k):
     out = run_gpu(A, "fp32", "none", k)
     P_ref = coeffs_lsq(A, out["piv"])
     assert np.linalg.norm(out["P"] - P_ref) <= 1e-10 * np.linalg.norm(P_ref)
+
+
+def test_lsq_fallback_to_cholqr2():
+    """When the fp16 R11 no longer preconditions A_I (true residuals far below the fp16
+    noise), R2's diagonal spread exceeds 1e3 and the call reruns as CholQR2
+    (id_stats.lsq_path = 2); the well-conditioned default stays on path 1."""
+    from paper_2012_00706_b200.mpid import MPID
+    from tests.gpu_helpers import to_dev
+    rng = np.random.default_rng(21)
+    m, n, r = 4096, 120, 40
+    A = rng.standard_normal((m, r)) @ rng.standard_normal((r, n)) + 3e-7 * rng.standard_normal((m, n))
+    A = np.asfortranarray(A)
+    h = MPID(to_dev(A), k_max=48)
+    q = h.qrcp("fp16", "pow2", k=48)
+    P = h.coeffs("lsq").cpu().numpy()
+    assert h.stats()["lsq_path"] == 2
+    P_ref = coeffs_lsq(A, q.piv)
+    assert np.linalg.norm(P - P_ref) <= 1e-7 * np.linalg.norm(P_ref)
+    h.close()
+    B = cfg("C1")
+    h = MPID(to_dev(B), k_max=24)
+    h.qrcp("fp16", "pow2", k=24)
+    h.coeffs("lsq")
+    assert h.stats()["lsq_path"] == 1
+    h.close()
