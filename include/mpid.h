@@ -61,8 +61,10 @@ typedef enum {
   ID_ERR_ARG = 1,        /* null pointer / invalid enum / bad leading dimension */
   ID_ERR_DIM = 2,        /* k out of range, shard geometry inconsistent, workspace too small */
   ID_ERR_OVERFLOW = 3,   /* A_L has an Inf after scaling and rounding */
-  ID_ERR_UNDERFLOW = 4,  /* selected pivot norm^2 below the fp32 normal range;
-                            k_out holds the completed steps, piv_out[0:k_out] valid */
+  ID_ERR_UNDERFLOW = 4,  /* selected pivot norm^2 below the normal range of the working
+                            precision (fp32; fp64 for ID_FP64 and the sketch), or, for Gram
+                            pivoting, a non-positive residual diagonal; k_out holds
+                            the completed steps, piv_out[0:k_out] valid */
   ID_ERR_DEGENERATE = 5, /* R11 or the skeleton Gram matrix is numerically singular */
   ID_ERR_DOMAIN = 6,     /* eps outside [0, 1) */
   ID_ERR_CUDA = 7,
@@ -162,7 +164,12 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
                           int32_t* piv_out);
 
 /* Step 3: P (k_out x n, column-major, leading dimension ldp >= k_out) in fp64 into
- * caller DEVICE memory P_out; P(:, I) is exactly I_k.  Requires a successful QRCP. */
+ * caller DEVICE memory P_out; P(:, I) is exactly I_k.  Requires a successful QRCP.
+ * ID_COEF_R: T = R11^{-1} R12 from the QRCP's R (fp64 triangular solve).  ID_COEF_LSQ:
+ * the fp64 least-squares fit of A_D(:, J) on A_D(:, I), by a Cholesky QR preconditioned
+ * with the QRCP's R11, rerun as CholeskyQR2 when that preconditioner is too weak
+ * (id_stats.lsq_path).  ID_ERR_DEGENERATE if A_D(:, I) is numerically rank deficient.
+ * Synchronises the stream. */
 id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t ldp);
 
 /* Step 4: ||A_D - A_D(:, I) P||_F and its ratio to ||A_D||_F (host scalars,
