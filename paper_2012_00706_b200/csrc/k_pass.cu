@@ -172,7 +172,10 @@ constexpr int PASS_BLOCK = 32 * (NCW + 2);   // + producer + prep
 constexpr int COLS_PER_WARP = 64;            // lane owns columns lane, lane + 32
 constexpr int RED_BYTES = 1024 * 2 * 8;      // cross-warp partials (WR * CW * 64 <= 1024 columns)
 
-template <typename T, int PMAX>
+// PMAX: capacity of the pending lists; EXACT: npend == PMAX at compile time (the common
+// npend <= 8 launches: the formation loops carry no runtime predicate); STORE: this launch
+// re-stores fl_L(A~) (p.store, as a compile-time flag)
+template <typename T, int PMAX, bool EXACT, bool STORE>
 __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
   if (p.sc->done) return;
   using W = typename Work<T>::W;
@@ -181,7 +184,9 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
   W* __restrict__ Ubuf = reinterpret_cast<W*>(p.U);
   const W* __restrict__ Fbuf = reinterpret_cast<const W*>(p.F);
   extern __shared__ __align__(128) unsigned char smem[];
-  const int n = p.n, j = p.j, npend = p.npend;
+  const int n = p.n, j = p.j;
+  const int npend = EXACT ? PMAX : p.npend;
+  constexpr int PA = PMAX > 0 ? PMAX : 1;        // array extent (npend = 0 at step 0)
   const int GS = p.gs, NST = p.nst;
   T* __restrict__ S = reinterpret_cast<T*>(p.S);
   const int c_lo = j + 32 * p.chunks_per_split * blockIdx.y;   // CTA column range
@@ -215,7 +220,7 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
   if (warp == 0) {
     // ======================= TMA producer (one lane) =======================
     if (lane != 0) return;
-    int slot_l[PMAX];
+    int slot_l[PA];
 #pragma unroll
     for (int l = 0; l < PMAX; ++l) slot_l[l] = (p.j0 + l) % NSLOT;
     auto issue_store = [&](int i) {
@@ -235,7 +240,7 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
       const int slot = i % NST;
       if (i >= NST) {
         mbar_wait(&empty[slot], ((i / NST) & 1) ^ 1);
-        if (p.store) {
+        if (STORE) {
           issue_store(i - NST);
           bulk_commit();
           bulk_wait_read0();
@@ -257,7 +262,7 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
           tma_load(base + geo.upend + l * GS * 8 * WSZ, Ubuf + (int64_t)slot_l[l] * p.m_pad + g0 * 8,
                    gsz * 8 * WSZ, &full[slot]);
     }
-    if (p.store) {
+    if (STORE) {
       for (int i = max(0, nst - NST); i < nst; ++i) {
         mbar_wait(&empty[i % NST], (i / NST) & 1);
         issue_store(i);
@@ -270,9 +275,9 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
 
   if (warp == 1) {
     // ========================= prep warp ==========================
-    W fj[PMAX];
-    double cl_[PMAX];
-    int64_t tstep[PMAX];
+    W fj[PA];
+    double cl_[PA];
+    int64_t tstep[PA];
 #pragma unroll
     for (int l = 0; l < PMAX; ++l) {
       const int sl = (p.j0 + l) % NSLOT;
@@ -308,7 +313,7 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
             a = upd1(-v, fj[l], a);
           }
         }
-        if (p.store) a = Chunk<T>::rnd(a);
+        if (STORE) a = Chunk<T>::rnd(a);
         const W u = (real && rg >= j) ? a : W(0);
         us[r] = u;
         if (blockIdx.y == 0) Uj[rl] = u;
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
   const int col1 = col0 + 32;
   const bool v0 = active && col0 < ncols, v1 = active && col1 < ncols;
   const int slot0 = p.j0 % NSLOT;
-  W2 f2[PMAX];
+  W2 f2[PA];
 #pragma unroll
   for (int l = 0; l < PMAX; ++l) {
     const int sl = (slot0 + l) % NSLOT;
@@ -369,7 +374,7 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
           }
         }
         // invalid lanes alias column 0's chunk: they must not write it back
-        if (p.store) Chunk<T>::round_store2(d0, d1, x, v0, v1);
+        if (STORE) Chunk<T>::round_store2(d0, d1, x, v0, v1);
         W uu[8];
         load8(us + gl * 8, uu);
         if (gl == gjs) {                                  // the group holding row j (rare)
@@ -395,7 +400,7 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
         as1 += (double)ps.y;
       }
     }
-    if (p.store) fence_async_smem();
+    if (STORE) fence_async_smem();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
     if (++slot == NST) { slot = 0; phase ^= 1; }
@@ -430,12 +435,34 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
 }
 
 // ---------------------------------------------------------------------------
-template <typename T, int PMAX>
+template <typename T, int PMAX, bool EXACT, bool STORE>
 static cudaError_t launch_ws_t(const PassParams& p, dim3 grid, size_t smem, cudaStream_t st) {
-  cudaError_t e = smem_attr((const void*)k_pass_ws<T, PMAX>, PASS_SMEM_MAX);
+  cudaError_t e = smem_attr((const void*)k_pass_ws<T, PMAX, EXACT, STORE>, PASS_SMEM_MAX);
   if (e != cudaSuccess) return e;
-  k_pass_ws<T, PMAX><<<grid, PASS_BLOCK, smem, st>>>(p);
+  k_pass_ws<T, PMAX, EXACT, STORE><<<grid, PASS_BLOCK, smem, st>>>(p);
   return cudaGetLastError();
+}
+
+template <typename T, bool STORE>
+static cudaError_t dispatch_store(const PassParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+  switch (p.npend) {
+    case 0: return launch_ws_t<T, 0, true, STORE>(p, grid, smem, st);
+    case 1: return launch_ws_t<T, 1, true, STORE>(p, grid, smem, st);
+    case 2: return launch_ws_t<T, 2, true, STORE>(p, grid, smem, st);
+    case 3: return launch_ws_t<T, 3, true, STORE>(p, grid, smem, st);
+    case 4: return launch_ws_t<T, 4, true, STORE>(p, grid, smem, st);
+    case 5: return launch_ws_t<T, 5, true, STORE>(p, grid, smem, st);
+    case 6: return launch_ws_t<T, 6, true, STORE>(p, grid, smem, st);
+    case 7: return launch_ws_t<T, 7, true, STORE>(p, grid, smem, st);
+    case 8: return launch_ws_t<T, 8, true, STORE>(p, grid, smem, st);
+    default:
+      if constexpr (sizeof(T) < 8) return launch_ws_t<T, 16, false, STORE>(p, grid, smem, st);   // fp64: nb <= 8
+      return cudaErrorInvalidValue;
+  }
+}
+template <typename T>
+static cudaError_t dispatch_ws(const PassParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+  return p.store ? dispatch_store<T, true>(p, grid, smem, st) : dispatch_store<T, false>(p, grid, smem, st);
 }
 
 template <typename T>
@@ -455,7 +482,7 @@ static cudaError_t launch_ws_fmt(PassParams p, int max_ctas, int* gx_out, cudaSt
   const int WR = NCW / CW;                                       // row-split warps
   p.cw = CW;
   p.wr = WR;
-  const int pmax = p.npend <= 1 ? 1 : p.npend <= 2 ? 2 : p.npend <= 4 ? 4 : p.npend <= 8 ? 8 : 16;
+  const int pmax = p.npend <= 8 ? p.npend : 16;     // exact pending count up to 8
   if (p.npend > pmax || pmax > NB_MAX || (wsz == 8 && pmax > 8)) return cudaErrorInvalidValue;
   // stage = GS row groups: ~48 KB of matrix data, a multiple of WR, at most 64 groups
   const int rowbytes = ncols * 8 * esz;
@@ -477,15 +504,7 @@ static cudaError_t launch_ws_fmt(PassParams p, int max_ctas, int* gx_out, cudaSt
   dim3 grid(gx, gy);
   p.gx_used = gx;
   *gx_out = gx;
-  switch (pmax) {
-    case 1: return launch_ws_t<T, 1>(p, grid, smem, st);
-    case 2: return launch_ws_t<T, 2>(p, grid, smem, st);
-    case 4: return launch_ws_t<T, 4>(p, grid, smem, st);
-    case 8: return launch_ws_t<T, 8>(p, grid, smem, st);
-    default:
-      if constexpr (sizeof(T) < 8) return launch_ws_t<T, 16>(p, grid, smem, st);   // fp64: nb <= 8
-      return cudaErrorInvalidValue;
-  }
+  return dispatch_ws<T>(p, grid, smem, st);
 }
 
 cudaError_t launch_pass_tma(int fmt, PassParams p, int max_ctas, int* gx_out, cudaStream_t st) {
