@@ -27,6 +27,7 @@
 // product-then-add as a separately rounded DMUL + DADD (the oracle's fp64 model, reading
 // R16); the interleaved layout and the pipeline are unchanged, with 4x the bytes.
 #include "mpid_internal.cuh"
+#include <cstdlib>
 
 namespace mpid {
 
@@ -484,9 +485,14 @@ static cudaError_t launch_ws_fmt(PassParams p, int max_ctas, int* gx_out, cudaSt
   p.wr = WR;
   const int pmax = p.npend <= 8 ? p.npend : 16;     // exact pending count up to 8
   if (p.npend > pmax || pmax > NB_MAX || (wsz == 8 && pmax > 8)) return cudaErrorInvalidValue;
-  // stage = GS row groups: ~48 KB of matrix data, a multiple of WR, at most 64 groups
+  // stage = GS row groups: ~64 KB of matrix data (tools/pass_tune.py: 48 -> 64 KB is ~1.5 %
+  // faster on C4, 80 KB slower), a multiple of WR, at most 64 groups
+  static const int stage_kb = [] {
+    const char* e = getenv("MPID_PASS_STAGE_KB");   // tuning experiments only
+    return e ? atoi(e) : 64;
+  }();
   const int rowbytes = ncols * 8 * esz;
-  int gpw = std::max(1, (48 * 1024) / (rowbytes * WR));
+  int gpw = std::max(1, (stage_kb * 1024) / (rowbytes * WR));
   int GS = std::min(64, WR * gpw);
   SlotGeom g = slot_geom(GS, ncols, esz, pmax, wsz);
   const size_t fixed = RED_BYTES + 3 * 8 * 8 + 64;
