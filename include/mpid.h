@@ -60,7 +60,8 @@ typedef enum {
   ID_OK = 0,
   ID_ERR_ARG = 1,        /* null pointer / invalid enum / bad leading dimension */
   ID_ERR_DIM = 2,        /* k out of range, shard geometry inconsistent, workspace too small */
-  ID_ERR_OVERFLOW = 3,   /* A_L has an Inf after scaling and rounding */
+  ID_ERR_OVERFLOW = 3,   /* A_L has an Inf after scaling and rounding, or A_D
+                            holds a NaN / Inf */
   ID_ERR_UNDERFLOW = 4,  /* selected pivot norm^2 below the normal range of the working
                             precision (fp32; fp64 for ID_FP64 and the sketch), or, for Gram
                             pivoting, a non-positive residual diagonal; k_out holds

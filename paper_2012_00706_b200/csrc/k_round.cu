@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int
           d = x;                                       // fp64: A_L = s A_D (one rounding of the product)
           v = x;
         }
-        inf |= isinf(d) ? 1 : 0;
+        inf |= (isinf(d) || isnan(d)) ? 1 : 0;         // non-finite A_L: ID_ERR_OVERFLOW
         colsq[q] = fma(d, d, colsq[q]);
         tile[cl][rr] = v;
       }

@@ -42,7 +42,7 @@ def run_gpu(A: np.ndarray, fmt: str, scaling: str, k: int, nb: int = 4, eps: flo
         At = torch.from_numpy(np.ascontiguousarray(np.asarray(A, dtype=np.float64).T)).pin_memory()
     else:
         At = to_dev(A)
-    h = MPID(At, k_max=k)
+    h = MPID(At, k_max=k, fp64=fmt == "fp64")
     q = h.qrcp(fmt, scaling, k=k, eps=eps, nb=nb, use_graph=use_graph, allow_underflow=allow_underflow,
                formation=formation)
     out = {"k": q.k, "piv": q.piv, "status": q.status}

@@ -340,3 +340,35 @@ def test_lsq_fallback_to_cholqr2():
     h.coeffs("lsq")
     assert h.stats()["lsq_path"] == 1
     h.close()
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "fp32", "fp64"])
+def test_degenerate_inputs(fmt):
+    """Edge cases: a NaN or Inf in A_D -> OVERFLOW; an all-zero matrix -> UNDERFLOW at
+    step 0 (no pivot); k > min(m, n) -> DIM; a single column; fewer rows than a group."""
+    from paper_2012_00706_b200.mpid import MPID, IDError
+    scaling = "pow2" if fmt == "fp16" else "none"
+    for bad in (np.nan, np.inf):
+        A = np.ones((64, 8))
+        A[7, 2] = bad
+        h = MPID(to_dev(A), k_max=2, fp64=fmt == "fp64")
+        with pytest.raises(IDError) as e:
+            h.qrcp(fmt, scaling, k=2)
+        assert e.value.name == "OVERFLOW"
+        h.close()
+    h = MPID(to_dev(np.zeros((64, 8))), k_max=3, fp64=fmt == "fp64")
+    q = h.qrcp(fmt, scaling, k=3, allow_underflow=True)
+    assert q.status == 4 and q.k == 0
+    h.close()
+    h = MPID(to_dev(np.ones((16, 4))), k_max=4, fp64=fmt == "fp64")
+    with pytest.raises(IDError) as e:
+        h.qrcp(fmt, scaling, k=5)
+    assert e.value.name == "DIM"
+    h.close()
+    rng = np.random.default_rng(1)
+    for (m, n, k) in [(100, 1, 1), (5, 3, 3), (7, 20, 4)]:
+        A = rng.standard_normal((m, n))
+        out = run_gpu(A, fmt, scaling, k, nb=1)
+        assert out["k"] == k
+        P_ref = coeffs_lsq(A, out["piv"])
+        assert np.linalg.norm(out["P"] - P_ref) <= 1e-10 * max(1.0, np.linalg.norm(P_ref))
