@@ -93,6 +93,39 @@ def test_C4_bench_configuration():
     h.close()
 
 
+def test_C4_fp32_and_next4_variants():
+    """configs[3] in fp32 (the other format BASELINE.json names for C4), and the two NEXT-4
+    pivoting variants at full size: the fp64 ID step checked in full against the oracle
+    given each run's I (and R for the R mode)."""
+    import torch
+    from paper_2012_00706_b200.mpid import MPID
+    spec = config_spec("C4")
+    fp = fourier_params(spec.extra["N"], spec.extra["L"], spec.n, 0)
+    At = gen_fourier(fp, 0, 0, spec.m, device="cuda")
+    A = At.cpu().numpy().T
+    k = spec.ks[0]
+    h = MPID(At, k_max=k)
+    # fp32: first pivot = argmax of the fp64 column norms of A_L = fl32(A) (no scaling)
+    h.round_only("fp32", "none")
+    AL = h.get_AL()
+    nrm = torch.zeros(spec.n, dtype=torch.float64, device="cuda")
+    for c0 in range(0, spec.n, 128):
+        blk = AL[:, c0:c0 + 128].double()
+        nrm[c0:c0 + 128] = (blk * blk).sum(0)
+    rows = np.sort(np.random.default_rng(2).choice(spec.m, 2048, replace=False))
+    g = AL[torch.as_tensor(rows, device="cuda")].cpu().numpy()
+    assert np.array_equal(g.view(np.uint32), A[rows].astype(np.float32).view(np.uint32))
+    del AL, blk
+    q = h.qrcp("fp32", "none", k=k, nb=4)
+    assert q.k == k and q.piv[0] == int(torch.argmax(nrm).item())
+    _fp64_checks(A, h, q, k)
+    for form in ("gram", "sketch"):
+        q = h.qrcp("fp16", "pow2", k=k, formation=form)
+        assert q.k == k
+        _fp64_checks(A, h, q, k)
+    h.close()
+
+
 @pytest.fixture(scope="module")
 def c3():
     return gen_config("C3", 0)
