@@ -96,11 +96,12 @@ typedef struct {
                         the condition number: pivots agree with the Householder QRCP
                         while the residual norms stay above ~sqrt(2048 u32) max||a||.
                         4 = sketched pivoting (NEXT-4, second option; R18):
-                        Y = Omega A_L with a Rademacher Omega of l = k_max + p rows
-                        (p = sketch_oversample, default 10; seed = sketch_seed) on tcgen05,
+                        Y = Omega A_L with a Rademacher Omega of l >= k_max + 10 rows
+                        (see sketch_oversample; seed = sketch_seed) on tcgen05,
                         then an fp64 Householder QRCP of Y; fp16 only; needs
                         l rounded up to 128 <= n.  R is the sketch's R factor. */
-  int32_t sketch_oversample; /* formation 4: l = k_max + sketch_oversample (0 = 10) */
+  int32_t sketch_oversample; /* formation 4: l = k_max + sketch_oversample; 0 = fill the
+                                128-row MMA tile that k_max + 10 needs (l = 128 for k = 100) */
   int32_t sketch_seed;       /* formation 4: seed of the Rademacher sketch */
   int32_t reserved[2];
 } id_qrcp_opts;

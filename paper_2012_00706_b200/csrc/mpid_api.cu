@@ -678,9 +678,11 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   if (formation >= 3 && fmt != ID_FP16)
     return fail(h, ID_ERR_ARG, "Gram / sketched pivoting (formation 3, 4) run on fp16 A_L (tcgen05 kind::f16)");
   if (formation == 4) {
+    // l = k_max + p; the default (p = 0 given) fills the 128-row tile that k_max + 10 needs
+    // anyway (the extra sketch rows cost no extra MMA tile), e.g. l = 128 for k = 100
     const int over = opts && opts->sketch_oversample > 0 ? opts->sketch_oversample : 10;
-    h->sk_l = k_max + over;
-    h->sk_lw = (h->sk_l + 127) / 128 * 128;
+    h->sk_lw = (k_max + over + 127) / 128 * 128;
+    h->sk_l = opts && opts->sketch_oversample > 0 ? k_max + over : h->sk_lw;
     h->sk_seed = opts ? (uint32_t)opts->sketch_seed : 0u;
     if (h->sk_lw > h->n || h->sk_l > 8192)
       return fail(h, ID_ERR_DIM, "sketch of %d rows (padded %d) exceeds n = %lld", h->sk_l, h->sk_lw, (long long)h->n);
