@@ -17,7 +17,8 @@
 //   vector f = x - w / beta (= tau A~^T v), the one-step downdated norms
 //   vn_i = s_i - R(j,i)^2 and the next pivot (warp-shuffle argmax, ties to the
 //   lowest original column index), all in device memory — no host sync.
-//   k_swap exchanges the pivot column into position j+1 (S, pending f, R, perm).
+//   The next pivot's bookkeeping (pending f, R, perm) is swapped by k_reflector; its
+//   data in S by the next pass's prologue (one column split) or k_swap (otherwise).
 //
 // Bound: HBM.  Per step the pass reads (m - j)(n - j) s bytes, plus
 // (m - j)(n - j) s bytes written on store steps (every nb-th), plus the
@@ -129,10 +130,10 @@ template <> __device__ __forceinline__ double to_w<double>(double x) { return x;
 
 template <typename W>
 __global__ void __launch_bounds__(1024) k_reflector(const double* __restrict__ red, int n, int j,
-                                                    int k_max, W* __restrict__ F,
+                                                    int k_max, int nb, W* __restrict__ F,
                                                     W* __restrict__ R, double* __restrict__ beta_out,
                                                     double* __restrict__ cvec, double* __restrict__ tau,
-                                                    const int* __restrict__ perm,
+                                                    int* __restrict__ perm,
                                                     DevScalars* __restrict__ sc) {
   if (sc->done) return;
   // tolerance stop on the exact norms of this step's formed trailing matrix (R8)
@@ -189,6 +190,30 @@ __global__ void __launch_bounds__(1024) k_reflector(const double* __restrict__ r
   }
   best = block_argmax(best);
   rest = block_sum(rest);
+  // the next step's pivot moves to position jn = j + 1: its bookkeeping (the pending f
+  // rows of the next panel, R's rows so far, perm) is swapped here; S's data is swapped
+  // by k_swap or inside the next pass
+  const int jn = j + 1, pn = best.pos;
+  if (jn < k_max && pn > jn) {
+    const int j0n = nb * (j / nb);                    // first pending step of step jn
+    for (int t = j0n + threadIdx.x; t < jn; t += blockDim.x) {
+      W* f = F + (int64_t)(t % NSLOT) * n;
+      const W x = f[jn];
+      f[jn] = f[pn];
+      f[pn] = x;
+    }
+    for (int t = threadIdx.x; t < jn; t += blockDim.x) {
+      W* r = R + (int64_t)t * n;
+      const W x = r[jn];
+      r[jn] = r[pn];
+      r[pn] = x;
+    }
+    if (threadIdx.x == 0) {
+      const int x = perm[jn];
+      perm[jn] = perm[pn];
+      perm[pn] = x;
+    }
+  }
   if (threadIdx.x == 0) {
     sc->k_out = j + 1;
     sc->resid2 = rest;
@@ -212,6 +237,10 @@ __global__ void __launch_bounds__(1024) k_init_pivot(const double* __restrict__ 
   best = block_argmax(best);
   tot = block_sum(tot);
   if (threadIdx.x == 0) {
+    if (best.pos > 0) {                               // step 0's pivot to position 0
+      perm[0] = best.pos;
+      perm[best.pos] = 0;
+    }
     sc->pivot = best.pos;
     sc->resid2 = tot;
     sc->k_out = 0;
@@ -221,8 +250,8 @@ __global__ void __launch_bounds__(1024) k_init_pivot(const double* __restrict__ 
   }
 }
 
-// swap columns jn <-> p (p = sc->pivot) in S (all row groups), in the pending
-// f vectors of steps [j0, jn), in R rows [0, jn), and in perm.
+// swap columns jn <-> p (p = sc->pivot) of S (all row groups) and copy the new pivot
+// column to Sj; F, R and perm are swapped by k_reflector / k_init_pivot
 template <typename T, typename W>
 __global__ void k_swap(T* __restrict__ S, int64_t ngroups, int n, int jn, int j0,
                        W* __restrict__ F, W* __restrict__ R, int* __restrict__ perm,
@@ -231,6 +260,8 @@ __global__ void k_swap(T* __restrict__ S, int64_t ngroups, int n, int jn, int j0
   const int p = sc->pivot;
   if (p < 0) return;
   const bool sw = p != jn;
+  (void)j0; (void)F; (void)R; (void)perm;
+  if (!sw && !Sj) return;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g < ngroups) {
     // the new pivot column jn, also copied to the contiguous buffer Sj (tcgen05 pass)
@@ -250,26 +281,6 @@ __global__ void k_swap(T* __restrict__ S, int64_t ngroups, int n, int jn, int j0
       for (int w = 0; w < NW; ++w) d[w] = tb[w];
     }
   }
-  if (!sw) return;
-  if (blockIdx.x == 0) {
-    for (int t = j0 + threadIdx.x; t < jn; t += blockDim.x) {
-      W* f = F + (int64_t)(t % NSLOT) * n;
-      const W x = f[jn];
-      f[jn] = f[p];
-      f[p] = x;
-    }
-    for (int t = threadIdx.x; t < jn; t += blockDim.x) {
-      W* r = R + (int64_t)t * n;
-      const W x = r[jn];
-      r[jn] = r[p];
-      r[p] = x;
-    }
-    if (threadIdx.x == 0) {
-      const int x = perm[jn];
-      perm[jn] = perm[p];
-      perm[p] = x;
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -280,13 +291,13 @@ cudaError_t launch_pass_reduce(const double* part, int gx, int n, int j, const d
   return cudaGetLastError();
 }
 
-cudaError_t launch_reflector(int fmt, const double* red, int n, int j, int k_max, void* F, void* R,
-                             double* beta, double* cvec, double* tau, const int* perm, DevScalars* sc,
+cudaError_t launch_reflector(int fmt, const double* red, int n, int j, int k_max, int nb, void* F, void* R,
+                             double* beta, double* cvec, double* tau, int* perm, DevScalars* sc,
                              cudaStream_t st) {
   if (fmt == 3)
-    k_reflector<double><<<1, 1024, 0, st>>>(red, n, j, k_max, (double*)F, (double*)R, beta, cvec, tau, perm, sc);
+    k_reflector<double><<<1, 1024, 0, st>>>(red, n, j, k_max, nb, (double*)F, (double*)R, beta, cvec, tau, perm, sc);
   else
-    k_reflector<float><<<1, 1024, 0, st>>>(red, n, j, k_max, (float*)F, (float*)R, beta, cvec, tau, perm, sc);
+    k_reflector<float><<<1, 1024, 0, st>>>(red, n, j, k_max, nb, (float*)F, (float*)R, beta, cvec, tau, perm, sc);
   return cudaGetLastError();
 }
 

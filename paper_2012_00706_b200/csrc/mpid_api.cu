@@ -579,9 +579,16 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     const int j0 = j == 0 ? 0 : nb * ((j - 1) / nb);
     const int npend = j - j0;
     const int store = (npend == nb) ? 1 : 0;
-    CK(launch_swap(fmt, h->S, h->m_pad / 8, (int)n, j, j0, j, h->F, h->R, h->perm,
-                   formation == 2 ? h->Sj : nullptr, h->sc, h->st));
+    // the pivot's S data: inside the pass when one CTA column split covers the trailing
+    // columns (FFMA formation), else a separate swap kernel (which also fills Sj for tcgen05)
+    const bool fuse_swap = formation == 1 && (n - j) <= 1024;
+    if (!fuse_swap) {
+      CK(launch_swap(fmt, h->S, h->m_pad / 8, (int)n, j, j0, j, h->F, h->R, h->perm,
+                     formation == 2 ? h->Sj : nullptr, h->sc, h->st));
+      h->kernel_launches += 1;
+    }
     PassParams p{};
+    p.fuse_swap = fuse_swap ? 1 : 0;
     p.S = h->S;
     p.ngroups = h->m_pad / 8;
     const int64_t jl = (int64_t)j - h->row_offset;
@@ -624,9 +631,9 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     CK(launch_pass_reduce(h->part, gx_used, (int)n, j, h->xr, own, h->red, h->sc, h->st));
     s = allreduce(h, h->red, (size_t)3 * n, NCCL_SUM);
     if (s) return s;
-    CK(launch_reflector(fmt, h->red, (int)n, j, k_max, h->F, h->R, h->beta, h->cvec, h->tau, h->perm,
+    CK(launch_reflector(fmt, h->red, (int)n, j, k_max, nb, h->F, h->R, h->beta, h->cvec, h->tau, h->perm,
                         h->sc, h->st));
-    h->kernel_launches += 4;
+    h->kernel_launches += 3;
     h->pass_launches += 1;
   }
   CK(rec(h, h->ev[2]));

@@ -57,6 +57,7 @@ struct PassParams {
   int nst;                 // pipeline depth (set by the launcher)
   int gx_used;             // gridDim.x (set by the launcher)
   int cw, wr;              // consumer warps: column-warps x row-split warps (launcher)
+  int fuse_swap;           // 1: swap S's columns j <-> sc->pivot for this CTA's rows first (gy == 1)
   const float* Vh;         // tcgen05 pass: the panel's V operand (hi / lo tf32), K-major
   const float* Vl;         //   core-matrix layout, nbw columns, (m_pad + 128) rows
   int nbw;                 // K width of the operand layouts (nb rounded up to 8)
@@ -143,8 +144,8 @@ cudaError_t launch_vop(const float* U, int64_t m_pad, int64_t m_local, int64_t r
 cudaError_t launch_pass_reduce(const double* part, int gx, int n, int j, const double* xr,
                                int own_row, double* red, const DevScalars* sc, cudaStream_t st);
 // F, R in the working precision: fp32 (fmt 1, 2) or fp64 (fmt 3)
-cudaError_t launch_reflector(int fmt, const double* red, int n, int j, int k_max, void* F, void* R,
-                             double* beta, double* cvec, double* tau, const int* perm, DevScalars* sc,
+cudaError_t launch_reflector(int fmt, const double* red, int n, int j, int k_max, int nb, void* F, void* R,
+                             double* beta, double* cvec, double* tau, int* perm, DevScalars* sc,
                              cudaStream_t st);
 cudaError_t launch_swap(int fmt, void* S, int64_t ngroups, int n, int jn, int j0, int steps_done,
                         void* F, void* R, int* perm, void* Sj, DevScalars* sc, cudaStream_t st);
