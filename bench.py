@@ -40,15 +40,11 @@ def flops(m, n, k, mode="lsq"):
 
 def pass_bytes(m, n, k, nb, s):
     """Algorithmic bytes of the dominant kernel (k_pass) summed over the k launches:
-    read (m-j)(n-j) s per step, plus a write of the same on store steps (j % nb == 0, j > 0),
-    plus, when the step's pivot swap runs in the pass prologue (n - j <= 1024), the
-    exchange of the two columns (read + write of 2 (m-j) s)."""
+    read (m-j)(n-j) s per step, plus a write of the same on store steps (j % nb == 0, j > 0)."""
     tot = 0.0
     for j in range(k):
         e = (m - j) * (n - j) * s
         tot += e * (2.0 if (j > 0 and j % nb == 0) else 1.0)
-        if n - j <= 1024:
-            tot += 4.0 * (m - j) * s
     return tot
 
 

@@ -216,26 +216,6 @@ __global__ void __launch_bounds__(PASS_BLOCK, 1) k_pass_ws(PassParams p) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (p.fuse_swap) {
-    // this step's pivot column (chosen by the last k_reflector) into position j, for the
-    // rows this CTA streams (the only column split: no other CTA reads them); the TMA
-    // loads below read them through the async proxy, hence the proxy fence
-    const int pv = p.sc->pivot;
-    if (pv > j) {
-      constexpr int NW = (int)sizeof(T) / 2;          // 16-byte words per 8-row chunk
-      for (int64_t g = gb + threadIdx.x; g < ge; g += blockDim.x) {
-        uint4* a = reinterpret_cast<uint4*>(S + (g * n + j) * RG);
-        uint4* b = reinterpret_cast<uint4*>(S + (g * n + pv) * RG);
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-          const uint4 x = a[w];
-          a[w] = b[w];
-          b[w] = x;
-        }
-      }
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-  }
   __syncthreads();
 
   if (warp == 0) {

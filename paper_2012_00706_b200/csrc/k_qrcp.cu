@@ -17,8 +17,8 @@
 //   vector f = x - w / beta (= tau A~^T v), the one-step downdated norms
 //   vn_i = s_i - R(j,i)^2 and the next pivot (warp-shuffle argmax, ties to the
 //   lowest original column index), all in device memory — no host sync.
-//   The next pivot's bookkeeping (pending f, R, perm) is swapped by k_reflector; its
-//   data in S by the next pass's prologue (one column split) or k_swap (otherwise).
+//   The next pivot's bookkeeping (pending f, R, perm) is swapped by k_reflector, its
+//   data in S by k_swap.
 //
 // Bound: HBM.  Per step the pass reads (m - j)(n - j) s bytes, plus
 // (m - j)(n - j) s bytes written on store steps (every nb-th), plus the
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(1024) k_reflector(const double* __restrict__ r
   rest = block_sum(rest);
   // the next step's pivot moves to position jn = j + 1: its bookkeeping (the pending f
   // rows of the next panel, R's rows so far, perm) is swapped here; S's data is swapped
-  // by k_swap or inside the next pass
+  // by k_swap
   const int jn = j + 1, pn = best.pos;
   if (jn < k_max && pn > jn) {
     const int j0n = nb * (j / nb);                    // first pending step of step jn

@@ -579,16 +579,13 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     const int j0 = j == 0 ? 0 : nb * ((j - 1) / nb);
     const int npend = j - j0;
     const int store = (npend == nb) ? 1 : 0;
-    // the pivot's S data: inside the pass when one CTA column split covers the trailing
-    // columns (FFMA formation), else a separate swap kernel (which also fills Sj for tcgen05)
-    const bool fuse_swap = formation == 1 && (n - j) <= 1024;
-    if (!fuse_swap) {
-      CK(launch_swap(fmt, h->S, h->m_pad / 8, (int)n, j, j0, j, h->F, h->R, h->perm,
-                     formation == 2 ? h->Sj : nullptr, h->sc, h->st));
-      h->kernel_launches += 1;
-    }
+    // the pivot's S data (its F / R / perm bookkeeping was swapped by the last k_reflector);
+    // an in-pass-prologue variant measured no faster: its scattered 16-byte accesses
+    // delay the CTA's TMA stream by as much as the separate launch costs
+    CK(launch_swap(fmt, h->S, h->m_pad / 8, (int)n, j, j0, j, h->F, h->R, h->perm,
+                   formation == 2 ? h->Sj : nullptr, h->sc, h->st));
+    h->kernel_launches += 1;
     PassParams p{};
-    p.fuse_swap = fuse_swap ? 1 : 0;
     p.S = h->S;
     p.ngroups = h->m_pad / 8;
     const int64_t jl = (int64_t)j - h->row_offset;

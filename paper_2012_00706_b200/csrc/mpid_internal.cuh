@@ -57,7 +57,6 @@ struct PassParams {
   int nst;                 // pipeline depth (set by the launcher)
   int gx_used;             // gridDim.x (set by the launcher)
   int cw, wr;              // consumer warps: column-warps x row-split warps (launcher)
-  int fuse_swap;           // 1: swap S's columns j <-> sc->pivot for this CTA's rows first (gy == 1)
   const float* Vh;         // tcgen05 pass: the panel's V operand (hi / lo tf32), K-major
   const float* Vl;         //   core-matrix layout, nbw columns, (m_pad + 128) rows
   int nbw;                 // K width of the operand layouts (nb rounded up to 8)
