@@ -48,6 +48,28 @@ def pass_bytes(m, n, k, nb, s):
     return tot
 
 
+PEAK_FP64_TFLOPS = 37.1   # tools/dmma_probe.cu on the box (register-resident DMMA m8n8k4); not in MEASURED_PEAKS
+
+
+def full_id_roofline(m, n, k, nb, s, hbm_gbs, f_coef, f_err, small_ms, t_total_ms):
+    """SURVEY §8(d) full-ID floor: round (8 + 8 + s B per element: max|a| pass + rounding)
+    and the QRCP pass bytes at the measured HBM bandwidth, the fp64 flops at the measured
+    DMMA peak (the error also bounded by one fp64 read of A_D), plus k times the measured
+    per-step cost of the small kernels (swap, reduce, reflector); fraction = floor / time."""
+    bw = hbm_gbs * 1e9
+    t_round = (8.0 + 8.0 + s) * m * n / bw
+    t_qrcp = pass_bytes(m, n, k, nb, s) / bw
+    p64 = PEAK_FP64_TFLOPS * 1e12
+    t_coef = f_coef / p64
+    t_err = max(f_err / p64, 8.0 * m * n / bw)
+    t_roof = (t_round + t_qrcp + t_coef + t_err) * 1e3 + max(0.0, small_ms)
+    return {"t_roof_ms": t_roof, "frac": t_roof / t_total_ms,
+            "parts_ms": {"round": t_round * 1e3, "qrcp_pass": t_qrcp * 1e3, "coef": t_coef * 1e3,
+                         "error": t_err * 1e3, "qrcp_small_kernels_measured": small_ms},
+            "peaks": {"hbm_gbs": hbm_gbs, "fp64_tflops": PEAK_FP64_TFLOPS,
+                      "fp64_source": "tools/dmma_probe.cu (register-resident DMMA) on a B200"}}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -388,6 +410,8 @@ def main():
                           "pass_total": pass_avg_ms},
             "tflops_parts": {"qrcp": fq / (statistics.mean(qr_ms) * 1e-3) / 1e12,
                              "fp64": (fc + fe) / ((statistics.mean(coef_ms) + statistics.mean(err_ms)) * 1e-3) / 1e12},
+            "full_id_roofline": full_id_roofline(m_loc, n, q.k, args.nb, s_bytes, peak, fc, fe,
+                                                 statistics.mean(qr_ms) - pass_avg_ms, ms_step),
             "k_out": q.k, "rel_err_fro": e[1], "errors_untimed": extra_err, "variants": variants,
             "roofline": {"kernel": "k_pass (per-step panel pass)", "bound": "hbm", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
