@@ -15,6 +15,7 @@
 // Bound: fp64 FMA pipe for the GEMM-shaped kernels (intensity ~k/4 flop/B).
 #include "mpid_internal.cuh"
 #include <math.h>
+#include <cstdlib>
 
 namespace mpid {
 
@@ -437,6 +438,194 @@ __global__ void __launch_bounds__(ERR_THREADS, 1) k_err_persist(GemmArgs g, int6
     double t = 0.0;
 #pragma unroll
     for (int w = 0; w < ERR_THREADS / 32; ++w) t += red[w];
+    g.out[blockIdx.x] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused error, warp-specialised: the same (tile, k-stage) walk and 4 x 4 consumer warps
+// as k_err_persist, but the operands arrive by bulk copies issued by one producer warp
+// into an EW_S-deep mbarrier ring, so no CTA-wide barrier sits in the DMMA loop (the
+// register-staged kernel spends ~20 % of its issue slots waiting at __syncthreads).
+//   A stage: EW_GK rows of A_I(m0 : m0 + 128, kb + l), one bulk copy per l (column-major
+//            A_I: each is contiguous);
+//   B stage: the EW_GK x 128 slab of T, pre-packed by k_pack_T into the padded
+//            [128 columns][EW_LDK] shared-memory image (one 12 KB bulk copy; zeros beyond
+//            k and beyond the last column, so the padded k rows of a ragged last stage add 0);
+//   A_D:     the tile's 128 column copies into Ds, issued once the previous tile's
+//            epilogue released Ds (dempty), EW_S - 1 stages into the tile.
+// Requires 16 B aligned A_I with an even row count (the copies move whole 16 B units).
+// ---------------------------------------------------------------------------
+constexpr int EW_GK = 8, EW_LDK = 12, EW_S = 4, EW_CONS = 16, EW_THREADS = (EW_CONS + 1) * 32;
+constexpr int EW_ASZ = EW_GK * LDM, EW_BSZ = GT * EW_LDK;
+__host__ __device__ inline int ew_nks(int64_t K) { return (int)((K + EW_GK - 1) / EW_GK); }
+size_t ew_tpack_doubles(int64_t n, int64_t k) {
+  return (size_t)((n + GT - 1) / GT) * ew_nks(k) * EW_BSZ;
+}
+
+__global__ void k_pack_T(const double* __restrict__ T, int64_t ldt, int K, int N, int nks, double* __restrict__ Tp,
+                         int64_t total) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = idx / EW_BSZ;
+    const int rem = (int)(idx - blk * EW_BSZ);
+    const int c = rem / EW_LDK, kk = rem - c * EW_LDK;
+    const int64_t ct = blk / nks, ks = blk - ct * nks;
+    const int64_t kg = ks * EW_GK + kk, col = ct * GT + c;
+    Tp[idx] = (kk < EW_GK && kg < K && col < N) ? T[col * ldt + kg] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(EW_THREADS, 1) k_err_ws(GemmArgs g, const double* __restrict__ Tp,
+                                                          int64_t ntiles, int ncb) {
+  extern __shared__ __align__(128) double dsm[];
+  double* As = dsm;                                   // [EW_S][EW_GK][LDM]
+  double* Bs = dsm + EW_S * EW_ASZ;                   // [EW_S][GT][EW_LDK]
+  double* Ds = Bs + EW_S * EW_BSZ;                    // [GT][DLD]
+  __shared__ __align__(8) uint64_t full[EW_S], empty[EW_S], dfull, dempty;
+  __shared__ double red[EW_CONS];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t K = g.K;
+  const int nks = ew_nks(K);
+  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  for (int i = tid; i < EW_S * EW_ASZ; i += EW_THREADS) As[i] = 0.0;   // finite stale rows
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < EW_S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], EW_CONS);
+    }
+    mbar_init(&dfull, 1);
+    mbar_init(&dempty, EW_CONS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto tile_of = [&](int64_t lt, int64_t& m0, int64_t& n0) {
+    const int64_t t = blockIdx.x + lt * gridDim.x;
+    m0 = (t / ncb) * GT;
+    n0 = (t % ncb) * GT;
+  };
+  if (warp == EW_CONS) {                              // producer warp
+    int64_t j = 0;
+    const int dstage = nks - 1 < EW_S - 1 ? nks - 1 : EW_S - 1;
+    for (int64_t lt = 0; lt < my_tiles; ++lt) {
+      int64_t m0, n0;
+      tile_of(lt, m0, n0);
+      const int64_t rows = (g.M - m0 < GT) ? g.M - m0 : (int64_t)GT;
+      const int cols = (int)((g.N - n0 < GT) ? g.N - n0 : (int64_t)GT);
+      const double* tsrc = Tp + (n0 / GT) * nks * EW_BSZ;
+      for (int ks = 0; ks < nks; ++ks, ++j) {
+        if (ks == dstage) {                           // A_D block of this tile
+          if (lt > 0) mbar_wait(&dempty, (uint32_t)((lt - 1) & 1));
+          int src[GT / 32];
+#pragma unroll
+          for (int q = 0; q < GT / 32; ++q) {
+            const int64_t c = n0 + lane + 32 * q;
+            src[q] = c < g.N ? (g.cmap ? g.cmap[c] : (int)c) : 0;
+          }
+          if (lane == 0) mbar_expect_tx(&dfull, (uint32_t)(rows * cols * 8));
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < GT / 32; ++q) {
+            const int c = lane + 32 * q;
+            if (c < cols) tma_load(Ds + c * DLD, g.A + (int64_t)src[q] * g.lda + m0, (uint32_t)(rows * 8), &dfull);
+          }
+        }
+        const int s = (int)(j % EW_S);
+        if (j >= EW_S) mbar_wait(&empty[s], (uint32_t)(((j / EW_S) - 1) & 1));
+        const int64_t kb = (int64_t)ks * EW_GK;
+        const int nk = (int)((K - kb < EW_GK) ? K - kb : (int64_t)EW_GK);
+        if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(nk * rows * 8 + EW_BSZ * 8));
+        __syncwarp();
+        if (lane < nk)
+          tma_load(As + s * EW_ASZ + lane * LDM, g.X + (kb + lane) * g.ldx + m0, (uint32_t)(rows * 8), &full[s]);
+        else if (lane == 31)
+          tma_load(Bs + s * EW_BSZ, tsrc + (int64_t)ks * EW_BSZ, (uint32_t)(EW_BSZ * 8), &full[s]);
+      }
+    }
+  } else {                                            // 16 consumer warps, 4 x 4, warp tile 32 x 32
+    const int gq = lane >> 2, tq = lane & 3;
+    const int wm = warp >> 2, wn = warp & 3;
+    double acc[ERR_MT][4][2];
+#pragma unroll
+    for (int a = 0; a < ERR_MT; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    double e2 = 0.0;
+    int64_t j = 0;
+    for (int64_t lt = 0; lt < my_tiles; ++lt) {
+      int64_t m0, n0;
+      tile_of(lt, m0, n0);
+      const bool active = m0 + wm * ERR_WM < g.M && n0 + wn * 32 < g.N;
+      for (int ks = 0; ks < nks; ++ks, ++j) {
+        const int s = (int)(j % EW_S);
+        mbar_wait(&full[s], (uint32_t)((j / EW_S) & 1));
+        const double* as = As + s * EW_ASZ + tq * LDM + wm * ERR_WM + gq;
+        const double* bs = Bs + s * EW_BSZ + (wn * 32 + gq) * EW_LDK + tq;
+        const int64_t kb = (int64_t)ks * EW_GK;
+        if (active) {
+#pragma unroll
+          for (int k4 = 0; k4 < EW_GK / 4; ++k4) {
+            if (kb + k4 * 4 >= K) break;
+            double af[ERR_MT], bf[4];
+#pragma unroll
+            for (int mt = 0; mt < ERR_MT; ++mt) af[mt] = as[k4 * 4 * LDM + mt * 8];
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) bf[nt] = bs[nt * 8 * EW_LDK + k4 * 4];
+#pragma unroll
+            for (int mt = 0; mt < ERR_MT; ++mt)
+#pragma unroll
+              for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+      // epilogue of tile lt
+      mbar_wait(&dfull, (uint32_t)(lt & 1));
+      if (m0 + GT <= g.M && n0 + GT <= g.N) {
+        const double* dbase = Ds + (wn * 32 + tq * 2) * DLD + wm * ERR_WM + gq;
+        double ea[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int mt = 0; mt < ERR_MT; ++mt) {
+              const double e = dbase[(nt * 8 + h) * DLD + mt * 8] - acc[mt][nt][h];
+              ea[(mt + 2 * h) & 3] = fma(e, e, ea[(mt + 2 * h) & 3]);
+              acc[mt][nt][h] = 0.0;
+            }
+        e2 += (ea[0] + ea[1]) + (ea[2] + ea[3]);
+      } else {
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
+#pragma unroll
+            for (int mt = 0; mt < ERR_MT; ++mt) {
+              const int64_t r = m0 + wm * ERR_WM + mt * 8 + gq;
+              if (r < g.M && c < g.N) {
+                const double e = Ds[(c - n0) * DLD + (r - m0)] - acc[mt][nt][h];
+                e2 = fma(e, e, e2);
+              }
+              acc[mt][nt][h] = 0.0;
+            }
+          }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dempty);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+    if (lane == 0) red[warp] = e2;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < EW_CONS; ++w) t += red[w];
     g.out[blockIdx.x] = t;
   }
 }
@@ -886,7 +1075,8 @@ cudaError_t launch_assemble_P(const double* T, int64_t ldt, int k, int n, const 
 }
 
 cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, const int* cmap, const double* X,
-                         int k, const double* T, int64_t ldt, double* part, int* nblk_out, cudaStream_t st) {
+                         int k, const double* T, int64_t ldt, double* part, int* nblk_out, cudaStream_t st,
+                         double* tpack, size_t tpack_cap) {
   GemmArgs g{};
   g.X = X; g.ldx = m;
   g.Y = T; g.ldy = ldt;
@@ -902,6 +1092,19 @@ cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, cons
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<int64_t>(ntiles, sms);
   *nblk_out = grid;
+  static const bool ws_off = getenv("MPID_ERR_NO_WS") != nullptr;   // A/B switch for measurements
+  if (!ws_off && g.d_tma && m % 2 == 0 && (((uintptr_t)X) & 15) == 0 && tpack &&
+      ew_tpack_doubles(ncols, k) <= tpack_cap) {
+    const int nks = ew_nks(k);
+    const int64_t tot = (int64_t)ew_tpack_doubles(ncols, k);
+    k_pack_T<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 4 * sms), 256, 0, st>>>(T, ldt, k, ncols, nks, tpack,
+                                                                                    tot);
+    const size_t smem_ws = (size_t)(EW_S * (EW_ASZ + EW_BSZ) + GT * DLD) * sizeof(double);
+    cudaError_t e = smem_attr((const void*)k_err_ws, (int)smem_ws);
+    if (e != cudaSuccess) return e;
+    k_err_ws<<<grid, EW_THREADS, smem_ws, st>>>(g, tpack, ntiles, (int)ncb);
+    return cudaGetLastError();
+  }
   const size_t smem = (size_t)(2 * GK * LDM + 2 * GT * LDK + GT * DLD) * sizeof(double);
   cudaError_t e = smem_attr((const void*)k_err_persist, (int)smem);
   if (e != cudaSuccess) return e;

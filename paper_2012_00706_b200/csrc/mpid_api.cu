@@ -73,7 +73,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t AD, S, U, F, Vh, Vl, Sj, R, part, red, xr, norms, perm, scal3, sc, maxpart, rpart;
-  size_t AI, Q1, G1, G2, W, tpart, Rd, T, Pw, epart, Ik, Rinv, py, pvec, gpart, G, Gc, misc;
+  size_t AI, Q1, G1, G2, W, tpart, Rd, T, Pw, epart, Tp, Ik, Rinv, py, pvec, gpart, G, Gc, misc;
   size_t total;
 };
 
@@ -169,6 +169,7 @@ Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
   L.T = take((size_t)k * n * 8);
   L.Pw = take((size_t)k * n * 8);
   L.epart = take((size_t)((m_local + 127) / 128) * ((n + 127) / 128) * 8);
+  L.Tp = take(ew_tpack_doubles(n, k) * 8);                            // error kernel: packed T slabs
   L.Ik = take((size_t)k * k * 8);
   L.Rinv = take((size_t)k * k * 8);
   L.py = take((size_t)m_local * 8);                                  // power iteration: y = E x
@@ -213,7 +214,7 @@ struct mpid_ctx {
   int* perm = nullptr;
   DevScalars* sc = nullptr;
   double *AI = nullptr, *Q1 = nullptr, *G1 = nullptr, *G2 = nullptr, *W = nullptr, *tpart = nullptr,
-         *Rd = nullptr, *T = nullptr, *Pw = nullptr, *epart = nullptr, *Ik = nullptr, *Rinv = nullptr,
+         *Rd = nullptr, *T = nullptr, *Pw = nullptr, *epart = nullptr, *Tp = nullptr, *Ik = nullptr, *Rinv = nullptr,
          *py = nullptr, *pvec = nullptr;
   double normAD_spec = -1.0;   // cached ||A_D||_2 (power iteration), < 0 = not yet
   int* info = nullptr;
@@ -341,6 +342,7 @@ static id_status relayout(mpid_ctx* h, int sbytes) {
   h->T = (double*)(w + L.T);
   h->Pw = (double*)(w + L.Pw);
   h->epart = (double*)(w + L.epart);
+  h->Tp = (double*)(w + L.Tp);
   h->Ik = (double*)(w + L.Ik);
   h->Rinv = (double*)(w + L.Rinv);
   h->py = (double*)(w + L.py);
@@ -912,7 +914,8 @@ id_status id_error(id_handle h, double* abs_fro, double* rel_fro) {
   // skeleton columns contribute exactly 0 (P(:, I) = I_k): sum over J = perm[k:] only
   const int nj = (int)h->n - k;
   if (nj > 0) {
-    CK(launch_error(h->AD, h->m_local, h->ld, nj, h->perm + k, h->AI, k, h->T, k, h->epart, &nblk, h->st));
+    CK(launch_error(h->AD, h->m_local, h->ld, nj, h->perm + k, h->AI, k, h->T, k, h->epart, &nblk, h->st, h->Tp,
+                          ew_tpack_doubles(h->n, h->k_cap)));
     CK(launch_sum_scalar(h->epart, nblk, h->err2, h->st));
   } else {
     CK(cudaMemsetAsync(h->err2, 0, sizeof(double), h->st));
@@ -991,7 +994,8 @@ id_status id_error_ex(id_handle h, int32_t skeleton, int32_t norm, int32_t iters
   if (norm == 0) {
     if (skeleton == 0) return id_error(h, abs_err, rel_err);
     int nblk = 0;   // all n columns: the low-precision skeleton columns are not reproduced exactly
-    CK(launch_error(h->AD, h->m_local, h->ld, n, nullptr, X, k, h->Pw, k, h->epart, &nblk, h->st));
+    CK(launch_error(h->AD, h->m_local, h->ld, n, nullptr, X, k, h->Pw, k, h->epart, &nblk, h->st, h->Tp,
+                          ew_tpack_doubles(h->n, h->k_cap)));
     CK(launch_sum_scalar(h->epart, nblk, h->err2, h->st));
     id_status s = allreduce(h, h->err2, 1, NCCL_SUM);
     if (s) return s;

@@ -172,7 +172,9 @@ cudaError_t launch_assemble_P(const double* T, int64_t ldt, int k, int n, const 
                               int64_t ldp, cudaStream_t st);
 // error over the columns J: sum_{r, c} (A(r, cmap[c]) - sum_l X(r, l) T(l, c))^2, c < ncols
 cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, const int* cmap, const double* X,
-                         int k, const double* T, int64_t ldt, double* part, int* nblk_out, cudaStream_t st);
+                         int k, const double* T, int64_t ldt, double* part, int* nblk_out, cudaStream_t st,
+                         double* tpack = nullptr, size_t tpack_cap = 0);
+size_t ew_tpack_doubles(int64_t n, int64_t k);   // packed T slabs of the warp-specialised error kernel
 // out(m x N) = X(m x K) B(K x N), all col-major
 cudaError_t launch_nn_store(const double* X, int64_t m, int64_t ldx, const double* B, int64_t ldb, int K,
                             int N, double* out, int64_t ldo, cudaStream_t st);

@@ -230,6 +230,24 @@ def test_ragged_and_edge_shapes(m, n, k):
         I = out["piv"]
         P_ref = coeffs_lsq(A, I)
         assert np.linalg.norm(out["P"] - P_ref) <= 1e-10 * max(np.linalg.norm(P_ref), 1e-300)
+        e = id_error(A, I, out["P"])                 # the fused error on the GPU's own P
+        assert abs(out["err"][0] - e[0]) <= 1e-9 * e[0] + 1e-300
+
+
+# The fused error kernels (Remark 2): the warp-specialised one needs an even row
+# count (odd m takes the register-staged kernel); k spans < 1 k-stage, a ragged last stage
+# (k % 8 != 0), whole stages; m x n spans one tile, ragged tiles and > 148 tiles (several
+# tiles per CTA, i.e. the ring and the A_D buffer wrap across tiles).
+@pytest.mark.parametrize("m,n,k", [(130, 50, 1), (1024, 140, 3), (1023, 140, 3), (2000, 300, 8),
+                                   (4098, 261, 13), (4097, 261, 13), (40000, 400, 100), (39999, 257, 64)])
+def test_error_kernel_shapes(m, n, k):
+    rng = np.random.default_rng(m * 7 + n + k)
+    A = np.asfortranarray(rng.standard_normal((m, n)) * np.exp(-np.arange(n) / 9.0)[None, :])
+    out = run_gpu(A, "fp32", "none", k, nb=4)
+    I = out["piv"]
+    e = id_error(A, I, out["P"])
+    assert abs(out["err"][0] - e[0]) <= 1e-9 * e[0]
+    assert abs(out["err"][1] - e[1]) <= 1e-9 * e[1]
 
 
 def test_tolerance_rank_matches_oracle():
