@@ -452,8 +452,8 @@ __global__ void __launch_bounds__(ERR_THREADS, 1) k_err_persist(GemmArgs g, int6
 //   B stage: the EW_GK x 128 slab of T, pre-packed by k_pack_T into the padded
 //            [128 columns][EW_LDK] shared-memory image (one 12 KB bulk copy; zeros beyond
 //            k and beyond the last column, so the padded k rows of a ragged last stage add 0);
-//   A_D:     the tile's 128 column copies into Ds, issued once the previous tile's
-//            epilogue released Ds (dempty), EW_S - 1 stages into the tile.
+//   A_D:     the tile's 128 column copies into Ds, 32 per stage from EW_S - 1 stages into
+//            the tile on, once the previous tile's epilogue released Ds (dempty).
 // Requires 16 B aligned A_I with an even row count (the copies move whole 16 B units).
 // ---------------------------------------------------------------------------
 constexpr int EW_GK = 8, EW_LDK = 12, EW_S = 4, EW_CONS = 16, EW_THREADS = (EW_CONS + 1) * 32;
@@ -514,23 +514,8 @@ __global__ void __launch_bounds__(EW_THREADS, 1) k_err_ws(GemmArgs g, const doub
       const int64_t rows = (g.M - m0 < GT) ? g.M - m0 : (int64_t)GT;
       const int cols = (int)((g.N - n0 < GT) ? g.N - n0 : (int64_t)GT);
       const double* tsrc = Tp + (n0 / GT) * nks * EW_BSZ;
+      int src[GT / 32];
       for (int ks = 0; ks < nks; ++ks, ++j) {
-        if (ks == dstage) {                           // A_D block of this tile
-          if (lt > 0) mbar_wait(&dempty, (uint32_t)((lt - 1) & 1));
-          int src[GT / 32];
-#pragma unroll
-          for (int q = 0; q < GT / 32; ++q) {
-            const int64_t c = n0 + lane + 32 * q;
-            src[q] = c < g.N ? (g.cmap ? g.cmap[c] : (int)c) : 0;
-          }
-          if (lane == 0) mbar_expect_tx(&dfull, (uint32_t)(rows * cols * 8));
-          __syncwarp();
-#pragma unroll
-          for (int q = 0; q < GT / 32; ++q) {
-            const int c = lane + 32 * q;
-            if (c < cols) tma_load(Ds + c * DLD, g.A + (int64_t)src[q] * g.lda + m0, (uint32_t)(rows * 8), &dfull);
-          }
-        }
         const int s = (int)(j % EW_S);
         if (j >= EW_S) mbar_wait(&empty[s], (uint32_t)(((j / EW_S) - 1) & 1));
         const int64_t kb = (int64_t)ks * EW_GK;
@@ -541,6 +526,27 @@ __global__ void __launch_bounds__(EW_THREADS, 1) k_err_ws(GemmArgs g, const doub
           tma_load(As + s * EW_ASZ + lane * LDM, g.X + (kb + lane) * g.ldx + m0, (uint32_t)(rows * 8), &full[s]);
         else if (lane == 31)
           tma_load(Bs + s * EW_BSZ, tsrc + (int64_t)ks * EW_BSZ, (uint32_t)(EW_BSZ * 8), &full[s]);
+        // the tile's A_D block, 32 columns per stage after that stage's operands (one
+        // 128 KB burst would queue ahead of the next stages' copies)
+        if (ks == dstage) {
+          if (lt > 0) mbar_wait(&dempty, (uint32_t)((lt - 1) & 1));
+#pragma unroll
+          for (int q = 0; q < GT / 32; ++q) {
+            const int64_t c = n0 + lane + 32 * q;
+            src[q] = c < g.N ? (g.cmap ? g.cmap[c] : (int)c) : 0;
+          }
+          if (lane == 0) mbar_expect_tx(&dfull, (uint32_t)(rows * cols * 8));
+          __syncwarp();
+        }
+        if (ks >= dstage) {
+          const int qi = ks - dstage;
+#pragma unroll
+          for (int q = 0; q < GT / 32; ++q) {
+            const int c = lane + 32 * q;
+            if ((q == qi || (ks == nks - 1 && q > qi)) && c < cols)
+              tma_load(Ds + c * DLD, g.A + (int64_t)src[q] * g.lda + m0, (uint32_t)(rows * 8), &dfull);
+          }
+        }
       }
     }
   } else {                                            // 16 consumer warps, 4 x 4, warp tile 32 x 32
