@@ -234,7 +234,7 @@ def test_ragged_and_edge_shapes(m, n, k):
         assert abs(out["err"][0] - e[0]) <= 1e-9 * e[0] + 1e-300
 
 
-# The fused error kernels (Remark 2): the warp-specialised one needs an even row
+# The fused error kernels (Remark 2) and the LSQ refit's TN GEMMs: the warp-specialised one needs an even row
 # count (odd m takes the register-staged kernel); k spans < 1 k-stage, a ragged last stage
 # (k % 8 != 0), whole stages; m x n spans one tile, ragged tiles and > 148 tiles (several
 # tiles per CTA, i.e. the ring and the A_D buffer wrap across tiles).
@@ -245,6 +245,10 @@ def test_error_kernel_shapes(m, n, k):
     A = np.asfortranarray(rng.standard_normal((m, n)) * np.exp(-np.arange(n) / 9.0)[None, :])
     out = run_gpu(A, "fp32", "none", k, nb=4)
     I = out["piv"]
+    # the LSQ products (Q1^T Q1, Q1^T A_J): m % 4 == 0 takes the warp-specialised TN GEMM,
+    # m % 4 == 2 the cp.async one, odd m the register-staged one
+    P_ref = coeffs_lsq(A, I)
+    assert np.linalg.norm(out["P"] - P_ref) <= 1e-10 * np.linalg.norm(P_ref)
     e = id_error(A, I, out["P"])
     assert abs(out["err"][0] - e[0]) <= 1e-9 * e[0]
     assert abs(out["err"][1] - e[1]) <= 1e-9 * e[1]
