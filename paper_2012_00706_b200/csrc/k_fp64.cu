@@ -476,6 +476,9 @@ __global__ void k_pack_T(const double* __restrict__ T, int64_t ldt, int K, int N
   }
 }
 
+// STORE = true: the same walk computes out = X T (Q1 = A_I R1^{-1} of the LSQ refit)
+// and stores it; no A_D block, no residual.
+template <bool STORE>
 __global__ void __launch_bounds__(EW_THREADS, 1) k_err_ws(GemmArgs g, const double* __restrict__ Tp,
                                                           int64_t ntiles, int ncb) {
   extern __shared__ __align__(128) double dsm[];
@@ -528,7 +531,7 @@ __global__ void __launch_bounds__(EW_THREADS, 1) k_err_ws(GemmArgs g, const doub
           tma_load(Bs + s * EW_BSZ, tsrc + (int64_t)ks * EW_BSZ, (uint32_t)(EW_BSZ * 8), &full[s]);
         // the tile's A_D block, 32 columns per stage after that stage's operands (one
         // 128 KB burst would queue ahead of the next stages' copies)
-        if (ks == dstage) {
+        if (!STORE && ks == dstage) {
           if (lt > 0) mbar_wait(&dempty, (uint32_t)((lt - 1) & 1));
 #pragma unroll
           for (int q = 0; q < GT / 32; ++q) {
@@ -538,7 +541,7 @@ __global__ void __launch_bounds__(EW_THREADS, 1) k_err_ws(GemmArgs g, const doub
           if (lane == 0) mbar_expect_tx(&dfull, (uint32_t)(rows * cols * 8));
           __syncwarp();
         }
-        if (ks >= dstage) {
+        if (!STORE && ks >= dstage) {
           const int qi = ks - dstage;
 #pragma unroll
           for (int q = 0; q < GT / 32; ++q) {
@@ -588,6 +591,21 @@ __global__ void __launch_bounds__(EW_THREADS, 1) k_err_ws(GemmArgs g, const doub
         if (lane == 0) mbar_arrive(&empty[s]);
       }
       // epilogue of tile lt
+      if (STORE) {
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
+#pragma unroll
+            for (int mt = 0; mt < ERR_MT; ++mt) {
+              const int64_t r = m0 + wm * ERR_WM + mt * 8 + gq;
+              if (r < g.M && c < g.N) g.out[c * g.ldo + r] = acc[mt][nt][h];
+              acc[mt][nt][h] = 0.0;
+            }
+          }
+        continue;
+      }
       mbar_wait(&dfull, (uint32_t)(lt & 1));
       if (m0 + GT <= g.M && n0 + GT <= g.N) {
         const double* dbase = Ds + (wn * 32 + tq * 2) * DLD + wm * ERR_WM + gq;
@@ -627,6 +645,7 @@ __global__ void __launch_bounds__(EW_THREADS, 1) k_err_ws(GemmArgs g, const doub
     for (int o = 16; o > 0; o >>= 1) e2 += __shfl_xor_sync(0xffffffffu, e2, o);
     if (lane == 0) red[warp] = e2;
   }
+  if (STORE) return;
   __syncthreads();
   if (tid == 0) {
     double t = 0.0;
@@ -1220,9 +1239,9 @@ cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, cons
     k_pack_T<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 4 * sms), 256, 0, st>>>(T, ldt, k, ncols, nks, tpack,
                                                                                     tot);
     const size_t smem_ws = (size_t)(EW_S * (EW_ASZ + EW_BSZ) + GT * DLD) * sizeof(double);
-    cudaError_t e = smem_attr((const void*)k_err_ws, (int)smem_ws);
+    cudaError_t e = smem_attr((const void*)k_err_ws<false>, (int)smem_ws);
     if (e != cudaSuccess) return e;
-    k_err_ws<<<grid, EW_THREADS, smem_ws, st>>>(g, tpack, ntiles, (int)ncb);
+    k_err_ws<false><<<grid, EW_THREADS, smem_ws, st>>>(g, tpack, ntiles, (int)ncb);
     return cudaGetLastError();
   }
   const size_t smem = (size_t)(2 * GK * LDM + 2 * GT * LDK + GT * DLD) * sizeof(double);
@@ -1234,12 +1253,29 @@ cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, cons
 }
 
 cudaError_t launch_nn_store(const double* X, int64_t m, int64_t ldx, const double* B, int64_t ldb, int K,
-                            int N, double* out, int64_t ldo, cudaStream_t st) {
+                            int N, double* out, int64_t ldo, cudaStream_t st, double* tpack, size_t tpack_cap) {
   GemmArgs g{};
   g.X = X; g.ldx = ldx;
   g.Y = B; g.ldy = ldb;
   g.M = m; g.N = N; g.K = K;
   g.out = out; g.ldo = ldo;
+  static const bool ws_off = getenv("MPID_NN_NO_WS") != nullptr;    // A/B switch for measurements
+  if (!ws_off && tpack && ew_tpack_doubles(N, K) <= tpack_cap && m % 2 == 0 && ldx % 2 == 0 &&
+      (((uintptr_t)X) & 15) == 0) {
+    // the warp-specialised walk of the fused error in STORE mode (packed B slabs, bulk copies)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ncb = (N + GT - 1) / GT, ntiles = ((m + GT - 1) / GT) * ncb;
+    const int nks = ew_nks(K);
+    const int64_t tot = (int64_t)ew_tpack_doubles(N, K);
+    k_pack_T<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 4 * sms), 256, 0, st>>>(B, ldb, K, N, nks, tpack, tot);
+    const size_t smem_ws = (size_t)(EW_S * (EW_ASZ + EW_BSZ) + GT * DLD) * sizeof(double);
+    cudaError_t e = smem_attr((const void*)k_err_ws<true>, (int)smem_ws);
+    if (e != cudaSuccess) return e;
+    k_err_ws<true><<<(unsigned)std::min<int64_t>(ntiles, sms), EW_THREADS, smem_ws, st>>>(g, tpack, ntiles, (int)ncb);
+    return cudaGetLastError();
+  }
   dim3 grid((unsigned)((m + GT - 1) / GT), (unsigned)((N + GT - 1) / GT), 1);
   return dgemm_launch<GM_NN_STORE>(g, grid, st, 8);
 }

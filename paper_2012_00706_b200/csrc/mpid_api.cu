@@ -847,7 +847,8 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
       // Q1 = A_I R1^{-1}: the k x k inverse by triangular solves on I_k, then one DMMA GEMM
       CK(launch_eye(h->Ik, k, h->st));
       CK(launch_trsm_left_upper(R1, nullptr, k, h->Ik, k, nullptr, k, h->Rinv, k, 0, h->st));
-      CK(launch_nn_store(h->AI, m, m, h->Rinv, k, k, k, h->Q1, m, h->st));
+      CK(launch_nn_store(h->AI, m, m, h->Rinv, k, k, k, h->Q1, m, h->st, h->Tp,
+                                 ew_tpack_doubles(h->n, h->k_cap)));
       // G2 = Q1^T Q1
       CK(launch_tsmm(h->Q1, m, k, h->Q1, m, k, m, h->tpart, sp, h->st));
       CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G2, h->st));

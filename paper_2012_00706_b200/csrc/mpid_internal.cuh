@@ -177,7 +177,8 @@ cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, cons
 size_t ew_tpack_doubles(int64_t n, int64_t k);   // packed T slabs of the warp-specialised error kernel
 // out(m x N) = X(m x K) B(K x N), all col-major
 cudaError_t launch_nn_store(const double* X, int64_t m, int64_t ldx, const double* B, int64_t ldb, int K,
-                            int N, double* out, int64_t ldo, cudaStream_t st);
+                            int N, double* out, int64_t ldo, cudaStream_t st, double* tpack = nullptr,
+                            size_t tpack_cap = 0);
 cudaError_t launch_eye(double* I, int k, cudaStream_t st);
 // NEXT-1 / NEXT-2 (k_norm2.cu): the low-precision skeleton and the 2-norm by power iteration
 cudaError_t launch_gather_lowp(const double* A, int64_t m, int64_t ld, const int* perm, int k, int fmt,
