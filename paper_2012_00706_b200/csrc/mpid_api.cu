@@ -101,7 +101,10 @@ int pass_gx_cap() { return num_sms(); }
 int round_gy(int64_t m_pad, int64_t n) {
   const int64_t gx = (n + 31) / 32;
   const int64_t ngroups = m_pad / 8;
-  int64_t gy = std::max<int64_t>(1, (4 * num_sms() + gx - 1) / gx);
+  // one wave: k_round holds 2 CTAs per SM (fp16 / fp32: 128 registers x 256 threads; the
+  // fp64 variant fits 3), and every CTA streams the same number of row tiles, so a grid
+  // of more than 2 x SMs leaves a tail wave of full-length CTAs (608 CTAs = 2.05 waves)
+  int64_t gy = std::max<int64_t>(1, (2 * num_sms()) / gx);
   gy = std::min<int64_t>(gy, std::max<int64_t>(1, ngroups / 8));
   return (int)std::min<int64_t>(gy, 4096);
 }
