@@ -880,10 +880,138 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_dgemm_tn_pipe(GemmArgs g) {
   }
 }
 
+// The same pipeline with an 8-row M granularity: all 8 consumer warps cover the CTA's
+// BM = 8 MR rows (MR m8 tiles) x 16 columns, so k = 100 pads to 104 rows instead of the
+// 112 of the (16 MT) x 128 tiling (7 % fewer DMMAs for the LSQ products at k = 100).
+template <int MR>
+__global__ void __launch_bounds__(TP_THREADS, 1) k_dgemm_tn_pipe8(GemmArgs g) {
+  constexpr int BM = 8 * MR;
+  extern __shared__ __align__(16) double dsm[];
+  double* As = dsm;                                  // [TP_S][BM][LDK]
+  double* Bs = dsm + TP_S * BM * LDK;                // [TP_S][GT][LDK]
+  __shared__ __align__(8) uint64_t full[TP_S], empty[TP_S];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int64_t n0 = (int64_t)blockIdx.y * GT;
+  const int64_t k_begin = (int64_t)blockIdx.z * g.k_per_split;
+  const int64_t k_end = min(g.K, k_begin + g.k_per_split);
+  const int nst = k_begin < k_end ? (int)((k_end - k_begin + GK - 1) / GK) : 0;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < TP_S; ++s) {
+      mbar_init(&full[s], TP_PROD);
+      mbar_init(&empty[s], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp >= 8) {                                   // producers
+    const int pt = tid - 256;
+    constexpr int BQ = GT * 8 / TP_PROD;
+    const double* bsrc[BQ];
+#pragma unroll
+    for (int q = 0; q < BQ; ++q) {
+      const int mn = (pt + q * TP_PROD) >> 3;
+      const int64_t c = n0 + mn;
+      bsrc[q] = c < g.N ? g.Y + (g.ycmap ? (int64_t)g.ycmap[c] : c) * g.ldy : nullptr;
+    }
+    for (int j = 0; j < nst; ++j) {
+      const int s = j % TP_S;
+      if (j >= TP_S) mbar_wait(&empty[s], (uint32_t)(((j / TP_S) - 1) & 1));
+      const int64_t kb = k_begin + (int64_t)j * GK;
+      for (int idx = pt; idx < BM * 8; idx += TP_PROD) {
+        const int mn = idx >> 3, kk = (idx & 7) * 2;
+        const int64_t i = m0 + mn, r = kb + kk;
+        const bool v = i < g.M && r < k_end;
+        cp_async16(&As[((size_t)s * BM + mn) * LDK + kk], v ? g.X + i * g.ldx + r : g.X, v);
+      }
+#pragma unroll
+      for (int q = 0; q < BQ; ++q) {
+        const int idx = pt + q * TP_PROD, mn = idx >> 3, kk = (idx & 7) * 2;
+        const int64_t r = kb + kk;
+        const bool v = bsrc[q] != nullptr && r < k_end;
+        cp_async16(&Bs[((size_t)s * GT + mn) * LDK + kk], v ? bsrc[q] + r : g.Y, v);
+      }
+      cp_async_mbar_arrive(&full[s]);
+    }
+    return;
+  }
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wn = warp;                               // 8 warps along N, 16 columns each
+  double acc[MR][2][2];
+#pragma unroll
+  for (int a = 0; a < MR; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const bool idle = n0 + wn * 16 >= g.N;
+  for (int it = 0; it < nst; ++it) {
+    const int s = it % TP_S;
+    mbar_wait(&full[s], (uint32_t)((it / TP_S) & 1));
+    const int64_t krem = (k_end - (k_begin + (int64_t)it * GK) + 3) / 4;
+    const int ksteps = idle ? 0 : (krem < GK / 4 ? (int)krem : GK / 4);
+    const double* Ab = As + (size_t)s * BM * LDK;
+    const double* Bb = Bs + (size_t)s * GT * LDK;
+#pragma unroll
+    for (int ks = 0; ks < GK / 4; ++ks) {
+      if (ks >= ksteps) break;
+      double af[MR], bf[2];
+#pragma unroll
+      for (int mt = 0; mt < MR; ++mt) af[mt] = Ab[(mt * 8 + gq) * LDK + ks * 4 + tq];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) bf[nt] = Bb[(wn * 16 + nt * 8 + gq) * LDK + ks * 4 + tq];
+#pragma unroll
+      for (int mt = 0; mt < MR; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  double* o = g.out + (int64_t)blockIdx.z * g.M * g.N;
+#pragma unroll
+  for (int mt = 0; mt < MR; ++mt) {
+    const int64_t i = m0 + mt * 8 + gq;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t c = n0 + wn * 16 + nt * 8 + tq * 2 + h;
+        if (i < g.M && c < g.N) o[c * g.M + i] = acc[mt][nt][h];
+      }
+  }
+}
+template <int MR>
+static cudaError_t tn_pipe8_launch_t(const GemmArgs& g, dim3 grid, cudaStream_t st) {
+  const size_t smem = (size_t)TP_S * (8 * MR + GT) * LDK * sizeof(double);
+  cudaError_t e = smem_attr((const void*)k_dgemm_tn_pipe8<MR>, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_dgemm_tn_pipe8<MR><<<grid, TP_THREADS, smem, st>>>(g);
+  return cudaGetLastError();
+}
+// M <= 128 whose 8-row padding is smaller than its 16-row padding: 8 MR rows per CTA
+static bool tn_pipe8_launch(const GemmArgs& g, dim3 grid, cudaStream_t st, cudaError_t* err) {
+  static const bool off = getenv("MPID_TN_NO_PIPE8") != nullptr;   // A/B switch for measurements
+  const int64_t M = g.M;
+  if (off || M > 128 || (M + 7) / 8 * 8 == (M + 15) / 16 * 16 || M <= 48) return false;
+  const int mr = (int)((M + 7) / 8);
+  grid.x = 1;
+  switch (mr) {
+    case 7: *err = tn_pipe8_launch_t<7>(g, grid, st); break;
+    case 9: *err = tn_pipe8_launch_t<9>(g, grid, st); break;
+    case 11: *err = tn_pipe8_launch_t<11>(g, grid, st); break;
+    case 13: *err = tn_pipe8_launch_t<13>(g, grid, st); break;
+    case 15: *err = tn_pipe8_launch_t<15>(g, grid, st); break;
+    default: return false;
+  }
+  return true;
+}
+
 template <int MT>
 static cudaError_t tn_async_launch_t(const GemmArgs& g, dim3 grid, cudaStream_t st) {
   static const bool pipe_off = getenv("MPID_TN_NO_PIPE") != nullptr;   // A/B switch for measurements
   if (!pipe_off) {
+    cudaError_t e8 = cudaSuccess;
+    if (tn_pipe8_launch(g, grid, st, &e8)) return e8;
     const size_t smem_p = (size_t)TP_S * (16 * MT + GT) * LDK * sizeof(double);
     cudaError_t e = smem_attr((const void*)k_dgemm_tn_pipe<MT>, (int)smem_p);
     if (e != cudaSuccess) return e;
