@@ -1,4 +1,5 @@
-"""The measurement switches (MPID_ERR_NO_WS, MPID_NN_NO_WS, MPID_TN_NO_PIPE)
+"""The measurement switches (MPID_ERR_NO_WS, MPID_NN_NO_WS, MPID_TN_NO_PIPE8,
+MPID_TN_NO_PIPE)
 select the previous fp64 kernels for A/B timing.  They are read once per process, so each
 runs in a subprocess; every one must give the LSQ coefficients to 1e-10 and the
 fused error (Remark 2) to 1e-9 against the oracle on the same skeleton.
@@ -23,8 +24,8 @@ import numpy as np
 sys.path.insert(0, sys.argv[1])
 from tests.gpu_helpers import run_gpu
 rng = np.random.default_rng(11)
-m, n, k = 6144, 300, 40
-A = np.asfortranarray(rng.standard_normal((m, n)) * np.exp(-np.arange(n) / 8.0)[None, :])
+m, n, k = 6144, 300, 100
+A = np.asfortranarray(rng.standard_normal((m, n)) * np.exp(-np.arange(n) / 20.0)[None, :])
 out = run_gpu(A, "fp32", "none", k, nb=4)
 print(json.dumps({"piv": [int(i) for i in out["piv"]], "P": out["P"].tolist(), "err": list(out["err"])}))
 """
@@ -33,13 +34,13 @@ print(json.dumps({"piv": [int(i) for i in out["piv"]], "P": out["P"].tolist(), "
 def _matrix():
     rng = np.random.default_rng(11)
     m, n = 6144, 300
-    return np.asfortranarray(rng.standard_normal((m, n)) * np.exp(-np.arange(n) / 8.0)[None, :])
+    return np.asfortranarray(rng.standard_normal((m, n)) * np.exp(-np.arange(n) / 20.0)[None, :])
 
 
-@pytest.mark.parametrize("switch", [None, "MPID_ERR_NO_WS", "MPID_NN_NO_WS", "MPID_TN_NO_PIPE"])
+@pytest.mark.parametrize("switch", [None, "MPID_ERR_NO_WS", "MPID_NN_NO_WS", "MPID_TN_NO_PIPE8", "MPID_TN_NO_PIPE"])
 def test_switch_matches_oracle(switch):
     env = dict(os.environ)
-    for s in ("MPID_ERR_NO_WS", "MPID_NN_NO_WS", "MPID_TN_NO_PIPE"):
+    for s in ("MPID_ERR_NO_WS", "MPID_NN_NO_WS", "MPID_TN_NO_PIPE8", "MPID_TN_NO_PIPE"):
         env.pop(s, None)
     if switch:
         env[switch] = "1"
