@@ -149,7 +149,10 @@ size_t id_workspace_bytes(int64_t m_local, int64_t n, int32_t k_max, int32_t nb,
  *   m_global   rows of the whole matrix; row_offset = first global row of the shard.
  *   workspace  caller-owned device memory, >= id_workspace_bytes(...) bytes,
  *              256-byte aligned.
- *   nccl_comm  ncclComm_t (as void*) when nranks > 1, else NULL.
+ *   nccl_comm  ncclComm_t (as void*) when nranks > 1, else NULL; a communicator
+ *              given with nranks == 1 is still used for every reduction.  A loopback
+ *              group from id_loopback_create (nranks handles on one device) is
+ *              accepted in its place.
  *   stream     cudaStream_t (as void*); NULL = legacy default stream. */
 id_status id_create(id_handle* h, const double* A_D, int64_t m_global, int64_t m_local,
                     int64_t row_offset, int64_t n, int64_t ld, void* workspace,
@@ -234,6 +237,19 @@ int32_t id_nccl_unique_id_bytes(void);
 id_status id_nccl_get_unique_id(void* out);
 id_status id_nccl_comm_init(void** comm, const void* unique_id, int32_t nranks, int32_t rank);
 id_status id_nccl_comm_destroy(void* comm);
+
+/* Loopback group: nranks handles of ONE process on ONE device stand in for nranks GPUs
+ * (the row-sharded path of SURVEY §8(e) exercised on a single GPU; SURVEY §4 tests/dist
+ * (i)).  Pass the returned pointer as nccl_comm to id_create of each rank's handle and
+ * drive each handle from its own host thread: every reduction synchronises the
+ * handle's stream, copies its buffer to the host, waits for all ranks (120 s timeout ->
+ * ID_ERR_NCCL) and receives the slots reduced in rank order 0..nranks-1 (sum or max), so
+ * every rank gets the same bits.  Handles on a loopback group never capture CUDA graphs.
+ * The group is caller-owned; destroy it after its handles.  id_loopback_calls returns
+ * the number of completed collectives (-1 for a pointer that is not a loopback group). */
+id_status id_loopback_create(void** comm, int32_t nranks);
+int64_t id_loopback_calls(void* comm);
+void id_loopback_destroy(void* comm);
 
 /* Library version and build target. */
 const char* id_version(void);

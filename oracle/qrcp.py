@@ -20,10 +20,18 @@ What is computed (PAPER.md):
         steps, after that step's pivot is chosen and before its reflector is
         formed — nb = 1 is SPEC's store-after-every-update, nb > 1 the blocked
         implementation the paper names as future work (P:402);
-      - reductions over rows (column norms, W^T u): fp32 fused multiply-add
-        chains over 8-row groups ("accumulate in single"), the group
-        partials added in fp64 (reading R5: sequential fp32 sums stagnate at
-        m = 2^24 rows);
+      - reductions over rows (column norms, W^T u): either ("chain8") fp32
+        fused multiply-add chains over 8-row groups ("accumulate in single",
+        P:209), the group partials added in fp64 (reading R5: sequential fp32
+        sums stagnate at m = 2^24 rows), or ("seq64") the exact fp32 x fp32
+        products added in fp64 in increasing row order — the plain definition
+        of the sum, independent of any kernel's order;
+      - the update W <- W - v f^T: "fma" one rounding per entry, or "rne" the
+        paper's per-operation rounding (north_star "correct RNE after
+        every op"): fl(W - fl(v f));
+      - model="paper" = update "rne" + acc "seq64": the oracle the CUDA path is
+        compared with by tolerance (DESIGN.md §2 R4b/R5, §Oracle); the "fma" +
+        "chain8" model is kept as the round-1 regression model of the FFMA pass;
       - pivot norms: the exact norms of the trailing matrix formed at step j-1,
         downdated by one step (reading R6); the recompute-every-step form of
         SPEC S:215 is kept as a cross-check (norms="recompute");
@@ -108,7 +116,25 @@ def chain8(X: np.ndarray, Y: np.ndarray, wdt) -> np.ndarray:
     acc = (Xg[:, 0].astype(np.float64) * Yg[:, 0].astype(np.float64)).astype(wdt)
     for i in range(1, 8):
         acc = _fma(Xg[:, i], Yg[:, i], acc, wdt)
-    return acc.astype(np.float64).sum(axis=0)
+    if G == 0:
+        return np.zeros(X.shape[1])
+    return np.add.accumulate(acc.astype(np.float64), axis=0)[-1].copy()
+
+
+def seq64(X: np.ndarray, Y: np.ndarray) -> np.ndarray:
+    """Column sums of X*Y: each product formed in fp64 (exact for fp32 / fp16 inputs) and
+    the products added in fp64 in increasing row order (np.add.accumulate is a
+    sequential running sum).  X: (r, c); Y: (r, c) or (r, 1)."""
+    P = X.astype(np.float64) * Y.astype(np.float64)
+    if P.shape[0] == 0:
+        return np.zeros(P.shape[1])
+    return np.add.accumulate(P, axis=0)[-1].copy()
+
+
+def _sum1(x) -> float:
+    """Sequential fp64 sum of a vector (first term first)."""
+    x = np.asarray(x, dtype=np.float64)
+    return float(np.add.accumulate(x)[-1]) if x.size else 0.0
 
 
 class _Local:
@@ -120,26 +146,10 @@ class _Local:
         return np.asarray(x, dtype=np.float64)
 
 
-def pair8(X: np.ndarray, Y: np.ndarray, wdt) -> np.ndarray:
-    """Column sums of X*Y in the tensor-core pass's order (reading R5b): within each
-    group of 8 consecutive rows two working-precision FMA chains, one over the even
-    rows (0, 2, 4, 6) and one over the odd rows (1, 3, 5, 7), started with a product;
-    the two chain values added in working precision; group partials added in fp64."""
-    G = X.shape[0] // 8
-    Xg = X.reshape(G, 8, -1)
-    Yg = Y.reshape(G, 8, -1)
-    ev = (Xg[:, 0].astype(np.float64) * Yg[:, 0].astype(np.float64)).astype(wdt)
-    od = (Xg[:, 1].astype(np.float64) * Yg[:, 1].astype(np.float64)).astype(wdt)
-    for i in (2, 4, 6):
-        ev = _fma(Xg[:, i], Yg[:, i], ev, wdt)
-        od = _fma(Xg[:, i + 1], Yg[:, i + 1], od, wdt)
-    tot = (ev.astype(np.float64) + od.astype(np.float64)).astype(wdt)
-    return tot.astype(np.float64).sum(axis=0)
-
-
 def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1,
                      eps: float = 0.0, norms: str = "downdate", acc: str = "auto",
-                     row_offset: int = 0, comm=None, formation: str = "fma") -> QRCPResult:
+                     row_offset: int = 0, comm=None, formation: str = "fma",
+                     update: str = "fma", model: str | None = None) -> QRCPResult:
     """Householder QRCP of the already-rounded A_L, in the precision model above.
 
     Step j (0-based), following Eq. (6)-(7):
@@ -150,13 +160,14 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
          the exact norms of the current trailing matrix (cross-check).
       2. every nb steps (j > 0, j % nb == 0): W(j:, j:) <- fl_L(W(j:, j:))      [store point, R4]
       3. s_i = ||W(j:m, i)||^2, w = W(j:m, j:)^T u with u = W(j:m, j), summed in
-         the blocked order `acc` ("chain8": 8-row fp32 FMA chains + fp64, R5;
-         "pair8": even/odd-row chains, the tensor-core pass's order, R5b; "fp64":
-         exact products summed in fp64; "auto": pair8 for formation="tc", else chain8)
+         the order `acc` ("chain8": 8-row fp32 FMA chains + fp64, R5; "seq64":
+         exact products summed in fp64 in row order; "fp64": exact products,
+         numpy's fp64 sum; "auto": seq64 for formation="tc", else chain8)
       4. beta = -sign(u_0) sqrt(s_j); c = 1/(u_0 - beta); v = fl(u c), v_0 = 1;
          tau = (beta - u_0)/beta; R(j, i) = w_i / beta (row sign-normalised so
          R_jj = |beta|); f = fl(x - w/beta) with x = W(j, j:) (= tau W^T v)
-      5. W(j:m, j:) <- fl(W - v f^T), one rounding per entry                     [update, R4b]
+      5. W(j:m, j:) <- fl(W - v f^T): update="fma" one rounding per entry, "rne"
+         fl(W - fl(v f)) (the product rounded, then the difference)            [update, R4b]
     The tolerance stop (reading R8) is tested before step j >= 1 on the exact
     norms of step 3: sqrt(sum_{i >= j} s_i) <= eps ||A_L||_F -> k = j.
 
@@ -168,15 +179,26 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
     beta, R, f, norms) is taken identically on all ranks from the summed values.
     With comm=None the matrix is the whole A_L.
 
-    formation="tc" (reading R14; the tensor-core pass): W is the
-    stored matrix S, updated only at store points, and each step forms the
-    trailing block as X = fl32(S - fl32(V_p F_p^T)) with the pending product
-    V_p F_p^T evaluated exactly (fp64; the GPU's 3xTF32 tcgen05 product is within
-    ~2^-21 of it) and rounded once to fp32 (the TMEM accumulator), then one fp32
-    subtraction.  The pivot column u = X(:, 0) (the GPU forms it in TMEM lane 127
-    of every CTA with the same operands), X(j, :) is the pivot row, and at a store
-    point fl_L(X) becomes the new S.
+    formation="tc" (reading R14; SURVEY's D-OTF form of the
+    tensor-core pass): W is the stored matrix S, updated only at store points,
+    and each step forms the trailing block as X = fl32(S - V_p F_p^T), the exact
+    trailing block rounded ONCE to fp32 (V_p F_p^T of the pending fp32 v / f
+    vectors evaluated in fp64: each product is exact and the <= 32-term sum is
+    within 2^-48 relative).  The pivot column u = X(:, 0), X(j, :) is the pivot
+    row, and at a store point fl_L(X) becomes the new S.
+
+    model="paper" selects update="rne", acc="seq64" (the default oracle the
+    CUDA path is compared with by tolerance); model="kernel" selects the
+    round-1 FFMA-pass model update="fma", acc="chain8".
     """
+    if model == "paper":
+        update, acc = "rne", "seq64"
+    elif model == "kernel":
+        update, acc = "fma", "chain8"
+    elif model is not None:
+        raise ValueError(model)
+    if update not in ("fma", "rne"):
+        raise ValueError(update)
     fmtL = fmt_of(fmt)
     wdt = _work_dtype(fmt)
     comm = _Local if comm is None else comm
@@ -195,21 +217,22 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
     V = np.zeros((m, k_max), dtype=np.float64)
     tau = np.zeros(k_max)
     top2 = np.zeros((k_max, 2))
-    col2 = comm.sum(np.sum(A_L * A_L, axis=0))
-    normAL = math.sqrt(float(np.sum(col2)))
+    if acc == "auto":
+        acc = "seq64" if formation == "tc" else "chain8"
+    col2 = comm.sum(seq64(A_L, A_L))                        # fp16 squares add exactly in fp64
+    normAL = math.sqrt(_sum1(col2))
     maxnorm0 = math.sqrt(float(np.max(col2))) if n else 0.0
     vn = col2.copy()                                        # exact initial norms^2
     tiny = DOUBLE.min_normal if fmtL is DOUBLE else SINGLE.min_normal
 
-    if acc == "auto":
-        acc = "pair8" if formation == "tc" else "chain8"
-
     def reduce(X, Y):
         if acc == "chain8":
             return comm.sum(chain8(X, Y, wdt))
-        if acc == "pair8":
-            return comm.sum(pair8(X, Y, wdt))
-        return comm.sum(np.sum(X.astype(np.float64) * Y.astype(np.float64), axis=0))
+        if acc == "seq64":
+            return comm.sum(seq64(X, Y))
+        if acc == "fp64":
+            return comm.sum(np.sum(X.astype(np.float64) * Y.astype(np.float64), axis=0))
+        raise ValueError(acc)
 
     def local(jg):
         """first local row whose global index is >= jg, and the first row of its 8-row group"""
@@ -225,8 +248,8 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
     def form_tc(j):
         """(X, u): the formed trailing block W(:, j:) and the pivot column u = X(:, 0)
         (formation='tc')."""
-        D = (Vp @ Fp[:, j:]).astype(np.float32) if Fp.shape[0] else np.zeros((m8, n - j), np.float32)
-        X = (W[:, j:].astype(np.float64) - D.astype(np.float64)).astype(wdt)
+        D = (Vp @ Fp[:, j:]) if Fp.shape[0] else np.zeros((m8, n - j))
+        X = (W[:, j:].astype(np.float64) - D).astype(wdt)
         return X, X[:, 0].copy()
 
     resid = []
@@ -269,7 +292,7 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
             Wj[: jl - g0] = 0
             u = Wj[:, :1]
         s = reduce(Wj, Wj)
-        resid.append(math.sqrt(float(np.sum(s))))           # exact remaining mass before step j
+        resid.append(math.sqrt(_sum1(s)))                  # exact remaining mass before step j
         if eps > 0.0 and j > 0 and resid[-1] <= eps * normAL:
             k_out = j                                       # tolerance stop (reading R8)
             break
@@ -301,13 +324,16 @@ def qrcp_householder(A_L: np.ndarray, k_max: int, fmt: str = "fp16", nb: int = 1
             Vp = np.concatenate([Vp, vfull[:, None]], axis=1)
             Fp = np.concatenate([Fp, frow[None, :]], axis=0)
         else:
-            W[jl:, j:] = _fma(-v[:, None], f[None, :], W[jl:, j:], wdt)   # step 5
+            if update == "fma":
+                W[jl:, j:] = _fma(-v[:, None], f[None, :], W[jl:, j:], wdt)   # step 5
+            else:                                           # fl(W - fl(v f)), per-op RNE
+                W[jl:, j:] = W[jl:, j:] - (v.astype(wdt)[:, None] * f.astype(wdt)[None, :])
         V[jl:, j] = v[: max(m - jl, 0)]
     if status == "ok" and k_out == k_max and k_max < min(m_glob, n):
         jl, g0 = local(k_max)
         Wj = (form_tc(k_max)[0][g0:] if tc else W[g0:, k_max:]).copy()
         Wj[: jl - g0] = 0
-        resid.append(math.sqrt(float(np.sum(reduce(Wj, Wj)))))   # exact mass after k steps
+        resid.append(math.sqrt(_sum1(reduce(Wj, Wj))))     # exact mass after k steps
     R = R[:k_out]
     return QRCPResult(perm, R, k_out, status, V[:, :k_out], tau[:k_out], top2[:k_out],
                       maxnorm0, normAL, resid)

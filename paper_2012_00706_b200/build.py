@@ -25,17 +25,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(d) <= t for d in deps):
             return LIB
-    objs = []
-    for s in srcs:
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(s):
         o = os.path.join(CSRC, os.path.basename(s).replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", s, "-o", o]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed on {s}")
-        if verbose:
-            sys.stderr.write(r.stderr)
-        objs.append(o)
+        r = subprocess.run([NVCC, *FLAGS, "-c", s, "-o", o], capture_output=True, text=True)
+        return s, o, r
+
+    objs = []
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        for s, o, r in ex.map(compile_one, srcs):
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed on {s}")
+            if verbose:
+                sys.stderr.write(r.stderr)
+            objs.append(o)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs,
            "-ldl", "-lcudart", "-Xlinker", "--no-undefined"]
     r = subprocess.run(cmd, capture_output=True, text=True)

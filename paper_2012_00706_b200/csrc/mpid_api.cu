@@ -132,7 +132,10 @@ size_t tpart_doubles(int64_t m_local, int64_t n, int64_t k) {
   for (int64_t k1 : {k, std::min<int64_t>(k, 128)})
     for (int64_t n1 : {k1, n, std::max<int64_t>(1, n - k1)})
       need = std::max<size_t>(need, (size_t)tsmm_splits(k1, n1, m_local) * k1 * n1);
-  return std::min<size_t>(need, (size_t)1024 * 128 * 128);
+  // cap the split-K room at 16M doubles, but never below one unsplit product (splits = 1
+  // writes k1 * n1 doubles; k x max(k, n) covers every product the coefficients use)
+  const size_t floor1 = (size_t)k * (size_t)std::max<int64_t>(k, n);
+  return std::max(std::min<size_t>(need, (size_t)1024 * 128 * 128), floor1);
 }
 int splits_for(int64_t k1, int64_t n1, int64_t m, size_t cap) {
   const int64_t s = tsmm_splits(k1, n1, m);
@@ -176,7 +179,7 @@ Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
   L.Ik = take((size_t)k * k * 8);
   L.Rinv = take((size_t)k * k * 8);
   L.py = take((size_t)m_local * 8);                                  // power iteration: y = E x
-  L.pvec = take((size_t)(4 * n + 2 * k + 256 + PW_NBLK * n) * 8);    // x, z, v, w, u, est, partials
+  L.pvec = take((size_t)(3 * n + 2 * k + 256 + PW_NBLK * (n + k)) * 8);  // x, z, v, w, u, est, partials (n + k cols)
   L.gpart = take(gram_part_doubles(mp / 8, (int)n, num_sms()) * 8);  // Gram pivoting: tile partials
   L.G = take((size_t)n * n * 8);                                      //   and G = A_L^T A_L
   L.Gc = take((size_t)n * n * 8);                                     //   Schur-complement working copy
@@ -192,6 +195,7 @@ struct mpid_ctx {
   int64_t m_global = 0, m_local = 0, row_offset = 0, n = 0, ld = 0, m_pad = 0;
   int32_t rank = 0, nranks = 1;
   void* comm = nullptr;
+  bool loop = false;              // comm is a LoopComm (id_loopback_create)
   cudaStream_t st = nullptr;      // current enqueue stream (user's, or cap during graph capture)
   cudaStream_t user_st = nullptr; // the caller's stream
   cudaStream_t cap = nullptr;     // internal non-blocking stream: graph capture and replay
@@ -269,8 +273,72 @@ static cudaError_t rec(mpid_ctx* h, cudaEvent_t e) {
                                              : cudaEventRecord(e, h->st);
 }
 
+// ----------------------------------------------------------------------------
+// Loopback "communicator": nranks handles on ONE device, each driven by its own host
+// thread (tests of the row-sharded path on one GPU; SURVEY §4 tests/dist (i)).  An
+// allreduce synchronises the caller's stream, copies its buffer to a host slot, waits
+// for all ranks (generation barrier), and the last arriver reduces the slots in rank
+// order 0..P-1 (SUM or MAX), so every rank receives the same bits.  Not capturable in
+// a CUDA graph: handles on a loopback group run the step loop eagerly.
+// ----------------------------------------------------------------------------
+#include <condition_variable>
+#include <set>
+struct LoopComm {
+  int nranks = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<std::vector<double>> slot;
+  std::vector<double> result;
+  int64_t calls = 0;                // completed collectives (diagnostics)
+};
+static std::mutex g_loop_mu;
+static std::set<void*> g_loops;
+static bool is_loop(void* c) {
+  std::lock_guard<std::mutex> lk(g_loop_mu);
+  return c && g_loops.count(c);
+}
+
+static id_status loop_allreduce(mpid_ctx* h, double* buf, size_t count, int op) {
+  LoopComm* L = (LoopComm*)h->comm;
+  std::vector<double> mine(count);
+  CK(cudaStreamSynchronize(h->st));
+  CK(cudaMemcpy(mine.data(), buf, count * sizeof(double), cudaMemcpyDeviceToHost));
+  std::vector<double> res;
+  {
+    std::unique_lock<std::mutex> lk(L->mu);
+    const uint64_t my_gen = L->gen;
+    L->slot[h->rank] = std::move(mine);
+    if (++L->arrived == L->nranks) {
+      L->result = L->slot[0];
+      for (int r = 1; r < L->nranks; ++r) {
+        if (L->slot[r].size() != count) {
+          L->result.assign(count, NAN);   // mismatched collective: every rank sees NaN
+          break;
+        }
+        for (size_t i = 0; i < count; ++i)
+          L->result[i] = op == NCCL_MAX ? std::max(L->result[i], L->slot[r][i]) : L->result[i] + L->slot[r][i];
+      }
+      L->arrived = 0;
+      L->calls++;
+      L->gen++;
+      L->cv.notify_all();
+    } else {
+      if (!L->cv.wait_for(lk, std::chrono::seconds(120), [&] { return L->gen != my_gen; }))
+        return fail(h, ID_ERR_NCCL, "loopback allreduce: rank %d timed out waiting for the others", h->rank);
+    }
+    res = L->result;
+  }
+  if (res.size() != count) return fail(h, ID_ERR_NCCL, "loopback allreduce: size mismatch");
+  CK(cudaMemcpy(buf, res.data(), count * sizeof(double), cudaMemcpyHostToDevice));
+  return ID_OK;
+}
+
 static id_status allreduce(mpid_ctx* h, double* buf, size_t count, int op) {
-  if (h->nranks <= 1) return ID_OK;
+  // a communicator given at nranks == 1 is still used (the NCCL-in-graph test)
+  if (h->nranks <= 1 && !h->comm) return ID_OK;
+  if (h->loop) return loop_allreduce(h, buf, count, op);
   NcclApi& api = nccl();
   if (!api.ok) return fail(h, ID_ERR_NCCL, "libnccl.so.2 not available");
   const nccl_result_t r = api.AllReduce(buf, buf, count, NCCL_FLOAT64, op, h->comm, h->st);
@@ -304,7 +372,9 @@ static id_status relayout(mpid_ctx* h, int sbytes) {
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
   h->graphs.clear();
   h->graph_launches.clear();
-  h->have_qr = h->have_coef = false;
+  // every buffer moves: results held in the old carve (QR, coefficients, Gram, sketch) are gone
+  h->have_qr = h->have_coef = h->have_gram = h->have_sketch = false;
+  h->perm_host.clear();
   h->sbytes = sbytes;
   const int64_t kmax = lo;
   h->k_cap = kmax;
@@ -397,6 +467,11 @@ id_status id_create(id_handle* hp, const double* A_D, int64_t m_global, int64_t 
   h->rank = rank;
   h->nranks = nranks;
   h->comm = nccl_comm;
+  h->loop = is_loop(nccl_comm);
+  if (h->loop && ((LoopComm*)nccl_comm)->nranks != nranks) {
+    delete h;
+    return ID_ERR_ARG;
+  }
   h->st = (cudaStream_t)stream;
   h->user_st = h->st;
   h->ws = (char*)workspace;
@@ -703,7 +778,7 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   int nb = opts && opts->nb > 0 ? opts->nb : (formation == 2 ? 16 : 4);
   if (nb > NB_MAX || (formation == 1 && nb > 16) || (fmt == ID_FP64 && nb > 8))
     return fail(h, ID_ERR_ARG, "nb=%d too large for formation %d / format %d", nb, formation, (int)fmt);
-  const bool use_graph = !(opts && opts->use_graph < 0);
+  const bool use_graph = !(opts && opts->use_graph < 0) && !h->loop;
   const bool profile = opts && opts->profile_pass;
   h->have_qr = h->have_coef = h->have_gram = h->have_sketch = false;
   if (profile && (int)h->pass_ev.size() < 2 * k_max) {
@@ -1080,6 +1155,35 @@ id_status id_get_stats(id_handle h, id_stats* out) {
   if (!h || !out) return ID_ERR_ARG;
   *out = h->stats;
   return ID_OK;
+}
+
+id_status id_loopback_create(void** comm, int32_t nranks) {
+  if (!comm || nranks < 1 || nranks > 1024) return ID_ERR_ARG;
+  LoopComm* L = new LoopComm();
+  L->nranks = nranks;
+  L->slot.resize(nranks);
+  {
+    std::lock_guard<std::mutex> lk(g_loop_mu);
+    g_loops.insert(L);
+  }
+  *comm = L;
+  return ID_OK;
+}
+
+int64_t id_loopback_calls(void* comm) {
+  if (!is_loop(comm)) return -1;
+  LoopComm* L = (LoopComm*)comm;
+  std::lock_guard<std::mutex> lk(L->mu);
+  return L->calls;
+}
+
+void id_loopback_destroy(void* comm) {
+  if (!is_loop(comm)) return;
+  {
+    std::lock_guard<std::mutex> lk(g_loop_mu);
+    g_loops.erase(comm);
+  }
+  delete (LoopComm*)comm;
 }
 
 int32_t id_nccl_unique_id_bytes(void) { return 128; }

@@ -33,7 +33,7 @@ COEF = {"R": ID_COEF_R, "r": ID_COEF_R, "lsq": ID_COEF_LSQ, "LSQ": ID_COEF_LSQ}
 EXPORTS = ["id_workspace_bytes", "id_create", "id_qrcp_lowprec", "id_coeffs_fp64", "id_error", "id_error_ex",
            "id_get_R", "id_get_R_fp64", "id_get_gram", "id_get_sketch", "id_get_perm", "id_get_AL", "id_round_only", "id_get_stats", "id_last_error", "id_destroy",
            "id_nccl_unique_id_bytes", "id_nccl_get_unique_id", "id_nccl_comm_init",
-           "id_nccl_comm_destroy", "id_version"]
+           "id_nccl_comm_destroy", "id_loopback_create", "id_loopback_calls", "id_loopback_destroy", "id_version"]
 
 
 class IDError(RuntimeError):
@@ -116,6 +116,12 @@ def lib():
     L.id_nccl_comm_init.argtypes = [C.POINTER(vp), vp, i32, i32]
     L.id_nccl_comm_destroy.restype = C.c_int
     L.id_nccl_comm_destroy.argtypes = [vp]
+    L.id_loopback_create.restype = C.c_int
+    L.id_loopback_create.argtypes = [C.POINTER(vp), i32]
+    L.id_loopback_calls.restype = i64
+    L.id_loopback_calls.argtypes = [vp]
+    L.id_loopback_destroy.restype = None
+    L.id_loopback_destroy.argtypes = [vp]
     L.id_version.restype = C.c_char_p
     L.id_version.argtypes = []
     _LIB = L
@@ -184,6 +190,22 @@ def id_nccl_comm_init(uid: bytes, nranks: int, rank: int) -> int:
 
 def id_nccl_comm_destroy(comm: int):
     lib().id_nccl_comm_destroy(C.c_void_p(comm))
+
+
+def id_loopback_create(nranks: int) -> int:
+    comm = C.c_void_p()
+    rc = lib().id_loopback_create(C.byref(comm), nranks)
+    if rc:
+        raise IDError(rc, "id_loopback_create failed")
+    return comm.value
+
+
+def id_loopback_calls(comm: int) -> int:
+    return int(lib().id_loopback_calls(C.c_void_p(comm)))
+
+
+def id_loopback_destroy(comm: int):
+    lib().id_loopback_destroy(C.c_void_p(comm))
 
 
 # ---------------------------------------------------------------------------

@@ -7,6 +7,12 @@ from oracle.qrcp import QRCPResult, certified_steps, make_AL, qrcp_householder
 
 _ORACLE = {}
 
+# tie certification constant (reading R10), calibrated by tools/calibrate_ctie.py
+# (the oracle against itself in two faithful orders over >= 20 seeds)
+import json as _json
+import os as _os
+C_TIE = _json.load(open(_os.path.join(_os.path.dirname(__file__), "golden", "ctie_calibration.json")))["c_tie"]
+
 
 def oracle_qrcp(key, A, fmt, scaling, k, nb, eps=0.0, formation="fma"):
     """Cached oracle QRCP of fl(s A).  A fixed-rank run's first k steps do not depend

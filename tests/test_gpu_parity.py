@@ -240,14 +240,15 @@ def test_ragged_and_edge_shapes(m, n, k):
 # tiles per CTA, i.e. the ring and the A_D buffer wrap across tiles).
 @pytest.mark.parametrize("m,n,k", [(130, 50, 1), (1024, 140, 3), (1023, 140, 3), (2000, 300, 8),
                                    (4098, 261, 13), (4097, 261, 13), (40000, 400, 100), (39999, 257, 64),
-                                   (6000, 200, 70), (8192, 300, 86), (12000, 260, 120)])
+                                   (6000, 200, 70), (8192, 300, 86), (12000, 260, 120),
+                                   (5000, 180, 52)])
 def test_error_kernel_shapes(m, n, k):
     rng = np.random.default_rng(m * 7 + n + k)
     A = np.asfortranarray(rng.standard_normal((m, n)) * np.exp(-np.arange(n) / 9.0)[None, :])
     out = run_gpu(A, "fp32", "none", k, nb=4)
     I = out["piv"]
     # the LSQ products (Q1^T Q1, Q1^T A_J): even m takes the mbarrier-pipelined TN GEMM
-    # (8-row M tiles when that pads less: k = 70 / 86 / 100 / 120), odd m the register-staged one
+    # (8-row M tiles when that pads less: k = 52 / 70 / 86 / 100 / 120 -> MR = 7 / 9 / 11 / 13 / 15), odd m the register-staged one
     P_ref = coeffs_lsq(A, I)
     assert np.linalg.norm(out["P"] - P_ref) <= 1e-10 * np.linalg.norm(P_ref)
     e = id_error(A, I, out["P"])

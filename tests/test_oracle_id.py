@@ -132,3 +132,34 @@ def test_low_skeleton_and_spectral_error_pins():
     assert abs(r2 - e2 / sigma[0]) <= 1e-12 * r2
     ef, _ = id_error_skeleton(A, A[:, I], P)
     assert abs(ef - id_error(A, I, P)[0]) <= 1e-12 * ef and e2 <= ef * (1 + 1e-12)
+
+
+def test_post_bound_reduces_to_the_exact_error_and_holds():
+    """B_post (reading R13) pins: (i) with u_L = u_acc = 0 it is rho_k / s, the QR's
+    residual mass, which in exact arithmetic IS the LSQ-ID error ||(I - Q Q^T) A||_F —
+    checked on fp64 QRCPs (no storage rounding, s = 1) to 1e-9; (ii) it is monotone in
+    u_L; (iii) it holds (err <= B_post) and is not vacuous (B_post < ||A||_F / 4) on
+    fp16 / fp32 runs of C1 (3 seeds), a C2 slice and a planted input."""
+    from oracle.rounding import SINGLE as S32
+    for seed in range(3):
+        A = gen_config("C1", seed)
+        r = qrcp_householder(A, 32, "fp64")
+        e = id_error(A, r.I, coeffs_lsq(A, r.I))[0]
+        B0 = post_bound(r.resid[32], 1.0, 5.0, np.linalg.norm(A), 0.0, 32, 32, 256, 0.0)
+        assert abs(B0 - e) <= 1e-9 * e
+    cases = [(gen_config("C1", s), "fp16", "pow2", 32, 32) for s in range(3)]
+    cases += [(gen_config("C1", 0), "fp32", "none", 32, 4)]
+    cases += [(np.asfortranarray(gen_config("C2", 0)[:, :256]), "fp16", "maxabs", 64, 4)]
+    A, _, _ = gen_planted(512, 128, 32, rho=1.1, eta=1e-9, seed=5)
+    cases += [(A, "fp16", "pow2", 32, 8)]
+    for A, fmt, sc, k, nb in cases:
+        AL, s = make_AL(A, fmt, sc)
+        r = qrcp_householder(AL, k, fmt, nb=nb)
+        P = coeffs_lsq(A, r.I)
+        ab, _ = id_error(A, r.I, P)
+        T2 = np.linalg.norm(coeffs_from_R(r.R, r.perm, k), 2)
+        uL = HALF.u if fmt == "fp16" else S32.u
+        B = post_bound(r.resid[k], s, T2, np.linalg.norm(A), uL, k, nb, A.shape[0], S32.u)
+        B2 = post_bound(r.resid[k], s, T2, np.linalg.norm(A), 2 * uL, k, nb, A.shape[0], S32.u)
+        assert ab <= B < B2
+        assert B < 0.25 * np.linalg.norm(A)

@@ -180,3 +180,66 @@ def test_chain8_is_an_accurate_sum():
     got = chain8(X, X, np.float32)
     ref = np.array([math.fsum(float(v) ** 2 for v in X[:, c]) for c in range(5)])
     assert np.all(np.abs(got - ref) <= 8 * SINGLE.u * ref)
+
+
+# ---- formation "tc" (the D-OTF form the tensor-core pass follows) and model "paper" ----
+# Pins: LAPACK dgeqp3 / the fp64 Householder QR of the same A_L (an exact-arithmetic
+# identity: every formation computes the same R), the right-looking formation (a
+# different order of the same operations), planted skeletons, and the QR invariants
+# A35 (factorisation residual) / A36 (|diag R| non-increasing).
+
+@pytest.mark.parametrize("nb", [8, 32])
+def test_tc_formation_R_matches_fp64_householder(nb):
+    """fp32 storage, no store inside the run (nb >= k) or every 8 steps: the D-OTF
+    formation's R equals the fp64 QR of the same A_L to a few fp32 units."""
+    A = gen_config("C1", 1)
+    AL, _ = make_AL(A, "fp32", "none")
+    k = 32
+    r = qrcp_householder(AL, k, "fp32", nb=nb, formation="tc")
+    r64 = qrcp_householder(AL, k, "fp64")
+    Q, R, P = sla.qr(AL, pivoting=True, mode="economic")
+    cert = certified_steps(r)
+    fu = int(np.argmin(cert)) if not cert.all() else k
+    assert fu >= 24
+    assert np.array_equal(r.perm[:fu], P[:fu]) and np.array_equal(r.perm[:fu], r64.perm[:fu])
+    mx = r.maxnorm0
+    assert np.max(np.abs(r.R[:fu, :] - r64.R[:fu, :])) <= 64 * k * SINGLE.u * mx
+
+
+@pytest.mark.parametrize("fmt,nb", [("fp16", 32), ("fp16", 8), ("fp32", 32)])
+def test_tc_formation_planted_and_invariants(fmt, nb):
+    A, skel, C = gen_planted(512, 128, 32, rho=1.1, eta=1e-9, seed=2)
+    AL, _ = make_AL(A, fmt, "pow2" if fmt == "fp16" else "none")
+    r = qrcp_householder(AL, 32, fmt, nb=nb, formation="tc")
+    assert np.array_equal(r.perm[:32], skel)
+    k = 32
+    u_L = HALF.u if fmt == "fp16" else SINGLE.u
+    u_acc = SINGLE.u
+    Q = form_Q(r.V, r.tau)
+    D = np.diag(np.sign(np.diag(Q.T @ AL[:, r.perm[:k]])))
+    res = np.linalg.norm(AL[:, r.perm[:k]] - (Q @ D) @ np.triu(r.R[:, :k]))
+    eta = (math.ceil(k / nb) + 2 * math.sqrt(k)) * u_L + 4 * k * 300 * u_acc
+    assert res <= (eta + u_acc) * np.linalg.norm(AL)                     # A35
+    d = np.diag(r.R)
+    assert np.all(d >= 0) and np.all(d[1:] <= d[:-1] * (1 + 4 * u_L) + 64 * u_acc * r.maxnorm0)   # A36
+
+
+@pytest.mark.parametrize("fmt,nb", [("fp16", 32), ("fp16", 4), ("fp32", 16)])
+def test_tc_and_paper_models_agree_with_kernel_model_on_certified_steps(fmt, nb):
+    """Three faithful orders of the same precision model — D-OTF formation with fp64
+    sums, right-looking with per-op rounding + fp64 sums ("paper"), right-looking with
+    one-rounding updates + 8-row fp32 chains ("kernel") — pick the same pivots on every
+    certified step and reach the same residual mass to a few storage units."""
+    A = gen_config("C1", 3)
+    AL, _ = make_AL(A, fmt, "pow2" if fmt == "fp16" else "none")
+    runs = [qrcp_householder(AL, 32, fmt, nb=nb, formation="tc"),
+            qrcp_householder(AL, 32, fmt, nb=nb, model="paper"),
+            qrcp_householder(AL, 32, fmt, nb=nb, model="kernel")]
+    cert = certified_steps(runs[1], c_tie=64)
+    fu = int(np.argmin(cert)) if not cert.all() else 32
+    assert fu >= 20
+    for r in runs[1:]:
+        assert np.array_equal(r.perm[:fu], runs[0].perm[:fu])
+    u_L = HALF.u if fmt == "fp16" else SINGLE.u
+    for r in runs[1:]:
+        assert abs(r.resid[fu] - runs[0].resid[fu]) <= 64 * u_L * runs[0].resid[0]
