@@ -1,31 +1,41 @@
-// k_pass_tc — the per-step panel pass with the pending trailing update formed on
-// the 5th-generation tensor cores (tcgen05 + TMEM), the "D-OTF" design of
-// Ã = S − V Fᵀ is formed tile by tile as a rank-npend GEMM
-// (npend ≤ nb ≤ 32 pending reflectors of the current panel) whose fp32
-// accumulator lives in TMEM and is never written to HBM; the epilogue computes the
-// u-weighted and squared column sums from it, and at the panel end (store steps)
-// writes fl_L(Ã) back — the blocked trailing-matrix update of Algorithm 2 line 4
-// as a tensor-core GEMM with K = nb.
+// k_pass_tc — the per-step panel pass of the low-precision pivoted Householder QR with the
+// trailing block formed on the 5th-generation tensor cores (tcgen05 + TMEM): SURVEY §8(a)
+// "D-OTF", the default for fp16 storage (Algorithm 2 line 4; Eq. (6)-(7),
+// P:115-128; the blocked trailing-matrix update of north_star / P:402 as a rank-nb
+// tensor-core GEMM with K = the pending reflectors of the panel).
 //
-// Operands (kind::tf32, fp32-accurate "3xTF32": V = Vh + Vl, F = Fh + Fl,
-// D = Fh·Vhᵀ + Fh·Vlᵀ + Fl·Vhᵀ, within ~2^-21 of the exact product — DESIGN.md R14):
-//   A = F tile  (M = 128 lanes: 124 matrix columns of this CTA + the pivot column j
-//               in lanes 0, 32, 64, 96, × K), built once per launch in shared memory;
-//   B = V block (N = 128 matrix rows × K), the panel's v vectors, kept in global
-//               memory by k_vop in exactly the smem operand layout, so one bulk copy
-//               per stage brings the tile in.
-// Both K-major, no-swizzle core-matrix layout (8 rows × 16 B per core matrix;
-// LBO = K-direction core stride = 128 B, SBO = 8-row stride).  D[col][row] sits in
-// TMEM with lane = matrix column and TMEM column = matrix row: the epilogue thread
-// of a column reads 8 consecutive rows with one tcgen05.ld.32x32b.x8 and the
-// matching 16-byte chunk of the interleaved S layout with one LDS.128.  Every
-// warp holds the pivot column's D values in its lane 0 and forms u = Ã(:, j) for
-// its own rows through a per-warp shared scratch — no cross-warp barrier per stage.
+// What one launch computes for step j (readings R4, R6, R14):
+//   X = S - V F^T, the current trailing block, formed ENTIRELY in the tensor core's fp32
+//   accumulator (TMEM), never written to HBM:
+//     D  = S^T I                       8 MMAs (N = 16 rows, K = 16 rows) per 128 x 128 unit:
+//                                      the stored fp16 tile itself is the A operand (the
+//                                      8-row interleaved layout IS the K-major core-matrix
+//                                      layout), B = a 16 x 16 identity -> D(c, r) = S(r, c)
+//     D += (-F_hi) V_hi^T + (-F_hi) V_lo^T + (-F_lo) V_hi^T      (kind::f16, K = 16 per MMA)
+//   with V, F the pending fp32 vectors split into fp16 hi / lo pairs (|rel. error| of the
+//   product <= ~2^-21, R14), so the epilogue reads X directly (no conversion, no
+//   subtraction on the CUDA cores);
+//   u = X(:, j) (the pivot column), w = X^T u and s_i = ||X(j:m, i)||^2 (16-row fp32 FFMA2
+//   chains added into fp64), the row x = X(j, :); on store steps (panel end, every nb
+//   steps) fl16(X) is written back to S (the storage rounding point).
 //
-// One CTA per SM, 18 warps: w0 TMA producer, w1 MMA issuer (+ TMEM allocator),
-// w2-17 epilogue (warp w reads TMEM lanes 32·(w%4).., rows 32·((w-2)/4).. of a stage).
-// Pipelines: smem ring full → (MMA → tmem_full) → epilogue → empty, and a
-// double-buffered TMEM accumulator (tmem_full / tmem_empty).
+// B200 structure: one persistent CTA per SM, 18 warps, warp-specialised.  A CTA owns a
+// contiguous range of 128-row blocks and walks, per row block, all column tiles of 128
+// (tile 0 starts at column j, so its TMEM lane 0 is the pivot column): unit = (row block,
+// tile).
+//   warp 0      TMA producer: per unit one 2-D tensor-map box of S (128 columns x 16 row
+//               groups = 32 KB) + the tile's F operand (bulk copy, L2-resident); per row
+//               block the V operand (bulk copy).  NST-deep ring; on store steps the
+//               rounded tile is written back by a tensor-map store before the slot is reused.
+//   warp 1      MMA issuer (one thread): 8 identity MMAs + 3 x ceil(npend / 16) formation
+//               MMAs per unit into one of 4 TMEM accumulators (128 columns each).
+//   warps 2-17  epilogue, 4 groups of 4 warps (one per TMEM lane quarter); group g takes the
+//               tiles t = g mod 4, so each thread owns one column per tile and keeps its
+//               column sums in registers for the whole launch.  Warp 4 (group 0, lane
+//               quarter 0) publishes u of each row block (TMEM lane 0 of tile 0) to shared
+//               memory and to U (global, for the next steps' V operand).
+// Bound: HBM — (m - j)(n - j) 2 bytes read per step (+ the same written on store steps);
+// tensor work per element: 32 flops (identity) + 6 * 16 * ceil(npend / 16) (formation).
 #include "mpid_internal.cuh"
 
 #include <cuda.h>
@@ -34,40 +44,48 @@
 namespace mpid {
 
 namespace {
-constexpr int TC_LANES = 128;    // MMA M = TMEM lanes
-constexpr int TC_CN = 124;       // matrix columns per CTA (lanes 0, 32, 64, 96 = the pivot column)
-constexpr int TC_R = 128;        // matrix rows per stage = MMA N
-constexpr int TC_RG = TC_R / 8;  // row groups per stage
-constexpr int TC_EPI_WARPS = 16;
-constexpr int TC_BLOCK = 32 * (2 + TC_EPI_WARPS);
-constexpr int TC_NACC = 2;         // TMEM accumulator ring depth
-constexpr int TC_TMEM_COLS = 128 * TC_NACC;  // accumulators of 128 fp32 columns
+constexpr int C_T = 128;            // columns per tile = MMA M = TMEM lanes
+constexpr int R_B = 128;            // rows per row block = formation MMA N = TMEM columns per accumulator
+constexpr int RG_B = R_B / 8;       // row groups per row block
+constexpr int EPI_WARPS = 16;
+constexpr int NGRP = 2;             // epilogue groups: group g takes the tiles t = g mod 2
+constexpr int EPI_GW = EPI_WARPS / NGRP;   // warps per group: 4 lane quarters x 2 row halves
+constexpr int TPG_MAX = 8;          // tiles per group (n - j <= 2048)
+constexpr int BLOCK = 32 * (2 + EPI_WARPS + 1);   // + producer, MMA issuer, u warp
+constexpr int NACC = 4;             // TMEM accumulators
+constexpr int TMEM_COLS = R_B * NACC;
+constexpr int S_BYTES = C_T * R_B * 2;   // one fp16 unit tile (32 KB)
+constexpr int CH_BYTES = 4096;      // one K chunk (16) of a 128-row / 128-column operand, fp16
+constexpr int UWARP = 2 + EPI_WARPS;  // the pivot-column (u) warp
+constexpr int TC_SMEM_MAX = 227 * 1024;   // the sm_100 opt-in maximum of dynamic shared memory per block
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // K-major, no swizzle; LBO = byte stride between core matrices adjacent along K, SBO =
+  // along M / N; bit 46 = the sm_100 descriptor version
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;  // sm_100 descriptor version; base offset 0, SWIZZLE_NONE
+  d |= (uint64_t)1 << 46;
   return d;
 }
-// kind::tf32, fp32 accumulate, K-major A and B, N = 128, M = 128
-__device__ __forceinline__ uint32_t idesc_tf32() {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_R >> 3) << 17) | ((uint32_t)(TC_LANES >> 4) << 24);
+// kind::f16: fp16 A and B, fp32 accumulator, both K-major, M = 128, N given
+__device__ __forceinline__ uint32_t idesc_f16(int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(C_T >> 4) << 24);
 }
-__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
+__device__ __forceinline__ void mma_f16(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
-      "l"(da), "l"(db), "r"(idesc_tf32()), "r"(acc)
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
                : "memory");
 }
-// 32 consecutive TMEM columns (= matrix rows) of this warp's 32 lanes -> v[0..31]; no wait
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
       "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -76,11 +94,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
         "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-// 2-D tensor-map TMA of S viewed as [ngroups][n * esz] 8-byte elements: one box row is a
-// whole row group of TC_CN columns (contiguous 16 B chunks), so the copy engine moves
-// ~2 KB runs; box {TC_CN * esz / 8 * 8 ... } -- see encode_tmap_S
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -93,151 +117,136 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, int c0, int 
                "r"(c0), "r"(c1), "r"(su32(src))
                : "memory");
 }
-// tf32 split: hi = RN to 10 mantissa bits, lo = x - hi (exact in fp32)
-__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  uint32_t h;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  hi = __uint_as_float(h);
-  lo = x - hi;
+// byte offset of (row-or-column i, pending l) inside one K-chunk operand block: [i / 8][l / 8 % 2][i % 8][l % 8]
+__host__ __device__ __forceinline__ int op_off(int i, int l) {
+  return (i >> 3) * 256 + ((l >> 3) & 1) * 128 + (i & 7) * 16 + (l & 7) * 2;
 }
-// byte offset of element (row r, k) in a K-major fp32 core-matrix tile (sbo = bytes per 8 rows)
-__host__ __device__ __forceinline__ int64_t cm_off(int64_t r, int k, int sbo) {
-  return (r >> 3) * sbo + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4;
+// one lane of a converged warp (the lowest) -> true
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.b32 %0, 1, 0, P;\n}" : "=r"(pred));
+  return pred != 0;
+}
+__device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
+  hi = __float2half_rn(x);
+  lo = __float2half_rn(x - __half2float(hi));   // x - hi is exact in fp32
 }
 
-template <typename T> struct Ch;
-template <> struct Ch<__half> {
-  __device__ static __forceinline__ void load(const __half* p, float* x) {
-    const uint4 v = *reinterpret_cast<const uint4*>(p);
-    const __half2* h = reinterpret_cast<const __half2*>(&v);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float2 f = __half22float2(h[i]);
-      x[2 * i] = f.x;
-      x[2 * i + 1] = f.y;
-    }
-  }
-  __device__ static __forceinline__ void round_store(__half* p, float* x) {
-    uint4 v;
-    __half2* h = reinterpret_cast<__half2*>(&v);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      h[i] = __floats2half2_rn(x[2 * i], x[2 * i + 1]);
-      const float2 f = __half22float2(h[i]);
-      x[2 * i] = f.x;
-      x[2 * i + 1] = f.y;
-    }
-    *reinterpret_cast<uint4*>(p) = v;
-  }
-  __device__ static __forceinline__ float rnd(float a) { return __half2float(__float2half_rn(a)); }
-  __device__ static __forceinline__ float get(const __half* p, int i) { return __half2float(p[i]); }
-};
-template <> struct Ch<float> {
-  __device__ static __forceinline__ void load(const float* p, float* x) {
-    const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
-    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-  }
-  __device__ static __forceinline__ void round_store(float* p, float* x) {
-    reinterpret_cast<float4*>(p)[0] = make_float4(x[0], x[1], x[2], x[3]);
-    reinterpret_cast<float4*>(p)[1] = make_float4(x[4], x[5], x[6], x[7]);
-  }
-  __device__ static __forceinline__ float rnd(float a) { return a; }
-  __device__ static __forceinline__ float get(const float* p, int i) { return p[i]; }
-};
-
-struct TcGeom {
-  int a_hi, a_lo;                 // F tile (hi, lo): 128 lanes x nbw fp32 each
-  int slot0, slot;                // first slot, slot stride
-  int data, ucol, vh, vl, us;     // offsets inside a slot
-  int red;                        // 2 x 128 x 2 doubles
-  int bars;                       // mbarriers
+struct Geo {
+  int slot;        // bytes per ring slot: the S unit tile (32 KB), then the tile's F operand (hi, lo)
+  int f_off;
+  int v0;          // per-row-block buffers (2): V operand (hi, lo) x kchw chunks, then the pivot column
+  int vsz;         // bytes of one row-block buffer
+  int pcol;        // pivot column offset inside a row-block buffer (16 row groups x 16 B)
+  int ident;       // 16 x 16 identity operand (512 B)
+  int ubuf;        // 2 x 128 floats: u of a row block
+  int fj;          // 2 x 32 floats: -F(j, l) hi / lo (the pivot column's F row)
+  int bars;
   int total;
 };
-__host__ __device__ inline int a128(int x) { return (x + 127) & ~127; }
-__host__ __device__ inline TcGeom tc_geom(int esz, int nbw, int nst) {
-  TcGeom g;
-  g.a_hi = 0;
-  g.a_lo = a128(TC_LANES * nbw * 4);
-  g.slot0 = g.a_lo + a128(TC_LANES * nbw * 4);
-  g.data = 0;
-  g.ucol = a128(TC_RG * TC_CN * 8 * esz);
-  g.vh = g.ucol + a128(TC_RG * 8 * esz);
-  g.vl = g.vh + TC_R * nbw * 4;
-  g.us = g.vl + TC_R * nbw * 4;
-  g.slot = a128(g.us + TC_R * 4);
-  g.red = g.slot0 + nst * g.slot;
-  g.bars = g.red + 4 * TC_LANES * 2 * 8 + TC_EPI_WARPS * 32 * 4;   // + per-warp u scratch
-  g.total = g.bars + (2 * nst + 2 * TC_NACC) * 8 + 16;
+__host__ __device__ inline Geo geo_of(int kchw, int nst) {
+  Geo g;
+  g.f_off = S_BYTES;
+  g.slot = S_BYTES + 2 * kchw * CH_BYTES;
+  g.v0 = nst * g.slot;
+  g.pcol = 2 * kchw * CH_BYTES;
+  g.vsz = g.pcol + RG_B * 16;
+  g.ident = g.v0 + 2 * g.vsz;
+  g.ubuf = g.ident + 512;
+  g.fj = g.ubuf + 2 * R_B * 4;
+  g.bars = g.fj + 2 * 32 * 4;
+  g.total = g.bars + (2 * nst + 2 * NACC + 8) * 8 + 16;
   return g;
 }
 }  // namespace
 
-template <typename T>
-__global__ void __launch_bounds__(TC_BLOCK, 1) k_pass_tc(PassParams p, const __grid_constant__ CUtensorMap tmS) {
+struct TcParams {
+  int64_t m_pad;       // rows of the shard, padded (multiple of 256)
+  int64_t m_local;
+  int64_t row_offset;
+  int64_t rb_first;    // first 128-row block holding rows >= j (local)
+  int64_t nrb;         // row blocks from rb_first to the end
+  int n, j, j0, npend, store, kchw, nst, ntiles;
+  const unsigned char* Vop;   // [m_pad / 128][kchw][hi 4 KB | lo 4 KB]
+  const unsigned char* Fop;   // [ntiles][kchw][hi 4 KB | lo 4 KB]
+  float* U;                   // [NSLOT][m_pad] u vectors (fp32)
+  double* part;               // [gridDim.x][2][n]
+  double* xr;                 // [n] row j of X (owner)
+  const DevScalars* sc;
+};
+
+// TPG: column tiles per epilogue group (4: n - j <= 1024, 8: <= 2048)
+template <int TPG>
+__global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_constant__ CUtensorMap tmS,
+                                                     const __grid_constant__ CUtensorMap tmC) {
   if (p.sc->done) return;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  const int n = p.n, j = p.j, npend = p.npend;
-  const int nbw = p.nbw;                      // K width of the operand layouts (multiple of 8)
-  const int kchunks = (npend + 7) / 8;
-  const int NST = p.nst;
-  const int esz = (int)sizeof(T);
-  const int sbo = nbw * 32;                   // bytes per 8 rows of a K-major tile: (nbw / 4) * 128
-  T* __restrict__ S = reinterpret_cast<T*>(p.S);
-  const int c_lo = j + TC_CN * blockIdx.y;
-  const int ncols = min(TC_CN, n - c_lo);
-  const TcGeom geo = tc_geom(esz, nbw, NST);
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int n = p.n, j = p.j, NST = p.nst, kchw = p.kchw, ntiles = p.ntiles, npend = p.npend;
+  const int kch = (npend + 15) >> 4;             // K chunks holding pending reflectors
+  const Geo geo = geo_of(kchw, NST);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + geo.bars);
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
-  uint64_t* tempty = tfull + TC_NACC;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + TC_NACC);
-  // row groups of this CTA
-  const int64_t g_lo = p.g_lo;
-  const int64_t nact = p.ngroups - g_lo;
-  // whole stages per CTA (the tensor-map stores write full boxes: a box must never
-  // reach into the next CTA's rows); only the last CTA ends inside a stage
-  const int64_t per = ((nact + gridDim.x - 1) / gridDim.x + TC_RG - 1) / TC_RG * TC_RG;
-  const int64_t gb = g_lo + (int64_t)blockIdx.x * per;
-  const int64_t ge = (gb + per < p.ngroups) ? gb + per : p.ngroups;
-  const int nst = gb < ge ? (int)((ge - gb + TC_RG - 1) / TC_RG) : 0;
+  uint64_t* tempty = tfull + NACC;
+  uint64_t* vfull = tempty + NACC;
+  uint64_t* vempty = vfull + 2;
+  uint64_t* ufull = vempty + 2;
+  uint64_t* ufree = ufull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ufree + 2);
+  float* ubuf = reinterpret_cast<float*>(smem + geo.ubuf);
+  float* fj = reinterpret_cast<float*>(smem + geo.fj);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // row blocks of this CTA
+  const int64_t per = (p.nrb + gridDim.x - 1) / gridDim.x;
+  const int64_t rb0 = (int64_t)blockIdx.x * per;
+  const int64_t rb1 = rb0 + per < p.nrb ? rb0 + per : p.nrb;
+  const int nrbc = rb0 < rb1 ? (int)(rb1 - rb0) : 0;
+  const int64_t units = (int64_t)nrbc * ntiles;
+  const int64_t jl = (int64_t)j - p.row_offset;   // local row of the pivot row (may be outside)
 
-  // ---------------- setup: barriers, TMEM, the F (A operand) tile ----------------
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], TC_EPI_WARPS);
+      mbar_init(&empty[s], p.store ? EPI_GW : 1);
     }
-    for (int a = 0; a < TC_NACC; ++a) {
+    for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], TC_EPI_WARPS);
+      mbar_init(&tempty[a], EPI_GW);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&vfull[b], 1);
+      mbar_init(&vempty[b], 1);          // the MMA issuer's commit after the row block's last unit
+      mbar_init(&ufull[b], 1);
+      mbar_init(&ufree[b], EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
-                 "r"(TC_TMEM_COLS));
+                 "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (warp >= 2 && kchunks > 0) {
-    // A operand: lane i = the pivot column j when i % 32 == 0, else CTA column
-    // (i / 32) * 31 + i % 32 - 1; k = pending step l; hi/lo tf32 split of f_l(column)
-    const int t = threadIdx.x - 64;
-    const int kw = kchunks * 8;
-    for (int e = t; e < TC_LANES * kw; e += 32 * TC_EPI_WARPS) {
-      const int i = e / kw, l = e - i * kw;
-      const int ci = (i >> 5) * 31 + (i & 31) - 1;
-      float f = 0.f;
-      if (l < npend) {
-        if ((i & 31) == 0) f = reinterpret_cast<const float*>(p.F)[(int64_t)((p.j0 + l) % NSLOT) * n + j];
-        else if (ci < ncols) f = reinterpret_cast<const float*>(p.F)[(int64_t)((p.j0 + l) % NSLOT) * n + c_lo + ci];
-      }
-      float hi, lo;
-      split_tf32(f, hi, lo);
-      *reinterpret_cast<float*>(smem + geo.a_hi + cm_off(i, l, sbo)) = hi;
-      *reinterpret_cast<float*>(smem + geo.a_lo + cm_off(i, l, sbo)) = lo;
+  if (warp == 2) {
+    // 16 x 16 identity as the B operand of the S^T I MMAs: [n / 8][k / 8][n % 8][k % 8]
+    __half* I = reinterpret_cast<__half*>(smem + geo.ident);
+    for (int e = lane; e < 256; e += 32) {
+      const int r = e >> 4, k = e & 15;
+      I[op_off(r, k) / 2] = __float2half(r == k ? 1.f : 0.f);
     }
     fence_async_smem();
+  }
+  if (warp == UWARP) {
+    // -F(j, l) (hi, lo) of the pivot column: row 0 of tile 0 of the F operand
+    const int l = lane;
+    float h = 0.f, lo = 0.f;
+    if (l < npend) {
+      const unsigned char* b = p.Fop + (size_t)(l >> 4) * 2 * CH_BYTES;
+      const int o = op_off(0, l & 15);
+      h = __half2float(*reinterpret_cast<const __half*>(b + o));
+      lo = __half2float(*reinterpret_cast<const __half*>(b + CH_BYTES + o));
+    }
+    fj[l] = h;
+    fj[32 + l] = lo;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -245,288 +254,409 @@ __global__ void __launch_bounds__(TC_BLOCK, 1) k_pass_tc(PassParams p, const __g
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ======================= TMA producer =======================
-    if (lane == 0) {
-      const int64_t ngroups = p.ngroups;
-      // the box is {TC_CN * u8 8-byte units, TC_RG row groups} for fp16 (u8 = 2); fp32 chunks are
-      // 32 B (u8 = 4), so its stage is two boxes of TC_CN / 2 columns.  The smem tile is then
-      // [box][row group][columns][8 rows]; the epilogue addresses it accordingly.
-      const int u8 = esz;                                 // 8-byte units per 8-row chunk
-      const int nbox = esz == 2 ? 1 : 2;
-      const int bcols = TC_CN / (esz == 2 ? 1 : 2);
-      auto issue_store = [&](int i, int slot) {   // whole boxes; out-of-range rows/columns are not written
-        const int64_t g0 = gb + (int64_t)i * TC_RG;
-        unsigned char* d = smem + geo.slot0 + (size_t)slot * geo.slot + geo.data;
-        for (int b = 0; b < (esz == 2 ? 1 : 2); ++b)
-          tma_store_2d(&tmS, (c_lo + b * bcols) * u8, (int)g0, d + (size_t)b * TC_RG * bcols * 8 * esz);
+    // ============================ TMA producer ============================
+    // the whole warp walks the loop (warp-uniform values stay in uniform registers); one
+    // elected lane (the lowest, always lane 0 here) issues the copies, commits and waits
+    if (units > 0) {
+      const uint32_t fbytes = (uint32_t)(kch * 2 * CH_BYTES);
+      auto unit_coords = [&](int64_t u, int& c0, int& g0) {
+        const int64_t rbi = u / ntiles;
+        const int t = (int)(u - rbi * ntiles);
+        c0 = (j + t * C_T) * 2;                                 // 8-byte units (fp16: 2 per chunk)
+        g0 = (int)((p.rb_first + rb0 + rbi) * RG_B);
       };
-      (void)nbox;
-      const uint32_t vbytes = (uint32_t)(TC_RG * sbo);    // one stage of the V operand (hi or lo)
-      const uint32_t dbytes = (uint32_t)(TC_RG * TC_CN * 8 * esz);   // one stage of S (full box)
-      const T* Sj = reinterpret_cast<const T*>(p.Sj);
       int slot = 0;
       uint32_t phase = 0;
-      for (int i = 0; i < nst; ++i) {
-        if (i >= NST) {
+      for (int64_t u = 0; u < units; ++u) {
+        const int64_t rbi = u / ntiles;
+        const int t = (int)(u - rbi * ntiles);
+        if (u >= NST) {
           mbar_wait(&empty[slot], phase ^ 1);
           if (p.store) {
-            issue_store(i - NST, slot);
-            bulk_commit();
-            bulk_wait_read0();
+            int c0, g0;
+            unit_coords(u - NST, c0, g0);
+            if (elect_one()) {
+              tma_store_2d(&tmS, c0, g0, smem + (size_t)slot * geo.slot);
+              bulk_commit();
+              bulk_wait_read0();
+            }
+            __syncwarp();
           }
         }
-        const int64_t g0 = gb + (int64_t)i * TC_RG;
-        const int gsz = (int)((ge - g0) < TC_RG ? (ge - g0) : TC_RG);
-        unsigned char* base = smem + geo.slot0 + (size_t)slot * geo.slot;
-        mbar_expect_tx(&full[slot], dbytes + (uint32_t)(gsz * 8 * esz) + (kchunks > 0 ? 2 * vbytes : 0));
-        for (int b = 0; b < (esz == 2 ? 1 : 2); ++b)
-          tma_load_2d(base + geo.data + (size_t)b * TC_RG * bcols * 8 * esz, &tmS, (c_lo + b * bcols) * u8, (int)g0,
-                      &full[slot]);
-        tma_load(base + geo.ucol, Sj + g0 * 8, (uint32_t)(gsz * 8 * esz), &full[slot]);
-        if (kchunks > 0) {   // V operand rows g0*8 .. g0*8+127 (the buffer is padded to whole stages)
-          tma_load(base + geo.vh, reinterpret_cast<const unsigned char*>(p.Vh) + g0 * sbo, vbytes, &full[slot]);
-          tma_load(base + geo.vl, reinterpret_cast<const unsigned char*>(p.Vl) + g0 * sbo, vbytes, &full[slot]);
+        int c0, g0;
+        unit_coords(u, c0, g0);
+        unsigned char* base = smem + (size_t)slot * geo.slot;
+        if (elect_one()) {
+          mbar_expect_tx(&full[slot], (uint32_t)S_BYTES + fbytes);
+          tma_load_2d(base, &tmS, c0, g0, &full[slot]);
+          // the tile's F operand (L2-resident)
+          if (kch > 0) tma_load(base + geo.f_off, p.Fop + (size_t)t * kchw * 2 * CH_BYTES, fbytes, &full[slot]);
         }
+        __syncwarp();
         if (++slot == NST) { slot = 0; phase ^= 1; }
       }
-      (void)ngroups;
       if (p.store) {
-        for (int i = max(0, nst - NST); i < nst; ++i) {
-          const int s2 = i % NST;
-          mbar_wait(&empty[s2], (uint32_t)((i / NST) & 1));
-          issue_store(i, s2);
+        for (int64_t u = units > NST ? units - NST : 0; u < units; ++u) {
+          const int s2 = (int)(u % NST);
+          mbar_wait(&empty[s2], (uint32_t)((u / NST) & 1));
+          int c0, g0;
+          unit_coords(u, c0, g0);
+          if (elect_one()) tma_store_2d(&tmS, c0, g0, smem + (size_t)s2 * geo.slot);
+          __syncwarp();
         }
-        bulk_commit();
+        if (elect_one()) bulk_commit();
+        __syncwarp();
       }
-      bulk_wait0();
+      if (elect_one()) bulk_wait0();
+      __syncwarp();
     }
   } else if (warp == 1) {
-    // ======================= MMA issuer (one thread) =======================
-    if (lane == 0) {
-      int slot = 0, acc = 0;
-      uint32_t phase = 0, aphase = 0;
-      const uint32_t ahi = su32(smem + geo.a_hi), alo = su32(smem + geo.a_lo);
-      for (int i = 0; i < nst; ++i) {
+    // ============================ MMA issuer ============================
+    // converged warp, one elected lane issues (descriptors in uniform registers)
+    if (units > 0) {
+      const uint32_t id16 = idesc_f16(16), id128 = idesc_f16(R_B);
+      const uint64_t dI = sdesc(su32(smem + geo.ident), 128, 256);
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int64_t u = 0; u < units; ++u) {
+        const int64_t rbi = u / ntiles;
+        const int t = (int)(u - rbi * ntiles);
+        const int acc = (int)(u % NACC);
+        const int vb = (int)(rbi & 1);
+        if (t == 0) mbar_wait(&vfull[vb], (uint32_t)((rbi >> 1) & 1));
         mbar_wait(&full[slot], phase);
-        mbar_wait(&tempty[acc], aphase ^ 1);
+        mbar_wait(&tempty[acc], (uint32_t)(((u / NACC) & 1) ^ 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (kchunks > 0) {
-          const uint32_t sbase = su32(smem + geo.slot0 + (size_t)slot * geo.slot);
-          const uint32_t d = tmem + (uint32_t)(acc * TC_R);
-          for (int kc = 0; kc < kchunks; ++kc) {
-            const uint32_t ko = (uint32_t)(kc * 2 * 128);   // 8 tf32 = 2 core matrices along K
-            const uint64_t dah = sdesc(ahi + ko, 128, sbo), dal = sdesc(alo + ko, 128, sbo);
-            const uint64_t dbh = sdesc(sbase + geo.vh + ko, 128, sbo), dbl = sdesc(sbase + geo.vl + ko, 128, sbo);
-            mma_tf32(d, dah, dbh, kc > 0 ? 1u : 0u);
-            mma_tf32(d, dah, dbl, 1u);
-            mma_tf32(d, dal, dbh, 1u);
+        const uint32_t sbase = su32(smem + (size_t)slot * geo.slot);
+        const uint32_t d = tmem + (uint32_t)(acc * R_B);
+        const uint32_t fb = sbase + (uint32_t)geo.f_off;
+        const uint32_t vbase = su32(smem + geo.v0 + vb * geo.vsz);
+        if (elect_one()) {
+          // D(c, r) = S(r, c): A = the S tile (M = columns, K = 16 rows = 2 row groups;
+          // LBO = 2048 B to the next row group, SBO = 128 B to the next 8 columns)
+#pragma unroll
+          for (int b = 0; b < RG_B / 2; ++b)
+            mma_f16(d + (uint32_t)(16 * b), sdesc(sbase + (uint32_t)(b * 2 * 2048), 2048, 128), dI, id16, 0u);
+          // D -= F V^T in 3 hi / lo products per K chunk (operands pre-negated)
+          for (int kc = 0; kc < kch; ++kc) {
+            const uint32_t fh = fb + (uint32_t)(kc * 2 * CH_BYTES), fl = fh + CH_BYTES;
+            const uint32_t vh = vbase + (uint32_t)(kc * 2 * CH_BYTES), vl = vh + CH_BYTES;
+            mma_f16(d, sdesc(fh, 128, 256), sdesc(vh, 128, 256), id128, 1u);
+            mma_f16(d, sdesc(fh, 128, 256), sdesc(vl, 128, 256), id128, 1u);
+            mma_f16(d, sdesc(fl, 128, 256), sdesc(vh, 128, 256), id128, 1u);
           }
           mma_commit(&tfull[acc]);
-        } else {
-          mbar_arrive(&tfull[acc]);
+          if (!p.store) mma_commit(&empty[slot]);
+          if (t == ntiles - 1) mma_commit(&vempty[vb]);
         }
+        __syncwarp();
         if (++slot == NST) { slot = 0; phase ^= 1; }
-        if (++acc == TC_NACC) { acc = 0; aphase ^= 1; }
       }
     }
-  } else {
-    // ======================= epilogue (16 warps) =======================
-    // warp w: TMEM lane quarter w % 4, rows [32 rp, 32 rp + 32) of every stage (rp = (w-2)/4)
-    const int quarter = warp & 3, rp = (warp - 2) >> 2, ew = warp - 2;
-    const int lanei = quarter * 32 + lane;                  // TMEM lane = A-operand row
-    const int ci = quarter * 31 + lane - 1;                 // CTA column of this lane (lane > 0)
-    const bool ulane = lane == 0;                           // lane 0 holds the pivot column
-    const bool valid = !ulane && ci < ncols;
-    const int ccol = valid ? ci : 0;
-    float* uw = reinterpret_cast<float*>(smem + geo.red + 4 * TC_LANES * 2 * 8) + ew * 32;  // u of my 32 rows
-    const int64_t jloc = (int64_t)j - p.row_offset;
-    const int64_t gj = (jloc >= 0 && jloc < p.m_local) ? (jloc >> 3) : -1;
-    const int jr = (int)(jloc & 7);
-    float* __restrict__ Uj = reinterpret_cast<float*>(p.U) + (int64_t)(j % NSLOT) * p.m_pad;
-    double aw = 0.0, as = 0.0;
-    int slot = 0, acc = 0;
-    uint32_t phase = 0, aphase = 0;
-    for (int i = 0; i < nst; ++i) {
-      const int64_t g0 = gb + (int64_t)i * TC_RG;
-      const int gsz = (int)((ge - g0) < TC_RG ? (ge - g0) : TC_RG);
-      const int gjs = (gj >= g0 && gj < g0 + gsz) ? (int)(gj - g0) : -1;
-      unsigned char* base = smem + geo.slot0 + (size_t)slot * geo.slot;
-      T* data = reinterpret_cast<T*>(base + geo.data);
-      const T* ucol = reinterpret_cast<const T*>(base + geo.ucol);
-      mbar_wait(&tfull[acc], aphase);
-      mbar_wait(&full[slot], phase);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t dr[32];
-      if (kchunks > 0) {
-        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * TC_R + rp * 32), dr);
-        tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int q = 0; q < 32; ++q) dr[q] = 0u;
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);            // accumulator is in registers
-      // u = Ã(:, j) for my 32 rows: lane 0 parks the pivot column's D values, then
-      // every lane forms one row
-      if (ulane) {
-#pragma unroll
-        for (int q = 0; q < 32; q += 4)
-          *reinterpret_cast<uint4*>(uw + q) = make_uint4(dr[q], dr[q + 1], dr[q + 2], dr[q + 3]);
+  } else if (warp == UWARP) {
+    // ============ u warp: V operand loads and the pivot column on CUDA cores ============
+    // Loads each row block's V operand and pivot column (bulk + tensor-map copies) one row
+    // block ahead, then u = S(:, j) - V F(j, :)^T for the row block's 128 rows (4 per lane)
+    // with the same fp16 hi / lo operands the tensor-core formation uses (3 FMAs per
+    // pending reflector), masked to rows >= j, rounded to the storage format on store
+    // steps; published to shared memory (the epilogue's w = X^T u) and to U (the next
+    // steps' V operand).
+    float* Uj = p.U + (int64_t)(j % NSLOT) * p.m_pad;
+    const uint32_t fbytes = (uint32_t)(kch * 2 * CH_BYTES);
+    auto issue_v = [&](int rbi) {
+      const int vb = rbi & 1;
+      if (rbi >= 2) mbar_wait(&vempty[vb], (uint32_t)(((rbi - 2) >> 1) & 1));   // MMA done with rbi - 2
+      unsigned char* vbuf = smem + geo.v0 + vb * geo.vsz;
+      if (elect_one()) {
+        mbar_expect_tx(&vfull[vb], fbytes + RG_B * 16);
+        if (kch > 0) tma_load(vbuf, p.Vop + (size_t)(p.rb_first + rb0 + rbi) * kchw * 2 * CH_BYTES, fbytes, &vfull[vb]);
+        tma_load_2d(vbuf + geo.pcol, &tmC, j * 2, (int)((p.rb_first + rb0 + rbi) * RG_B), &vfull[vb]);
       }
       __syncwarp();
-      {
-        const int rb = rp * 32 + lane;                        // stage row
-        float u = 0.f;
-        if ((rb >> 3) < gsz) {
-          u = Ch<T>::get(ucol, rb) - uw[lane];
-          if (p.store) u = Ch<T>::rnd(u);
-          const int64_t rl = g0 * 8 + rb;
-          const bool keep = rl < p.m_local && p.row_offset + rl >= j;
-          u = keep ? u : 0.f;
-          if (blockIdx.y == 0 && quarter == 0) Uj[rl] = u;
-        }
-        uw[lane] = u;
-      }
-      __syncwarp();
-      // form, (round + write back), reduce: 4 row groups of 8
+    };
+    if (nrbc > 0) issue_v(0);
+    if (nrbc > 1) issue_v(1);
+    for (int rbi = 0; rbi < nrbc; ++rbi) {
+      const int vb = rbi & 1, ub = rbi & 1;
+      const int64_t r0 = (p.rb_first + rb0 + rbi) * R_B;
+      mbar_wait(&vfull[vb], (uint32_t)((rbi >> 1) & 1));
+      if (rbi >= 2) mbar_wait(&ufree[ub], (uint32_t)(((rbi - 2) >> 1) & 1));
+      const unsigned char* vbuf = smem + geo.v0 + vb * geo.vsz;
+      const __half* pc = reinterpret_cast<const __half*>(vbuf + geo.pcol);   // [16 groups][8 rows]
+      float x[4];
 #pragma unroll
-      for (int gg = 0; gg < 4; ++gg) {
-        const int gl = rp * 4 + gg;
-        if (gl < gsz) {                                       // warp-uniform
-          T* chunk;
-          if (sizeof(T) == 2) chunk = data + (size_t)(gl * TC_CN + ccol) * 8;
-          else {
-            const int bc = TC_CN / 2, b = ccol / bc;
-            chunk = data + ((size_t)b * TC_RG * bc + (size_t)gl * bc + (ccol - b * bc)) * 8;
+      for (int i = 0; i < 4; ++i) x[i] = __half2float(pc[lane * 4 + i]);
+      for (int l0 = 0; l0 < npend; l0 += 8) {
+        const unsigned char* vc = vbuf + (size_t)(l0 >> 4) * 2 * CH_BYTES;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int o = op_off(lane * 4 + i, l0 & 15);             // 8 consecutive l: 16 B
+          const uint4 hv = *reinterpret_cast<const uint4*>(vc + o);
+          const uint4 lv = *reinterpret_cast<const uint4*>(vc + CH_BYTES + o);
+          const __half* hh = reinterpret_cast<const __half*>(&hv);
+          const __half* ll = reinterpret_cast<const __half*>(&lv);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (l0 + q < npend) {
+              const float vh = __half2float(hh[q]), vl = __half2float(ll[q]);
+              const float fh = fj[l0 + q], fl = fj[32 + l0 + q];
+              x[i] = fmaf(fh, vh, x[i]);
+              x[i] = fmaf(fh, vl, x[i]);
+              x[i] = fmaf(fl, vh, x[i]);
+            }
           }
-          float x[8];
-          Ch<T>::load(chunk, x);
-          float2* x2 = reinterpret_cast<float2*>(x);
+        }
+      }
+      float* uu = ubuf + ub * R_B;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            x2[q] = __fadd2_rn(x2[q], make_float2(-__uint_as_float(dr[gg * 8 + 2 * q]),
-                                                  -__uint_as_float(dr[gg * 8 + 2 * q + 1])));
+      for (int i = 0; i < 4; ++i) {
+        const int64_t rl = r0 + lane * 4 + i;
+        float v = p.store ? __half2float(__float2half_rn(x[i])) : x[i];
+        if (rl < jl) v = 0.f;
+        uu[lane * 4 + i] = v;
+        if (rl < p.m_pad) Uj[rl] = v;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ufull[ub]);
+      if (rbi + 2 < nrbc) issue_v(rbi + 2);          // into this buffer once the MMA is done with it
+    }
+  } else if (warp >= 2 && warp < 2 + EPI_WARPS) {
+    // ============================ epilogue ============================
+    const int e = warp - 2;
+    const int grp = e / EPI_GW;                 // tiles t = grp, grp + 2, ...
+    const int hf = (e >> 2) & 1;                // rows [64 hf, 64 hf + 64) of a unit
+    const int q = warp & 3;                     // TMEM lane quarter (hardware: warp % 4)
+    double aw[TPG], as[TPG];
+#pragma unroll
+    for (int z = 0; z < TPG; ++z) { aw[z] = 0.0; as[z] = 0.0; }
+    for (int rbi = 0; rbi < nrbc; ++rbi) {
+      const int64_t r0 = (p.rb_first + rb0 + rbi) * R_B;   // first local row of the block
+      const bool mask = jl > r0;                           // rows < j inside this block
+      const bool hasj = jl >= r0 && jl < r0 + R_B;
+      const int ub = rbi & 1;
+      const float* uu = ubuf + ub * R_B;
+      mbar_wait(&ufull[ub], (uint32_t)((rbi >> 1) & 1));
+      int ti = 0;
+      for (int t = grp; t < ntiles; t += NGRP, ++ti) {
+        const int64_t u = (int64_t)rbi * ntiles + t;
+        const int acc = (int)(u % NACC);
+        const int slot = (int)(u % NST);
+        mbar_wait(&tfull[acc], (uint32_t)((u / NACC) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int col = t * C_T + q * 32 + lane;          // column offset from j
+        // this unit's 64-row sums: 4 packed fp32 accumulator pairs (8 chains of 8 rows),
+        // folded pairwise in fp32 and added to the fp64 column sums once per unit
+        float2 w4[4], s4[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) { w4[a] = make_float2(0.f, 0.f); s4[a] = w4[a]; }
+#pragma unroll 1
+        for (int cb = 4 * hf; cb < 4 * hf + 4; ++cb) {      // 16-row chunks of this warp's 64 rows
+          float x[16];
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * R_B + cb * 16), x);
           if (p.store) {
-            if (valid) Ch<T>::round_store(chunk, x);
-            else {
+            // round to the storage format and write the 2 row groups of this chunk back
+            // into the S tile (the producer stores the tile once the group is done)
+            unsigned char* tile = smem + (size_t)slot * geo.slot;
 #pragma unroll
-              for (int q = 0; q < 8; ++q) x[q] = Ch<T>::rnd(x[q]);
+            for (int g = 0; g < 2; ++g) {
+              uint4 v;
+              __half2* h = reinterpret_cast<__half2*>(&v);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                h[i] = __floats2half2_rn(x[g * 8 + 2 * i], x[g * 8 + 2 * i + 1]);
+                const float2 f = __half22float2(h[i]);
+                x[g * 8 + 2 * i] = f.x;
+                x[g * 8 + 2 * i + 1] = f.y;
+              }
+              *reinterpret_cast<uint4*>(tile + (cb * 2 + g) * 2048 + (q * 32 + lane) * 16) = v;
             }
           }
-          if (gl == gjs) {                                   // the group holding row j
-            float xj = x[0];
+          if (hasj) {                                      // the owner's row j of X
+            const int rj = (int)(jl - r0) - cb * 16;
+            if (rj >= 0 && rj < 16) {
+              float xj = x[0];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              if (q == jr) xj = x[q];
-              if (q < jr) x[q] = 0.f;
+              for (int i = 1; i < 16; ++i) xj = i == rj ? x[i] : xj;
+              if (j + col < n) p.xr[j + col] = (double)xj;
             }
-            if (valid) p.xr[c_lo + ci] = xj;
           }
-          // 8-row group: even-row and odd-row fp32 chains in one packed FFMA2 each
-          // (R5b), then their fp32 sum into the fp64 column accumulators
-          const float4 ua = *reinterpret_cast<const float4*>(uw + gg * 8);
-          const float4 ub = *reinterpret_cast<const float4*>(uw + gg * 8 + 4);
-          const float2 u2[4] = {make_float2(ua.x, ua.y), make_float2(ua.z, ua.w), make_float2(ub.x, ub.y),
-                                make_float2(ub.z, ub.w)};
-          float2 w2 = __fmul2_rn(x2[0], u2[0]), s2 = __fmul2_rn(x2[0], x2[0]);
+          if (mask) {
 #pragma unroll
-          for (int q = 1; q < 4; ++q) {
-            w2 = __ffma2_rn(x2[q], u2[q], w2);
-            s2 = __ffma2_rn(x2[q], x2[q], s2);
+            for (int i = 0; i < 16; ++i)
+              if (r0 + cb * 16 + i < jl) x[i] = 0.f;
           }
-          const float pw = w2.x + w2.y, ps = s2.x + s2.y;
-          aw += (double)pw;
-          as += (double)ps;
+          {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+              const float4 u4 = *reinterpret_cast<const float4*>(uu + cb * 16 + i);
+              const float2 xa = make_float2(x[i], x[i + 1]);
+              const float2 xb = make_float2(x[i + 2], x[i + 3]);
+              const int a = (i >> 2) & 1;
+              w4[a] = __ffma2_rn(xa, make_float2(u4.x, u4.y), w4[a]);
+              s4[a] = __ffma2_rn(xa, xa, s4[a]);
+              w4[a + 2] = __ffma2_rn(xb, make_float2(u4.z, u4.w), w4[a + 2]);
+              s4[a + 2] = __ffma2_rn(xb, xb, s4[a + 2]);
+            }
+          }
+        }
+        const float2 wp = __fadd2_rn(__fadd2_rn(w4[0], w4[1]), __fadd2_rn(w4[2], w4[3]));
+        const float2 sp = __fadd2_rn(__fadd2_rn(s4[0], s4[1]), __fadd2_rn(s4[2], s4[3]));
+        double uw = (double)(wp.x + wp.y), us = (double)(sp.x + sp.y);
+#pragma unroll
+        for (int z = 0; z < TPG; ++z)
+          if (z == ti) { aw[z] += uw; as[z] += us; }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (p.store) {
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[slot]);
         }
       }
-      if (p.store) fence_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-      if (++slot == NST) { slot = 0; phase ^= 1; }
-      if (++acc == TC_NACC) { acc = 0; aphase ^= 1; }
+      if (lane == 0) mbar_arrive(&ufree[ub]);
     }
-    // combine the four row parts in fixed order and write the CTA's partials
-    double* red = reinterpret_cast<double*>(smem + geo.red);
-    red[(rp * TC_LANES + lanei) * 2 + 0] = aw;
-    red[(rp * TC_LANES + lanei) * 2 + 1] = as;
-    asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
-    if (rp == 0 && valid) {
-      double w = 0.0, s2 = 0.0;
+    // the CTA's column partials, one row of the partials buffer per row half
+    // (k_pass_reduce adds the 2 gridDim.x rows in fixed order)
+    int ti = 0;
+    for (int t = grp; t < ntiles; t += NGRP, ++ti) {
+      const int c = j + t * C_T + q * 32 + lane;
+      double w = 0.0, s = 0.0;
 #pragma unroll
-      for (int r4 = 0; r4 < 4; ++r4) {
-        w += red[(r4 * TC_LANES + lanei) * 2 + 0];
-        s2 += red[(r4 * TC_LANES + lanei) * 2 + 1];
+      for (int z = 0; z < TPG; ++z)
+        if (z == ti) { w = aw[z]; s = as[z]; }
+      if (c < n) {
+        p.part[((int64_t)(2 * blockIdx.x + hf) * 2 + 0) * n + c] = w;
+        p.part[((int64_t)(2 * blockIdx.x + hf) * 2 + 1) * n + c] = s;
       }
-      p.part[((int64_t)blockIdx.x * 2 + 0) * n + c_lo + ci] = w;
-      p.part[((int64_t)blockIdx.x * 2 + 1) * n + c_lo + ci] = s2;
     }
   }
-  // ---------------- teardown ----------------
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
 // ---------------------------------------------------------------------------
-// k_vop: the newest pending Householder vector v_t = fl32(u_t c_t) (v_t(t) = 1,
-// zero above row t and on padding rows), split hi/lo for tf32, written as column
-// k = t - j0 of the panel's V operand in the K-major core-matrix layout.
-__global__ void k_vop(const float* __restrict__ U, int64_t m_pad, int64_t m_local, int64_t row_offset,
-                      int t, int k, const double* __restrict__ cvec, float* __restrict__ Vh,
-                      float* __restrict__ Vl, int sbo, const DevScalars* __restrict__ sc) {
+// k_tc_ops: the step's operands for k_pass_tc.
+//   blocks [0, nvb): column l = t - j0 of the panel's V operand, v_t = fl32(u_t c_t)
+//     (v_t(t) = 1, zero above row t and on padding rows), split into fp16 hi / lo;
+//   blocks [nvb, ...): the F operand of every column tile for this step's column order,
+//     -F(j0 + l)(j + c) split into fp16 hi / lo (zero for l >= npend or columns >= n).
+__global__ void k_tc_ops(const float* __restrict__ U, int64_t m_pad, int64_t m_local, int64_t row_offset, int t,
+                         int lnew, const double* __restrict__ cvec, unsigned char* __restrict__ Vop, int nvb,
+                         const float* __restrict__ F, int n, int j, int j0, int npend, int ntiles, int kchw,
+                         unsigned char* __restrict__ Fop, const DevScalars* __restrict__ sc) {
   if (sc->done) return;
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= m_pad) return;
-  const int64_t rg = row_offset + r;
-  float v = 0.f;
-  if (r < m_local) {
-    if (rg == t) v = 1.f;
-    else if (rg > t) v = __double2float_rn((double)U[(int64_t)(t % NSLOT) * m_pad + r] * cvec[t]);
+  if ((int)blockIdx.x < nvb) {
+    if (lnew < 0) return;
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m_pad) return;
+    const int64_t rg = row_offset + r;
+    float v = 0.f;
+    if (r < m_local) {
+      if (rg == t) v = 1.f;
+      else if (rg > t) v = __double2float_rn((double)U[(int64_t)(t % NSLOT) * m_pad + r] * cvec[t]);
+    }
+    __half hi, lo;
+    split_f16(v, hi, lo);
+    const int64_t rb = r >> 7;
+    unsigned char* base = Vop + (size_t)rb * kchw * 2 * CH_BYTES + (size_t)(lnew >> 4) * 2 * CH_BYTES;
+    const int o = op_off((int)(r & 127), lnew & 15);
+    *reinterpret_cast<__half*>(base + o) = hi;
+    *reinterpret_cast<__half*>(base + CH_BYTES + o) = lo;
+    return;
   }
-  float hi, lo;
-  split_tf32(v, hi, lo);
-  const int64_t o = cm_off(r, k, sbo) / 4;
-  Vh[o] = hi;
-  Vl[o] = lo;
+  const int64_t e = (int64_t)(blockIdx.x - nvb) * blockDim.x + threadIdx.x;   // (tile, column, l)
+  const int KW = kchw * 16;
+  if (e >= (int64_t)ntiles * C_T * KW) return;
+  const int l = (int)(e % KW);
+  const int64_t tc = e / KW;
+  const int c = (int)(tc % C_T), tt = (int)(tc / C_T);
+  const int col = j + tt * C_T + c;
+  float f = 0.f;
+  if (l < npend && col < n) f = -F[(int64_t)((j0 + l) % NSLOT) * n + col];
+  __half hi, lo;
+  split_f16(f, hi, lo);
+  unsigned char* base = Fop + ((size_t)tt * kchw + (l >> 4)) * 2 * CH_BYTES;
+  const int o = op_off(c, l & 15);
+  *reinterpret_cast<__half*>(base + o) = hi;
+  *reinterpret_cast<__half*>(base + CH_BYTES + o) = lo;
 }
 
 // ---------------------------------------------------------------------------
-template <typename T>
-static cudaError_t launch_tc_t(PassParams p, const void* tmap, int max_ctas, int* gx_out, cudaStream_t st) {
-  const int n = p.n, j = p.j;
-  const int esz = (int)sizeof(T);
-  if (p.npend > p.nbw || p.nbw > 32 || (p.nbw % 8)) return cudaErrorInvalidValue;
-  const int gy = (n - j + TC_CN - 1) / TC_CN;
-  p.ncols_slot = TC_CN;
-  int nst = 4;
-  TcGeom g = tc_geom(esz, p.nbw, nst);
-  while (nst > 2 && (size_t)g.total > (size_t)PASS_SMEM_MAX) {
-    --nst;
-    g = tc_geom(esz, p.nbw, nst);
-  }
-  if ((size_t)g.total > (size_t)PASS_SMEM_MAX) return cudaErrorInvalidConfiguration;
-  p.nst = nst;
-  p.gs = TC_RG;
-  const int64_t nact = p.ngroups - p.g_lo;
-  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, max_ctas / gy), (nact + TC_RG - 1) / TC_RG));
-  p.gx_used = gx;
-  *gx_out = gx;
-  cudaError_t e = smem_attr((const void*)k_pass_tc<T>, PASS_SMEM_MAX);
-  if (e != cudaSuccess) return e;
-  k_pass_tc<T><<<dim3(gx, gy), TC_BLOCK, g.total, st>>>(p, *reinterpret_cast<const CUtensorMap*>(tmap));
+int tc_kchw(int nb) { return (nb + 15) / 16; }
+
+size_t tc_vop_bytes(int64_t m_pad, int nb) { return (size_t)(m_pad / 128 + 1) * tc_kchw(nb) * 2 * CH_BYTES; }
+size_t tc_fop_bytes(int n, int nb) { return (size_t)((n + C_T - 1) / C_T) * tc_kchw(nb) * 2 * CH_BYTES; }
+
+cudaError_t launch_tc_ops(const float* U, int64_t m_pad, int64_t m_local, int64_t row_offset, int t, int lnew,
+                          const double* cvec, void* Vop, const float* F, int n, int j, int j0, int npend, int nb,
+                          void* Fop, const DevScalars* sc, cudaStream_t st) {
+  const int kchw = tc_kchw(nb);
+  const int ntiles = (n - j + C_T - 1) / C_T;
+  const int nvb = lnew >= 0 ? (int)((m_pad + 255) / 256) : 0;
+  const int64_t fe = (int64_t)ntiles * C_T * kchw * 16;
+  const int nfb = (int)((fe + 255) / 256);
+  k_tc_ops<<<nvb + nfb, 256, 0, st>>>(U, m_pad, m_local, row_offset, t, lnew, cvec, (unsigned char*)Vop, nvb, F, n, j,
+                                      j0, npend, ntiles, kchw, (unsigned char*)Fop, sc);
   return cudaGetLastError();
 }
 
-cudaError_t launch_pass_tc(int fmt, PassParams p, const void* tmap, int max_ctas, int* gx_out, cudaStream_t st) {
-  return fmt == 1 ? launch_tc_t<__half>(p, tmap, max_ctas, gx_out, st)
-                  : launch_tc_t<float>(p, tmap, max_ctas, gx_out, st);
+int tc_smem_bytes(int nb, int* nst_out) {
+  const int kchw = tc_kchw(nb);
+  int nst = 4;
+  while (nst > 2 && geo_of(kchw, nst).total > TC_SMEM_MAX) --nst;
+  if (nst_out) *nst_out = nst;
+  return geo_of(kchw, nst).total;
 }
 
-// tensor map of S: 8-byte elements, dims {n * esz / 2 * ... = n * (16 * esz / 2) / 8, ngroups},
-// row stride n * 8 * esz bytes, box {(TC_CN or TC_CN / 2 for fp32) * esz / 2, TC_RG}; the
-// driver entry point is taken through the runtime (no -lcuda)
-int encode_tmap_S(void* tmap_out, void* S, int fmt, int64_t ngroups, int n) {
+cudaError_t launch_pass_tc(const PassParams& pp, int nb, const void* Vop, const void* Fop, const void* tmap,
+                           const void* tmapc, int max_ctas, int* gx_out, cudaStream_t st) {
+  TcParams p{};
+  p.m_pad = pp.m_pad;
+  p.m_local = pp.m_local;
+  p.row_offset = pp.row_offset;
+  p.rb_first = pp.g_lo / RG_B;
+  p.nrb = pp.m_pad / R_B - p.rb_first;
+  if (p.nrb < 0) p.nrb = 0;
+  p.n = pp.n;
+  p.j = pp.j;
+  p.j0 = pp.j0;
+  p.npend = pp.npend;
+  p.store = pp.store;
+  p.kchw = tc_kchw(nb);
+  p.ntiles = (pp.n - pp.j + C_T - 1) / C_T;
+  if (p.npend > p.kchw * 16 || p.kchw > 2 || p.ntiles > 16) return cudaErrorInvalidValue;
+  int nst = 0;
+  const int smem = tc_smem_bytes(nb, &nst);
+  if (smem > TC_SMEM_MAX) return cudaErrorInvalidConfiguration;
+  p.nst = nst;
+  p.Vop = (const unsigned char*)Vop;
+  p.Fop = (const unsigned char*)Fop;
+  p.U = (float*)pp.U;
+  p.part = pp.part;
+  p.xr = pp.xr;
+  p.sc = pp.sc;
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(max_ctas / 2, p.nrb));
+  *gx_out = 2 * gx;                                   // partial rows: 2 per CTA (row halves)
+  const bool wide = p.ntiles > 2 * 4;
+  const void* fn = wide ? (const void*)k_pass_tc<8> : (const void*)k_pass_tc<4>;
+  cudaError_t e = smem_attr(fn, smem);
+  if (e != cudaSuccess) return e;
+  if (wide)
+    k_pass_tc<8><<<gx, BLOCK, smem, st>>>(p, *reinterpret_cast<const CUtensorMap*>(tmap),
+                                          *reinterpret_cast<const CUtensorMap*>(tmapc));
+  else
+    k_pass_tc<4><<<gx, BLOCK, smem, st>>>(p, *reinterpret_cast<const CUtensorMap*>(tmap),
+                                          *reinterpret_cast<const CUtensorMap*>(tmapc));
+  return cudaGetLastError();
+}
+
+// tensor maps of fp16 S viewed as [ngroups][n * 2] 8-byte units: box = 128 columns x 16 row
+// groups (one unit tile, 32 KB; which = 0) or 1 column x 16 row groups (the pivot column of a
+// row block, 256 B; which = 1); the driver entry point is taken through the runtime
+int encode_tmap_S(void* tmap_out, void* S, int64_t ngroups, int n, int which) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     cudaDriverEntryPointQueryResult q;
@@ -535,24 +665,14 @@ int encode_tmap_S(void* tmap_out, void* S, int fmt, int64_t ngroups, int n) {
       return -1;
     enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  const int esz = fmt == 1 ? 2 : 4;
-  const int u8 = esz;                              // 8-byte units per 8-row chunk of one column
-  const int bcols = fmt == 1 ? TC_CN : TC_CN / 2;  // columns per box (box dim 0 <= 256 units)
-  const cuuint64_t dims[2] = {(cuuint64_t)n * u8, (cuuint64_t)ngroups};
-  const cuuint64_t strides[1] = {(cuuint64_t)n * 8 * esz};
-  const cuuint32_t box[2] = {(cuuint32_t)(bcols * u8), (cuuint32_t)TC_RG};
+  const cuuint64_t dims[2] = {(cuuint64_t)n * 2, (cuuint64_t)ngroups};
+  const cuuint64_t strides[1] = {(cuuint64_t)n * 16};
+  const cuuint32_t box[2] = {(cuuint32_t)(which ? 2 : C_T * 2), (cuuint32_t)RG_B};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = enc(reinterpret_cast<CUtensorMap*>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, S, dims,
                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return (int)r;
-}
-
-cudaError_t launch_vop(const float* U, int64_t m_pad, int64_t m_local, int64_t row_offset, int t, int k,
-                       const double* cvec, float* Vh, float* Vl, int nbw, const DevScalars* sc, cudaStream_t st) {
-  k_vop<<<(unsigned)((m_pad + 255) / 256), 256, 0, st>>>(U, m_pad, m_local, row_offset, t, k, cvec, Vh, Vl,
-                                                          nbw * 32, sc);
-  return cudaGetLastError();
 }
 
 }  // namespace mpid

@@ -72,7 +72,7 @@ constexpr int NCCL_SUM = 0, NCCL_MAX = 2;
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t AD, S, U, F, Vh, Vl, Sj, R, part, red, xr, norms, perm, scal3, sc, maxpart, rpart;
+  size_t AD, S, U, F, Vop, Fop, R, part, red, xr, norms, perm, scal3, sc, maxpart, rpart;
   size_t AI, Q1, G1, G2, W, tpart, Rd, T, Pw, epart, Tp, Ik, Rinv, py, pvec, gpart, G, Gc, misc;
   size_t total;
 };
@@ -96,8 +96,9 @@ int64_t m_pad_of(int64_t m_local) {
   const int64_t T = PASS_TILE_G * RG;
   return std::max<int64_t>(T, (m_local + T - 1) / T * T);
 }
-// rows of per-CTA partials the panel pass may write: its grid.x never exceeds the SM count
-int pass_gx_cap() { return num_sms(); }
+// rows of per-CTA partials the panel pass may write: the FFMA pass one per CTA (grid.x <= SMs),
+// the tcgen05 pass one per CTA row half (grid.x <= SMs)
+int pass_gx_cap() { return 2 * num_sms(); }
 int round_gy(int64_t m_pad, int64_t n) {
   const int64_t gx = (n + 31) / 32;
   const int64_t ngroups = m_pad / 8;
@@ -152,9 +153,8 @@ Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
   L.S = take((size_t)mp * n * sbytes);
   L.U = take((size_t)NSLOT * mp * sbytes);
   L.F = take((size_t)NSLOT * n * sbytes);
-  L.Vh = take((size_t)(mp + 128) * NB_MAX * 4);   // tcgen05 pass: panel V operand (hi / lo)
-  L.Vl = take((size_t)(mp + 128) * NB_MAX * 4);
-  L.Sj = take((size_t)(mp + 128) * 4);             // the pivot column of S, contiguous
+  L.Vop = take(tc_vop_bytes(mp, NB_MAX));            // tcgen05 pass: the panel's V operand (fp16 hi / lo)
+  L.Fop = take(tc_fop_bytes((int)n, NB_MAX));         //   and the step's F operand
   L.R = take((size_t)k * n * sbytes);
   L.part = take((size_t)pass_gx_cap() * 2 * n * 8);
   L.red = take((size_t)3 * n * 8);
@@ -209,10 +209,10 @@ struct mpid_ctx {
   // device pointers (U, F, R in the working precision: fp32, fp64 for ID_FP64)
   void* S = nullptr;
   void *U = nullptr, *F = nullptr, *R = nullptr;
-  float *Vh = nullptr, *Vl = nullptr;
-  void* Sj = nullptr;
-  alignas(64) unsigned char tmapS[2][128];   // CUtensorMap of S for fp16 / fp32 (tcgen05 pass)
-  int tmap_ok[2] = {-1, -1};
+  void *Vop = nullptr, *Fop = nullptr;
+  alignas(64) unsigned char tmapS[128];      // CUtensorMap of fp16 S (tcgen05 pass, 128 x 128 unit tiles)
+  alignas(64) unsigned char tmapC[128];      //   and of one column x 128 rows (the pass's pivot column)
+  int tmap_ok = -1;
   alignas(64) unsigned char tmapG[128];      // CUtensorMap of fp16 S for the Gram kernel
   int tmapG_ok = -1;
   double *gpart = nullptr, *G = nullptr, *Gc = nullptr;
@@ -384,11 +384,10 @@ static id_status relayout(mpid_ctx* h, int sbytes) {
   h->S = w + L.S;
   h->U = w + L.U;
   h->F = w + L.F;
-  h->Vh = (float*)(w + L.Vh);
-  h->Vl = (float*)(w + L.Vl);
-  h->Sj = w + L.Sj;
-  h->tmap_ok[0] = encode_tmap_S(h->tmapS[0], h->S, 1, h->m_pad / 8, (int)n);
-  h->tmap_ok[1] = encode_tmap_S(h->tmapS[1], h->S, 2, h->m_pad / 8, (int)n);
+  h->Vop = w + L.Vop;
+  h->Fop = w + L.Fop;
+  h->tmap_ok = encode_tmap_S(h->tmapS, h->S, h->m_pad / 8, (int)n, 0) |
+               encode_tmap_S(h->tmapC, h->S, h->m_pad / 8, (int)n, 1);
   h->tmapG_ok = encode_tmap_gram(h->tmapG, h->S, h->m_pad / 8, (int)n);
   h->gpart = (double*)(w + L.gpart);
   h->G = (double*)(w + L.G);
@@ -426,8 +425,7 @@ static id_status relayout(mpid_ctx* h, int sbytes) {
   // zero U (padding rows must stay 0); S is fully written by the rounding kernel
   if (cudaMemsetAsync(h->U, 0, (size_t)NSLOT * h->m_pad * sbytes, h->st) != cudaSuccess ||
       // the V operand's unused K columns are multiplied by zero F entries: keep them finite
-      cudaMemsetAsync(h->Vh, 0, (size_t)(h->m_pad + 128) * NB_MAX * 4, h->st) != cudaSuccess ||
-      cudaMemsetAsync(h->Vl, 0, (size_t)(h->m_pad + 128) * NB_MAX * 4, h->st) != cudaSuccess)
+      cudaMemsetAsync(h->Vop, 0, tc_vop_bytes(h->m_pad, NB_MAX), h->st) != cudaSuccess)
     return fail(h, ID_ERR_CUDA, "workspace memset failed");
   return ID_OK;
 }
@@ -662,8 +660,7 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     // the pivot's S data (its F / R / perm bookkeeping was swapped by the last k_reflector);
     // an in-pass-prologue variant measured no faster: its scattered 16-byte accesses
     // delay the CTA's TMA stream by as much as the separate launch costs
-    CK(launch_swap(fmt, h->S, h->m_pad / 8, (int)n, j, j0, j, h->F, h->R, h->perm,
-                   formation == 2 ? h->Sj : nullptr, h->sc, h->st));
+    CK(launch_swap(fmt, h->S, h->m_pad / 8, (int)n, j, j0, j, h->F, h->R, h->perm, nullptr, h->sc, h->st));
     h->kernel_launches += 1;
     PassParams p{};
     p.S = h->S;
@@ -685,22 +682,17 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     p.xr = h->xr;
     p.sc = h->sc;
     int gx_used = 0;
-    if (profile) CK(rec(h, h->pass_ev[2 * j]));
     if (formation == 2) {
-      p.Vh = h->Vh;
-      p.Vl = h->Vl;
-      p.nbw = (nb + 7) & ~7;
-      if (npend > 0) {   // the newest pending reflector t = j - 1 joins the panel's V operand
-        CK(launch_vop((const float*)h->U, h->m_pad, h->m_local, h->row_offset, j - 1, j - 1 - j0, h->cvec, h->Vh, h->Vl,
-                      p.nbw, h->sc, h->st));
-        h->kernel_launches += 1;
-      }
-      p.Sj = h->Sj;
-      if (h->tmap_ok[fmt - 1] != 0)
-        return fail(h, ID_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", h->tmap_ok[fmt - 1]);
-      CK(launch_pass_tc(fmt, p, h->tmapS[fmt - 1], pass_gx_cap(), &gx_used, h->st));
+      // the newest pending reflector t = j - 1 joins the panel's V operand (column t - j0),
+      // and the step's F operand is laid out for the current column order
+      CK(launch_tc_ops((const float*)h->U, h->m_pad, h->m_local, h->row_offset, j - 1, npend > 0 ? j - 1 - j0 : -1,
+                       h->cvec, h->Vop, (const float*)h->F, (int)n, j, j0, npend, nb, h->Fop, h->sc, h->st));
+      h->kernel_launches += 1;
+      if (h->tmap_ok != 0) return fail(h, ID_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", h->tmap_ok);
     }
-    else CK(launch_pass_tma(fmt, p, pass_gx_cap(), &gx_used, h->st));
+    if (profile) CK(rec(h, h->pass_ev[2 * j]));
+    if (formation == 2) CK(launch_pass_tc(p, nb, h->Vop, h->Fop, h->tmapS, h->tmapC, pass_gx_cap(), &gx_used, h->st));
+    else CK(launch_pass_tma(fmt, p, num_sms(), &gx_used, h->st));
     if (gx_used < 1 || gx_used > pass_gx_cap())
       return fail(h, ID_ERR_STATE, "panel pass grid %d exceeds the partials buffer (%d)", gx_used, pass_gx_cap());
     if (profile) CK(rec(h, h->pass_ev[2 * j + 1]));
@@ -754,10 +746,16 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
     return fail(h, ID_ERR_DIM, "k_max=%d outside [1, min(m, n)]", k_max);
   if (k_max > h->k_cap) return fail(h, ID_ERR_DIM, "workspace too small for k_max=%d (cap %lld)", k_max,
                                     (long long)h->k_cap);
-  // formation of the pending trailing update: 1 = CUDA-core FFMA pass (bit-identical to the
-  // oracle's sequential FMA model; the faster one on C4), 2 = tcgen05 pass
+  // formation of the pending trailing update: 1 = CUDA-core FFMA pass (short store interval,
+  // fp16 / fp32 / fp64), 2 = tcgen05 pass (fp16).  Default: tcgen05 whenever it
+  // applies — fp16 storage, range scaling (max |a| <= 1 keeps |F| <= 2 sqrt(2 m) inside the
+  // fp16 operand range), n - 0 <= 2048 columns — else FFMA.
+  const bool tc_ok = fmt == ID_FP16 && scaling != ID_SCALE_NONE && h->n <= 2048 &&
+                     2.83 * sqrt((double)h->m_global) < 60000.0;
   int formation = opts ? opts->formation : 0;
-  if (formation == 0) formation = 1;
+  if (formation == 0) formation = tc_ok ? 2 : 1;
+  if (formation == 2 && !tc_ok)
+    return fail(h, ID_ERR_ARG, "the tcgen05 pass needs fp16 storage with range scaling, n <= 2048, m < 4.4e8");
   if (formation < 1 || formation > 4) return fail(h, ID_ERR_ARG, "bad formation %d", formation);
   if (formation >= 3 && fmt != ID_FP16)
     return fail(h, ID_ERR_ARG, "Gram / sketched pivoting (formation 3, 4) run on fp16 A_L (tcgen05 kind::f16)");
@@ -773,8 +771,6 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
     const int r = encode_tmap_gram(h->tmapO, (char*)h->S + (size_t)h->m_pad * h->n * 2, h->m_pad / 8, h->sk_lw);
     if (r != 0) return fail(h, ID_ERR_CUDA, "cuTensorMapEncodeTiled (sketch) failed (%d)", r);
   }
-  if (formation == 2 && fmt == ID_FP64)
-    return fail(h, ID_ERR_ARG, "the tcgen05 formation models the low-precision pass (fp16 / fp32 only)");
   int nb = opts && opts->nb > 0 ? opts->nb : (formation == 2 ? 16 : 4);
   if (nb > NB_MAX || (formation == 1 && nb > 16) || (fmt == ID_FP64 && nb > 8))
     return fail(h, ID_ERR_ARG, "nb=%d too large for formation %d / format %d", nb, formation, (int)fmt);

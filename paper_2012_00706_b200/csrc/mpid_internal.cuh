@@ -57,10 +57,6 @@ struct PassParams {
   int nst;                 // pipeline depth (set by the launcher)
   int gx_used;             // gridDim.x (set by the launcher)
   int cw, wr;              // consumer warps: column-warps x row-split warps (launcher)
-  const float* Vh;         // tcgen05 pass: the panel's V operand (hi / lo tf32), K-major
-  const float* Vl;         //   core-matrix layout, nbw columns, (m_pad + 128) rows
-  int nbw;                 // K width of the operand layouts (nb rounded up to 8)
-  const void* Sj;          // tcgen05 pass: the pivot column j of S, contiguous (m_pad rows)
   void* U;                 // [NSLOT][m_pad] raw u vectors (working precision: fp32, fp64 for fmt 3)
   const void* F;           // [NSLOT][n]   f vectors (current column order, working precision)
   const double* cvec;      // [k_max] c_t = 1/(u_t - beta_t) per step
@@ -99,6 +95,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     if (spin > (1u << 26)) __trap();
   }
 }
+// the same wait with the PTX suspend-time hint: a thread whose phase is not complete is
+// suspended until it completes (or the 1 ms hint elapses) instead of re-polling shared
+// memory, so waiting warps do not steal shared-memory cycles from TMA and the tensor cores
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t spin = 0;; ++spin) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(su32(b)), "r"(parity), "r"(1000000u)
+        : "memory");
+    if (done) return;
+    if (spin > (1u << 16)) __trap();
+  }
+}
 // global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0, 16 B aligned)
 __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -135,11 +148,16 @@ cudaError_t launch_round(int fmt, const double* A, int64_t m, int64_t m_pad, int
 cudaError_t launch_init_pivot(const double* norms, int n, int* perm, DevScalars* sc,
                               cudaStream_t st);
 cudaError_t launch_pass_tma(int fmt, PassParams p, int num_sms, int* gx_out, cudaStream_t st);
-cudaError_t launch_pass_tc(int fmt, PassParams p, const void* tmap, int max_ctas, int* gx_out, cudaStream_t st);
-// 3-D tensor map of the stored matrix S ([ngroups][n][8] elements) for the tcgen05 pass
-int encode_tmap_S(void* tmap_out, void* S, int fmt, int64_t ngroups, int n);
-cudaError_t launch_vop(const float* U, int64_t m_pad, int64_t m_local, int64_t row_offset, int t, int k,
-                       const double* cvec, float* Vh, float* Vl, int nbw, const DevScalars* sc, cudaStream_t st);
+// tcgen05 pass (fp16 storage; k_pass_tc.cu): operands, launch, tensor map of S
+int tc_kchw(int nb);
+size_t tc_vop_bytes(int64_t m_pad, int nb);
+size_t tc_fop_bytes(int n, int nb);
+cudaError_t launch_tc_ops(const float* U, int64_t m_pad, int64_t m_local, int64_t row_offset, int t, int lnew,
+                          const double* cvec, void* Vop, const float* F, int n, int j, int j0, int npend, int nb,
+                          void* Fop, const DevScalars* sc, cudaStream_t st);
+cudaError_t launch_pass_tc(const PassParams& p, int nb, const void* Vop, const void* Fop, const void* tmap,
+                           const void* tmapc, int max_ctas, int* gx_out, cudaStream_t st);
+int encode_tmap_S(void* tmap_out, void* S, int64_t ngroups, int n, int which);
 cudaError_t launch_pass_reduce(const double* part, int gx, int n, int j, const double* xr,
                                int own_row, double* red, const DevScalars* sc, cudaStream_t st);
 // F, R in the working precision: fp32 (fmt 1, 2) or fp64 (fmt 3)

@@ -1,0 +1,205 @@
+"""Parity at BASELINE.json's configurations (SURVEY §8(c) acceptance matrix), with bounds.
+
+Every run goes through the C ABI with the library defaults (fp16 + range scaling: the
+tcgen05 pass, nb = 16; fp32: the FFMA pass, nb = 4) and is compared with the oracle's
+QRCP run IN FULL at the same size — oracle/cqrcp.c, the paper model (per-operation RNE
+update, fp64 row-order sums), which shares neither the formation nor the reduction order
+with either GPU pass — on the same A_L bytes:
+
+  * pivots: the ordered prefix up to the first step the oracle does not certify (reading
+    R10, c_tie calibrated by tools/calibrate_ctie.py); on inputs with a gap at k (the C5
+    analogue, planted skeletons) the pivot SET equals the oracle's;
+  * the relative Frobenius error within 5 % of the oracle pipeline's (same fmt, nb, LSQ);
+  * P within 1e-10 of the oracle's LSQ solve from the GPU's I;
+  * bounds (north_star; R13): the Eckart-Young-Mirsky lower bound
+    sqrt(sum_{j>k} sigma_j^2) <= err <= B_post, with sigma from the generator's closed form
+    (C1-C3: prescribed spectra; C4/C5: the 2L x n factor, exact by discrete orthogonality)
+    lowered by Weyl's inequality for the additive noise.
+
+C1, C2, the 32^3-row C4 analogue, C3 (k = 256 and eps = 1e-3), full C4 (2,097,152 x 1024, the
+bench workload) and the 64^3-row C5 analogue (262,144 x 2048, 256 modes, k = 512) run here;
+full C5 (256 GiB of A_D) does not fit one GPU or this host.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle.fast import qrcp_c
+from oracle.id import coeffs_from_R, coeffs_lsq, id_error_blocked, post_bound
+from oracle.qrcp import make_AL
+from oracle.rounding import HALF, SINGLE
+from synth import config_spec, gen_config
+from synth.generators import fourier_params, gen_fourier
+from tests.gpu_helpers import C_TIE, prefix_match
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2012_00706_b200 import mpid
+    mpid.lib()
+
+
+def _run(At, fmt, sc, k, eps=0.0, nb=0):
+    from paper_2012_00706_b200.mpid import MPID
+    h = MPID(At, k_max=k)
+    q = h.qrcp(fmt, sc, k=k, eps=eps, nb=nb)
+    st = h.stats()
+    out = {"k": q.k, "piv": q.piv, "stats": st, "R": h.get_R().cpu().numpy().astype(np.float64),
+           "perm": h.get_perm()}
+    out["P"] = h.coeffs("lsq").cpu().numpy()
+    out["err"] = h.error()
+    h.close()
+    return out
+
+
+def _fourier_sigma(fp, noise=True):
+    """sigma(A_clean) = sigma(diag(sqrt(m/2) [a, a]) T) for distinct lattice modes (discrete
+    orthogonality of the grid cosines / sines; checked in tests/test_synth.py), and the
+    spectral norm bound of the additive noise."""
+    t = np.arange(fp.n, dtype=np.float64)
+    T = np.concatenate([np.cos(np.outer(fp.omega, t)), np.sin(np.outer(fp.omega, t))], axis=0)
+    D = np.concatenate([fp.amp, fp.amp]) * math.sqrt(fp.m / 2)
+    s = np.linalg.svd(D[:, None] * T, compute_uv=False)
+    nrm = 1.1 * fp.noise_std * (math.sqrt(fp.m) + math.sqrt(fp.n)) if noise else 0.0
+    return s, nrm
+
+
+def _ey_lower(sigma, k, noise2):
+    """Eckart-Young-Mirsky with Weyl: sigma_j(A_D) >= sigma_j(A_clean) - ||N||_2."""
+    tail = np.maximum(np.asarray(sigma, dtype=np.float64)[k:] - noise2, 0.0)
+    return math.sqrt(float(np.sum(tail ** 2)))
+
+
+def _check(A, out, fmt, sc, k, nb, sigma, noise2, eps=0.0, gap=False, r=None):
+    """the acceptance checks above for one GPU run; returns the oracle run"""
+    AL, s = make_AL(A, fmt, sc)
+    if r is None:
+        r = qrcp_c(AL, k, fmt, nb=nb, eps=eps, model="paper")
+    kk = min(out["k"], r.k_out)
+    agree, fu = prefix_match(out["piv"], r, c_tie=C_TIE)
+    assert agree >= fu, (agree, fu, out["piv"][:12], r.perm[:12])
+    if gap:
+        assert set(out["piv"][:kk].tolist()) == set(r.perm[:kk].tolist())
+    normA = float(np.linalg.norm(A))
+    P_or = coeffs_lsq(A, r.I)
+    e_or = id_error_blocked(A, r.I, P_or)[1]
+    e_gpu = out["err"][1]
+    assert abs(e_gpu - e_or) <= 0.05 * e_or, (e_gpu, e_or)
+    I = out["piv"]
+    P_ref = coeffs_lsq(A, I)
+    assert np.linalg.norm(out["P"] - P_ref) <= 1e-10 * np.linalg.norm(P_ref)
+    # bounds on the GPU's own error
+    lo = _ey_lower(sigma, out["k"], noise2) / normA
+    T2 = float(np.linalg.norm(coeffs_from_R(out["R"], out["perm"], out["k"]), 2))
+    uL = HALF.u if fmt == "fp16" else SINGLE.u
+    st = out["stats"]
+    B = post_bound(st["resid_est"], st["scale"], T2, normA, uL, out["k"], st["nb"], A.shape[0], SINGLE.u) / normA
+    assert lo * (1 - 1e-9) <= e_gpu <= B, (lo, e_gpu, B)
+    return r, agree, fu
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("fmt,sc", [("fp16", "pow2"), ("fp32", "none")])
+def test_C1(seed, fmt, sc):
+    from tests.gpu_helpers import to_dev
+    A = gen_config("C1", seed)
+    out = _run(to_dev(A), fmt, sc, 32)
+    sigma = 10.0 ** (-np.arange(128) / 8.0)
+    _check(A, out, fmt, sc, 32, out["stats"]["nb"], sigma, 0.0)
+
+
+@pytest.mark.parametrize("k", [16, 64, 128])
+@pytest.mark.parametrize("fmt,sc", [("fp16", "maxabs"), ("fp32", "none")])
+def test_C2(k, fmt, sc):
+    from tests.gpu_helpers import to_dev
+    A = gen_config("C2", 1)
+    out = _run(to_dev(A), fmt, sc, k)
+    sigma = np.arange(1, 1025, dtype=np.float64) ** -2.0
+    _check(A, out, fmt, sc, k, out["stats"]["nb"], sigma, 1.1 * 1e-8 * (64 + 32))
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_C4_analogue(seed):
+    """32^3 rows x 1024 snapshots, 64 modes, k = 100: the C4 generator law at 1/64 size."""
+    import torch
+    fp = fourier_params(32, 64, 1024, seed)
+    At = gen_fourier(fp, seed, device="cuda")
+    A = np.asfortranarray(At.cpu().numpy().T)
+    out = _run(At, "fp16", "pow2", 100)
+    sigma, nrm = _fourier_sigma(fp)
+    _check(A, out, "fp16", "pow2", 100, out["stats"]["nb"], sigma, nrm)
+    del At
+    torch.cuda.empty_cache()
+
+
+@pytest.fixture(scope="module")
+def c3():
+    return gen_config("C3", 0)
+
+
+def _c3_sigma():
+    m, n = 65536, 2048
+    sig = np.exp(-np.arange(1, 301, dtype=np.float64) / 30.0)
+    std = 1e-6 * math.sqrt(float(np.sum(sig ** 2))) / math.sqrt(m * n)
+    return sig, 1.1 * std * (math.sqrt(m) + math.sqrt(n))
+
+
+def test_C3_fixed_rank(c3):
+    """configs[2]: 65536 x 2048, k = 256, fp16 — the whole 256-step QRCP against the oracle."""
+    from tests.gpu_helpers import to_dev
+    out = _run(to_dev(c3), "fp16", "pow2", 256)
+    assert out["k"] == 256 and out["stats"]["formation"] == 2
+    sigma, nrm = _c3_sigma()
+    r, agree, fu = _check(c3, out, "fp16", "pow2", 256, out["stats"]["nb"], sigma, nrm)
+    assert fu >= 64                      # the comparison covers a real prefix
+
+
+def test_C3_tolerance_rank(c3):
+    """configs[2] with eps = 1e-3 in fp16: k_eps equal to the oracle's (+-1 only when the
+    crossing lies within rounding of the threshold), error within 5 %, bounds."""
+    from tests.gpu_helpers import to_dev
+    eps = 1e-3
+    out = _run(to_dev(c3), "fp16", "pow2", 512, eps=eps)
+    AL, s = make_AL(c3, "fp16", "pow2")
+    r = qrcp_c(AL, 512, "fp16", nb=out["stats"]["nb"], eps=eps, model="paper")
+    assert abs(out["k"] - r.k_out) <= 1, (out["k"], r.k_out)
+    if out["k"] != r.k_out:
+        kk = min(out["k"], r.k_out)
+        assert abs(r.resid[kk] - eps * r.normAL) <= 2e-3 * eps * r.normAL
+    sigma, nrm = _c3_sigma()
+    _check(c3, out, "fp16", "pow2", out["k"], out["stats"]["nb"], sigma, nrm, r=r)
+
+
+def test_C4_full():
+    """configs[3] in full — bench.py's workload: 2,097,152 x 1024, k = 100, fp16."""
+    import torch
+    spec = config_spec("C4")
+    fp = fourier_params(spec.extra["N"], spec.extra["L"], spec.n, 0)
+    At = gen_fourier(fp, 0, 0, spec.m, device="cuda")
+    A = np.asfortranarray(At.cpu().numpy().T)
+    out = _run(At, "fp16", "pow2", 100)
+    del At
+    torch.cuda.empty_cache()
+    sigma, nrm = _fourier_sigma(fp)
+    _check(A, out, "fp16", "pow2", 100, out["stats"]["nb"], sigma, nrm)
+
+
+def test_C5_analogue_pivot_set():
+    """configs[4]'s generator law (256 modes, 2048 snapshots, k = 512) on 64^3 = 262,144 rows:
+    a spectral gap at k (clean rank 2L = 512), so the pivot SET must equal the oracle's."""
+    import torch
+    fp = fourier_params(64, 256, 2048, 0)
+    At = gen_fourier(fp, 0, device="cuda")
+    A = np.asfortranarray(At.cpu().numpy().T)
+    out = _run(At, "fp16", "pow2", 512)
+    del At
+    torch.cuda.empty_cache()
+    sigma, nrm = _fourier_sigma(fp)
+    assert sigma[511] > 10 * nrm                      # the gap at k the set equality relies on
+    _check(A, out, "fp16", "pow2", 512, out["stats"]["nb"], sigma, nrm, gap=True)
