@@ -92,8 +92,16 @@ def scale_factor(A_D: np.ndarray, scaling: str) -> float:
 def make_AL(A_D: np.ndarray, fmt: str, scaling: str = "none"):
     """A_L = fl_L(s * A_D) with a single RNE rounding from fp64 (reading R7)."""
     s = scale_factor(A_D, scaling)
-    AL = round_to(np.asarray(A_D, dtype=np.float64) * s, fmt).reshape(A_D.shape)
-    return np.asfortranarray(AL), s
+    A_D = np.asarray(A_D, dtype=np.float64)
+    if A_D.size <= (1 << 24):
+        AL = round_to(A_D * s, fmt).reshape(A_D.shape)
+        return np.asfortranarray(AL), s
+    # large inputs: the same elementwise rounding, 16 columns at a time (bounded temporaries)
+    AL = np.empty(A_D.shape, dtype=np.float64, order="F")
+    for c0 in range(0, A_D.shape[1], 16):
+        blk = A_D[:, c0:c0 + 16] * s
+        AL[:, c0:c0 + 16] = round_to(blk, fmt).reshape(blk.shape)
+    return AL, s
 
 
 def _work_dtype(fmt):
