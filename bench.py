@@ -38,36 +38,55 @@ def flops(m, n, k, mode="lsq"):
     return fq, fc, fe
 
 
-def pass_bytes(m, n, k, nb, s):
-    """Algorithmic bytes of the dominant kernel (k_pass) summed over the k launches:
-    read (m-j)(n-j) s per step, plus a write of the same on store steps (j % nb == 0, j > 0)."""
+def alg_qrcp_bytes(m, n, k, s):
+    """SURVEY §8(d) B_QRCP, the algorithmic bytes of the low-precision QRCP: one read of the
+    trailing matrix per step, s (m-j)(n-j), plus a write and a read of it at each panel end of
+    the survey's blocked algorithm (panel width min(k, 128): panel ends at j = 128, 256, ...
+    below k).  For C4 (k = 100) there is no panel end: 4.087e11 B."""
+    nb_s = min(k, 128)
+    tot = 0.0
+    for j in range(k):
+        e = (m - j) * (n - j) * s
+        tot += e * (3.0 if (j > 0 and j % nb_s == 0) else 1.0)
+    return tot
+
+
+def design_pass_bytes(m, n, k, nb, s, formation):
+    """Bytes the dominant kernel actually moves per ID with this design: every step reads the
+    trailing matrix, store steps (every nb) also write it back, and the tcgen05 pass reads the
+    panel's V operand (m rows x 16 pending per K chunk x 2 (hi, lo) x 2 B) once per step."""
     tot = 0.0
     for j in range(k):
         e = (m - j) * (n - j) * s
         tot += e * (2.0 if (j > 0 and j % nb == 0) else 1.0)
+        if formation == 2:
+            npend = j - (0 if j == 0 else nb * ((j - 1) // nb))
+            tot += (m - j) * 64.0 * ((npend + 15) // 16)
     return tot
 
 
-PEAK_FP64_TFLOPS = 37.1   # tools/dmma_probe.cu on the box (register-resident DMMA m8n8k4); not in MEASURED_PEAKS
+def load_fp64_peak():
+    p = os.path.join(ROOT, "profiles", "r02_fp64_peak.json")
+    d = json.load(open(p))
+    return float(d["used_as_peak"]), "profiles/r02_fp64_peak.json (tools/dmma_probe.cu on a B200: DMMA register-resident; cuBLAS DGEMM 35.5)"
 
 
-def full_id_roofline(m, n, k, nb, s, hbm_gbs, f_coef, f_err, small_ms, t_total_ms):
+def full_id_roofline(m, n, k, s, hbm_gbs, f_coef, f_err, small_ms, t_total_ms):
     """SURVEY §8(d) full-ID floor: round (8 + 8 + s B per element: max|a| pass + rounding)
-    and the QRCP pass bytes at the measured HBM bandwidth, the fp64 flops at the measured
-    DMMA peak (the error also bounded by one fp64 read of A_D), plus k times the measured
-    per-step cost of the small kernels (swap, reduce, reflector); fraction = floor / time."""
+    and the ALGORITHMIC QRCP bytes (B_QRCP) at the measured HBM bandwidth, the fp64 flops at
+    the measured DMMA peak (the error also bounded by one fp64 read of A_D), plus k times the
+    measured per-step cost of the small kernels; fraction = floor / time."""
     bw = hbm_gbs * 1e9
+    p64, src = load_fp64_peak()
     t_round = (8.0 + 8.0 + s) * m * n / bw
-    t_qrcp = pass_bytes(m, n, k, nb, s) / bw
-    p64 = PEAK_FP64_TFLOPS * 1e12
-    t_coef = f_coef / p64
-    t_err = max(f_err / p64, 8.0 * m * n / bw)
+    t_qrcp = alg_qrcp_bytes(m, n, k, s) / bw
+    t_coef = f_coef / (p64 * 1e12)
+    t_err = max(f_err / (p64 * 1e12), 8.0 * m * n / bw)
     t_roof = (t_round + t_qrcp + t_coef + t_err) * 1e3 + max(0.0, small_ms)
     return {"t_roof_ms": t_roof, "frac": t_roof / t_total_ms,
             "parts_ms": {"round": t_round * 1e3, "qrcp_pass": t_qrcp * 1e3, "coef": t_coef * 1e3,
                          "error": t_err * 1e3, "qrcp_small_kernels_measured": small_ms},
-            "peaks": {"hbm_gbs": hbm_gbs, "fp64_tflops": PEAK_FP64_TFLOPS,
-                      "fp64_source": "tools/dmma_probe.cu (register-resident DMMA) on a B200"}}
+            "peaks": {"hbm_gbs": hbm_gbs, "fp64_tflops": p64, "fp64_source": src}}
 
 
 def load_peaks():
@@ -125,23 +144,23 @@ class Clocks:
 
 
 def cpu_oracle_sample(rows, k, nb, fmt, seed=0, repeats=1):
-    """The oracle (as it stands) on a bounded row sample of the workload; returns (seconds, flops, cores)."""
+    """The oracle, as it stands, on a bounded row sample of the workload: the first `rows`
+    rows of C4, A_L by the oracle's rounding, the oracle's QRCP (oracle/cqrcp.c, the paper
+    model, OpenMP over all host cores), its Householder LSQ coefficients and its error.
+    Returns (seconds, flops, cores)."""
     import numpy as np
-    from oracle.id import coeffs_lsq, id_error
-    from oracle.qrcp import make_AL, qrcp_householder
+    from oracle.fast import qrcp_c
+    from oracle.id import coeffs_lsq, id_error_blocked
+    from oracle.qrcp import make_AL
     from synth import gen_config
     A = gen_config("C4", seed, row0=0, m_loc=rows)
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([t.get("num_threads", 1) for t in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count()
+    cores = os.cpu_count() or 1
     t0 = time.perf_counter()
     for _ in range(repeats):
         AL, s = make_AL(A, fmt, "pow2" if fmt == "fp16" else "none")
-        r = qrcp_householder(AL, k, fmt, nb=nb)
+        r = qrcp_c(AL, k, fmt, nb=nb, model="paper", threads=cores)
         P = coeffs_lsq(A, r.I)
-        id_error(A, r.I, P)
+        id_error_blocked(A, r.I, P)
     dt = (time.perf_counter() - t0) / repeats
     fq, fc, fe = flops(rows, A.shape[1], k)
     return dt, fq + fc + fe, cores
@@ -156,14 +175,15 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--fmt", default="fp16")
     ap.add_argument("--k", type=int, default=0)
-    ap.add_argument("--nb", type=int, default=4)
+    ap.add_argument("--nb", type=int, default=0, help="store interval; 0 = library default (tcgen05: 16, FFMA: 4)")
+    ap.add_argument("--formation", default="auto", help="auto | tc | ffma")
     ap.add_argument("--mode", default="lsq")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--rows", type=int, default=0, help="override rows per GPU (debug)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-rows", type=int, default=4096)
+    ap.add_argument("--cpu-rows", type=int, default=65536)
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -176,13 +196,14 @@ def main():
     rows = args.rows or spec.m
     scaling = spec.scaling[args.fmt]
 
+    nb_lib = args.nb or (16 if args.fmt == "fp16" and args.formation != "ffma" else 4)
     if args.impl == "reference":
         if rank != 0:
             return 0
         # the oracle, as it stands, on the host cores; each step one bounded sample
         wsteps = []
         for i in range(args.warmup + args.steps):
-            dt, fl, cores = cpu_oracle_sample(args.cpu_rows, k, args.nb, args.fmt, args.seed)
+            dt, fl, cores = cpu_oracle_sample(args.cpu_rows, k, nb_lib, args.fmt, args.seed)
             if i >= args.warmup:
                 wsteps.append(dt)
         T = sum(wsteps) / len(wsteps)
@@ -193,7 +214,8 @@ def main():
                 "vs_baseline": None, "dtype": "f32+f64 (simulated fp16)" if args.fmt == "fp16" else "f32+f64",
                 "data": "synthetic",
                 "config": {"workload": f"{args.config} row sample", "rows": args.cpu_rows, "n": spec.n,
-                           "k": k, "fmt": args.fmt, "nb": args.nb, "coef": args.mode},
+                           "k": k, "fmt": args.fmt, "nb": nb_lib, "coef": args.mode,
+                           "oracle": "oracle/cqrcp.c paper model + numpy fp64 LSQ / error"},
                 "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
                                  "sample": f"first {args.cpu_rows} rows of {args.config} ({args.cpu_rows}x{spec.n}, k={k})"},
                 "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -242,7 +264,7 @@ def main():
     s_bytes = 2 if args.fmt == "fp16" else 4
 
     def one_step(profile):
-        q = h.qrcp(args.fmt, scaling, k=k, nb=args.nb, profile=profile)
+        q = h.qrcp(args.fmt, scaling, k=k, nb=args.nb, profile=profile, formation=args.formation)
         P = h.coeffs(args.mode)
         e = h.error()
         return q, P, e
@@ -324,7 +346,7 @@ def main():
                 g0 = torch.cuda.Event(enable_timing=True)
                 g1 = torch.cuda.Event(enable_timing=True)
                 g0.record(stream)
-                qr = h.qrcp(args.fmt, scaling, k=k, nb=args.nb)
+                qr = h.qrcp(args.fmt, scaling, k=k, nb=args.nb, formation=args.formation)
                 h.coeffs("R")
                 er = h.error()
                 g1.record(stream)
@@ -338,18 +360,28 @@ def main():
         except Exception as ex:  # reported, never silently replaced
             variants["algorithm2_R_mode_coefficients"] = {"error": str(ex)}
         # the headline handle state (last QRCP) is restored for the checks below
-        q = h.qrcp(args.fmt, scaling, k=k, nb=args.nb)
+        q = h.qrcp(args.fmt, scaling, k=k, nb=args.nb, formation=args.formation)
 
-    # ---- roofline of the dominant kernel (k_pass), per launch -----------------
+    # ---- roofline of the dominant kernel (the panel pass), per launch ----------
+    # achieved = SURVEY §8(d)'s ALGORITHMIC bytes B_QRCP / the summed device time of the k
+    # pass launches (CUDA events on the library's stream around each launch); the bytes the
+    # design moves beyond B_QRCP (store-step write-backs every nb steps, the tcgen05 pass's V
+    # operand) are reported separately, as is the ncu-measured DRAM traffic per launch.
     peak, peak_kind, peaks = load_peaks()
-    pb = pass_bytes(m_loc, n, q.k, args.nb, s_bytes)
+    form = int(st0["formation"])
+    nb_used = int(st0["nb"])
+    alg = alg_qrcp_bytes(m_loc, n, q.k, s_bytes)
+    design = design_pass_bytes(m_loc, n, q.k, nb_used, s_bytes, form)
     pass_avg_ms = statistics.mean(pass_ms)
-    achieved = pb / (pass_avg_ms * 1e-3) / 1e9          # GB/s over the k launches of a step
-    traffic = None
+    achieved = alg / (pass_avg_ms * 1e-3) / 1e9          # GB/s of algorithmic bytes
+    traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", "pass_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("bytes_per_launch")
+            pt = json.load(open(prof))
+            ent = pt.get("kernels", {}).get("k_pass_tc" if form == 2 else "k_pass_ws")
+            if ent and ent.get("nb") == nb_used and ent.get("workload") == args.config:
+                traffic, traffic_src = ent["dram_bytes_per_launch"], ent["source"]
         except Exception:
             traffic = None
 
@@ -367,7 +399,7 @@ def main():
             t0 = time.perf_counter()
             hh = mpid.MPID(Ah, k_max=k, m_global=m_glob, row_offset=row0, comm=comm, rank=rank,
                            nranks=world, stream=stream, device=dev)
-            qq = hh.qrcp(args.fmt, scaling, k=k, nb=args.nb)
+            qq = hh.qrcp(args.fmt, scaling, k=k, nb=args.nb, formation=args.formation)
             PP = hh.coeffs(args.mode)
             P_host = PP.cpu()
             ee = hh.error()
@@ -387,7 +419,7 @@ def main():
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        dt_c, fl_c, cores = cpu_oracle_sample(args.cpu_rows, k, args.nb, args.fmt, args.seed)
+        dt_c, fl_c, cores = cpu_oracle_sample(args.cpu_rows, k, nb_used, args.fmt, args.seed)
         cpu = {"value": fl_c / dt_c / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
                "sample": f"first {args.cpu_rows} rows of {args.config} ({args.cpu_rows}x{n}, k={k}), one full ID",
                "seconds": dt_c}
@@ -401,8 +433,9 @@ def main():
             "dtype": "f16 storage / f32 arithmetic QRCP + f64 ID" if args.fmt == "fp16" else "f32 QRCP + f64 ID",
             "data": "synthetic",
             "config": {"workload": f"{args.config}: {m_glob}x{n} fp64 Fourier snapshots, k={k}, "
-                                   f"{args.fmt} QRCP (nb={args.nb}), {args.mode.upper()} coefficients",
-                       "rows_per_gpu": m_loc, "n": n, "k": k, "fmt": args.fmt, "nb": args.nb,
+                                   f"{args.fmt} QRCP ({'tcgen05' if form == 2 else 'FFMA'} pass, nb={nb_used}), "
+                                   f"{args.mode.upper()} coefficients",
+                       "rows_per_gpu": m_loc, "n": n, "k": k, "fmt": args.fmt, "nb": nb_used,
                        "coef": args.mode, "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (A_D 16 GiB, A_L 4 GiB per GPU); no flush"},
             "stages_ms": {"round": statistics.mean(round_ms), "qrcp": statistics.mean(qr_ms),
@@ -410,13 +443,19 @@ def main():
                           "pass_total": pass_avg_ms},
             "tflops_parts": {"qrcp": fq / (statistics.mean(qr_ms) * 1e-3) / 1e12,
                              "fp64": (fc + fe) / ((statistics.mean(coef_ms) + statistics.mean(err_ms)) * 1e-3) / 1e12},
-            "full_id_roofline": full_id_roofline(m_loc, n, q.k, args.nb, s_bytes, peak, fc, fe,
+            "full_id_roofline": full_id_roofline(m_loc, n, q.k, s_bytes, peak, fc, fe,
                                                  statistics.mean(qr_ms) - pass_avg_ms, ms_step),
             "k_out": q.k, "rel_err_fro": e[1], "errors_untimed": extra_err, "variants": variants,
-            "roofline": {"kernel": "k_pass (per-step panel pass)", "bound": "hbm", "achieved": achieved,
-                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "roofline": {"kernel": ("k_pass_tc (tcgen05 panel pass)" if form == 2 else "k_pass_ws (FFMA panel pass)"),
+                         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_kind": peak_kind, "launches_per_step": q.k,
-                         "algorithmic_bytes_per_step": pb},
+                         "algorithmic_bytes_per_step": alg, "algorithmic_bytes_per_launch": alg / q.k,
+                         "bytes_def": "SURVEY 8(d) B_QRCP: s * sum_j (m-j)(n-j) (+ 2 s (m-j)(n-j) per panel end of width min(k,128))",
+                         "design_bytes_per_step": design, "design_extra_bytes": design - alg,
+                         "design_over_algorithmic": design / alg,
+                         "traffic_over_algorithmic": (traffic * q.k / alg) if traffic else None,
+                         "formation": form, "nb": nb_used},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(st0["kernel_launches"]) * args.steps,

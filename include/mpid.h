@@ -131,8 +131,9 @@ typedef struct {
 } id_stats;
 
 /* Bytes of device workspace for a shard of m_local rows, n columns, rank <= k_max,
- * store interval nb (0 = default), storage format fmt.  host_AD != 0 reserves room
- * for a device copy of a host-resident A_D.  ID_FP16 and ID_FP32 share one layout;
+ * store interval nb (0 = default), storage format fmt.  host_AD = 1 reserves room
+ * for a device copy of a host-resident A_D, host_AD = 2 only the staging buffers of a
+ * host A_D streamed in row blocks (id_create_ex).  ID_FP16 and ID_FP32 share one layout;
  * ID_FP64 sizes the larger fp64 layout.  The handle carves its workspace for the
  * format of the current call (id_qrcp_lowprec / id_round_only); switching between a
  * low format and ID_FP64 re-carves it, which drops the cached CUDA graphs and the
@@ -158,6 +159,26 @@ id_status id_create(id_handle* h, const double* A_D, int64_t m_global, int64_t m
                     int64_t row_offset, int64_t n, int64_t ld, void* workspace,
                     size_t ws_bytes, void* nccl_comm, int32_t rank, int32_t nranks,
                     void* stream);
+
+/* id_create with flags.  ID_CREATE_STREAM_HOST: a host A_D is streamed in row blocks
+ * (SURVEY §8(b) ownership clause; needed when the shard does not fit the GPU, e.g. C5 at
+ * P <= 2) instead of being copied whole: the workspace is sized with host_AD = 2 in
+ * id_workspace_bytes (two staging blocks of <= 1 GiB instead of m_local x n doubles).  The
+ * rounding (a max |a| pass when scaling, then the rounding pass), the LSQ product
+ * W = Q1^T A_D(:, J) and the error read A_D block by block through two staging buffers,
+ * the copies (on an internal stream) overlapped with the kernels of the previous block;
+ * A_D(:, I) is copied column by column.  Pinned host memory is needed for the copies to
+ * overlap; A_D must stay valid and unchanged for the handle's life.  With a streamed A_D
+ * id_error_ex offers only (skeleton 0, norm 0), and the QRCP is not captured in a CUDA
+ * graph.  Without the flag a host A_D is copied whole when the workspace holds it
+ * (host_AD = 1 sizing) and streamed otherwise. */
+#define ID_CREATE_STREAM_HOST 1
+/* optional: stream blocks of 2^x rows (x >= 8; default ~1 GiB per block) */
+#define ID_CREATE_STREAM_ROWS_LOG2(x) ((x) << 8)
+id_status id_create_ex(id_handle* h, const double* A_D, int64_t m_global, int64_t m_local,
+                       int64_t row_offset, int64_t n, int64_t ld, void* workspace,
+                       size_t ws_bytes, void* nccl_comm, int32_t rank, int32_t nranks,
+                       void* stream, int32_t flags);
 
 /* Steps 1-2: scale, round, pivoted QR.  eps <= 0: fixed rank k_max; eps in (0,1):
  * stop at the first k with sqrt(sum_{unpivoted} ||r_i||^2) <= eps ||A_L||_F

@@ -1362,9 +1362,9 @@ cudaError_t launch_assemble_P(const double* T, int64_t ldt, int k, int n, const 
 
 cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, const int* cmap, const double* X,
                          int k, const double* T, int64_t ldt, double* part, int* nblk_out, cudaStream_t st,
-                         double* tpack, size_t tpack_cap) {
+                         double* tpack, size_t tpack_cap, int64_t ldx, int pack) {
   GemmArgs g{};
-  g.X = X; g.ldx = m;
+  g.X = X; g.ldx = ldx > 0 ? ldx : m;
   g.Y = T; g.ldy = ldt;
   g.M = m; g.N = ncols; g.K = k;
   g.out = part;
@@ -1383,8 +1383,9 @@ cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, cons
       ew_tpack_doubles(ncols, k) <= tpack_cap) {
     const int nks = ew_nks(k);
     const int64_t tot = (int64_t)ew_tpack_doubles(ncols, k);
-    k_pack_T<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 4 * sms), 256, 0, st>>>(T, ldt, k, ncols, nks, tpack,
-                                                                                    tot);
+    if (pack)
+      k_pack_T<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 4 * sms), 256, 0, st>>>(T, ldt, k, ncols, nks, tpack,
+                                                                                      tot);
     const size_t smem_ws = (size_t)(EW_S * (EW_ASZ + EW_BSZ) + GT * DLD) * sizeof(double);
     cudaError_t e = smem_attr((const void*)k_err_ws<false>, (int)smem_ws);
     if (e != cudaSuccess) return e;

@@ -205,6 +205,30 @@ __global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int
   if (threadIdx.x == 0 && shi) atomicOr(&sc->overflow, 1);
 }
 
+// acc[c] = (add ? acc[c] : 0) + sum_y part[y*stride + c] (fixed order; the host-streamed
+// round / W / error accumulate row blocks with it)
+__global__ void k_acc_rows(const double* __restrict__ part, int rows, int64_t stride, int64_t len,
+                           double* __restrict__ acc, int add) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= len) return;
+  double t = 0.0;
+  for (int y = 0; y < rows; ++y) t += part[(int64_t)y * stride + c];
+  acc[c] = add ? acc[c] + t : t;
+}
+__global__ void k_max_into(const double* __restrict__ part, int nblk, double* __restrict__ acc) {
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) mx = fmax(mx, part[i]);
+  __shared__ double sh[32];
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    v = warp_max(v);
+    if (threadIdx.x == 0) acc[0] = v;
+  }
+}
+
 // out[c] = sum_y part[y*stride + c] (fixed order: deterministic)
 __global__ void k_sum_rows(const double* __restrict__ part, int rows, int64_t stride, int64_t len,
                            double* __restrict__ out) {
@@ -226,6 +250,15 @@ __global__ void k_export(const T* __restrict__ S, int64_t m, int64_t n, T* __res
 }
 
 // ---------------------------------------------------------------------------
+cudaError_t launch_acc_rows(const double* part, int rows, int64_t stride, int64_t len, double* acc, int add,
+                            cudaStream_t st) {
+  k_acc_rows<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(part, rows, stride, len, acc, add);
+  return cudaGetLastError();
+}
+cudaError_t launch_max_into(const double* part, int nblk, double* acc, cudaStream_t st) {
+  k_max_into<<<1, 1024, 0, st>>>(part, nblk, acc);
+  return cudaGetLastError();
+}
 cudaError_t launch_maxabs(const double* A, int64_t m, int64_t n, int64_t ld, double* part,
                           int nblk, cudaStream_t st) {
   k_maxabs<<<nblk, 256, 0, st>>>(A, m, n, ld, part);

@@ -143,13 +143,25 @@ int splits_for(int64_t k1, int64_t n1, int64_t m, size_t cap) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(s, (int64_t)(cap / (size_t)(k1 * n1))));
 }
 
+// rows per host-streamed block of A_D (a multiple of the rounding kernel's 256-row tile)
+int64_t stream_rows(int64_t m_local, int64_t n) {
+  // two staging blocks of <= 1 GiB each
+  int64_t r = ((int64_t)1 << 27) / std::max<int64_t>(n, 1);
+  r = std::max<int64_t>(256, r / 256 * 256);
+  return std::min<int64_t>(r, m_pad_of(m_local));
+}
+
 // sbytes: 4 = room for fp16/fp32 storage with fp32 working vectors; 8 = also the fp64 QRCP
+// host_AD: 0 = A_D in device memory, 1 = a host A_D copied whole into the workspace,
+// 2 = a host A_D streamed in row blocks through two staging buffers (plus a k x n block of W)
 Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
   Layout L{};
   const int64_t mp = m_pad_of(m_local);
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
-  L.AD = take(host_AD ? (size_t)m_local * n * 8 : 0);
+  L.AD = take(host_AD == 1 ? (size_t)m_local * n * 8
+                            : host_AD == 2 ? (size_t)2 * stream_rows(m_local, n) * n * 8 + (size_t)k * n * 8 + 4096 * 8
+                                           : 0);
   L.S = take((size_t)mp * n * sbytes);
   L.U = take((size_t)NSLOT * mp * sbytes);
   L.F = take((size_t)NSLOT * n * sbytes);
@@ -204,7 +216,15 @@ struct mpid_ctx {
   size_t ws_bytes = 0;
   Layout L{};
   int64_t k_cap = 0;
-  bool host_AD = false;
+  int host_AD = 0;                // 0 device A_D, 1 host A_D copied whole, 2 host A_D streamed
+  const double* AD_host = nullptr; // mode 2: the caller's host A_D (ld_host)
+  int64_t ld_host = 0, srows = 0;
+  int srows_log2 = 0;              // mode 2: block rows 2^srows_log2 (0 = automatic, ~1 GiB blocks)
+  double* stage[2] = {nullptr, nullptr};
+  double* Wb = nullptr;            // mode 2: one row block's W partial sum
+  double* sacc = nullptr;          // mode 2: per-block scalars (max |a|, error^2)
+  cudaStream_t cps = nullptr;      // mode 2: copy stream
+  cudaEvent_t copied[2]{}, freed[2]{};
   int sbytes = 4;                 // workspace layout: 8 = sized for the fp64 QRCP too
   // device pointers (U, F, R in the working precision: fp32, fp64 for ID_FP64)
   void* S = nullptr;
@@ -303,8 +323,10 @@ static bool is_loop(void* c) {
 static id_status loop_allreduce(mpid_ctx* h, double* buf, size_t count, int op) {
   LoopComm* L = (LoopComm*)h->comm;
   std::vector<double> mine(count);
+  // copies on the handle's own stream, synchronised: a plain cudaMemcpy from pageable memory
+  // may return before its DMA lands, and the handle's stream need not sync with the legacy one
+  CK(cudaMemcpyAsync(mine.data(), buf, count * sizeof(double), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
-  CK(cudaMemcpy(mine.data(), buf, count * sizeof(double), cudaMemcpyDeviceToHost));
   std::vector<double> res;
   {
     std::unique_lock<std::mutex> lk(L->mu);
@@ -331,7 +353,8 @@ static id_status loop_allreduce(mpid_ctx* h, double* buf, size_t count, int op) 
     res = L->result;
   }
   if (res.size() != count) return fail(h, ID_ERR_NCCL, "loopback allreduce: size mismatch");
-  CK(cudaMemcpy(buf, res.data(), count * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpyAsync(buf, res.data(), count * sizeof(double), cudaMemcpyHostToDevice, h->st));
+  CK(cudaStreamSynchronize(h->st));   // `res` goes out of scope
   return ID_OK;
 }
 
@@ -381,6 +404,14 @@ static id_status relayout(mpid_ctx* h, int sbytes) {
   h->L = layout(m_local, n, kmax, h->host_AD, sbytes);
   const Layout& L = h->L;
   char* w = h->ws;
+  if (h->host_AD == 2) {
+    h->srows = stream_rows(m_local, n);
+    if (h->srows_log2 >= 8) h->srows = std::min<int64_t>(h->srows, (int64_t)1 << h->srows_log2);
+    h->stage[0] = (double*)(w + L.AD);
+    h->stage[1] = h->stage[0] + (size_t)h->srows * n;
+    h->Wb = h->stage[1] + (size_t)h->srows * n;
+    h->sacc = h->Wb + (size_t)kmax * n;
+  }
   h->S = w + L.S;
   h->U = w + L.U;
   h->F = w + L.F;
@@ -449,6 +480,13 @@ size_t id_workspace_bytes(int64_t m_local, int64_t n, int32_t k_max, int32_t nb,
 id_status id_create(id_handle* hp, const double* A_D, int64_t m_global, int64_t m_local,
                     int64_t row_offset, int64_t n, int64_t ld, void* workspace, size_t ws_bytes,
                     void* nccl_comm, int32_t rank, int32_t nranks, void* stream) {
+  return id_create_ex(hp, A_D, m_global, m_local, row_offset, n, ld, workspace, ws_bytes, nccl_comm, rank, nranks,
+                      stream, 0);
+}
+
+id_status id_create_ex(id_handle* hp, const double* A_D, int64_t m_global, int64_t m_local,
+                       int64_t row_offset, int64_t n, int64_t ld, void* workspace, size_t ws_bytes,
+                       void* nccl_comm, int32_t rank, int32_t nranks, void* stream, int32_t flags) {
   if (!hp || !A_D || !workspace) return ID_ERR_ARG;
   *hp = nullptr;
   if (m_local <= 0 || n <= 0 || ld < m_local || m_global < m_local || row_offset < 0 ||
@@ -478,7 +516,11 @@ id_status id_create(id_handle* hp, const double* A_D, int64_t m_global, int64_t 
   cudaPointerAttributes pa{};
   cudaError_t pe = cudaPointerGetAttributes(&pa, A_D);
   if (pe != cudaSuccess) cudaGetLastError();
-  h->host_AD = (pe != cudaSuccess) || pa.type == cudaMemoryTypeHost || pa.type == cudaMemoryTypeUnregistered;
+  const bool host = (pe != cudaSuccess) || pa.type == cudaMemoryTypeHost || pa.type == cudaMemoryTypeUnregistered;
+  // a host A_D is copied whole when the workspace holds it (host_AD = 1 sizing), else it is
+  // streamed in row blocks (host_AD = 2 sizing)
+  h->host_AD = host ? (((flags & ID_CREATE_STREAM_HOST) || layout(m_local, n, 1, 1, 4).total > ws_bytes) ? 2 : 1) : 0;
+  h->srows_log2 = (flags >> 8) & 0xFF;
   if (relayout(h, 4) != ID_OK) {
     delete h;
     return ID_ERR_DIM;
@@ -492,7 +534,19 @@ id_status id_create(id_handle* hp, const double* A_D, int64_t m_global, int64_t 
     delete h;
     return ID_ERR_CUDA;
   }
-  if (h->host_AD) {
+  if (h->host_AD == 2) {
+    h->AD_host = A_D;
+    h->ld_host = ld;
+    h->AD = nullptr;
+    h->ld = m_local;
+    if (cudaStreamCreateWithFlags(&h->cps, cudaStreamNonBlocking) != cudaSuccess) { delete h; return ID_ERR_CUDA; }
+    for (int b = 0; b < 2; ++b)
+      if (cudaEventCreateWithFlags(&h->copied[b], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->freed[b], cudaEventDisableTiming) != cudaSuccess) {
+        delete h;
+        return ID_ERR_CUDA;
+      }
+  } else if (h->host_AD == 1) {
     double* dst = (double*)(h->ws + h->L.AD);
     cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)m_local * 8, A_D, (size_t)ld * 8, (size_t)m_local * 8,
                                       (size_t)n, cudaMemcpyHostToDevice, h->st);
@@ -519,6 +573,11 @@ void id_destroy(id_handle h) {
   if (h->fork_ev) cudaEventDestroy(h->fork_ev);
   if (h->join_ev) cudaEventDestroy(h->join_ev);
   if (h->cap) cudaStreamDestroy(h->cap);
+  if (h->cps) cudaStreamDestroy(h->cps);
+  for (int b = 0; b < 2; ++b) {
+    if (h->copied[b]) cudaEventDestroy(h->copied[b]);
+    if (h->freed[b]) cudaEventDestroy(h->freed[b]);
+  }
   delete h;
 }
 
@@ -581,8 +640,86 @@ __global__ void k_set_max(double* buf, const DevScalars* sc) { buf[0] = sc->maxa
 __global__ void k_get_max(const double* buf, DevScalars* sc) { sc->maxabs = buf[0]; }
 
 
+// Host-streamed A_D (host_AD = 2): row blocks of srows rows are copied into two staging
+// buffers on the copy stream, double-buffered against the kernels on h->st that consume
+// them; fn(b, r0, rows, stage) enqueues block b's kernels.  Blocks run in row order, so
+// every accumulation over blocks is in a fixed order.
+template <typename Fn>
+static id_status stream_blocks(mpid_ctx* h, Fn&& fn) {
+  const int64_t m = h->m_local, n = h->n, R = h->srows;
+  const int64_t nblk = (m + R - 1) / R;
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int buf = (int)(b & 1);
+    const int64_t r0 = b * R, rows = std::min<int64_t>(R, m - r0);
+    // the staging buffer's previous users: block b - 2's kernels, or (first two blocks)
+    // everything enqueued on h->st so far
+    if (b < 2) CK(cudaEventRecord(h->freed[buf], h->st));
+    CK(cudaStreamWaitEvent(h->cps, h->freed[buf], 0));
+    CK(cudaMemcpy2DAsync(h->stage[buf], (size_t)R * 8, h->AD_host + r0, (size_t)h->ld_host * 8, (size_t)rows * 8,
+                         (size_t)n, cudaMemcpyHostToDevice, h->cps));
+    CK(cudaEventRecord(h->copied[buf], h->cps));
+    CK(cudaStreamWaitEvent(h->st, h->copied[buf], 0));
+    id_status s = fn(b, r0, rows, h->stage[buf]);
+    if (s) return s;
+    CK(cudaEventRecord(h->freed[buf], h->st));
+  }
+  return ID_OK;
+}
+
+__global__ void k_reset_scalars(DevScalars* sc, double eps);
+__global__ void k_finish_round(const double* __restrict__ nb, int n, DevScalars* sc);
+__global__ void k_set_max(double* buf, const DevScalars* sc);
+__global__ void k_get_max(const double* buf, DevScalars* sc);
+__global__ void k_overflow_into(const DevScalars* sc, double* dst) { dst[0] = sc->overflow ? 1.0 : 0.0; }
+
+// the round of a host-streamed A_D: (scaling) a max |a| pass over the blocks, then the
+// rounding pass, A_L written block by block into S; column norms and ||A_D||_F^2
+// accumulated over the blocks in row order (eager: not captured in the QRCP graph)
+static id_status enqueue_round_streamed(mpid_ctx* h, int fmt, int scaling, double eps) {
+  const int64_t n = h->n, R = h->srows;
+  const int64_t nblk = (h->m_local + R - 1) / R;
+  if (nblk > 4000) return fail(h, ID_ERR_DIM, "host-streamed A_D: too many row blocks (%lld)", (long long)nblk);
+  k_reset_scalars<<<1, 1, 0, h->st>>>(h->sc, eps);
+  id_status s;
+  if (scaling != ID_SCALE_NONE) {
+    s = stream_blocks(h, [&](int64_t b, int64_t, int64_t rows, const double* blk) -> id_status {
+      const int nb = (int)std::min<int64_t>(1024, std::max<int64_t>(1, (rows * n + 255) / 256));
+      CK(launch_maxabs(blk, rows, n, R, h->maxpart, nb, h->st));
+      CK(launch_max_into(h->maxpart, nb, h->sacc + b, h->st));
+      return ID_OK;
+    });
+    if (s) return s;
+    CK(launch_maxabs_finish(h->sacc, (int)nblk, h->sc, scaling, h->st));
+    if (h->nranks > 1 || h->comm) {
+      k_set_max<<<1, 1, 0, h->st>>>(h->maxpart, h->sc);
+      s = allreduce(h, h->maxpart, 1, NCCL_MAX);
+      if (s) return s;
+      k_get_max<<<1, 1, 0, h->st>>>(h->maxpart, h->sc);
+    }
+  }
+  CK(launch_scale_from_max(h->sc, scaling, h->st));
+  const int gy = round_gy(R, n);
+  const int naux = gy * (int)((n + 31) / 32);
+  s = stream_blocks(h, [&](int64_t b, int64_t r0, int64_t rows, const double* blk) -> id_status {
+    // rows up to the next 256-row tile of this block (the last block also covers m_pad's padding)
+    const int64_t rpad = std::min<int64_t>(R, h->m_pad - r0);
+    void* Sb = (char*)h->S + (size_t)(r0 / 8) * n * 8 * (fmt == ID_FP16 ? 2 : fmt == ID_FP32 ? 4 : 8);
+    CK(launch_round(fmt, blk, rows, rpad, n, R, Sb, h->rpart, gy, h->sc, h->st));
+    CK(launch_acc_rows(h->rpart, gy, n, n, h->norms, b > 0 ? 1 : 0, h->st));                   // column norms
+    CK(launch_acc_rows(h->rpart + (int64_t)gy * n, naux, 1, 1, h->norms + n, b > 0 ? 1 : 0, h->st));  // ||A_D||^2
+    return ID_OK;
+  });
+  if (s) return s;
+  k_overflow_into<<<1, 1, 0, h->st>>>(h->sc, h->norms + n + 1);
+  s = allreduce(h, h->norms, (size_t)n + 2, NCCL_SUM);
+  if (s) return s;
+  k_finish_round<<<1, 1024, 0, h->st>>>(h->norms, (int)n, h->sc);
+  return ID_OK;
+}
+
 // enqueue scale + round + initial norms (+ collectives)
 static id_status enqueue_round(mpid_ctx* h, int fmt, int scaling, double eps) {
+  if (h->host_AD == 2) return enqueue_round_streamed(h, fmt, scaling, eps);
   const int64_t m = h->m_local, n = h->n;
   k_reset_scalars<<<1, 1, 0, h->st>>>(h->sc, eps);
   h->kernel_launches += 1;
@@ -774,7 +911,9 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   int nb = opts && opts->nb > 0 ? opts->nb : (formation == 2 ? 16 : 4);
   if (nb > NB_MAX || (formation == 1 && nb > 16) || (fmt == ID_FP64 && nb > 8))
     return fail(h, ID_ERR_ARG, "nb=%d too large for formation %d / format %d", nb, formation, (int)fmt);
-  const bool use_graph = !(opts && opts->use_graph < 0) && !h->loop;
+  // no graph capture for a loopback group (host-side reductions) or a host-streamed A_D
+  // (its copies may come from pageable memory)
+  const bool use_graph = !(opts && opts->use_graph < 0) && !h->loop && h->host_AD != 2;
   const bool profile = opts && opts->profile_pass;
   h->have_qr = h->have_coef = h->have_gram = h->have_sketch = false;
   if (profile && (int)h->pass_ev.size() < 2 * k_max) {
@@ -885,8 +1024,14 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
   if ((size_t)k * 33 * 8 > 200 * 1024) return fail(h, ID_ERR_DIM, "k=%d too large for the P solve", k);
   CK(cudaEventRecord(h->ev[3], h->st));
   int launches = 0;
-  CK(launch_gather_cols(h->AD, m, h->ld, h->perm, k, h->AI, h->st));
-  launches++;
+  if (h->host_AD == 2) {   // A_I = A_D(:, I) straight from the host columns
+    for (int i = 0; i < k; ++i)
+      CK(cudaMemcpyAsync(h->AI + (size_t)i * m, h->AD_host + (size_t)h->perm_host[i] * h->ld_host, (size_t)m * 8,
+                         cudaMemcpyHostToDevice, h->st));
+  } else {
+    CK(launch_gather_cols(h->AD, m, h->ld, h->perm, k, h->AI, h->st));
+    launches++;
+  }
   if (mode == ID_COEF_R) {
     h->stats.lsq_path = 0;
     CK(launch_R_to_fp64(h->fmt == ID_FP64, h->R, k, n, h->Rd, h->st));
@@ -934,9 +1079,19 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
       // W = Q1^T A_D(:, J), J = perm[k:] (W(:, I) is never needed)
       const int nj = n - k;
       if (nj > 0) {
-        const int spw = splits_for(k, nj, m, tcap);
-        CK(launch_tsmm(h->Q1, m, k, h->AD, h->ld, nj, m, h->tpart, spw, h->st, h->perm + k));
-        CK(launch_sum_partials(h->tpart, spw, (int64_t)k * nj, h->W, h->st));
+        if (h->host_AD == 2) {   // W = sum over row blocks of Q1(blk)^T A_D(blk, J)
+          const int spw = splits_for(k, nj, h->srows, tcap);
+          id_status ss = stream_blocks(h, [&](int64_t b, int64_t r0, int64_t rows, const double* blk) -> id_status {
+            CK(launch_tsmm(h->Q1 + r0, m, k, blk, h->srows, nj, rows, h->tpart, spw, h->st, h->perm + k));
+            CK(launch_acc_rows(h->tpart, spw, (int64_t)k * nj, (int64_t)k * nj, h->W, b > 0 ? 1 : 0, h->st));
+            return ID_OK;
+          });
+          if (ss) return ss;
+        } else {
+          const int spw = splits_for(k, nj, m, tcap);
+          CK(launch_tsmm(h->Q1, m, k, h->AD, h->ld, nj, m, h->tpart, spw, h->st, h->perm + k));
+          CK(launch_sum_partials(h->tpart, spw, (int64_t)k * nj, h->W, h->st));
+        }
         s = allreduce(h, h->W, (size_t)k * nj, NCCL_SUM);
         if (s) return s;
         CK(launch_trsm_left_upper(R1, h->G2, k, h->W, k, nullptr, nj, h->T, k, 1, h->st));
@@ -988,7 +1143,15 @@ id_status id_error(id_handle h, double* abs_fro, double* rel_fro) {
   int nblk = 0;
   // skeleton columns contribute exactly 0 (P(:, I) = I_k): sum over J = perm[k:] only
   const int nj = (int)h->n - k;
-  if (nj > 0) {
+  if (nj > 0 && h->host_AD == 2) {   // sum over row blocks, in row order
+    id_status ss = stream_blocks(h, [&](int64_t b, int64_t r0, int64_t rows, const double* blk) -> id_status {
+      CK(launch_error(blk, rows, h->srows, nj, h->perm + k, h->AI + r0, k, h->T, k, h->epart, &nblk, h->st, h->Tp,
+                      ew_tpack_doubles(h->n, h->k_cap), h->m_local, b == 0 ? 1 : 0));
+      CK(launch_acc_rows(h->epart, nblk, 1, 1, h->err2, b > 0 ? 1 : 0, h->st));
+      return ID_OK;
+    });
+    if (ss) return ss;
+  } else if (nj > 0) {
     CK(launch_error(h->AD, h->m_local, h->ld, nj, h->perm + k, h->AI, k, h->T, k, h->epart, &nblk, h->st, h->Tp,
                           ew_tpack_doubles(h->n, h->k_cap)));
     CK(launch_sum_scalar(h->epart, nblk, h->err2, h->st));
@@ -1059,6 +1222,8 @@ id_status id_error_ex(id_handle h, int32_t skeleton, int32_t norm, int32_t iters
   if (norm != 0 && norm != 2) return fail(h, ID_ERR_ARG, "norm must be 0 (Frobenius) or 2 (spectral)");
   if (iters < 0 || iters > 256) return fail(h, ID_ERR_ARG, "iters must be in [0, 256]");
   if (iters == 0) iters = 40;
+  if (h->host_AD == 2 && (skeleton != 0 || norm != 0))
+    return fail(h, ID_ERR_STATE, "id_error_ex: the low-precision skeleton and the 2-norm need a device-resident A_D");
   const int k = h->k_out;
   const int n = (int)h->n;
   const double* X = h->AI;                                     // A_D(:, I)

@@ -189,15 +189,21 @@ cudaError_t launch_R_export(int r64, const void* R, int k, int n, void* out, int
 cudaError_t launch_assemble_P(const double* T, int64_t ldt, int k, int n, const int* perm, double* P,
                               int64_t ldp, cudaStream_t st);
 // error over the columns J: sum_{r, c} (A(r, cmap[c]) - sum_l X(r, l) T(l, c))^2, c < ncols
+// X has leading dimension ldx (<= 0: m); pack = 0 reuses the T slabs packed by an earlier call
 cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, const int* cmap, const double* X,
                          int k, const double* T, int64_t ldt, double* part, int* nblk_out, cudaStream_t st,
-                         double* tpack = nullptr, size_t tpack_cap = 0);
+                         double* tpack = nullptr, size_t tpack_cap = 0, int64_t ldx = -1, int pack = 1);
 size_t ew_tpack_doubles(int64_t n, int64_t k);   // packed T slabs of the warp-specialised error kernel
 // out(m x N) = X(m x K) B(K x N), all col-major
 cudaError_t launch_nn_store(const double* X, int64_t m, int64_t ldx, const double* B, int64_t ldb, int K,
                             int N, double* out, int64_t ldo, cudaStream_t st, double* tpack = nullptr,
                             size_t tpack_cap = 0);
 cudaError_t launch_eye(double* I, int k, cudaStream_t st);
+// host-streamed A_D (mpid_api.cu): acc[i] (+)= sum_y part[y * stride + i] for i < len, fixed order
+cudaError_t launch_acc_rows(const double* part, int rows, int64_t stride, int64_t len, double* acc, int add,
+                            cudaStream_t st);
+// acc[slot] = max(part[0:nblk])
+cudaError_t launch_max_into(const double* part, int nblk, double* acc, cudaStream_t st);
 // NEXT-1 / NEXT-2 (k_norm2.cu): the low-precision skeleton and the 2-norm by power iteration
 cudaError_t launch_gather_lowp(const double* A, int64_t m, int64_t ld, const int* perm, int k, int fmt,
                                const DevScalars* sc, double* X, cudaStream_t st);

@@ -30,7 +30,7 @@ SCALING = {"none": ID_SCALE_NONE, "maxabs": ID_SCALE_MAXABS, "pow2": ID_SCALE_PO
 COEF = {"R": ID_COEF_R, "r": ID_COEF_R, "lsq": ID_COEF_LSQ, "LSQ": ID_COEF_LSQ}
 
 # every function declared in include/mpid.h
-EXPORTS = ["id_workspace_bytes", "id_create", "id_qrcp_lowprec", "id_coeffs_fp64", "id_error", "id_error_ex",
+EXPORTS = ["id_workspace_bytes", "id_create", "id_create_ex", "id_qrcp_lowprec", "id_coeffs_fp64", "id_error", "id_error_ex",
            "id_get_R", "id_get_R_fp64", "id_get_gram", "id_get_sketch", "id_get_perm", "id_get_AL", "id_round_only", "id_get_stats", "id_last_error", "id_destroy",
            "id_nccl_unique_id_bytes", "id_nccl_get_unique_id", "id_nccl_comm_init",
            "id_nccl_comm_destroy", "id_loopback_create", "id_loopback_calls", "id_loopback_destroy", "id_version"]
@@ -79,6 +79,8 @@ def lib():
     L.id_workspace_bytes.argtypes = [i64, i64, i32, i32, C.c_int, i32]
     L.id_create.restype = C.c_int
     L.id_create.argtypes = [C.POINTER(vp), vp, i64, i64, i64, i64, i64, vp, C.c_size_t, vp, i32, i32, vp]
+    L.id_create_ex.restype = C.c_int
+    L.id_create_ex.argtypes = [C.POINTER(vp), vp, i64, i64, i64, i64, i64, vp, C.c_size_t, vp, i32, i32, vp, i32]
     L.id_qrcp_lowprec.restype = C.c_int
     L.id_qrcp_lowprec.argtypes = [vp, C.c_int, C.c_int, i32, dbl, C.POINTER(QRCPOpts),
                                   C.POINTER(i32), C.POINTER(i32)]
@@ -136,11 +138,11 @@ def id_workspace_bytes(m_local, n, k_max, nb=0, fmt=ID_FP16, host_AD=0) -> int:
 
 
 def id_create(A_ptr, m_global, m_local, row_offset, n, ld, ws_ptr, ws_bytes, comm=None, rank=0,
-              nranks=1, stream=None):
+              nranks=1, stream=None, flags=0):
     h = C.c_void_p()
-    rc = lib().id_create(C.byref(h), C.c_void_p(A_ptr), m_global, m_local, row_offset, n, ld,
-                         C.c_void_p(ws_ptr), ws_bytes, C.c_void_p(comm) if comm else None, rank,
-                         nranks, C.c_void_p(stream) if stream else None)
+    rc = lib().id_create_ex(C.byref(h), C.c_void_p(A_ptr), m_global, m_local, row_offset, n, ld,
+                            C.c_void_p(ws_ptr), ws_bytes, C.c_void_p(comm) if comm else None, rank,
+                            nranks, C.c_void_p(stream) if stream else None, flags)
     return rc, h
 
 
@@ -228,8 +230,10 @@ class MPID:
 
     def __init__(self, A_D, k_max: int, m_global: int | None = None, row_offset: int = 0,
                  comm: int | None = None, rank: int = 0, nranks: int = 1, stream=None,
-                 device=None, fp64: bool = False):
-        """fp64=True sizes the workspace for the double ID too (fmt "fp64")."""
+                 device=None, fp64: bool = False, stream_host: bool = False, stream_rows_log2: int = 0):
+        """fp64=True sizes the workspace for the double ID too (fmt "fp64"); stream_host=True
+        streams a host A_D in row blocks (id_create_ex ID_CREATE_STREAM_HOST) instead of
+        copying it whole."""
         import torch
         assert A_D.dtype == torch.float64 and A_D.dim() == 2 and A_D.is_contiguous()
         n, m_local = A_D.shape
@@ -239,7 +243,7 @@ class MPID:
         self.device = torch.device(device) if device is not None else (
             A_D.device if A_D.is_cuda else torch.device("cuda", torch.cuda.current_device()))
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-        host = 0 if A_D.is_cuda else 1
+        host = 0 if A_D.is_cuda else (2 if stream_host else 1)
         self.ws_bytes = id_workspace_bytes(self.m_local, self.n, self.k_max, 0, ID_FP64 if fp64 else ID_FP32,
                                            host)
         self.ws = torch.empty(self.ws_bytes + 256, dtype=torch.uint8, device=self.device)
@@ -247,7 +251,8 @@ class MPID:
         self.ws_ptr = (base + 255) // 256 * 256
         self.A_D = A_D
         rc, h = id_create(A_D.data_ptr(), self.m_global, self.m_local, row_offset, self.n, self.m_local,
-                          self.ws_ptr, self.ws_bytes, comm, rank, nranks, self.stream.cuda_stream)
+                          self.ws_ptr, self.ws_bytes, comm, rank, nranks, self.stream.cuda_stream,
+                          flags=(1 | (stream_rows_log2 << 8)) if (host == 2) else 0)
         if rc:
             raise IDError(rc, "id_create failed")
         self.h = h

@@ -107,13 +107,18 @@ def _compare(A, fmt, scaling, k, nb, min_prefix_frac=0.0, eps=0.0, key=None, for
          else qrcp_householder(AL, k, fmt, nb=nb, eps=eps, formation=oform))
     rp = qrcp_c(AL, k, fmt, nb=nb, eps=eps, model="paper")
     assert out["piv"][0] == int(np.argmax(np.linalg.norm(AL, axis=0)))
-    for ref in (r, rp):
+    for ref, own in ((r, True), (rp, False)):
         agree, first_unc = prefix_match(out["piv"], ref, c_tie=C_TIE)
         assert agree >= first_unc, (agree, first_unc, out["piv"][:10], ref.perm[:10])
-        # error parity (same fmt, nb, LSQ mode): GPU error vs oracle pipeline error
+        # error parity (same fmt, nb, LSQ mode): GPU error vs oracle pipeline error — within
+        # 5 % of the formation's own model always; of the paper model when the comparison
+        # covers every pivot (with a store after every step, nb = 1, two faithful fp16
+        # models part at the uncertified steps and their errors differ by up to ~15 %,
+        # SURVEY App. A)
         err_or = id_error(A, ref.I, coeffs_lsq(A, ref.I))[1]
         err_gpu = out["err"][1]
-        assert abs(err_gpu - err_or) <= 0.05 * err_or, (err_gpu, err_or)
+        tol = 0.05 if (own or first_unc >= k or nb > 1) else 0.20
+        assert abs(err_gpu - err_or) <= tol * err_or, (err_gpu, err_or, own)
     agree, first_unc = prefix_match(out["piv"], r, c_tie=C_TIE)
     # P parity given the same I: oracle LSQ from the GPU's I
     I = out["piv"]
