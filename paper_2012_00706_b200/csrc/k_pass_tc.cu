@@ -15,9 +15,11 @@
 //   with V, F the pending fp32 vectors split into fp16 hi / lo pairs (|rel. error| of the
 //   product <= ~2^-21, R14), so the epilogue reads X directly (no conversion, no
 //   subtraction on the CUDA cores);
-//   u = X(:, j) (the pivot column), w = X^T u and s_i = ||X(j:m, i)||^2 (16-row fp32 FFMA2
-//   chains added into fp64), the row x = X(j, :); on store steps (panel end, every nb
-//   steps) fl16(X) is written back to S (the storage rounding point).
+//   u = X(:, j) (the pivot column), w = X^T u and s_i = ||X(j:m, i)||^2 (8-row fp32 FFMA2
+//   chains, folded per unit and added into fp64), the row x = X(j, :); on store steps (panel
+//   end, every nb steps) fl16(X) is written back to S (the storage rounding point).
+//   V holds the pending u_l (rows < l zero) and F the pending c_l f_l, so V F^T =
+//   sum_l v_l f_l^T with v_l = c_l u_l (Householder vector, v_l(l) = 1 in exact arithmetic).
 //
 // B200 structure: one persistent CTA per SM, 18 warps, warp-specialised.  A CTA owns a
 // contiguous range of 128-row blocks and walks, per row block, all column tiles of 128
@@ -167,7 +169,8 @@ struct TcParams {
   int64_t rb_first;    // first 128-row block holding rows >= j (local)
   int64_t nrb;         // row blocks from rb_first to the end
   int n, j, j0, npend, store, kchw, nst, ntiles;
-  const unsigned char* Vop;   // [m_pad / 128][kchw][hi 4 KB | lo 4 KB]
+  unsigned char* Vop;         // [m_pad / 128][kchw][hi 4 KB | lo 4 KB]
+  int lnext;                  // V operand column of u_j for the next step (j mod nb)
   const unsigned char* Fop;   // [ntiles][kchw][hi 4 KB | lo 4 KB]
   float* U;                   // [NSLOT][m_pad] u vectors (fp32)
   double* part;               // [gridDim.x][2][n]
@@ -361,7 +364,6 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
     // pending reflector), masked to rows >= j, rounded to the storage format on store
     // steps; published to shared memory (the epilogue's w = X^T u) and to U (the next
     // steps' V operand).
-    float* Uj = p.U + (int64_t)(j % NSLOT) * p.m_pad;
     const uint32_t fbytes = (uint32_t)(kch * 2 * CH_BYTES);
     auto issue_v = [&](int rbi) {
       const int vb = rbi & 1;
@@ -408,13 +410,21 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
         }
       }
       float* uu = ubuf + ub * R_B;
+      // u_j also becomes column lnext of the V operand the next steps read (the Householder
+      // vector v_j = c_j u_j, with c_j folded into the F operand by k_reflector): fp16 hi / lo
+      unsigned char* vg = p.Vop + (size_t)(p.rb_first + rb0 + rbi) * kchw * 2 * CH_BYTES +
+                          (size_t)(p.lnext >> 4) * 2 * CH_BYTES;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int64_t rl = r0 + lane * 4 + i;
         float v = p.store ? __half2float(__float2half_rn(x[i])) : x[i];
         if (rl < jl) v = 0.f;
         uu[lane * 4 + i] = v;
-        if (rl < p.m_pad) Uj[rl] = v;
+        __half hi, lo;
+        split_f16(v, hi, lo);
+        const int o = op_off(lane * 4 + i, p.lnext & 15);
+        *reinterpret_cast<__half*>(vg + o) = hi;
+        *reinterpret_cast<__half*>(vg + CH_BYTES + o) = lo;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&ufull[ub]);
@@ -538,70 +548,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
 }
 
 // ---------------------------------------------------------------------------
-// k_tc_ops: the step's operands for k_pass_tc.
-//   blocks [0, nvb): column l = t - j0 of the panel's V operand, v_t = fl32(u_t c_t)
-//     (v_t(t) = 1, zero above row t and on padding rows), split into fp16 hi / lo;
-//   blocks [nvb, ...): the F operand of every column tile for this step's column order,
-//     -F(j0 + l)(j + c) split into fp16 hi / lo (zero for l >= npend or columns >= n).
-__global__ void k_tc_ops(const float* __restrict__ U, int64_t m_pad, int64_t m_local, int64_t row_offset, int t,
-                         int lnew, const double* __restrict__ cvec, unsigned char* __restrict__ Vop, int nvb,
-                         const float* __restrict__ F, int n, int j, int j0, int npend, int ntiles, int kchw,
-                         unsigned char* __restrict__ Fop, const DevScalars* __restrict__ sc) {
-  if (sc->done) return;
-  if ((int)blockIdx.x < nvb) {
-    if (lnew < 0) return;
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= m_pad) return;
-    const int64_t rg = row_offset + r;
-    float v = 0.f;
-    if (r < m_local) {
-      if (rg == t) v = 1.f;
-      else if (rg > t) v = __double2float_rn((double)U[(int64_t)(t % NSLOT) * m_pad + r] * cvec[t]);
-    }
-    __half hi, lo;
-    split_f16(v, hi, lo);
-    const int64_t rb = r >> 7;
-    unsigned char* base = Vop + (size_t)rb * kchw * 2 * CH_BYTES + (size_t)(lnew >> 4) * 2 * CH_BYTES;
-    const int o = op_off((int)(r & 127), lnew & 15);
-    *reinterpret_cast<__half*>(base + o) = hi;
-    *reinterpret_cast<__half*>(base + CH_BYTES + o) = lo;
-    return;
-  }
-  const int64_t e = (int64_t)(blockIdx.x - nvb) * blockDim.x + threadIdx.x;   // (tile, column, l)
-  const int KW = kchw * 16;
-  if (e >= (int64_t)ntiles * C_T * KW) return;
-  const int l = (int)(e % KW);
-  const int64_t tc = e / KW;
-  const int c = (int)(tc % C_T), tt = (int)(tc / C_T);
-  const int col = j + tt * C_T + c;
-  float f = 0.f;
-  if (l < npend && col < n) f = -F[(int64_t)((j0 + l) % NSLOT) * n + col];
-  __half hi, lo;
-  split_f16(f, hi, lo);
-  unsigned char* base = Fop + ((size_t)tt * kchw + (l >> 4)) * 2 * CH_BYTES;
-  const int o = op_off(c, l & 15);
-  *reinterpret_cast<__half*>(base + o) = hi;
-  *reinterpret_cast<__half*>(base + CH_BYTES + o) = lo;
-}
-
-// ---------------------------------------------------------------------------
 int tc_kchw(int nb) { return (nb + 15) / 16; }
 
 size_t tc_vop_bytes(int64_t m_pad, int nb) { return (size_t)(m_pad / 128 + 1) * tc_kchw(nb) * 2 * CH_BYTES; }
 size_t tc_fop_bytes(int n, int nb) { return (size_t)((n + C_T - 1) / C_T) * tc_kchw(nb) * 2 * CH_BYTES; }
-
-cudaError_t launch_tc_ops(const float* U, int64_t m_pad, int64_t m_local, int64_t row_offset, int t, int lnew,
-                          const double* cvec, void* Vop, const float* F, int n, int j, int j0, int npend, int nb,
-                          void* Fop, const DevScalars* sc, cudaStream_t st) {
-  const int kchw = tc_kchw(nb);
-  const int ntiles = (n - j + C_T - 1) / C_T;
-  const int nvb = lnew >= 0 ? (int)((m_pad + 255) / 256) : 0;
-  const int64_t fe = (int64_t)ntiles * C_T * kchw * 16;
-  const int nfb = (int)((fe + 255) / 256);
-  k_tc_ops<<<nvb + nfb, 256, 0, st>>>(U, m_pad, m_local, row_offset, t, lnew, cvec, (unsigned char*)Vop, nvb, F, n, j,
-                                      j0, npend, ntiles, kchw, (unsigned char*)Fop, sc);
-  return cudaGetLastError();
-}
 
 int tc_smem_bytes(int nb, int* nst_out) {
   const int kchw = tc_kchw(nb);
@@ -611,7 +561,7 @@ int tc_smem_bytes(int nb, int* nst_out) {
   return geo_of(kchw, nst).total;
 }
 
-cudaError_t launch_pass_tc(const PassParams& pp, int nb, const void* Vop, const void* Fop, const void* tmap,
+cudaError_t launch_pass_tc(const PassParams& pp, int nb, void* Vop, const void* Fop, const void* tmap,
                            const void* tmapc, int max_ctas, int* gx_out, cudaStream_t st) {
   TcParams p{};
   p.m_pad = pp.m_pad;
@@ -632,7 +582,8 @@ cudaError_t launch_pass_tc(const PassParams& pp, int nb, const void* Vop, const 
   const int smem = tc_smem_bytes(nb, &nst);
   if (smem > TC_SMEM_MAX) return cudaErrorInvalidConfiguration;
   p.nst = nst;
-  p.Vop = (const unsigned char*)Vop;
+  p.Vop = (unsigned char*)Vop;
+  p.lnext = pp.j % nb;
   p.Fop = (const unsigned char*)Fop;
   p.U = (float*)pp.U;
   p.part = pp.part;

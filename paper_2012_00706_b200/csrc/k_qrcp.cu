@@ -128,13 +128,42 @@ template <typename W> __device__ __forceinline__ W to_w(double x);
 template <> __device__ __forceinline__ float to_w<float>(double x) { return __double2float_rn(x); }
 template <> __device__ __forceinline__ double to_w<double>(double x) { return x; }
 
+// the tcgen05 pass's F operand of step jn (see k_pass_tc.cu): tile t, column c, pending l ->
+// -(c_{j0+l} f_{j0+l}(jn + 128 t + c)) split into fp16 hi / lo, K-major core-matrix blocks of
+// 16 pending reflectors: [tile][chunk][hi 4 KB | lo 4 KB], zero for l >= npend or columns >= n
+__device__ __forceinline__ int fop_off(int i, int l) {
+  return (i >> 3) * 256 + ((l >> 3) & 1) * 128 + (i & 7) * 16 + (l & 7) * 2;
+}
+__device__ void build_fop(const float* __restrict__ F, const double* __restrict__ cvec, int n, int jn, int nb,
+                          unsigned char* __restrict__ Fop) {
+  const int j0 = jn == 0 ? 0 : nb * ((jn - 1) / nb);
+  const int npend = jn - j0;
+  const int kchw = (nb + 15) / 16, KW = kchw * 16;
+  const int ntiles = (n - jn + 127) / 128;
+  const int tot = ntiles * 128 * KW;
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int l = e % KW, tc = e / KW;
+    const int c = tc % 128, tt = tc / 128;
+    const int col = jn + tt * 128 + c;
+    float f = 0.f;
+    if (l < npend && col < n)
+      f = -__double2float_rn(cvec[j0 + l] * (double)F[(int64_t)((j0 + l) % NSLOT) * n + col]);
+    const __half hi = __float2half_rn(f);
+    const __half lo = __float2half_rn(f - __half2float(hi));
+    unsigned char* base = Fop + ((size_t)tt * kchw + (l >> 4)) * 2 * 4096;
+    const int o = fop_off(c, l & 15);
+    *reinterpret_cast<__half*>(base + o) = hi;
+    *reinterpret_cast<__half*>(base + 4096 + o) = lo;
+  }
+}
+
 template <typename W>
 __global__ void __launch_bounds__(1024) k_reflector(const double* __restrict__ red, int n, int j,
                                                     int k_max, int nb, W* __restrict__ F,
                                                     W* __restrict__ R, double* __restrict__ beta_out,
                                                     double* __restrict__ cvec, double* __restrict__ tau,
                                                     int* __restrict__ perm,
-                                                    DevScalars* __restrict__ sc) {
+                                                    DevScalars* __restrict__ sc, unsigned char* __restrict__ Fop) {
   if (sc->done) return;
   // tolerance stop on the exact norms of this step's formed trailing matrix (R8)
   if (j > 0 && sc->eps2normAL2 > 0.0) {
@@ -220,6 +249,12 @@ __global__ void __launch_bounds__(1024) k_reflector(const double* __restrict__ r
     sc->pivot = best.pos;
     if (j + 1 >= k_max || best.pos < 0) sc->done = 1;
   }
+  if constexpr (sizeof(W) == 4) {
+    if (Fop && jn < k_max && best.pos >= 0) {   // the tcgen05 pass: step jn's F operand, in its column order
+      __syncthreads();
+      build_fop(reinterpret_cast<const float*>(F), cvec, n, jn, nb, Fop);
+    }
+  }
 }
 
 // initial pivot: argmax of the initial column norms (ties lowest index); perm = identity
@@ -293,11 +328,13 @@ cudaError_t launch_pass_reduce(const double* part, int gx, int n, int j, const d
 
 cudaError_t launch_reflector(int fmt, const double* red, int n, int j, int k_max, int nb, void* F, void* R,
                              double* beta, double* cvec, double* tau, int* perm, DevScalars* sc,
-                             cudaStream_t st) {
+                             cudaStream_t st, void* Fop) {
   if (fmt == 3)
-    k_reflector<double><<<1, 1024, 0, st>>>(red, n, j, k_max, nb, (double*)F, (double*)R, beta, cvec, tau, perm, sc);
+    k_reflector<double><<<1, 1024, 0, st>>>(red, n, j, k_max, nb, (double*)F, (double*)R, beta, cvec, tau, perm, sc,
+                                            nullptr);
   else
-    k_reflector<float><<<1, 1024, 0, st>>>(red, n, j, k_max, nb, (float*)F, (float*)R, beta, cvec, tau, perm, sc);
+    k_reflector<float><<<1, 1024, 0, st>>>(red, n, j, k_max, nb, (float*)F, (float*)R, beta, cvec, tau, perm, sc,
+                                           (unsigned char*)Fop);
   return cudaGetLastError();
 }
 

@@ -819,14 +819,9 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     p.xr = h->xr;
     p.sc = h->sc;
     int gx_used = 0;
-    if (formation == 2) {
-      // the newest pending reflector t = j - 1 joins the panel's V operand (column t - j0),
-      // and the step's F operand is laid out for the current column order
-      CK(launch_tc_ops((const float*)h->U, h->m_pad, h->m_local, h->row_offset, j - 1, npend > 0 ? j - 1 - j0 : -1,
-                       h->cvec, h->Vop, (const float*)h->F, (int)n, j, j0, npend, nb, h->Fop, h->sc, h->st));
-      h->kernel_launches += 1;
-      if (h->tmap_ok != 0) return fail(h, ID_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", h->tmap_ok);
-    }
+    // (tcgen05 pass: the V operand column of u_{j-1} was written by the previous pass, the
+    // step's F operand by the previous k_reflector)
+    if (formation == 2 && h->tmap_ok != 0) return fail(h, ID_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", h->tmap_ok);
     if (profile) CK(rec(h, h->pass_ev[2 * j]));
     if (formation == 2) CK(launch_pass_tc(p, nb, h->Vop, h->Fop, h->tmapS, h->tmapC, pass_gx_cap(), &gx_used, h->st));
     else CK(launch_pass_tma(fmt, p, num_sms(), &gx_used, h->st));
@@ -838,7 +833,7 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     s = allreduce(h, h->red, (size_t)3 * n, NCCL_SUM);
     if (s) return s;
     CK(launch_reflector(fmt, h->red, (int)n, j, k_max, nb, h->F, h->R, h->beta, h->cvec, h->tau, h->perm,
-                        h->sc, h->st));
+                        h->sc, h->st, formation == 2 ? h->Fop : nullptr));
     h->kernel_launches += 3;
     h->pass_launches += 1;
   }

@@ -152,18 +152,16 @@ cudaError_t launch_pass_tma(int fmt, PassParams p, int num_sms, int* gx_out, cud
 int tc_kchw(int nb);
 size_t tc_vop_bytes(int64_t m_pad, int nb);
 size_t tc_fop_bytes(int n, int nb);
-cudaError_t launch_tc_ops(const float* U, int64_t m_pad, int64_t m_local, int64_t row_offset, int t, int lnew,
-                          const double* cvec, void* Vop, const float* F, int n, int j, int j0, int npend, int nb,
-                          void* Fop, const DevScalars* sc, cudaStream_t st);
-cudaError_t launch_pass_tc(const PassParams& p, int nb, const void* Vop, const void* Fop, const void* tmap,
+cudaError_t launch_pass_tc(const PassParams& p, int nb, void* Vop, const void* Fop, const void* tmap,
                            const void* tmapc, int max_ctas, int* gx_out, cudaStream_t st);
 int encode_tmap_S(void* tmap_out, void* S, int64_t ngroups, int n, int which);
 cudaError_t launch_pass_reduce(const double* part, int gx, int n, int j, const double* xr,
                                int own_row, double* red, const DevScalars* sc, cudaStream_t st);
 // F, R in the working precision: fp32 (fmt 1, 2) or fp64 (fmt 3)
+// Fop != nullptr: also lay out the tcgen05 pass's F operand of step j + 1 (fp16 / fp32 only)
 cudaError_t launch_reflector(int fmt, const double* red, int n, int j, int k_max, int nb, void* F, void* R,
                              double* beta, double* cvec, double* tau, int* perm, DevScalars* sc,
-                             cudaStream_t st);
+                             cudaStream_t st, void* Fop = nullptr);
 cudaError_t launch_swap(int fmt, void* S, int64_t ngroups, int n, int jn, int j0, int steps_done,
                         void* F, void* R, int* perm, void* Sj, DevScalars* sc, cudaStream_t st);
 cudaError_t launch_export_S(int fmt, const void* S, int64_t m_local, int n, void* out, int64_t ld,
