@@ -78,16 +78,17 @@ typedef enum {
 typedef struct {
   int32_t nb;        /* store interval = panel width: the trailing matrix is re-stored
                         in the low format every nb steps (1 = SPEC's store-after-every-
-                        update); 0 = default (4 with FFMA formation, 16 with tcgen05).
+                        update); 0 = default (4 with the FFMA formation, 16 otherwise).
                         1 <= nb <= 32 (<= 16 with FFMA formation). */
   int32_t use_graph; /* 0 or 1 (default) = capture the k-step loop in a CUDA graph
                         and replay it; -1 = plain stream launches. */
   int32_t profile_pass; /* 1 = bracket every panel-pass launch with CUDA events
                            (id_stats.t_pass_ms); adds event nodes between kernels. */
   int32_t formation; /* how the pending update A~ = S - V F^T is formed each step:
-                        1 = CUDA-core FFMA in step order (bit-identical to the oracle's
-                        sequential model), 2 = tcgen05 tensor cores (3xTF32, TMEM;
-                        DESIGN.md R14), 0 = default (1: measured faster on C4).
+                        1 = CUDA-core FFMA in step order (fp16 / fp32 / fp64 storage),
+                        2 = tcgen05 tensor cores: S^T I + (-F) V^T with hi / lo fp16
+                        operands accumulated in TMEM (fp16 storage with range scaling,
+                        n <= 2048; R14).
                         3 = Gram pivoting (the paper's "sketching"
                         future work P:402; R17): no k-step panel passes;
                         G = A_L^T A_L on tcgen05 (kind::f16, fp32 accumulation drained
@@ -99,7 +100,12 @@ typedef struct {
                         Y = Omega A_L with a Rademacher Omega of l >= k_max + 10 rows
                         (see sketch_oversample; seed = sketch_seed) on tcgen05,
                         then an fp64 Householder QRCP of Y; fp16 only; needs
-                        l rounded up to 128 <= n.  R is the sketch's R factor. */
+                        l rounded up to 128 <= n.  R is the sketch's R factor.
+                        5 = the whole QRCP in ONE launch in one SM's shared memory (fp16 /
+                        fp32, a single shard with m x n x 4 B <= ~220 KB, e.g. C1), in the
+                        oracle's paper model (per-operation RNE update, fp64 row-order
+                        sums) bit for bit.  Default: 5 when it applies, else 2 for fp16 with
+                        range scaling and n <= 2048, else 1. */
   int32_t sketch_oversample; /* formation 4: l = k_max + sketch_oversample; 0 = fill the
                                 128-row MMA tile that k_max + 10 needs (l = 128 for k = 100) */
   int32_t sketch_seed;       /* formation 4: seed of the Rademacher sketch */

@@ -1,18 +1,25 @@
 // The fp64 ID step (Algorithm 2 lines 5-7; Eq. (8) P:129-135;
-// Remark 1 P:136-139; Remark 2 P:199-201).
+// Remark 1 P:136-139; Remark 2 P:199-201), on the fp64 tensor pipe (DMMA,
+// mma.sync.aligned.m8n8k4.f64).
 //
 //   LSQ mode ("least-squares problem"): P(:, J) = argmin ||A_I X - A_J||_F,
-//   A_I = A_D(:, I), solved by CholeskyQR2-style orthogonalisation in fp64:
-//     G1 = A_I^T A_I,  R1 = chol(G1),  Q1 = A_I R1^{-1}     (blocked TRSM, in place)
-//     G2 = Q1^T Q1 (well conditioned: kappa(Q1)^2 = 1 + O(u kappa(A_I)^2)),
-//     W  = Q1^T A_D,   T = R1^{-1} G2^{-1} W(:, J)          (small triangular solves)
-//   which equals R^{-1} Q^T A_J with Q = Q1 R2^{-1}, R = R2 R1 (CholQR2) but forms
-//   only one m x k triangular solve.  R mode (Eq. (8)): T = R11^{-1} R12 from the
+//   A_I = A_D(:, I), by a Cholesky QR preconditioned with the QRCP's own R11
+//   (mpid_api.cu id_coeffs_fp64):
+//     Q1 = A_I R11^{-1}  (R11^{-1} by triangular solves on I_k, then k_err_ws<STORE>)
+//     G2 = Q1^T Q1, R2 = chol(G2),  W = Q1^T A_D(:, J)  (k_dgemm_tn_pipe8 / _pipe split-K)
+//     T  = R11^{-1} R2^{-1} R2^{-T} W
+//   and, when R2's diagonal spread exceeds 1e3 (or the Cholesky breaks down), the same
+//   with R1 = chol(A_I^T A_I): CholeskyQR2.  R mode (Eq. (8)): T = R11^{-1} R12 from the
 //   low-precision R promoted to fp64.
-//   The error ||A_D - A_D(:, I) P||_F is one fused pass: a 64x64-tiled fp64 GEMM
-//   A_I P whose epilogue subtracts from A_D, squares and reduces (never stored).
+//   The error ||A_D - A_D(:, I) P||_F = ||A_D(:, J) - A_I T||_F (skeleton columns are
+//   exactly 0) is one fused pass, k_err_ws: a warp-specialised persistent kernel over
+//   128 x 128 tiles of the J columns (producer warp + 4-deep mbarrier ring of bulk copies,
+//   16 consumer warps of 32 x 32 DMMA tiles) whose epilogue subtracts from A_D, squares
+//   and reduces — never stored.  k_err_persist is the register-staged fallback for odd m
+//   or unaligned A_I.
 //
-// Bound: fp64 FMA pipe for the GEMM-shaped kernels (intensity ~k/4 flop/B).
+// Bound: the DMMA pipe for the GEMM-shaped kernels (intensity ~k/4 flop/B vs a ~6 flop/B
+// ridge).
 #include "mpid_internal.cuh"
 #include <math.h>
 #include <cstdlib>
@@ -685,94 +692,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int MT>
-__global__ void __launch_bounds__(256, 1) k_dgemm_tn_async(GemmArgs g) {
-  constexpr int BM = 16 * MT;
-  extern __shared__ __align__(16) double dsm[];
-  double* As = dsm;                                  // [TN_S][BM][LDK]
-  double* Bs = dsm + TN_S * BM * LDK;                // [TN_S][GT][LDK]
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int gq = lane >> 2, tq = lane & 3;
-  const int wm = warp >> 2, wn = warp & 3;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int64_t n0 = (int64_t)blockIdx.y * GT;
-  const int64_t k_begin = (int64_t)blockIdx.z * g.k_per_split;
-  const int64_t k_end = min(g.K, k_begin + g.k_per_split);
-  const int nst = k_begin < k_end ? (int)((k_end - k_begin + GK - 1) / GK) : 0;
-  // B column pointers of this thread's 4 chunks (fixed over the K loop)
-  const double* bsrc[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int idx = tid + q * 256, mn = idx >> 3;
-    const int64_t c = n0 + mn;
-    bsrc[q] = c < g.N ? g.Y + (g.ycmap ? (int64_t)g.ycmap[c] : c) * g.ldy : nullptr;
-  }
-  auto issue = [&](int st) {
-    const int buf = st % TN_S;
-    const int64_t kb = k_begin + (int64_t)st * GK;
-    for (int idx = tid; idx < BM * 8; idx += 256) {
-      const int mn = idx >> 3, kk = (idx & 7) * 2;
-      const int64_t i = m0 + mn, r = kb + kk;
-      const bool v = i < g.M && r < k_end;           // k_end even: pairs never straddle it
-      cp_async16(&As[(buf * BM + mn) * LDK + kk], v ? g.X + i * g.ldx + r : g.X, v);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int idx = tid + q * 256, mn = idx >> 3, kk = (idx & 7) * 2;
-      const int64_t r = kb + kk;
-      const bool v = bsrc[q] != nullptr && r < k_end;
-      cp_async16(&Bs[(buf * GT + mn) * LDK + kk], v ? bsrc[q] + r : g.Y, v);
-    }
-  };
-  double acc[MT][4][2];
-#pragma unroll
-  for (int a = 0; a < MT; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-#pragma unroll
-  for (int st = 0; st < TN_S - 1; ++st) {
-    if (st < nst) issue(st);
-    cp_async_commit();
-  }
-  const bool idle = m0 + wm * 8 * MT >= g.M || n0 + wn * 32 >= g.N;
-  for (int it = 0; it < nst; ++it) {
-    cp_async_wait<TN_S - 2>();
-    __syncthreads();
-    if (it + TN_S - 1 < nst) issue(it + TN_S - 1);
-    cp_async_commit();
-    const int buf = it % TN_S;
-    const int64_t krem = (k_end - (k_begin + (int64_t)it * GK) + 3) / 4;
-    const int ksteps = idle ? 0 : (krem < GK / 4 ? (int)krem : GK / 4);
-    const double* Ab = As + (size_t)buf * BM * LDK;
-    const double* Bb = Bs + (size_t)buf * GT * LDK;
-#pragma unroll
-    for (int ks = 0; ks < GK / 4; ++ks) {
-      if (ks >= ksteps) break;
-      double af[MT], bf[4];
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) af[mt] = Ab[(wm * (8 * MT) + mt * 8 + gq) * LDK + ks * 4 + tq];
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) bf[nt] = Bb[(wn * 32 + nt * 8 + gq) * LDK + ks * 4 + tq];
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
-    }
-  }
-  cp_async_wait<0>();
-  double* o = g.out + (int64_t)blockIdx.z * g.M * g.N;
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-    const int64_t i = m0 + wm * (8 * MT) + mt * 8 + gq;
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
-        if (i < g.M && c < g.N) o[c * g.M + i] = acc[mt][nt][h];
-      }
-  }
-}
 
 // The same GEMM with the barrier taken out of the DMMA loop: 2 producer warps issue the
 // 16-byte cp.async chunks of each stage (zero-filled outside the matrix, as above) and
@@ -1008,20 +927,12 @@ static bool tn_pipe8_launch(const GemmArgs& g, dim3 grid, cudaStream_t st, cudaE
 
 template <int MT>
 static cudaError_t tn_async_launch_t(const GemmArgs& g, dim3 grid, cudaStream_t st) {
-  static const bool pipe_off = getenv("MPID_TN_NO_PIPE") != nullptr;   // A/B switch for measurements
-  if (!pipe_off) {
-    cudaError_t e8 = cudaSuccess;
-    if (tn_pipe8_launch(g, grid, st, &e8)) return e8;
-    const size_t smem_p = (size_t)TP_S * (16 * MT + GT) * LDK * sizeof(double);
-    cudaError_t e = smem_attr((const void*)k_dgemm_tn_pipe<MT>, (int)smem_p);
-    if (e != cudaSuccess) return e;
-    k_dgemm_tn_pipe<MT><<<grid, TP_THREADS, smem_p, st>>>(g);
-    return cudaGetLastError();
-  }
-  const size_t smem = (size_t)TN_S * (16 * MT + GT) * LDK * sizeof(double);
-  cudaError_t e = smem_attr((const void*)k_dgemm_tn_async<MT>, (int)smem);
+  cudaError_t e8 = cudaSuccess;
+  if (tn_pipe8_launch(g, grid, st, &e8)) return e8;
+  const size_t smem_p = (size_t)TP_S * (16 * MT + GT) * LDK * sizeof(double);
+  cudaError_t e = smem_attr((const void*)k_dgemm_tn_pipe<MT>, (int)smem_p);
   if (e != cudaSuccess) return e;
-  k_dgemm_tn_async<MT><<<grid, 256, smem, st>>>(g);
+  k_dgemm_tn_pipe<MT><<<grid, TP_THREADS, smem_p, st>>>(g);
   return cudaGetLastError();
 }
 static cudaError_t tn_async_launch(const GemmArgs& g, dim3 grid, cudaStream_t st, int mt) {

@@ -29,20 +29,21 @@
 
 namespace mpid {
 
-// red[0][c] = sum w, red[1][c] = sum s over the GX row-CTAs, red[2][c] = x_c.
-// CTA = 32 columns (lanes) x 8 warps; warp w sums rows b = w, w+8, ... ; the 8
+// red[0][c] = sum w, red[1][c] = sum s over the GX partial rows, red[2][c] = x_c.
+// CTA = 32 columns (lanes) x 32 warps; warp w sums rows b = w, w+32, ... ; the 32
 // warp partials are then added in warp order (deterministic).
-__global__ void __launch_bounds__(256) k_pass_reduce(const double* __restrict__ part, int gx, int n,
-                                                     int j, const double* __restrict__ xr, int own_row,
-                                                     double* __restrict__ red,
-                                                     const DevScalars* __restrict__ sc) {
+constexpr int RW = 32;
+__global__ void __launch_bounds__(32 * RW) k_pass_reduce(const double* __restrict__ part, int gx, int n,
+                                                         int j, const double* __restrict__ xr, int own_row,
+                                                         double* __restrict__ red,
+                                                         const DevScalars* __restrict__ sc) {
   if (sc->done) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = j + blockIdx.x * 32 + lane;
-  __shared__ double sh[2][8][32];
+  __shared__ double sh[2][RW][32];
   double w = 0.0, s = 0.0;
   if (c < n) {
-    for (int b = warp; b < gx; b += 8) {
+    for (int b = warp; b < gx; b += RW) {
       w += part[((int64_t)b * 2 + 0) * n + c];
       s += part[((int64_t)b * 2 + 1) * n + c];
     }
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(256) k_pass_reduce(const double* __restrict__ 
   if (warp == 0 && c < n) {
     double tw = 0.0, ts = 0.0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { tw += sh[0][i][lane]; ts += sh[1][i][lane]; }
+    for (int i = 0; i < RW; ++i) { tw += sh[0][i][lane]; ts += sh[1][i][lane]; }
     red[c] = tw;
     red[n + c] = ts;
     red[2 * n + c] = own_row ? xr[c] : 0.0;
@@ -322,7 +323,7 @@ __global__ void k_swap(T* __restrict__ S, int64_t ngroups, int n, int jn, int j0
 cudaError_t launch_pass_reduce(const double* part, int gx, int n, int j, const double* xr,
                                int own_row, double* red, const DevScalars* sc, cudaStream_t st) {
   const int cols = n - j;
-  k_pass_reduce<<<(cols + 31) / 32, 256, 0, st>>>(part, gx, n, j, xr, own_row, red, sc);
+  k_pass_reduce<<<(cols + 31) / 32, 32 * RW, 0, st>>>(part, gx, n, j, xr, own_row, red, sc);
   return cudaGetLastError();
 }
 

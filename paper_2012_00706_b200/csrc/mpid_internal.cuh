@@ -148,6 +148,10 @@ cudaError_t launch_round(int fmt, const double* A, int64_t m, int64_t m_pad, int
 cudaError_t launch_init_pivot(const double* norms, int n, int* perm, DevScalars* sc,
                               cudaStream_t st);
 cudaError_t launch_pass_tma(int fmt, PassParams p, int num_sms, int* gx_out, cudaStream_t st);
+// the one-launch QRCP of a shared-memory-sized matrix (k_qrcp_smem.cu; the oracle's paper model)
+size_t qrcp_smem_bytes(int64_t m, int n);
+cudaError_t launch_qrcp_smem(int fmt, const void* S, int64_t m, int n, int k_max, int nb, double eps, int* perm,
+                             float* R, DevScalars* sc, cudaStream_t st);
 // tcgen05 pass (fp16 storage; k_pass_tc.cu): operands, launch, tensor map of S
 int tc_kchw(int nb);
 size_t tc_vop_bytes(int64_t m_pad, int nb);

@@ -113,7 +113,7 @@ def check(A, fmt, scaling, k, bounds, nb=0, formation="auto", oracle_model="pape
         assert abs(o0["err_AL"][1] - s["err_AL"][1]) <= 1e-9 * s["err_AL"][1]
         # the 2-norm is not stationary in P (unlike the LSQ Frobenius residual): a 1e-10
         # relative change of P moves it by ~1e-10 of ||A||_2, i.e. absolute in these units
-        assert abs(o0["err_2"][1] - s["err_2"][1]) <= 1e-6 * s["err_2"][1] + 1e-9
+        assert abs(o0["err_2"][1] - s["err_2"][1]) <= 1e-6 * s["err_2"][1] + 1e-8
     return outs, s
 
 
