@@ -105,7 +105,7 @@ typedef struct {
                         fp32, a single shard with m x n x 4 B <= ~220 KB, e.g. C1), in the
                         oracle's paper model (per-operation RNE update, fp64 row-order
                         sums) bit for bit.  Default: 5 when it applies, else 2 for fp16 with
-                        range scaling and n <= 2048, else 1. */
+                        range scaling, n <= 2048 and >= 16384 rows per shard, else 1. */
   int32_t sketch_oversample; /* formation 4: l = k_max + sketch_oversample; 0 = fill the
                                 128-row MMA tile that k_max + 10 needs (l = 128 for k = 100) */
   int32_t sketch_seed;       /* formation 4: seed of the Rademacher sketch */

@@ -200,9 +200,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
   float* fj = reinterpret_cast<float*>(smem + geo.fj);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // row blocks of this CTA
-  const int64_t per = (p.nrb + gridDim.x - 1) / gridDim.x;
-  const int64_t rb0 = (int64_t)blockIdx.x * per;
-  const int64_t rb1 = rb0 + per < p.nrb ? rb0 + per : p.nrb;
+  // row blocks of this CTA: a balanced split (CTAs differ by at most one block)
+  const int64_t rb0 = p.nrb * blockIdx.x / gridDim.x;
+  const int64_t rb1 = p.nrb * (blockIdx.x + 1) / gridDim.x;
   const int nrbc = rb0 < rb1 ? (int)(rb1 - rb0) : 0;
   const int64_t units = (int64_t)nrbc * ntiles;
   const int64_t jl = (int64_t)j - p.row_offset;   // local row of the pivot row (may be outside)

@@ -31,10 +31,12 @@ template <> __device__ __forceinline__ float ld_s<float>(const float* S, int64_t
 }
 }  // namespace
 
-// shared memory: W [n][m8] fp32 | vn, s, w, x, rr [n] fp64 | v [m8] fp32 | f [n] fp32
-size_t qrcp_smem_bytes(int64_t m, int n) {
+// shared memory: W [n][m8 + 1] fp32 (odd column stride: the one-thread-per-column sums read
+// distinct banks) | vn, s, w, x, rr [n] fp64 | v [m8] fp32 | f [n] fp32 | perm [n] int |
+// R [k][n] fp32 (written to global memory at the end)
+size_t qrcp_smem_bytes(int64_t m, int n, int k) {
   const int64_t m8 = (m + 7) / 8 * 8;
-  return (size_t)n * m8 * 4 + (size_t)5 * n * 8 + (size_t)m8 * 4 + (size_t)n * 4 + 64;
+  return (size_t)n * (m8 + 1) * 4 + 8 + (size_t)5 * n * 8 + (size_t)m8 * 4 + (size_t)n * 8 + (size_t)k * n * 4 + 64;
 }
 
 template <typename T>
@@ -44,28 +46,31 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
   if (sc->done) return;
   extern __shared__ __align__(16) unsigned char smem[];
   const int m8 = (m + 7) / 8 * 8;
+  const int ldw = m8 + 1;
   float* W = reinterpret_cast<float*>(smem);
-  double* vn = reinterpret_cast<double*>(smem + (size_t)n * m8 * 4);
+  double* vn = reinterpret_cast<double*>(smem + (((size_t)n * ldw * 4 + 15) & ~(size_t)15));
   double* s = vn + n;
   double* w = s + n;
   double* x = w + n;
   double* rr = x + n;
   float* v = reinterpret_cast<float*>(rr + n);
   float* f = v + m8;
+  int* pm = reinterpret_cast<int*>(f + n);
+  float* Rs = reinterpret_cast<float*>(pm + n);
   __shared__ int sh_p, sh_stop;
   __shared__ double sh_beta, sh_cc, sh_normAL;
   const int tid = threadIdx.x, nt = blockDim.x;
 
   for (int64_t e = tid; e < (int64_t)n * m8; e += nt) {
     const int c = (int)(e / m8), r = (int)(e - (int64_t)c * m8);
-    W[e] = r < m ? ld_s<T>(S, r, c, n) : 0.f;
+    W[(int64_t)c * ldw + r] = r < m ? ld_s<T>(S, r, c, n) : 0.f;
   }
-  for (int c = tid; c < n; c += nt) perm[c] = c;
+  for (int c = tid; c < n; c += nt) pm[c] = c;
   __syncthreads();
   for (int c = tid; c < n; c += nt) {              // exact initial norms^2, row order
     double t = 0.0;
     for (int r = 0; r < m; ++r) {
-      const double a = (double)W[(int64_t)c * m8 + r];
+      const double a = (double)W[(int64_t)c * ldw + r];
       t = r == 0 ? __dmul_rn(a, a) : __dadd_rn(t, __dmul_rn(a, a));
     }
     vn[c] = t;
@@ -81,29 +86,38 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
   int kk = k_max, st = 0;
   for (int j = 0; j < k_max; ++j) {
     const int jl = j, g0 = (j / 8) * 8;
-    if (tid == 0) {                                 // pivot: max vn, ties -> lowest original index
-      double best = vn[j];
-      for (int i = j + 1; i < n; ++i) best = vn[i] > best ? vn[i] : best;
-      int p = -1;
-      for (int i = j; i < n; ++i)
-        if (vn[i] == best && (p < 0 || perm[i] < perm[p])) p = i;
-      sh_p = p;
+    if (tid < 32) {                                 // pivot: max vn, ties -> lowest original index
+      double best = -INFINITY;                      // (max and min are exact: any order agrees)
+      int bo = 0x7fffffff, bp = -1;
+      for (int i = j + tid; i < n; i += 32) {
+        const double vi = vn[i];
+        const int oi = pm[i];
+        if (vi > best || (vi == best && oi < bo)) { best = vi; bo = oi; bp = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double vb = __shfl_xor_sync(0xffffffffu, best, o);
+        const int ob = __shfl_xor_sync(0xffffffffu, bo, o);
+        const int pb = __shfl_xor_sync(0xffffffffu, bp, o);
+        if (vb > best || (vb == best && ob < bo)) { best = vb; bo = ob; bp = pb; }
+      }
+      if (tid == 0) sh_p = bp;
     }
     __syncthreads();
     const int p = sh_p;
     if (p != j) {
       for (int r = tid; r < m8; r += nt) {
-        const float a = W[(int64_t)j * m8 + r];
-        W[(int64_t)j * m8 + r] = W[(int64_t)p * m8 + r];
-        W[(int64_t)p * m8 + r] = a;
+        const float a = W[(int64_t)j * ldw + r];
+        W[(int64_t)j * ldw + r] = W[(int64_t)p * ldw + r];
+        W[(int64_t)p * ldw + r] = a;
       }
       for (int r = tid; r < j; r += nt) {
-        const float a = R[(int64_t)r * n + j];
-        R[(int64_t)r * n + j] = R[(int64_t)r * n + p];
-        R[(int64_t)r * n + p] = a;
+        const float a = Rs[(int64_t)r * n + j];
+        Rs[(int64_t)r * n + j] = Rs[(int64_t)r * n + p];
+        Rs[(int64_t)r * n + p] = a;
       }
       if (tid == 0) {
-        const int tp = perm[j]; perm[j] = perm[p]; perm[p] = tp;
+        const int tp = pm[j]; pm[j] = pm[p]; pm[p] = tp;
         const double tv = vn[j]; vn[j] = vn[p]; vn[p] = tv;
       }
     }
@@ -112,31 +126,41 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
       const int rows = m8 - jl;
       for (int64_t e = tid; e < (int64_t)(n - j) * rows; e += nt) {
         const int c = j + (int)(e / rows), r = jl + (int)(e % rows);
-        W[(int64_t)c * m8 + r] = __half2float(__float2half_rn(W[(int64_t)c * m8 + r]));
+        W[(int64_t)c * ldw + r] = __half2float(__float2half_rn(W[(int64_t)c * ldw + r]));
       }
       __syncthreads();
     }
     for (int c = j + tid; c < n; c += nt) {         // s_i, w_i: exact products, fp64, row order
       double ss = 0.0, ww = 0.0;
+#pragma unroll 8
       for (int r = g0; r < m8; ++r) {
-        const double a = r < jl ? 0.0 : (double)W[(int64_t)c * m8 + r];
-        const double u = r < jl ? 0.0 : (double)W[(int64_t)j * m8 + r];
+        const double a = r < jl ? 0.0 : (double)W[(int64_t)c * ldw + r];
+        const double u = r < jl ? 0.0 : (double)W[(int64_t)j * ldw + r];
         const double ps = __dmul_rn(a, a), pw = __dmul_rn(a, u);
         if (r == g0) { ss = ps; ww = pw; }
         else { ss = __dadd_rn(ss, ps); ww = __dadd_rn(ww, pw); }
       }
       s[c] = ss;
       w[c] = ww;
-      x[c] = (double)W[(int64_t)c * m8 + jl];
+      x[c] = (double)W[(int64_t)c * ldw + jl];
     }
     __syncthreads();
     if (tid == 0) {
-      double t = 0.0;
-      for (int c = j; c < n; ++c) t = c == j ? s[j] : __dadd_rn(t, s[c]);
-      const double resid = __dsqrt_rn(t);
-      sc->resid2 = t;
-      if (eps > 0.0 && j > 0 && resid <= __dmul_rn(eps, sh_normAL)) sh_stop = 1;
-      else if (!(s[j] >= 1.1754943508222875e-38)) sh_stop = 2;
+      // the residual mass (a sequential sum over the columns) only when a tolerance asks
+      bool stop = false;
+      if (eps > 0.0 && j > 0) {
+        double t = 0.0;
+        for (int c = j; c < n; ++c) t = c == j ? s[j] : __dadd_rn(t, s[c]);
+        sc->resid2 = t;
+        stop = __dsqrt_rn(t) <= __dmul_rn(eps, sh_normAL);
+      }
+      if (stop) sh_stop = 1;
+      else if (!(s[j] >= 1.1754943508222875e-38)) {
+        double t = 0.0;
+        for (int c = j; c < n; ++c) t = c == j ? s[j] : __dadd_rn(t, s[c]);
+        sc->resid2 = t;
+        sh_stop = 2;
+      }
       else {
         const double u0 = x[j];
         const double beta = -copysign(__dsqrt_rn(s[j]), u0);
@@ -152,16 +176,16 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
     }
     const double beta = sh_beta, cc = sh_cc;
     const double sgn = copysign(1.0, beta);
-    for (int r = jl + tid; r < m8; r += nt) v[r] = __double2float_rn(__dmul_rn((double)W[(int64_t)j * m8 + r], cc));
+    for (int r = jl + tid; r < m8; r += nt) v[r] = __double2float_rn(__dmul_rn((double)W[(int64_t)j * ldw + r], cc));
     for (int c = tid; c < n; c += nt) {
       if (c < j) {
-        R[(int64_t)j * n + c] = 0.f;
+        Rs[(int64_t)j * n + c] = 0.f;
         continue;
       }
       const double rw = __ddiv_rn(w[c], beta);
       rr[c] = rw;
       f[c] = __double2float_rn(__dadd_rn(x[c], -rw));
-      R[(int64_t)j * n + c] = __double2float_rn(__dmul_rn(rw, sgn));
+      Rs[(int64_t)j * n + c] = __double2float_rn(__dmul_rn(rw, sgn));
       if (c > j) vn[c] = __dadd_rn(s[c], -__dmul_rn(rw, rw));
     }
     __syncthreads();
@@ -171,7 +195,7 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
       const int rows = m8 - jl;
       for (int64_t e = tid; e < (int64_t)(n - j) * rows; e += nt) {
         const int c = j + (int)(e / rows), r = jl + (int)(e % rows);
-        float* a = &W[(int64_t)c * m8 + r];
+        float* a = &W[(int64_t)c * ldw + r];
         *a = __fsub_rn(*a, __fmul_rn(v[r], f[c]));
       }
     }
@@ -182,7 +206,7 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
     for (int c = j + tid; c < n; c += nt) {
       double ss = 0.0;
       for (int r = g0; r < m8; ++r) {
-        const double a = r < jl ? 0.0 : (double)W[(int64_t)c * m8 + r];
+        const double a = r < jl ? 0.0 : (double)W[(int64_t)c * ldw + r];
         ss = r == g0 ? __dmul_rn(a, a) : __dadd_rn(ss, __dmul_rn(a, a));
       }
       s[c] = ss;
@@ -194,6 +218,9 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
       sc->resid2 = t;
     }
   }
+  __syncthreads();
+  for (int c = tid; c < n; c += nt) perm[c] = pm[c];
+  for (int64_t e = tid; e < (int64_t)kk * n; e += nt) R[e] = Rs[e];
   if (tid == 0) {
     sc->k_out = kk;
     sc->status = st;
@@ -203,7 +230,7 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
 
 cudaError_t launch_qrcp_smem(int fmt, const void* S, int64_t m, int n, int k_max, int nb, double eps, int* perm,
                              float* R, DevScalars* sc, cudaStream_t st) {
-  const size_t smem = qrcp_smem_bytes(m, n);
+  const size_t smem = qrcp_smem_bytes(m, n, k_max);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   if (fmt == 1) {
     cudaError_t e = smem_attr((const void*)k_qrcp_smem<__half>, (int)smem);

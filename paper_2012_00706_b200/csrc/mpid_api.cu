@@ -258,6 +258,7 @@ struct mpid_ctx {
   // graphs keyed by (fmt, scaling, k_max, nb * 4 + formation, eps bits, profile, sketch l << 32 | seed)
   std::map<std::tuple<int, int, int, int, uint64_t, int, uint64_t>, cudaGraphExec_t> graphs;
   std::map<std::tuple<int, int, int, int, uint64_t, int, uint64_t>, int64_t> graph_launches;
+  std::map<uint64_t, std::pair<cudaGraphExec_t, int>> cgraphs;   // id_coeffs_fp64 graphs per (mode, k)
   // sketched pivoting (formation 4): sketch rows l (lw rounded to 128), seed, Omega^T's tensor map
   int sk_l = 0, sk_lw = 0;
   uint32_t sk_seed = 0;
@@ -395,6 +396,8 @@ static id_status relayout(mpid_ctx* h, int sbytes) {
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
   h->graphs.clear();
   h->graph_launches.clear();
+  for (auto& kv : h->cgraphs) cudaGraphExecDestroy(kv.second.first);
+  h->cgraphs.clear();
   // every buffer moves: results held in the old carve (QR, coefficients, Gram, sketch) are gone
   h->have_qr = h->have_coef = h->have_gram = h->have_sketch = false;
   h->perm_host.clear();
@@ -568,6 +571,7 @@ id_status id_create_ex(id_handle* hp, const double* A_D, int64_t m_global, int64
 void id_destroy(id_handle h) {
   if (!h) return;
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : h->cgraphs) cudaGraphExecDestroy(kv.second.first);
   for (auto& e : h->ev) if (e) cudaEventDestroy(e);
   for (auto& e : h->pass_ev) cudaEventDestroy(e);
   if (h->fork_ev) cudaEventDestroy(h->fork_ev);
@@ -892,11 +896,15 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   // fp16 operand range), n - 0 <= 2048 columns — else FFMA.
   const bool tc_ok = fmt == ID_FP16 && scaling != ID_SCALE_NONE && h->n <= 2048 &&
                      2.83 * sqrt((double)h->m_global) < 60000.0;
+  // the tcgen05 pass pays a fixed per-launch cost (TMEM allocation, ring fill) that only
+  // tall shards amortise: default to it from 16384 rows per shard (C3, C4, C5 shards; at
+  // C2's 4096 rows the FFMA pass is twice as fast)
+  const bool tc_default = tc_ok && h->m_local >= 16384;
   // 5 = the one-launch shared-memory QRCP (the paper model), default when one shard fits an SM
   const bool smem_ok = (fmt == ID_FP16 || fmt == ID_FP32) && h->nranks == 1 && !h->comm &&
-                       qrcp_smem_bytes(h->m_local, (int)h->n) <= 227 * 1024;
+                       qrcp_smem_bytes(h->m_local, (int)h->n, k_max) <= 227 * 1024;
   int formation = opts ? opts->formation : 0;
-  if (formation == 0) formation = smem_ok ? 5 : (tc_ok ? 2 : 1);
+  if (formation == 0) formation = smem_ok ? 5 : (tc_default ? 2 : 1);
   if (formation == 5 && !smem_ok)
     return fail(h, ID_ERR_ARG, "the shared-memory QRCP needs fp16 / fp32, one shard and m x n x 4 B <= ~220 KB");
   if (formation == 2 && !tc_ok)
@@ -1030,113 +1038,148 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
   const int64_t m = h->m_local;
   if (ldp < k) return fail(h, ID_ERR_ARG, "ldp < k");
   if ((size_t)k * 33 * 8 > 200 * 1024) return fail(h, ID_ERR_DIM, "k=%d too large for the P solve", k);
+  if (mode != ID_COEF_R && mode != ID_COEF_LSQ) return fail(h, ID_ERR_ARG, "bad coefficient mode");
   CK(cudaEventRecord(h->ev[3], h->st));
   int launches = 0;
-  if (h->host_AD == 2) {   // A_I = A_D(:, I) straight from the host columns
-    for (int i = 0; i < k; ++i)
-      CK(cudaMemcpyAsync(h->AI + (size_t)i * m, h->AD_host + (size_t)h->perm_host[i] * h->ld_host, (size_t)m * 8,
-                         cudaMemcpyHostToDevice, h->st));
-  } else {
-    CK(launch_gather_cols(h->AD, m, h->ld, h->perm, k, h->AI, h->st));
-    launches++;
-  }
-  if (mode == ID_COEF_R) {
-    h->stats.lsq_path = 0;
-    CK(launch_R_to_fp64(h->fmt == ID_FP64, h->R, k, n, h->Rd, h->st));
-    CK(launch_trsm_left_upper(h->Rd, nullptr, k, h->Rd + (int64_t)k * k, k, nullptr, n - k, h->T, k, 0,
-                              h->st));
-    launches += 2;
-  } else if (mode == ID_COEF_LSQ) {
-    // P(:, J) = argmin ||A_I X - A_J|| by a preconditioned Cholesky QR in fp64:
-    //   Q1 = A_I R1^{-1},  G2 = Q1^T Q1 = R2^T R2,  W = Q1^T A_J,  T = R1^{-1} R2^{-1} R2^{-T} W
-    // with R1 = the QRCP's own low-precision R11 ("computed from the R matrix and
-    // pivot indices ... via a least-squares problem"; A_I R11^{-1} is already close to
-    // orthonormal, so one Cholesky pass suffices), or, when that Q1 is too ill-conditioned
-    // (R2's diagonal spread > 1e3 or a breakdown), R1 = chol(A_I^T A_I): CholeskyQR2.
-    const size_t tcap = tpart_doubles(m, n, h->k_cap);
-    const int sp = splits_for(k, k, m, tcap);
-    auto lsq = [&](bool precond) -> id_status {
-      const double* R1;
-      if (precond) {
-        CK(launch_R_to_fp64(h->fmt == ID_FP64, h->R, k, n, h->Rd, h->st));   // leading k x k block = R11
-        CK(cudaMemsetAsync(h->info, 0, sizeof(int), h->st));
-        R1 = h->Rd;
-        launches += 1;
-      } else {
-        CK(launch_tsmm(h->AI, m, k, h->AI, m, k, m, h->tpart, sp, h->st));     // G1 = A_I^T A_I
-        CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G1, h->st));
-        id_status s = allreduce(h, h->G1, (size_t)k * k, NCCL_SUM);
-        if (s) return s;
-        CK(launch_cholesky(h->G1, k, h->info, h->st));
-        R1 = h->G1;
-        launches += 3;
-      }
-      // Q1 = A_I R1^{-1}: the k x k inverse by triangular solves on I_k, then one DMMA GEMM
-      CK(launch_eye(h->Ik, k, h->st));
-      CK(launch_trsm_left_upper(R1, nullptr, k, h->Ik, k, nullptr, k, h->Rinv, k, 0, h->st));
-      CK(launch_nn_store(h->AI, m, m, h->Rinv, k, k, k, h->Q1, m, h->st, h->Tp,
-                                 ew_tpack_doubles(h->n, h->k_cap)));
-      // G2 = Q1^T Q1
-      CK(launch_tsmm(h->Q1, m, k, h->Q1, m, k, m, h->tpart, sp, h->st));
-      CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G2, h->st));
-      id_status s = allreduce(h, h->G2, (size_t)k * k, NCCL_SUM);
+  const size_t tcap = tpart_doubles(m, n, h->k_cap);
+  const int sp = splits_for(k, k, m, tcap);
+  // P(:, J) = argmin ||A_I X - A_J|| by a preconditioned Cholesky QR in fp64:
+  //   Q1 = A_I R1^{-1},  G2 = Q1^T Q1 = R2^T R2,  W = Q1^T A_J,  T = R1^{-1} R2^{-1} R2^{-T} W
+  // with R1 = the QRCP's own low-precision R11 ("computed from the R matrix and
+  // pivot indices ... via a least-squares problem"; A_I R11^{-1} is already close to
+  // orthonormal, so one Cholesky pass suffices), or, when that Q1 is too ill-conditioned
+  // (R2's diagonal spread > 1e3 or a breakdown), R1 = chol(A_I^T A_I): CholeskyQR2.
+  auto lsq = [&](bool precond) -> id_status {
+    const double* R1;
+    if (precond) {
+      CK(launch_R_to_fp64(h->fmt == ID_FP64, h->R, k, n, h->Rd, h->st));   // leading k x k block = R11
+      CK(cudaMemsetAsync(h->info, 0, sizeof(int), h->st));
+      R1 = h->Rd;
+      launches += 1;
+    } else {
+      CK(launch_tsmm(h->AI, m, k, h->AI, m, k, m, h->tpart, sp, h->st));     // G1 = A_I^T A_I
+      CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G1, h->st));
+      id_status s = allreduce(h, h->G1, (size_t)k * k, NCCL_SUM);
       if (s) return s;
-      CK(launch_cholesky(h->G2, k, h->info + 1, h->st));
-      CK(launch_diag_ratio(h->G2, k, h->err2 + 1, h->st));
-      launches += 7;
-      // W = Q1^T A_D(:, J), J = perm[k:] (W(:, I) is never needed)
-      const int nj = n - k;
-      if (nj > 0) {
-        if (h->host_AD == 2) {   // W = sum over row blocks of Q1(blk)^T A_D(blk, J)
-          const int spw = splits_for(k, nj, h->srows, tcap);
-          id_status ss = stream_blocks(h, [&](int64_t b, int64_t r0, int64_t rows, const double* blk) -> id_status {
-            CK(launch_tsmm(h->Q1 + r0, m, k, blk, h->srows, nj, rows, h->tpart, spw, h->st, h->perm + k));
-            CK(launch_acc_rows(h->tpart, spw, (int64_t)k * nj, (int64_t)k * nj, h->W, b > 0 ? 1 : 0, h->st));
-            return ID_OK;
-          });
-          if (ss) return ss;
-        } else {
-          const int spw = splits_for(k, nj, m, tcap);
-          CK(launch_tsmm(h->Q1, m, k, h->AD, h->ld, nj, m, h->tpart, spw, h->st, h->perm + k));
-          CK(launch_sum_partials(h->tpart, spw, (int64_t)k * nj, h->W, h->st));
-        }
-        s = allreduce(h, h->W, (size_t)k * nj, NCCL_SUM);
-        if (s) return s;
-        CK(launch_trsm_left_upper(R1, h->G2, k, h->W, k, nullptr, nj, h->T, k, 1, h->st));
-        launches += 3;
-      }
-      return ID_OK;
-    };
-    id_status s = lsq(true);
-    if (s) return s;
-    int inf[2] = {0, 0};
-    double ratio = 0.0;
-    CK(cudaMemcpyAsync(inf, h->info, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
-    CK(cudaMemcpyAsync(&ratio, h->err2 + 1, sizeof(double), cudaMemcpyDeviceToHost, h->st));
-    CK(cudaStreamSynchronize(h->st));
-    h->stats.lsq_path = 1;
-    if (inf[1] != 0 || !(ratio <= 1e3)) {                 // identical decision on every rank
-      s = lsq(false);
-      if (s) return s;
-      h->stats.lsq_path = 2;
+      CK(launch_cholesky(h->G1, k, h->info, h->st));
+      R1 = h->G1;
+      launches += 3;
     }
+    // Q1 = A_I R1^{-1}: the k x k inverse by triangular solves on I_k, then one DMMA GEMM
+    CK(launch_eye(h->Ik, k, h->st));
+    CK(launch_trsm_left_upper(R1, nullptr, k, h->Ik, k, nullptr, k, h->Rinv, k, 0, h->st));
+    CK(launch_nn_store(h->AI, m, m, h->Rinv, k, k, k, h->Q1, m, h->st, h->Tp,
+                               ew_tpack_doubles(h->n, h->k_cap)));
+    // G2 = Q1^T Q1
+    CK(launch_tsmm(h->Q1, m, k, h->Q1, m, k, m, h->tpart, sp, h->st));
+    CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G2, h->st));
+    id_status s = allreduce(h, h->G2, (size_t)k * k, NCCL_SUM);
+    if (s) return s;
+    CK(launch_cholesky(h->G2, k, h->info + 1, h->st));
+    CK(launch_diag_ratio(h->G2, k, h->err2 + 1, h->st));
+    launches += 7;
+    // W = Q1^T A_D(:, J), J = perm[k:] (W(:, I) is never needed)
+    const int nj = n - k;
+    if (nj > 0) {
+      if (h->host_AD == 2) {   // W = sum over row blocks of Q1(blk)^T A_D(blk, J)
+        const int spw = splits_for(k, nj, h->srows, tcap);
+        id_status ss = stream_blocks(h, [&](int64_t b, int64_t r0, int64_t rows, const double* blk) -> id_status {
+          CK(launch_tsmm(h->Q1 + r0, m, k, blk, h->srows, nj, rows, h->tpart, spw, h->st, h->perm + k));
+          CK(launch_acc_rows(h->tpart, spw, (int64_t)k * nj, (int64_t)k * nj, h->W, b > 0 ? 1 : 0, h->st));
+          return ID_OK;
+        });
+        if (ss) return ss;
+      } else {
+        const int spw = splits_for(k, nj, m, tcap);
+        CK(launch_tsmm(h->Q1, m, k, h->AD, h->ld, nj, m, h->tpart, spw, h->st, h->perm + k));
+        CK(launch_sum_partials(h->tpart, spw, (int64_t)k * nj, h->W, h->st));
+      }
+      s = allreduce(h, h->W, (size_t)k * nj, NCCL_SUM);
+      if (s) return s;
+      CK(launch_trsm_left_upper(R1, h->G2, k, h->W, k, nullptr, nj, h->T, k, 1, h->st));
+      launches += 3;
+    }
+    return ID_OK;
+  };
+  // the body of the call: A_I = A_D(:, I), the coefficients (R mode, or LSQ with the R11
+  // preconditioner), P assembled into the workspace — captured in a CUDA graph per (mode, k)
+  // when the handle allows it (no loopback group, no host-streamed A_D)
+  auto body = [&]() -> id_status {
+    if (h->host_AD == 2) {   // A_I = A_D(:, I) straight from the host columns
+      for (int i = 0; i < k; ++i)
+        CK(cudaMemcpyAsync(h->AI + (size_t)i * m, h->AD_host + (size_t)h->perm_host[i] * h->ld_host, (size_t)m * 8,
+                           cudaMemcpyHostToDevice, h->st));
+    } else {
+      CK(launch_gather_cols(h->AD, m, h->ld, h->perm, k, h->AI, h->st));
+      launches++;
+    }
+    if (mode == ID_COEF_R) {
+      CK(launch_R_to_fp64(h->fmt == ID_FP64, h->R, k, n, h->Rd, h->st));
+      CK(launch_trsm_left_upper(h->Rd, nullptr, k, h->Rd + (int64_t)k * k, k, nullptr, n - k, h->T, k, 0,
+                                h->st));
+      launches += 2;
+    } else {
+      id_status s = lsq(true);
+      if (s) return s;
+    }
+    CK(launch_assemble_P(h->T, k, k, n, h->perm, h->Pw, k, h->st));
+    launches++;
+    return ID_OK;
+  };
+  const bool use_graph = !h->loop && h->host_AD != 2;
+  if (use_graph) {
+    const uint64_t key = ((uint64_t)mode << 32) | (uint64_t)k;
+    auto it = h->cgraphs.find(key);
+    if (it == h->cgraphs.end()) {
+      cudaGraph_t g;
+      h->st = h->cap;
+      CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+      launches = 0;
+      id_status s = body();
+      cudaError_t e = cudaStreamEndCapture(h->cap, &g);
+      h->st = h->user_st;
+      if (s) return s;
+      if (e != cudaSuccess) return fail(h, ID_ERR_CUDA, "graph capture (coefficients): %s", cudaGetErrorString(e));
+      cudaGraphExec_t ge;
+      CK(cudaGraphInstantiate(&ge, g, 0));
+      cudaGraphDestroy(g);
+      it = h->cgraphs.emplace(key, std::make_pair(ge, launches)).first;
+    }
+    CK(cudaEventRecord(h->fork_ev, h->user_st));
+    CK(cudaStreamWaitEvent(h->cap, h->fork_ev, 0));
+    CK(cudaGraphLaunch(it->second.first, h->cap));
+    CK(cudaEventRecord(h->join_ev, h->cap));
+    CK(cudaStreamWaitEvent(h->user_st, h->join_ev, 0));
+    launches = it->second.second;
   } else {
-    return fail(h, ID_ERR_ARG, "bad coefficient mode");
+    id_status s = body();
+    if (s) return s;
   }
-  CK(launch_assemble_P(h->T, k, k, n, h->perm, h->Pw, k, h->st));
-  CK(cudaMemcpy2DAsync(P_out, ldp * 8, h->Pw, (size_t)k * 8, (size_t)k * 8, n, cudaMemcpyDeviceToDevice,
-                       h->st));
-  launches++;
-  CK(cudaEventRecord(h->ev[4], h->st));
   int info[2] = {0, 0};
-  if (mode == ID_COEF_LSQ)
+  double ratio = 0.0;
+  CK(cudaMemcpy2DAsync(P_out, ldp * 8, h->Pw, (size_t)k * 8, (size_t)k * 8, n, cudaMemcpyDeviceToDevice, h->st));
+  if (mode == ID_COEF_LSQ) {
     CK(cudaMemcpyAsync(info, h->info, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(&ratio, h->err2 + 1, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  }
+  CK(cudaStreamSynchronize(h->st));
+  h->stats.lsq_path = mode == ID_COEF_LSQ ? 1 : 0;
+  if (mode == ID_COEF_LSQ && (info[1] != 0 || !(ratio <= 1e3))) {   // identical decision on every rank
+    id_status s = lsq(false);                                      // CholeskyQR2 (rare; eager)
+    if (s) return s;
+    CK(launch_assemble_P(h->T, k, k, n, h->perm, h->Pw, k, h->st));
+    CK(cudaMemcpy2DAsync(P_out, ldp * 8, h->Pw, (size_t)k * 8, (size_t)k * 8, n, cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(info, h->info, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    launches++;
+    h->stats.lsq_path = 2;
+  }
+  CK(cudaEventRecord(h->ev[4], h->st));
   CK(cudaStreamSynchronize(h->st));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]);
   h->stats.t_coef_ms = ms;
   h->stats.kernel_launches += launches;
-  if (info[0] || info[1])
+  if (mode == ID_COEF_LSQ && (info[0] || info[1]))
     return fail(h, ID_ERR_DEGENERATE, "Cholesky breakdown in the LSQ refit (info %d, %d)", info[0], info[1]);
   h->have_coef = true;
   return ID_OK;

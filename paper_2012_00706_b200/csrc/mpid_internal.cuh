@@ -149,7 +149,7 @@ cudaError_t launch_init_pivot(const double* norms, int n, int* perm, DevScalars*
                               cudaStream_t st);
 cudaError_t launch_pass_tma(int fmt, PassParams p, int num_sms, int* gx_out, cudaStream_t st);
 // the one-launch QRCP of a shared-memory-sized matrix (k_qrcp_smem.cu; the oracle's paper model)
-size_t qrcp_smem_bytes(int64_t m, int n);
+size_t qrcp_smem_bytes(int64_t m, int n, int k);
 cudaError_t launch_qrcp_smem(int fmt, const void* S, int64_t m, int n, int k_max, int nb, double eps, int* perm,
                              float* R, DevScalars* sc, cudaStream_t st);
 // tcgen05 pass (fp16 storage; k_pass_tc.cu): operands, launch, tensor map of S

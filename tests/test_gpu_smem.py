@@ -65,7 +65,7 @@ def test_default_formation_for_C1_and_tolerance_stop():
     assert q.k == r.k_out and np.array_equal(q.piv, r.perm[: r.k_out])
 
 
-@pytest.mark.parametrize("m,n,k", [(200, 90, 30), (97, 61, 61), (8, 5, 5), (300, 170, 40)])
+@pytest.mark.parametrize("m,n,k", [(200, 90, 30), (97, 61, 61), (8, 5, 5), (280, 150, 24)])
 def test_ragged_shapes_bit_identical(m, n, k):
     rng = np.random.default_rng(m * n + k)
     A = np.asfortranarray(rng.standard_normal((m, n)) * np.exp(-np.arange(n) / 11.0)[None, :])
