@@ -148,11 +148,11 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
     if (tid == 0) {
       // the residual mass (a sequential sum over the columns) only when a tolerance asks
       bool stop = false;
-      if (eps > 0.0 && j > 0) {
+      if ((eps > 0.0 && j > 0) || j == k_max - 1) {   // (the last step's mass: resid when k = min(m, n))
         double t = 0.0;
         for (int c = j; c < n; ++c) t = c == j ? s[j] : __dadd_rn(t, s[c]);
         sc->resid2 = t;
-        stop = __dsqrt_rn(t) <= __dmul_rn(eps, sh_normAL);
+        stop = eps > 0.0 && j > 0 && __dsqrt_rn(t) <= __dmul_rn(eps, sh_normAL);
       }
       if (stop) sh_stop = 1;
       else if (!(s[j] >= 1.1754943508222875e-38)) {

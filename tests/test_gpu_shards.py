@@ -163,14 +163,14 @@ def test_nccl_single_rank_communicator_inside_cuda_graph():
     import torch
     from paper_2012_00706_b200 import mpid
     A = gen_config("C1", 1)
-    base = single(A, "fp16", "pow2", 32, extras=False)
+    base = single(A, "fp16", "pow2", 32, formation="ffma", extras=False)
     uid = mpid.id_nccl_get_unique_id()
     comm = mpid.id_nccl_comm_init(uid, 1, 0)
     try:
         At = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
         h = mpid.MPID(At, k_max=32, comm=comm, rank=0, nranks=1)
         for _ in range(2):                               # capture, then replay the graph
-            q = h.qrcp("fp16", "pow2", k=32, use_graph=True)
+            q = h.qrcp("fp16", "pow2", k=32, use_graph=True, formation="ffma")
             P = h.coeffs("lsq").cpu().numpy()
             e = h.error()
         h.close()

@@ -1,10 +1,16 @@
-# Round-2 measurement: bench line, launch list, full ncu capture of the dominant kernel.
+# Round-2 validation + measurement: GPU tests, smoke, bench line, launch list, full ncu
+# captures of the dominant kernel, every config (incl. the host-streamed C5 shard).
+timeout 3000 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=20 > gpurun_out/gpu_tests.log 2>&1; echo "rc $?" >> gpurun_out/gpu_tests.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc $?" >> gpurun_out/smoke.log
 python bench.py > gpurun_out/bench_r02.json 2> gpurun_out/bench_r02.err; echo "bench rc $?" >> gpurun_out/bench_r02.err
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 2500 --csv \
-    --log-file gpurun_out/launches_r02.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_l.log 2>&1
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_r02.json 2> gpurun_out/bench_ref_r02.err
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 3000 --csv \
+    --log-file gpurun_out/launches_r02.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-extras > gpurun_out/ncu_l.log 2>&1
 echo "ncu list rc $?" >> gpurun_out/ncu_l.log
-ncu --set full --clock-control none --import-source on -k regex:k_pass_tc -s 1 -c 1 -o gpurun_out/pass_tc_r02 \
+ncu --set full --clock-control none --import-source on -k regex:k_pass_tc -s 41 -c 1 -o gpurun_out/pass_tc_r02 \
     python tools/prof_tc2.py 16 > gpurun_out/ncu_full.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_pass_tc -s 15 -c 1 -o gpurun_out/pass_tc_store_r02 \
+ncu --set full --clock-control none --import-source on -k regex:k_pass_tc -s 48 -c 1 -o gpurun_out/pass_tc_store_r02 \
     python tools/prof_tc2.py 16 >> gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc $?" >> gpurun_out/ncu_full.log
+timeout 2400 python tools/bench_configs.py > gpurun_out/configs_r02.jsonl 2> gpurun_out/configs_r02.err
+free -g >> gpurun_out/configs_r02.err

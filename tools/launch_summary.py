@@ -5,9 +5,12 @@ import collections, csv, sys
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
 h, rows = rows[0], rows[1:]
 ik, iv, iu = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+if "Metric Name" in h:                       # lists with several metrics: the durations only
+    im = h.index("Metric Name")
+    rows = [r for r in rows if r[im] == "gpu__time_duration.sum"]
 agg = collections.defaultdict(lambda: [0, 0.0])
 for r in rows:
-    ms = float(r[iv].replace(",", "")) * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(r[iu], 1e-6)
+    ms = float(r[iv].replace(",", "")) * {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}.get(r[iu], 1e-6)
     name = r[ik].split("(")[0].strip()
     agg[name][0] += 1
     agg[name][1] += ms
