@@ -256,6 +256,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  double aw[TPG], as[TPG];                       // epilogue: the column sums of its tiles
+#pragma unroll
+  for (int z = 0; z < TPG; ++z) { aw[z] = 0.0; as[z] = 0.0; }
   if (warp == 0) {
     // ============================ TMA producer ============================
     // the whole warp walks the loop (warp-uniform values stay in uniform registers); one
@@ -436,9 +439,6 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
     const int grp = e / EPI_GW;                 // tiles t = grp, grp + 2, ...
     const int hf = (e >> 2) & 1;                // rows [64 hf, 64 hf + 64) of a unit
     const int q = warp & 3;                     // TMEM lane quarter (hardware: warp % 4)
-    double aw[TPG], as[TPG];
-#pragma unroll
-    for (int z = 0; z < TPG; ++z) { aw[z] = 0.0; as[z] = 0.0; }
     for (int rbi = 0; rbi < nrbc; ++rbi) {
       const int64_t r0 = (p.rb_first + rb0 + rbi) * R_B;   // first local row of the block
       const bool mask = jl > r0;                           // rows < j inside this block
@@ -527,23 +527,45 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
       __syncwarp();
       if (lane == 0) mbar_arrive(&ufree[ub]);
     }
-    // the CTA's column partials, one row of the partials buffer per row half
-    // (k_pass_reduce adds the 2 gridDim.x rows in fixed order)
-    int ti = 0;
-    for (int t = grp; t < ntiles; t += NGRP, ++ti) {
-      const int c = j + t * C_T + q * 32 + lane;
-      double w = 0.0, s = 0.0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();   // every role is done: the smem ring (and its async stores) is idle
+  // the CTA's column partials: the two row halves of each column added in fixed order
+  // (half 0 + half 1) through shared memory, one partials row per CTA
+  {
+    const int e = warp - 2;
+    const bool epi = warp >= 2 && warp < 2 + EPI_WARPS;
+    const int grp = e / EPI_GW, hf = (e >> 2) & 1, q = warp & 3;
+    double* red = reinterpret_cast<double*>(smem);          // [NGRP][TPG][128][2]
+    if (epi && hf == 1) {
+      int ti = 0;
+      for (int t = grp; t < ntiles; t += NGRP, ++ti) {
+        double w = 0.0, s2 = 0.0;
 #pragma unroll
-      for (int z = 0; z < TPG; ++z)
-        if (z == ti) { w = aw[z]; s = as[z]; }
-      if (c < n) {
-        p.part[((int64_t)(2 * blockIdx.x + hf) * 2 + 0) * n + c] = w;
-        p.part[((int64_t)(2 * blockIdx.x + hf) * 2 + 1) * n + c] = s;
+        for (int z = 0; z < TPG; ++z)
+          if (z == ti) { w = aw[z]; s2 = as[z]; }
+        double* r = red + (((size_t)grp * TPG + ti) * C_T + q * 32 + lane) * 2;
+        r[0] = w;
+        r[1] = s2;
+      }
+    }
+    __syncthreads();
+    if (epi && hf == 0) {
+      int ti = 0;
+      for (int t = grp; t < ntiles; t += NGRP, ++ti) {
+        const int c = j + t * C_T + q * 32 + lane;
+        double w = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int z = 0; z < TPG; ++z)
+          if (z == ti) { w = aw[z]; s2 = as[z]; }
+        const double* r = red + (((size_t)grp * TPG + ti) * C_T + q * 32 + lane) * 2;
+        if (c < n) {
+          p.part[((int64_t)blockIdx.x * 2 + 0) * n + c] = w + r[0];
+          p.part[((int64_t)blockIdx.x * 2 + 1) * n + c] = s2 + r[1];
+        }
       }
     }
   }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
@@ -590,7 +612,7 @@ cudaError_t launch_pass_tc(const PassParams& pp, int nb, void* Vop, const void* 
   p.xr = pp.xr;
   p.sc = pp.sc;
   const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(max_ctas / 2, p.nrb));
-  *gx_out = 2 * gx;                                   // partial rows: 2 per CTA (row halves)
+  *gx_out = gx;
   const bool wide = p.ntiles > 2 * 4;
   const void* fn = wide ? (const void*)k_pass_tc<8> : (const void*)k_pass_tc<4>;
   cudaError_t e = smem_attr(fn, smem);

@@ -136,13 +136,13 @@ __device__ __forceinline__ int fop_off(int i, int l) {
   return (i >> 3) * 256 + ((l >> 3) & 1) * 128 + (i & 7) * 16 + (l & 7) * 2;
 }
 __device__ void build_fop(const float* __restrict__ F, const double* __restrict__ cvec, int n, int jn, int nb,
-                          unsigned char* __restrict__ Fop) {
+                          unsigned char* __restrict__ Fop, int t0, int nthreads) {
   const int j0 = jn == 0 ? 0 : nb * ((jn - 1) / nb);
   const int npend = jn - j0;
   const int kchw = (nb + 15) / 16, KW = kchw * 16;
   const int ntiles = (n - jn + 127) / 128;
   const int tot = ntiles * 128 * KW;
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+  for (int e = t0; e < tot; e += nthreads) {
     const int l = e % KW, tc = e / KW;
     const int c = tc % 128, tt = tc / 128;
     const int col = jn + tt * 128 + c;
@@ -250,12 +250,7 @@ __global__ void __launch_bounds__(1024) k_reflector(const double* __restrict__ r
     sc->pivot = best.pos;
     if (j + 1 >= k_max || best.pos < 0) sc->done = 1;
   }
-  if constexpr (sizeof(W) == 4) {
-    if (Fop && jn < k_max && best.pos >= 0) {   // the tcgen05 pass: step jn's F operand, in its column order
-      __syncthreads();
-      build_fop(reinterpret_cast<const float*>(F), cvec, n, jn, nb, Fop);
-    }
-  }
+  (void)Fop;
 }
 
 // initial pivot: argmax of the initial column norms (ties lowest index); perm = identity
@@ -291,8 +286,15 @@ __global__ void __launch_bounds__(1024) k_init_pivot(const double* __restrict__ 
 template <typename T, typename W>
 __global__ void k_swap(T* __restrict__ S, int64_t ngroups, int n, int jn, int j0,
                        W* __restrict__ F, W* __restrict__ R, int* __restrict__ perm,
-                       T* __restrict__ Sj, const DevScalars* __restrict__ sc) {
+                       T* __restrict__ Sj, const DevScalars* __restrict__ sc, int nsw, unsigned char* __restrict__ Fop,
+                       const double* __restrict__ cvec, int nb) {
   if (sc->done) return;
+  if ((int)blockIdx.x >= nsw) {   // the tcgen05 pass's F operand of step jn (its column order)
+    if constexpr (sizeof(W) == 4)
+      build_fop(reinterpret_cast<const float*>(F), cvec, n, jn, nb, Fop, (blockIdx.x - nsw) * blockDim.x + threadIdx.x,
+                (gridDim.x - nsw) * blockDim.x);
+    return;
+  }
   const int p = sc->pivot;
   if (p < 0) return;
   const bool sw = p != jn;
@@ -346,18 +348,22 @@ cudaError_t launch_init_pivot(const double* norms, int n, int* perm, DevScalars*
 }
 
 cudaError_t launch_swap(int fmt, void* S, int64_t ngroups, int n, int jn, int j0, int steps_done,
-                        void* F, void* R, int* perm, void* Sj, DevScalars* sc, cudaStream_t st) {
+                        void* F, void* R, int* perm, void* Sj, DevScalars* sc, cudaStream_t st, void* Fop,
+                        const double* cvec, int nb) {
   (void)steps_done;
-  const unsigned nb = (unsigned)((ngroups + 255) / 256);
+  const unsigned nsw = (unsigned)((ngroups + 255) / 256);
+  // + the F operand blocks (tcgen05 pass, from the second step: the first has no pending reflector)
+  const unsigned nfo = (Fop && jn > 0) ? (unsigned)((((n - jn + 127) / 128) * 128 * ((nb + 15) / 16) * 16 + 255) / 256) : 0u;
+  const unsigned nbk = nsw + nfo;
   if (fmt == 1)
-    k_swap<__half, float><<<nb, 256, 0, st>>>((__half*)S, ngroups, n, jn, j0, (float*)F, (float*)R, perm,
-                                               (__half*)Sj, sc);
+    k_swap<__half, float><<<nbk, 256, 0, st>>>((__half*)S, ngroups, n, jn, j0, (float*)F, (float*)R, perm,
+                                               (__half*)Sj, sc, (int)nsw, (unsigned char*)Fop, cvec, nb);
   else if (fmt == 2)
-    k_swap<float, float><<<nb, 256, 0, st>>>((float*)S, ngroups, n, jn, j0, (float*)F, (float*)R, perm,
-                                              (float*)Sj, sc);
+    k_swap<float, float><<<nbk, 256, 0, st>>>((float*)S, ngroups, n, jn, j0, (float*)F, (float*)R, perm,
+                                              (float*)Sj, sc, (int)nsw, (unsigned char*)Fop, cvec, nb);
   else
-    k_swap<double, double><<<nb, 256, 0, st>>>((double*)S, ngroups, n, jn, j0, (double*)F, (double*)R, perm,
-                                                (double*)Sj, sc);
+    k_swap<double, double><<<nsw, 256, 0, st>>>((double*)S, ngroups, n, jn, j0, (double*)F, (double*)R, perm,
+                                                (double*)Sj, sc, (int)nsw, nullptr, cvec, nb);
   return cudaGetLastError();
 }
 

@@ -809,7 +809,8 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     // the pivot's S data (its F / R / perm bookkeeping was swapped by the last k_reflector);
     // an in-pass-prologue variant measured no faster: its scattered 16-byte accesses
     // delay the CTA's TMA stream by as much as the separate launch costs
-    CK(launch_swap(fmt, h->S, h->m_pad / 8, (int)n, j, j0, j, h->F, h->R, h->perm, nullptr, h->sc, h->st));
+    CK(launch_swap(fmt, h->S, h->m_pad / 8, (int)n, j, j0, j, h->F, h->R, h->perm, nullptr, h->sc, h->st,
+                   formation == 2 ? h->Fop : nullptr, h->cvec, nb));
     h->kernel_launches += 1;
     PassParams p{};
     p.S = h->S;
@@ -832,7 +833,7 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     p.sc = h->sc;
     int gx_used = 0;
     // (tcgen05 pass: the V operand column of u_{j-1} was written by the previous pass, the
-    // step's F operand by the previous k_reflector)
+    // step's F operand is laid out by extra blocks of k_swap)
     if (formation == 2 && h->tmap_ok != 0) return fail(h, ID_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", h->tmap_ok);
     if (profile) CK(rec(h, h->pass_ev[2 * j]));
     if (formation == 2) CK(launch_pass_tc(p, nb, h->Vop, h->Fop, h->tmapS, h->tmapC, pass_gx_cap(), &gx_used, h->st));
@@ -845,7 +846,7 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     s = allreduce(h, h->red, (size_t)3 * n, NCCL_SUM);
     if (s) return s;
     CK(launch_reflector(fmt, h->red, (int)n, j, k_max, nb, h->F, h->R, h->beta, h->cvec, h->tau, h->perm,
-                        h->sc, h->st, formation == 2 ? h->Fop : nullptr));
+                        h->sc, h->st));
     h->kernel_launches += 3;
     h->pass_launches += 1;
   }

@@ -166,8 +166,10 @@ cudaError_t launch_pass_reduce(const double* part, int gx, int n, int j, const d
 cudaError_t launch_reflector(int fmt, const double* red, int n, int j, int k_max, int nb, void* F, void* R,
                              double* beta, double* cvec, double* tau, int* perm, DevScalars* sc,
                              cudaStream_t st, void* Fop = nullptr);
+// + (Fop != nullptr) the tcgen05 pass's F operand of step jn, laid out by extra blocks
 cudaError_t launch_swap(int fmt, void* S, int64_t ngroups, int n, int jn, int j0, int steps_done,
-                        void* F, void* R, int* perm, void* Sj, DevScalars* sc, cudaStream_t st);
+                        void* F, void* R, int* perm, void* Sj, DevScalars* sc, cudaStream_t st, void* Fop = nullptr,
+                        const double* cvec = nullptr, int nb = 16);
 cudaError_t launch_export_S(int fmt, const void* S, int64_t m_local, int n, void* out, int64_t ld,
                             cudaStream_t st);
 
