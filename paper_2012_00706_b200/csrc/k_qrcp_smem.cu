@@ -36,7 +36,8 @@ template <> __device__ __forceinline__ float ld_s<float>(const float* S, int64_t
 // R [k][n] fp32 (written to global memory at the end)
 size_t qrcp_smem_bytes(int64_t m, int n, int k) {
   const int64_t m8 = (m + 7) / 8 * 8;
-  return (size_t)n * (m8 + 1) * 4 + 8 + (size_t)5 * n * 8 + (size_t)m8 * 4 + (size_t)n * 8 + (size_t)k * n * 4 + 64;
+  return (size_t)n * (m8 + 1) * 4 + 8 + (size_t)5 * n * 8 + (size_t)m8 * 4 + (size_t)n * 8 + (size_t)k * n * 4 + 64 +
+         (size_t)m8 * 8 + 16;
 }
 
 template <typename T>
@@ -57,14 +58,15 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
   float* f = v + m8;
   int* pm = reinterpret_cast<int*>(f + n);
   float* Rs = reinterpret_cast<float*>(pm + n);
+  double* u64 = reinterpret_cast<double*>(smem + ((((size_t)n * ldw * 4 + 15) & ~(size_t)15) + (size_t)5 * n * 8 +
+                                                   (size_t)m8 * 4 + (size_t)n * 8 + (size_t)k_max * n * 4 + 15) / 16 * 16);
   __shared__ int sh_p, sh_stop;
   __shared__ double sh_beta, sh_cc, sh_normAL;
   const int tid = threadIdx.x, nt = blockDim.x;
 
-  for (int64_t e = tid; e < (int64_t)n * m8; e += nt) {
-    const int c = (int)(e / m8), r = (int)(e - (int64_t)c * m8);
-    W[(int64_t)c * ldw + r] = r < m ? ld_s<T>(S, r, c, n) : 0.f;
-  }
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  for (int c = warp; c < n; c += nw)
+    for (int r = lane; r < m8; r += 32) W[c * ldw + r] = r < m ? ld_s<T>(S, r, c, n) : 0.f;
   for (int c = tid; c < n; c += nt) pm[c] = c;
   __syncthreads();
   for (int c = tid; c < n; c += nt) {              // exact initial norms^2, row order
@@ -123,19 +125,18 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
     }
     __syncthreads();
     if (store16 && j > 0 && j % nb == 0) {          // the storage rounding point (reading R4)
-      const int rows = m8 - jl;
-      for (int64_t e = tid; e < (int64_t)(n - j) * rows; e += nt) {
-        const int c = j + (int)(e / rows), r = jl + (int)(e % rows);
-        W[(int64_t)c * ldw + r] = __half2float(__float2half_rn(W[(int64_t)c * ldw + r]));
-      }
+      for (int c = j + warp; c < n; c += nw)
+        for (int r = jl + lane; r < m8; r += 32) W[c * ldw + r] = __half2float(__float2half_rn(W[c * ldw + r]));
       __syncthreads();
     }
+    for (int r = g0 + tid; r < m8; r += nt) u64[r] = r < jl ? 0.0 : (double)W[j * ldw + r];
+    __syncthreads();
     for (int c = j + tid; c < n; c += nt) {         // s_i, w_i: exact products, fp64, row order
       double ss = 0.0, ww = 0.0;
 #pragma unroll 8
       for (int r = g0; r < m8; ++r) {
-        const double a = r < jl ? 0.0 : (double)W[(int64_t)c * ldw + r];
-        const double u = r < jl ? 0.0 : (double)W[(int64_t)j * ldw + r];
+        const double a = r < jl ? 0.0 : (double)W[c * ldw + r];
+        const double u = u64[r];
         const double ps = __dmul_rn(a, a), pw = __dmul_rn(a, u);
         if (r == g0) { ss = ps; ww = pw; }
         else { ss = __dadd_rn(ss, ps); ww = __dadd_rn(ww, pw); }
@@ -191,13 +192,9 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
     __syncthreads();
     if (tid == 0) v[jl] = 1.f;
     __syncthreads();
-    {                                               // W(j:, j:) <- fl(W - fl(v f))
-      const int rows = m8 - jl;
-      for (int64_t e = tid; e < (int64_t)(n - j) * rows; e += nt) {
-        const int c = j + (int)(e / rows), r = jl + (int)(e % rows);
-        float* a = &W[(int64_t)c * ldw + r];
-        *a = __fsub_rn(*a, __fmul_rn(v[r], f[c]));
-      }
+    for (int c = j + warp; c < n; c += nw) {       // W(j:, j:) <- fl(W - fl(v f))
+      const float fc = f[c];
+      for (int r = jl + lane; r < m8; r += 32) W[c * ldw + r] = __fsub_rn(W[c * ldw + r], __fmul_rn(v[r], fc));
     }
     __syncthreads();
   }

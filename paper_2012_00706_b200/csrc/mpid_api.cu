@@ -1399,6 +1399,7 @@ void id_loopback_destroy(void* comm) {
   delete (LoopComm*)comm;
 }
 
+
 int32_t id_nccl_unique_id_bytes(void) { return 128; }
 
 id_status id_nccl_get_unique_id(void* out) {
