@@ -999,10 +999,12 @@ __global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ G, int k
     const double djj = L[j + (int64_t)j * k];
     for (int i = j + 1 + threadIdx.x; i < k; i += blockDim.x) L[i + (int64_t)j * k] /= djj;
     __syncthreads();
-    const int w = k - j - 1;
-    for (int64_t idx = threadIdx.x; idx < (int64_t)w * w; idx += blockDim.x) {
-      const int i = j + 1 + (int)(idx % w), l = j + 1 + (int)(idx / w);
-      if (l <= i) L[i + (int64_t)l * k] -= L[i + (int64_t)j * k] * L[l + (int64_t)j * k];
+    {   // trailing update, warps over columns l, lanes over rows i >= l (no integer division)
+      const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+      for (int l = j + 1 + (threadIdx.x >> 5); l < k; l += nw) {
+        const double ljl = L[l + (int64_t)j * k];
+        for (int i = l + lane; i < k; i += 32) L[i + (int64_t)l * k] -= L[i + (int64_t)j * k] * ljl;
+      }
     }
     __syncthreads();
   }
@@ -1107,14 +1109,24 @@ __global__ void __launch_bounds__(1024) k_trsm_left_block(const double* __restri
                                                           const int* __restrict__ map, int ncols,
                                                           double* __restrict__ T, int64_t ldt,
                                                           int mode) {
-  extern __shared__ double sb[];  // [k][33]
+  extern __shared__ double sb[];  // [k][33], then (k <= 128) the triangular factor in use, k x k
+  double* su = sb + (size_t)k * 33;
+  const bool u_smem = k <= 128;
   const int c = threadIdx.x & 31, rg = threadIdx.x >> 5;  // column in block, row group (32)
   const int col = blockIdx.x * 32 + c;
   const bool valid = col < ncols;
   const int64_t src = valid ? (int64_t)(map ? map[col] : col) : 0;
   for (int r = rg; r < k; r += 32) sb[r * 33 + c] = valid ? B[src * ldb + r] : 0.0;
   __syncthreads();
+  auto stage = [&](const double* U) -> const double* {   // the factor into shared memory (k <= 128)
+    if (!u_smem) return U;
+    __syncthreads();
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) su[e] = U[e];
+    __syncthreads();
+    return su;
+  };
   auto back = [&](const double* U) {          // solve U x = b (upper), column sweep
+    U = stage(U);
     for (int i = k - 1; i >= 0; --i) {
       const double xi = sb[i * 33 + c] / U[i + (int64_t)i * k];
       __syncthreads();
@@ -1124,6 +1136,7 @@ __global__ void __launch_bounds__(1024) k_trsm_left_block(const double* __restri
     }
   };
   auto fwdT = [&](const double* U) {          // solve U^T x = b (lower), column sweep
+    U = stage(U);
     for (int i = 0; i < k; ++i) {
       const double xi = sb[i * 33 + c] / U[i + (int64_t)i * k];
       __syncthreads();
@@ -1238,7 +1251,7 @@ cudaError_t launch_trsm_left_upper(const double* R1, const double* R2, int k, co
                                    int64_t ldb, const int* map, int ncols, double* T, int64_t ldt,
                                    int mode, cudaStream_t st) {
   if (ncols <= 0) return cudaSuccess;
-  const size_t smem = (size_t)k * 33 * sizeof(double);
+  const size_t smem = (size_t)k * 33 * sizeof(double) + (k <= 128 ? (size_t)k * k * sizeof(double) : 0);
   cudaError_t e = smem_attr((const void*)k_trsm_left_block, 200 * 1024);
   if (e != cudaSuccess) return e;
   k_trsm_left_block<<<(unsigned)((ncols + 31) / 32), 1024, smem, st>>>(R1, R2, k, B, ldb, map, ncols,
