@@ -131,7 +131,10 @@ typedef struct {
   int32_t formation;     /* formation used by the last QRCP (see id_qrcp_opts) */
   int32_t lsq_path;      /* last id_coeffs_fp64: 0 R mode, 1 LSQ preconditioned by the QRCP's R11
                             (one Cholesky QR pass), 2 LSQ by CholeskyQR2 (fallback) */
-  int32_t reserved[3];
+  int32_t fp64_engine;     /* engine of the last id_coeffs_fp64's LSQ GEMMs (W, G2): 1 DMMA, 2 int8
+                              tensor cores (Ozaki scheme; id_set_fp64_engine); 0 for R mode */
+  int32_t fp64_engine_err; /* engine of the last id_error's fused GEMM (1 DMMA, 2 int8 Ozaki) */
+  int32_t reserved[1];
   double t_host_launch_ms; /* host time of the QRCP graph launch call */
   double t_call_gpu_ms;    /* device time of the whole id_qrcp_lowprec call on the caller's stream */
 } id_stats;
@@ -207,6 +210,20 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
 /* Step 4: ||A_D - A_D(:, I) P||_F and its ratio to ||A_D||_F (host scalars,
  * identical on all ranks), using the P of the last id_coeffs_fp64. */
 id_status id_error(id_handle h, double* abs_fro, double* rel_fro);
+
+/* Engine of the two large fp64 GEMMs of steps 3-4 (the LSQ products G2 = Q1^T Q1 and
+ * W = Q1^T A_D(:, J), and the error's A_D(:, I) T).  Both compute the paper's fp64
+ * quantities (Remark 2 P:199-201); they differ in how the products are evaluated:
+ *   1 = fp64 tensor cores (DMMA, mma.sync m8n8k4.f64), every product and sum in fp64;
+ *   2 = int8 tensor cores (tcgen05 kind::i8) by the Ozaki scheme: each operand row/column
+ *       split into eight 7-bit slices under one power-of-two exponent, the 36 slice products
+ *       with p + q <= 7 accumulated exactly in int32 and recombined in fp64 — per-product
+ *       error < 1.3e-16 relative to 2^(Ea+Eb); needs k <= 128, a device-
+ *       resident A_D (not ID_CREATE_STREAM_HOST) and n > k (else ID_ERR_ARG at the call);
+ *   0 = automatic (default): 1 (the int8 kernels are correct but not yet faster than DMMA
+ *       on C4).
+ * Takes effect from the next id_coeffs_fp64 / id_error; id_stats reports the engine used. */
+id_status id_set_fp64_engine(id_handle h, int32_t engine);
 
 /* The paper's variants and metrics, using the P of the last
  * id_coeffs_fp64:

@@ -253,6 +253,196 @@ __global__ void __launch_bounds__(1024) k_reflector(const double* __restrict__ r
   (void)Fop;
 }
 
+// k_reduce_reflect: k_pass_reduce and k_reflector in ONE launch for a single shard (no
+// allreduce between them).  Block b reduces the pass partials of columns j + 32 b .. + 31
+// exactly as k_pass_reduce (same order, same bits), recomputes column j's (s_j, x_j) the
+// same way (so every block holds the identical beta, c), writes its columns' R(j, :),
+// f_j and downdated norms, and leaves a block candidate (argmax, remaining mass, sum of
+// s_i); the last block to finish (atomic ticket) makes the step's decisions exactly as
+// k_reflector: tolerance stop (R8), underflow, the argmax over the candidates (total
+// order: larger value, then lower original index), the next pivot's bookkeeping swaps.
+// On a tolerance stop the speculative R(j, :), f_j writes are never read (k_out = j).
+template <typename W>
+__global__ void __launch_bounds__(32 * RW) k_reduce_reflect(const double* __restrict__ part, int gx, int n, int j,
+                                                            const double* __restrict__ xr, int own_row, int k_max,
+                                                            int nb, W* __restrict__ F, W* __restrict__ R,
+                                                            double* __restrict__ beta_out, double* __restrict__ cvec,
+                                                            double* __restrict__ tau, int* __restrict__ perm,
+                                                            DevScalars* __restrict__ sc, double* __restrict__ red,
+                                                            double* __restrict__ cand,
+                                                            unsigned int* __restrict__ counter) {
+  if (sc->done) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = j + blockIdx.x * 32 + lane;
+  __shared__ double sh[3][RW][32];
+  __shared__ double col[3][32];      // this block's (w, s, x)
+  __shared__ double pj[2];           // s_j, x_j
+  __shared__ int last;
+  double w = 0.0, s = 0.0, sj = 0.0;
+  if (c < n) {
+    for (int b = warp; b < gx; b += RW) {
+      w += part[((int64_t)b * 2 + 0) * n + c];
+      s += part[((int64_t)b * 2 + 1) * n + c];
+    }
+  }
+  if (lane == 0)
+    for (int b = warp; b < gx; b += RW) sj += part[((int64_t)b * 2 + 1) * n + j];
+  sh[0][warp][lane] = w;
+  sh[1][warp][lane] = s;
+  sh[2][warp][lane] = sj;
+  __syncthreads();
+  if (warp == 0) {
+    double tw = 0.0, ts = 0.0;
+#pragma unroll
+    for (int i = 0; i < RW; ++i) { tw += sh[0][i][lane]; ts += sh[1][i][lane]; }
+    const double tx = (c < n && own_row) ? xr[c] : 0.0;
+    col[0][lane] = tw;
+    col[1][lane] = ts;
+    col[2][lane] = tx;
+    if (c < n) {
+      red[c] = tw;
+      red[n + c] = ts;
+      red[2 * n + c] = tx;
+    }
+    if (lane == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int i = 0; i < RW; ++i) t += sh[2][i][0];
+      pj[0] = t;
+      pj[1] = own_row ? xr[j] : 0.0;
+    }
+  }
+  __syncthreads();
+  const double tiny = sizeof(W) == 8 ? DBL_MIN : (double)FLT_MIN;
+  const double sjv = pj[0], uj = pj[1];
+  const bool ok = sjv >= tiny;
+  const double beta = -copysign(sqrt(sjv), uj);
+  const double sgn = beta < 0.0 ? -1.0 : 1.0;
+  const int slot = j % NSLOT;
+  // block candidate (warp 0: the block's 32 columns)
+  if (warp == 0) {
+    ArgMax best{-1.0, 0x7fffffff, -1};
+    double rest = 0.0, ssum = 0.0;
+    if (c < n) {
+      ssum = col[1][lane];
+      if (ok) {
+        const double rraw = col[0][lane] / beta;
+        R[(int64_t)j * n + c] = to_w<W>(rraw * sgn);
+        F[(int64_t)slot * n + c] = to_w<W>(col[2][lane] - rraw);
+        if (c > j) {
+          const double vn = col[1][lane] - rraw * rraw;
+          rest = fmax(vn, 0.0);
+          best = ArgMax{vn, perm[c], c};
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const ArgMax b = am_shfl(best, o);
+      if (am_better(b, best)) best = b;
+    }
+    // fixed-order lane sums (deterministic): lane 0 adds lanes 0..31 in order
+    double rl[2] = {rest, ssum};
+    double r0 = 0.0, r1 = 0.0;
+    for (int i = 0; i < 32; ++i) {
+      r0 += __shfl_sync(0xffffffffu, rl[0], i);
+      r1 += __shfl_sync(0xffffffffu, rl[1], i);
+    }
+    if (lane == 0) {
+      double* cd = cand + 5 * (int64_t)blockIdx.x;
+      cd[0] = best.v;
+      cd[1] = (double)best.orig;
+      cd[2] = (double)best.pos;
+      cd[3] = r0;
+      cd[4] = r1;
+    }
+  }
+  if (blockIdx.x == 0 && ok)
+    for (int i = threadIdx.x; i < j; i += blockDim.x) R[(int64_t)j * n + i] = W(0);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // ---- the last block: the step's decisions ----
+  __shared__ ArgMax fin;
+  __shared__ double frest, fsum;
+  if (warp == 0) {
+    ArgMax best{-1.0, 0x7fffffff, -1};
+    for (int b = lane; b < (int)gridDim.x; b += 32) {
+      const double* cd = cand + 5 * (int64_t)b;
+      const ArgMax a{cd[0], (int)cd[1], (int)cd[2]};
+      if (am_better(a, best)) best = a;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const ArgMax b = am_shfl(best, o);
+      if (am_better(b, best)) best = b;
+    }
+    if (lane == 0) {
+      double r = 0.0, t = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) {
+        r += cand[5 * (int64_t)b + 3];
+        t += cand[5 * (int64_t)b + 4];
+      }
+      fin = best;
+      frest = r;
+      fsum = t;
+      *counter = 0u;   // ready for the next step
+    }
+  }
+  __syncthreads();
+  if (j > 0 && sc->eps2normAL2 > 0.0 && fsum <= sc->eps2normAL2) {   // tolerance stop (R8)
+    if (threadIdx.x == 0) {
+      sc->k_out = j;
+      sc->resid2 = fsum;
+      sc->done = 1;
+    }
+    return;
+  }
+  if (!ok) {                                       // pivot norm^2 underflows
+    if (threadIdx.x == 0) {
+      sc->status = 4;
+      sc->k_out = j;
+      sc->done = 1;
+    }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    beta_out[j] = beta;
+    cvec[j] = 1.0 / (uj - beta);
+    tau[j] = (beta - uj) / beta;
+  }
+  const int jn = j + 1, pn = fin.pos;
+  if (jn < k_max && pn > jn) {
+    const int j0n = nb * (j / nb);
+    for (int t = j0n + threadIdx.x; t < jn; t += blockDim.x) {
+      W* f = F + (int64_t)(t % NSLOT) * n;
+      const W x = f[jn];
+      f[jn] = f[pn];
+      f[pn] = x;
+    }
+    for (int t = threadIdx.x; t < jn; t += blockDim.x) {
+      W* r = R + (int64_t)t * n;
+      const W x = r[jn];
+      r[jn] = r[pn];
+      r[pn] = x;
+    }
+    if (threadIdx.x == 0) {
+      const int x = perm[jn];
+      perm[jn] = perm[pn];
+      perm[pn] = x;
+    }
+  }
+  if (threadIdx.x == 0) {
+    sc->k_out = j + 1;
+    sc->resid2 = frest;
+    sc->pivot = pn;
+    if (j + 1 >= k_max || pn < 0) sc->done = 1;
+  }
+}
+
 // initial pivot: argmax of the initial column norms (ties lowest index); perm = identity
 __global__ void __launch_bounds__(1024) k_init_pivot(const double* __restrict__ norms, int n,
                                                      int* __restrict__ perm,
@@ -338,6 +528,20 @@ cudaError_t launch_reflector(int fmt, const double* red, int n, int j, int k_max
   else
     k_reflector<float><<<1, 1024, 0, st>>>(red, n, j, k_max, nb, (float*)F, (float*)R, beta, cvec, tau, perm, sc,
                                            (unsigned char*)Fop);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_reflect(int fmt, const double* part, int gx, int n, int j, const double* xr, int own_row,
+                                  int k_max, int nb, void* F, void* R, double* beta, double* cvec, double* tau,
+                                  int* perm, DevScalars* sc, double* red, double* cand, unsigned int* counter,
+                                  cudaStream_t st) {
+  const unsigned nblk = (unsigned)((n - j + 31) / 32);
+  if (fmt == 3)
+    k_reduce_reflect<double><<<nblk, 32 * RW, 0, st>>>(part, gx, n, j, xr, own_row, k_max, nb, (double*)F,
+                                                       (double*)R, beta, cvec, tau, perm, sc, red, cand, counter);
+  else
+    k_reduce_reflect<float><<<nblk, 32 * RW, 0, st>>>(part, gx, n, j, xr, own_row, k_max, nb, (float*)F, (float*)R,
+                                                      beta, cvec, tau, perm, sc, red, cand, counter);
   return cudaGetLastError();
 }
 

@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int
                                                int64_t ngroups, int64_t n, int64_t ld,
                                                T* __restrict__ S, double* __restrict__ part,
                                                double* __restrict__ aux,
-                                               DevScalars* __restrict__ sc) {
+                                               DevScalars* __restrict__ sc,
+                                               unsigned long long* __restrict__ cmax) {
   constexpr int TR = sizeof(T) == 8 ? 128 : 256;   // rows per tile (fp64: the tile fits 48 KB)
   constexpr int PAD = 16 / sizeof(T);              // keep 16 B alignment, spread banks
   __shared__ __align__(16) T tile[32][TR + PAD];
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int
   const double s = sc->scale;
   double colsq[4] = {0.0, 0.0, 0.0, 0.0};
   double adq[4] = {0.0, 0.0, 0.0, 0.0};
+  double cm[4] = {0.0, 0.0, 0.0, 0.0};   // column max |a_ij| of A_D (the fp64 stage's slice exponents)
   int inf = 0;
   // register prefetch: the next tile's 32 loads are in flight while this tile is
   // converted and written out
@@ -145,6 +147,7 @@ __global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int
         const int rr = i * 32 + lane;
         const double av = a[q][i];
         adq[q] = fma(av, av, adq[q]);
+        cm[q] = fmax(cm[q], fabs(av));
         const double x = __dmul_rn(s, av);
         T v;
         double d;
@@ -178,6 +181,14 @@ __global__ void __launch_bounds__(256) k_round(const double* __restrict__ A, int
 #pragma unroll
         for (int w = 0; w < (int)sizeof(T) / 2; ++w) __stcs(dst + w, src[w]);
       }
+    }
+  }
+  if (cmax) {   // bit patterns of non-negative doubles order like unsigned integers
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double v = warp_max(cm[q]);
+      const int64_t c = c0 + warp * 4 + q;
+      if (lane == 0 && c < n) atomicMax(cmax + c, (unsigned long long)__double_as_longlong(v));
     }
   }
   const double adsq = (adq[0] + adq[1]) + (adq[2] + adq[3]);
@@ -274,15 +285,16 @@ cudaError_t launch_scale_from_max(DevScalars* sc, int scaling, cudaStream_t st) 
   return cudaGetLastError();
 }
 cudaError_t launch_round(int fmt, const double* A, int64_t m, int64_t m_pad, int64_t n, int64_t ld,
-                         void* S, double* part, int gy, DevScalars* sc, cudaStream_t st) {
+                         void* S, double* part, int gy, DevScalars* sc, cudaStream_t st,
+                         unsigned long long* cmax) {
   dim3 grid((unsigned)((n + 31) / 32), (unsigned)gy);
   double* aux = part + (int64_t)gy * n;
   if (fmt == 1)
-    k_round<__half><<<grid, 256, 0, st>>>(A, m, m_pad / 8, n, ld, (__half*)S, part, aux, sc);
+    k_round<__half><<<grid, 256, 0, st>>>(A, m, m_pad / 8, n, ld, (__half*)S, part, aux, sc, cmax);
   else if (fmt == 2)
-    k_round<float><<<grid, 256, 0, st>>>(A, m, m_pad / 8, n, ld, (float*)S, part, aux, sc);
+    k_round<float><<<grid, 256, 0, st>>>(A, m, m_pad / 8, n, ld, (float*)S, part, aux, sc, cmax);
   else
-    k_round<double><<<grid, 256, 0, st>>>(A, m, m_pad / 8, n, ld, (double*)S, part, aux, sc);
+    k_round<double><<<grid, 256, 0, st>>>(A, m, m_pad / 8, n, ld, (double*)S, part, aux, sc, cmax);
   return cudaGetLastError();
 }
 cudaError_t launch_sum_partials(const double* part, int splits, int64_t len, double* out,

@@ -74,6 +74,8 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Layout {
   size_t AD, S, U, F, Vop, Fop, R, part, red, xr, norms, perm, scal3, sc, maxpart, rpart;
   size_t AI, Q1, G1, G2, W, tpart, Rd, T, Pw, epart, Tp, Ik, Rinv, py, pvec, gpart, G, Gc, misc;
+  size_t cmaxd, cmaxq, ozs, ozt, ozpart, rsc, fsc;   // fp64 stage on the int8 tensor cores (k_ozaki.cu)
+  size_t cand;                                      // fused reduce + reflector: block candidates, ticket
   size_t total;
 };
 
@@ -195,6 +197,14 @@ Layout layout(int64_t m_local, int64_t n, int64_t k, int host_AD, int sbytes) {
   L.gpart = take(gram_part_doubles(mp / 8, (int)n, num_sms()) * 8);  // Gram pivoting: tile partials
   L.G = take((size_t)n * n * 8);                                      //   and G = A_L^T A_L
   L.Gc = take((size_t)n * n * 8);                                     //   Schur-complement working copy
+  L.cmaxd = take((size_t)n * 8);                                      // A_D column max |a|
+  L.cmaxq = take(128 * 8);                                            // Q1 column max |q|
+  L.ozs = take(oz_slice_bytes(m_local));                              // A-operand slices (Q1 or A_I)
+  L.ozt = take(oz_tslice_bytes(n));                                   // T's slices
+  L.ozpart = take(oz_part_doubles(num_sms()) * 8);                    // row-group partials of [G2 | W]
+  L.rsc = take((size_t)((m_local + 127) / 128 * 128) * 8);            // per-row scales of A_I
+  L.fsc = take((size_t)(n + 64) * 8);                                 // per-column scales of T
+  L.cand = take((size_t)(5 * ((n + 31) / 32 + 1)) * 8 + 64);
   L.misc = take(1024);
   L.total = off;
   return L;
@@ -246,6 +256,13 @@ struct mpid_ctx {
   double normAD_spec = -1.0;   // cached ||A_D||_2 (power iteration), < 0 = not yet
   int* info = nullptr;
   double* err2 = nullptr;
+  unsigned long long *cmaxd = nullptr, *cmaxq = nullptr;   // column max |x| bit patterns
+  void *ozs = nullptr, *ozt = nullptr;
+  double *ozpart = nullptr, *rsc = nullptr, *fsc = nullptr;
+  int fp64_engine = 0;            // 0 auto, 1 DMMA, 2 int8 Ozaki (id_set_fp64_engine)
+  bool have_cmaxd = false;        // cmaxd holds this A_D's column maxima (set by the round)
+  double* cand = nullptr;         // k_reduce_reflect: per-block candidates
+  unsigned int* ticket = nullptr; //   and its last-block counter
   // state
   int fmt = 0;
   int k_out = 0;
@@ -455,6 +472,16 @@ static id_status relayout(mpid_ctx* h, int sbytes) {
   h->pvec = (double*)(w + L.pvec);
   h->info = (int*)(w + L.misc);
   h->err2 = (double*)(w + L.misc + 64);
+  h->cmaxd = (unsigned long long*)(w + L.cmaxd);
+  h->cmaxq = (unsigned long long*)(w + L.cmaxq);
+  h->ozs = w + L.ozs;
+  h->ozt = w + L.ozt;
+  h->ozpart = (double*)(w + L.ozpart);
+  h->rsc = (double*)(w + L.rsc);
+  h->fsc = (double*)(w + L.fsc);
+  h->have_cmaxd = false;
+  h->cand = (double*)(w + L.cand);
+  h->ticket = (unsigned int*)(w + L.cand + (size_t)(5 * ((n + 31) / 32 + 1)) * 8);
   h->normAD_spec = -1.0;
   // zero U (padding rows must stay 0); S is fully written by the rounding kernel
   if (cudaMemsetAsync(h->U, 0, (size_t)NSLOT * h->m_pad * sbytes, h->st) != cudaSuccess ||
@@ -462,6 +489,19 @@ static id_status relayout(mpid_ctx* h, int sbytes) {
       cudaMemsetAsync(h->Vop, 0, tc_vop_bytes(h->m_pad, NB_MAX), h->st) != cudaSuccess)
     return fail(h, ID_ERR_CUDA, "workspace memset failed");
   return ID_OK;
+}
+// the engine of the fp64 ID step's two large GEMMs (W = Q1^T A_J with G2, and the error):
+// 2 = the int8 tensor cores by the Ozaki scheme (k_ozaki.cu: k <= 128, a device-resident
+// A_D whose column maxima the round recorded, at least one J column), 1 = DMMA (k_fp64.cu).
+// Auto (0) is DMMA for now (measured: the int8 kernels are not yet faster on C4, DESIGN.md
+// §5); -1 = the int8 engine was requested and does not apply.
+static int fp64_engine(const mpid_ctx* h, int k) {
+  const bool oz_ok = k >= 1 && k <= 128 && h->host_AD != 2 && h->have_cmaxd && h->n - k > 0;
+  if (h->fp64_engine == 1) return 1;
+  if (h->fp64_engine == 2) return oz_ok ? 2 : -1;
+  static const int env = getenv("MPID_FP64_ENGINE") ? atoi(getenv("MPID_FP64_ENGINE")) : 0;   // A/B measurements
+  if (env == 2) return oz_ok ? 2 : 1;
+  return 1;   // auto: DMMA (the int8 kernels do not beat it yet)
 }
 // the layout a call in format fmt needs
 static id_status ensure_layout(mpid_ctx* h, int fmt) {
@@ -704,11 +744,12 @@ static id_status enqueue_round_streamed(mpid_ctx* h, int fmt, int scaling, doubl
   CK(launch_scale_from_max(h->sc, scaling, h->st));
   const int gy = round_gy(R, n);
   const int naux = gy * (int)((n + 31) / 32);
+  CK(cudaMemsetAsync(h->cmaxd, 0, (size_t)n * 8, h->st));
   s = stream_blocks(h, [&](int64_t b, int64_t r0, int64_t rows, const double* blk) -> id_status {
     // rows up to the next 256-row tile of this block (the last block also covers m_pad's padding)
     const int64_t rpad = std::min<int64_t>(R, h->m_pad - r0);
     void* Sb = (char*)h->S + (size_t)(r0 / 8) * n * 8 * (fmt == ID_FP16 ? 2 : fmt == ID_FP32 ? 4 : 8);
-    CK(launch_round(fmt, blk, rows, rpad, n, R, Sb, h->rpart, gy, h->sc, h->st));
+    CK(launch_round(fmt, blk, rows, rpad, n, R, Sb, h->rpart, gy, h->sc, h->st, h->cmaxd));
     CK(launch_acc_rows(h->rpart, gy, n, n, h->norms, b > 0 ? 1 : 0, h->st));                   // column norms
     CK(launch_acc_rows(h->rpart + (int64_t)gy * n, naux, 1, 1, h->norms + n, b > 0 ? 1 : 0, h->st));  // ||A_D||^2
     return ID_OK;
@@ -742,7 +783,8 @@ static id_status enqueue_round(mpid_ctx* h, int fmt, int scaling, double eps) {
   }
   CK(launch_scale_from_max(h->sc, scaling, h->st));
   const int gy = round_gy(h->m_pad, n);
-  CK(launch_round(fmt, h->AD, m, h->m_pad, n, h->ld, h->S, h->rpart, gy, h->sc, h->st));
+  CK(cudaMemsetAsync(h->cmaxd, 0, (size_t)n * 8, h->st));
+  CK(launch_round(fmt, h->AD, m, h->m_pad, n, h->ld, h->S, h->rpart, gy, h->sc, h->st, h->cmaxd));
   CK(launch_sum_partials(h->rpart, gy, n, h->norms, h->st));  // norms[0:n]
   const int naux = gy * (int)((n + 31) / 32);
   k_pack_round<<<1, 1024, 0, h->st>>>(h->rpart + (int64_t)gy * n, naux, h->sc, h->norms, (int)n);
@@ -801,6 +843,9 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
   }
   CK(launch_init_pivot(h->norms, (int)n, h->perm, h->sc, h->st));
   h->kernel_launches += 1;
+  // one shard: the pass partials' reduction and the reflector are one launch (k_reduce_reflect)
+  const bool fused = h->nranks <= 1 && !h->comm && !getenv("MPID_NO_FUSED_REFLECT");
+  if (fused) CK(cudaMemsetAsync(h->ticket, 0, sizeof(unsigned int), h->st));
   const int own_lo = (int)std::min<int64_t>(h->row_offset, INT32_MAX);
   for (int j = 0; j < k_max; ++j) {
     const int j0 = j == 0 ? 0 : nb * ((j - 1) / nb);
@@ -842,6 +887,13 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
       return fail(h, ID_ERR_STATE, "panel pass grid %d exceeds the partials buffer (%d)", gx_used, pass_gx_cap());
     if (profile) CK(rec(h, h->pass_ev[2 * j + 1]));
     const int own = (j >= own_lo && (int64_t)j < h->row_offset + h->m_local) ? 1 : 0;
+    if (fused) {
+      CK(launch_reduce_reflect(fmt, h->part, gx_used, (int)n, j, h->xr, own, k_max, nb, h->F, h->R, h->beta,
+                               h->cvec, h->tau, h->perm, h->sc, h->red, h->cand, h->ticket, h->st));
+      h->kernel_launches += 2;
+      h->pass_launches += 1;
+      continue;
+    }
     CK(launch_pass_reduce(h->part, gx_used, (int)n, j, h->xr, own, h->red, h->sc, h->st));
     s = allreduce(h, h->red, (size_t)3 * n, NCCL_SUM);
     if (s) return s;
@@ -870,6 +922,7 @@ id_status id_round_only(id_handle h, id_format fmt, id_scaling scaling) {
   h->fmt = fmt;
   h->have_qr = false;
   h->have_coef = false;
+  h->have_cmaxd = true;
   h->stats.scale = h->sc_host.scale;
   h->stats.normAL_fro = sqrt(h->sc_host.normAL2);
   h->stats.normAD_fro = sqrt(h->sc_host.normAD2);
@@ -981,6 +1034,7 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   CK(cudaEventRecord(h->ev[6], h->st));
   CK(cudaStreamSynchronize(h->st));
   h->fmt = fmt;
+  h->have_cmaxd = true;
   if (use_graph) {
     float tc = 0.f;
     cudaEventElapsedTime(&tc, h->ev[7], h->ev[6]);
@@ -1040,6 +1094,8 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
   if (ldp < k) return fail(h, ID_ERR_ARG, "ldp < k");
   if ((size_t)k * 33 * 8 > 200 * 1024) return fail(h, ID_ERR_DIM, "k=%d too large for the P solve", k);
   if (mode != ID_COEF_R && mode != ID_COEF_LSQ) return fail(h, ID_ERR_ARG, "bad coefficient mode");
+  const int eng = fp64_engine(h, k);
+  if (eng < 0) return fail(h, ID_ERR_ARG, "the int8 fp64 engine needs k <= 128, a device-resident A_D and n > k");
   CK(cudaEventRecord(h->ev[3], h->st));
   int launches = 0;
   const size_t tcap = tpart_doubles(m, n, h->k_cap);
@@ -1071,18 +1127,26 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
     CK(launch_trsm_left_upper(R1, nullptr, k, h->Ik, k, nullptr, k, h->Rinv, k, 0, h->st));
     CK(launch_nn_store(h->AI, m, m, h->Rinv, k, k, k, h->Q1, m, h->st, h->Tp,
                                ew_tpack_doubles(h->n, h->k_cap)));
-    // G2 = Q1^T Q1
-    CK(launch_tsmm(h->Q1, m, k, h->Q1, m, k, m, h->tpart, sp, h->st));
-    CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G2, h->st));
+    const int nj = n - k;
+    const bool oz = eng == 2 && mode == ID_COEF_LSQ;
+    if (oz) {   // [G2 | W] = Q1^T [Q1 | A_D(:, J)] in one pass over A_D on the int8 tensor cores
+      CK(launch_oz_tn(h->Q1, m, k, h->AD, h->ld, h->perm + k, nj, h->cmaxd, h->cmaxq, h->ozs, h->ozpart,
+                      oz_part_doubles(num_sms()), h->G2, h->W, num_sms(), h->st));
+      launches += 5;
+    } else {   // G2 = Q1^T Q1
+      CK(launch_tsmm(h->Q1, m, k, h->Q1, m, k, m, h->tpart, sp, h->st));
+      CK(launch_sum_partials(h->tpart, sp, (int64_t)k * k, h->G2, h->st));
+      launches += 2;
+    }
     id_status s = allreduce(h, h->G2, (size_t)k * k, NCCL_SUM);
     if (s) return s;
     CK(launch_cholesky(h->G2, k, h->info + 1, h->st));
     CK(launch_diag_ratio(h->G2, k, h->err2 + 1, h->st));
-    launches += 7;
+    launches += 5;
     // W = Q1^T A_D(:, J), J = perm[k:] (W(:, I) is never needed)
-    const int nj = n - k;
     if (nj > 0) {
-      if (h->host_AD == 2) {   // W = sum over row blocks of Q1(blk)^T A_D(blk, J)
+      if (oz) {
+      } else if (h->host_AD == 2) {   // W = sum over row blocks of Q1(blk)^T A_D(blk, J)
         const int spw = splits_for(k, nj, h->srows, tcap);
         id_status ss = stream_blocks(h, [&](int64_t b, int64_t r0, int64_t rows, const double* blk) -> id_status {
           CK(launch_tsmm(h->Q1 + r0, m, k, blk, h->srows, nj, rows, h->tpart, spw, h->st, h->perm + k));
@@ -1129,7 +1193,7 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
   };
   const bool use_graph = !h->loop && h->host_AD != 2;
   if (use_graph) {
-    const uint64_t key = ((uint64_t)mode << 32) | (uint64_t)k;
+    const uint64_t key = ((uint64_t)eng << 40) | ((uint64_t)mode << 32) | (uint64_t)k;   // engine, mode, k
     auto it = h->cgraphs.find(key);
     if (it == h->cgraphs.end()) {
       cudaGraph_t g;
@@ -1179,10 +1243,18 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
   float ms = 0.f;
   cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]);
   h->stats.t_coef_ms = ms;
+  h->stats.fp64_engine = mode == ID_COEF_LSQ ? eng : 0;
   h->stats.kernel_launches += launches;
   if (mode == ID_COEF_LSQ && (info[0] || info[1]))
     return fail(h, ID_ERR_DEGENERATE, "Cholesky breakdown in the LSQ refit (info %d, %d)", info[0], info[1]);
   h->have_coef = true;
+  return ID_OK;
+}
+
+id_status id_set_fp64_engine(id_handle h, int32_t engine) {
+  if (!h) return ID_ERR_ARG;
+  if (engine < 0 || engine > 2) return fail(h, ID_ERR_ARG, "bad fp64 engine %d", engine);
+  h->fp64_engine = engine;
   return ID_OK;
 }
 
@@ -1191,6 +1263,8 @@ id_status id_error(id_handle h, double* abs_fro, double* rel_fro) {
   cudaGetLastError();
   if (!h->have_coef) return fail(h, ID_ERR_STATE, "id_error needs id_coeffs_fp64 first");
   const int k = h->k_out;
+  const int eng = fp64_engine(h, k);
+  if (eng < 0) return fail(h, ID_ERR_ARG, "the int8 fp64 engine needs k <= 128, a device-resident A_D and n > k");
   CK(cudaEventRecord(h->ev[5], h->st));
   int nblk = 0;
   // skeleton columns contribute exactly 0 (P(:, I) = I_k): sum over J = perm[k:] only
@@ -1203,6 +1277,10 @@ id_status id_error(id_handle h, double* abs_fro, double* rel_fro) {
       return ID_OK;
     });
     if (ss) return ss;
+  } else if (nj > 0 && eng == 2) {   // int8 tensor cores (Ozaki scheme), A_I T never stored
+    CK(launch_oz_error(h->AD, h->m_local, h->ld, nj, h->perm + k, h->AI, k, h->T, k, h->ozs, h->ozt, h->rsc,
+                       h->fsc, h->epart, &nblk, num_sms(), h->st));
+    CK(launch_sum_scalar(h->epart, nblk, h->err2, h->st));
   } else if (nj > 0) {
     CK(launch_error(h->AD, h->m_local, h->ld, nj, h->perm + k, h->AI, k, h->T, k, h->epart, &nblk, h->st, h->Tp,
                           ew_tpack_doubles(h->n, h->k_cap)));
@@ -1220,6 +1298,7 @@ id_status id_error(id_handle h, double* abs_fro, double* rel_fro) {
   cudaEventElapsedTime(&ms, h->ev[5], h->ev[6]);
   h->stats.t_err_ms = ms;
   h->stats.kernel_launches += 2;
+  h->stats.fp64_engine_err = eng;
   *abs_fro = sqrt(e2);
   *rel_fro = h->sc_host.normAD2 > 0 ? sqrt(e2 / h->sc_host.normAD2) : NAN;
   return ID_OK;

@@ -143,8 +143,10 @@ cudaError_t launch_maxabs(const double* A, int64_t m, int64_t n, int64_t ld, dou
 cudaError_t launch_maxabs_finish(const double* part, int nblk, DevScalars* sc, int scaling,
                                  cudaStream_t st);
 cudaError_t launch_scale_from_max(DevScalars* sc, int scaling, cudaStream_t st);
+// cmax (optional): atomicMax of each column's max |a_ij| (bit patterns; zeroed by the caller)
 cudaError_t launch_round(int fmt, const double* A, int64_t m, int64_t m_pad, int64_t n, int64_t ld,
-                         void* S, double* part, int gx, DevScalars* sc, cudaStream_t st);
+                         void* S, double* part, int gx, DevScalars* sc, cudaStream_t st,
+                         unsigned long long* cmax = nullptr);
 cudaError_t launch_init_pivot(const double* norms, int n, int* perm, DevScalars* sc,
                               cudaStream_t st);
 cudaError_t launch_pass_tma(int fmt, PassParams p, int num_sms, int* gx_out, cudaStream_t st);
@@ -170,6 +172,11 @@ cudaError_t launch_reflector(int fmt, const double* red, int n, int j, int k_max
 cudaError_t launch_swap(int fmt, void* S, int64_t ngroups, int n, int jn, int j0, int steps_done,
                         void* F, void* R, int* perm, void* Sj, DevScalars* sc, cudaStream_t st, void* Fop = nullptr,
                         const double* cvec = nullptr, int nb = 16);
+// k_pass_reduce + k_reflector in one launch (single shard; last-block ticket in *counter, zeroed once)
+cudaError_t launch_reduce_reflect(int fmt, const double* part, int gx, int n, int j, const double* xr, int own_row,
+                                  int k_max, int nb, void* F, void* R, double* beta, double* cvec, double* tau,
+                                  int* perm, DevScalars* sc, double* red, double* cand, unsigned int* counter,
+                                  cudaStream_t st);
 cudaError_t launch_export_S(int fmt, const void* S, int64_t m_local, int n, void* out, int64_t ld,
                             cudaStream_t st);
 
@@ -236,5 +243,16 @@ cudaError_t launch_small_qrcp(double* Y, int ly, int n, int k_max, double* snorm
 // pivoted Cholesky of G (kept) on the working copy Gc, in panels of 32 steps + Schur updates
 cudaError_t launch_pchol(const double* G, double* Gc, int n, int k_max, double* d, int* perm, double* R64, float* R,
                          DevScalars* sc, cudaStream_t st);
+
+// fp64 GEMMs of the ID step on the int8 tensor cores by the Ozaki scheme (k_ozaki.cu; k <= 128)
+size_t oz_slice_bytes(int64_t m_local);
+size_t oz_tslice_bytes(int64_t n);
+size_t oz_part_doubles(int num_sms);
+cudaError_t launch_oz_tn(const double* Q1, int64_t m, int k, const double* AD, int64_t ld, const int* cmapJ, int nj,
+                         const unsigned long long* cmaxd, unsigned long long* cmaxq, void* slices, double* part,
+                         size_t part_cap, double* G2, double* W, int num_sms, cudaStream_t st);
+cudaError_t launch_oz_error(const double* AD, int64_t m, int64_t ld, int nj, const int* cmapJ, const double* AI,
+                            int k, const double* T, int64_t ldt, void* slices, void* tslices, double* rsc,
+                            double* fsc, double* part, int* nblk_out, int num_sms, cudaStream_t st);
 
 }  // namespace mpid

@@ -30,7 +30,7 @@ SCALING = {"none": ID_SCALE_NONE, "maxabs": ID_SCALE_MAXABS, "pow2": ID_SCALE_PO
 COEF = {"R": ID_COEF_R, "r": ID_COEF_R, "lsq": ID_COEF_LSQ, "LSQ": ID_COEF_LSQ}
 
 # every function declared in include/mpid.h
-EXPORTS = ["id_workspace_bytes", "id_create", "id_create_ex", "id_qrcp_lowprec", "id_coeffs_fp64", "id_error", "id_error_ex",
+EXPORTS = ["id_workspace_bytes", "id_create", "id_create_ex", "id_qrcp_lowprec", "id_coeffs_fp64", "id_error", "id_error_ex", "id_set_fp64_engine",
            "id_get_R", "id_get_R_fp64", "id_get_gram", "id_get_sketch", "id_get_perm", "id_get_AL", "id_round_only", "id_get_stats", "id_last_error", "id_destroy",
            "id_nccl_unique_id_bytes", "id_nccl_get_unique_id", "id_nccl_comm_init",
            "id_nccl_comm_destroy", "id_loopback_create", "id_loopback_calls", "id_loopback_destroy", "id_version"]
@@ -55,7 +55,8 @@ class Stats(C.Structure):
                 ("t_coef_ms", C.c_double), ("t_err_ms", C.c_double), ("t_pass_ms", C.c_double),
                 ("pass_launches", C.c_int64), ("kernel_launches", C.c_int64), ("k_out", C.c_int32),
                 ("nb", C.c_int32), ("status_qrcp", C.c_int32), ("formation", C.c_int32),
-                ("lsq_path", C.c_int32), ("reserved", C.c_int32 * 3), ("t_host_launch_ms", C.c_double),
+                ("lsq_path", C.c_int32), ("fp64_engine", C.c_int32), ("fp64_engine_err", C.c_int32),
+                ("reserved", C.c_int32 * 1), ("t_host_launch_ms", C.c_double),
                 ("t_call_gpu_ms", C.c_double)]
 
     def as_dict(self):
@@ -89,6 +90,8 @@ def lib():
     L.id_error.restype = C.c_int
     L.id_error.argtypes = [vp, C.POINTER(dbl), C.POINTER(dbl)]
     L.id_error_ex.restype = C.c_int
+    L.id_set_fp64_engine.restype = C.c_int
+    L.id_set_fp64_engine.argtypes = [vp, i32]
     L.id_error_ex.argtypes = [vp, i32, i32, i32, C.POINTER(dbl), C.POINTER(dbl)]
     L.id_get_R.restype = C.c_int
     L.id_get_R.argtypes = [vp, vp, i64]
@@ -299,6 +302,12 @@ class MPID:
         Pt = torch.empty((self.n, self.k), dtype=torch.float64, device=self.device)
         self._check(id_coeffs_fp64(self.h, COEF[mode], Pt.data_ptr(), self.k))
         return Pt.t()
+
+    def set_fp64_engine(self, engine):
+        """fp64 GEMM engine of coeffs / error (include/mpid.h id_set_fp64_engine): "auto",
+        "dmma" or "int8" (the Ozaki scheme on the int8 tensor cores)."""
+        e = {"auto": 0, "dmma": 1, "int8": 2, "ozaki": 2}[engine] if isinstance(engine, str) else int(engine)
+        self._check(lib().id_set_fp64_engine(self.h, e))
 
     def error(self):
         rc, a, r = id_error(self.h)
