@@ -71,7 +71,7 @@ def load_fp64_peak():
     return float(d["used_as_peak"]), "profiles/r02_fp64_peak.json (tools/dmma_probe.cu on a B200: DMMA register-resident; cuBLAS DGEMM 35.5)"
 
 
-def full_id_roofline(m, n, k, s, hbm_gbs, f_coef, f_err, small_ms, t_total_ms, engine=1, i8_tops=None):
+def full_id_roofline(m, n, k, s, hbm_gbs, f_coef, f_err, small_ms, t_total_ms, engine=1, i8_tops=None, engine_err=None):
     """SURVEY §8(d) full-ID floor: round (8 + 8 + s B per element: max|a| pass + rounding)
     and the ALGORITHMIC QRCP bytes (B_QRCP) at the measured HBM bandwidth, the fp64 work at
     its engine's peak, plus k times the measured per-step cost of the small kernels;
@@ -85,18 +85,22 @@ def full_id_roofline(m, n, k, s, hbm_gbs, f_coef, f_err, small_ms, t_total_ms, e
     t_round = (8.0 + 8.0 + s) * m * n / bw
     t_qrcp = alg_qrcp_bytes(m, n, k, s) / bw
     nj = n - k
+    engine_err = engine if engine_err is None else engine_err
     if engine == 2 and i8_tops:
         t_coef = 2.0 * m * k * k / (p64 * 1e12) + max(36.0 * 2.0 * m * k * n / (i8_tops * 1e12),
                                                       8.0 * m * (n + k) / bw)
-        t_err = max(36.0 * 2.0 * m * k * nj / (i8_tops * 1e12), 8.0 * m * nj / bw)
     else:
         t_coef = f_coef / (p64 * 1e12)
+    if engine_err == 2 and i8_tops:
+        t_err = max(36.0 * 2.0 * m * k * nj / (i8_tops * 1e12), 8.0 * m * nj / bw)
+    else:
         t_err = max(f_err / (p64 * 1e12), 8.0 * m * nj / bw)
     t_roof = (t_round + t_qrcp + t_coef + t_err) * 1e3 + max(0.0, small_ms)
     return {"t_roof_ms": t_roof, "frac": t_roof / t_total_ms,
             "parts_ms": {"round": t_round * 1e3, "qrcp_pass": t_qrcp * 1e3, "coef": t_coef * 1e3,
                          "error": t_err * 1e3, "qrcp_small_kernels_measured": small_ms},
-            "fp64_engine": {1: "DMMA", 2: "int8 Ozaki"}.get(engine, str(engine)),
+            "fp64_engine": {"coef": {1: "DMMA", 2: "int8 Ozaki"}.get(engine, str(engine)),
+                            "error": {1: "DMMA", 2: "int8 Ozaki"}.get(engine_err, str(engine_err))},
             "peaks": {"hbm_gbs": hbm_gbs, "fp64_tflops": p64, "fp64_source": src,
                       "int8_tops": i8_tops,
                       "int8_source": "2 x MEASURED_PEAKS.json bf16_tflops (B200_PROFILING.md nominal int8 / bf16 = 4.5 / 2.25)"}}
@@ -377,27 +381,28 @@ def main():
             variants["algorithm2_R_mode_coefficients"] = {"error": str(ex)}
         # the headline handle state (last QRCP) is restored for the checks below
         q = h.qrcp(args.fmt, scaling, k=k, nb=args.nb, formation=args.formation)
-        # the fp64 stage on the other engine (DMMA <-> int8 Ozaki) for the same skeleton
-        other = "int8" if int(st_last.get("fp64_engine", 1)) == 1 else "dmma"
-        vname = f"fp64_stage_on_{other}"
-        try:
-            cm, em = [], []
-            h.set_fp64_engine(other)
-            for i in range(3):
-                h.coeffs(args.mode)
-                ed = h.error()
-                sd = h.stats()
-                cm.append(sd["t_coef_ms"])
-                em.append(sd["t_err_ms"])
-            h.set_fp64_engine("auto")
-            P_a = h.coeffs(args.mode)
-            e_a = h.error()
-            variants[vname] = {
-                "coef_ms": statistics.mean(cm[1:]), "error_ms": statistics.mean(em[1:]), "rel_err_fro": ed[1],
-                "rel_err_fro_headline_engine": e_a[1], "engine": sd["fp64_engine"],
-                "note": f"same QRCP, coefficients + error with id_set_fp64_engine({other}); 2 timed calls"}
-        except Exception as ex:  # reported, never silently replaced
-            variants[vname] = {"error": str(ex)}
+        # the fp64 stage with each engine forced (same skeleton): DMMA and int8 (Ozaki scheme)
+        for other in ("dmma", "int8"):
+            vname = f"fp64_stage_all_{other}"
+            try:
+                cm, em = [], []
+                h.set_fp64_engine(other)
+                for i in range(3):
+                    h.coeffs(args.mode)
+                    ed = h.error()
+                    sd = h.stats()
+                    cm.append(sd["t_coef_ms"])
+                    em.append(sd["t_err_ms"])
+                h.set_fp64_engine("auto")
+                variants[vname] = {
+                    "coef_ms": statistics.mean(cm[1:]), "error_ms": statistics.mean(em[1:]), "rel_err_fro": ed[1],
+                    "rel_err_fro_headline": e[1], "engines": [sd["fp64_engine"], sd["fp64_engine_err"]],
+                    "note": f"same QRCP, coefficients + error with id_set_fp64_engine({other}); 2 timed calls"}
+            except Exception as ex:  # reported, never silently replaced
+                h.set_fp64_engine("auto")
+                variants[vname] = {"error": str(ex)}
+        h.coeffs(args.mode)
+        h.error()
 
     # ---- roofline of the dominant kernel (the panel pass), per launch ----------
     # achieved = SURVEY §8(d)'s ALGORITHMIC bytes B_QRCP / the summed device time of the k
@@ -468,14 +473,15 @@ def main():
             "higher_is_better": True, "scaling": "strong" if args.config == "C5" else "weak",
             "vs_baseline": None,
             "dtype": ("f16 storage / f32 arithmetic QRCP + f64 ID" if args.fmt == "fp16" else "f32 QRCP + f64 ID")
-                     + (" (f64 GEMMs on the int8 tensor cores, Ozaki scheme)" if int(st_last.get("fp64_engine", 1)) == 2 else ""),
+                     + (" (f64 error GEMM on the int8 tensor cores, Ozaki scheme)" if int(st_last.get("fp64_engine_err", 1)) == 2 else ""),
             "data": "synthetic",
             "config": {"workload": f"{args.config}: {m_glob}x{n} fp64 Fourier snapshots, k={k}, "
                                    f"{args.fmt} QRCP ({'tcgen05' if form == 2 else 'FFMA'} pass, nb={nb_used}), "
                                    f"{args.mode.upper()} coefficients",
                        "rows_per_gpu": m_loc, "n": n, "k": k, "fmt": args.fmt, "nb": nb_used,
                        "coef": args.mode, "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU",
-                       "fp64_engine": {1: "dmma", 2: "int8-ozaki"}.get(int(st_last.get("fp64_engine", 1)), "?"),
+                       "fp64_engine": {"coef": {1: "dmma", 2: "int8-ozaki"}.get(int(st_last.get("fp64_engine", 1)), "?"),
+                                       "error": {1: "dmma", 2: "int8-ozaki"}.get(int(st_last.get("fp64_engine_err", 1)), "?")},
                        "l2": "inputs larger than L2 (A_D 16 GiB, A_L 4 GiB per GPU); no flush"},
             "stages_ms": {"round": statistics.mean(round_ms), "qrcp": statistics.mean(qr_ms),
                           "coef": statistics.mean(coef_ms), "error": statistics.mean(err_ms),
@@ -485,7 +491,8 @@ def main():
             "full_id_roofline": full_id_roofline(m_loc, n, q.k, s_bytes, peak, fc, fe,
                                                  statistics.mean(qr_ms) - pass_avg_ms, ms_step,
                                                  engine=int(st_last.get("fp64_engine", 1)),
-                                                 i8_tops=2.0 * peaks["bf16_tflops"] if peaks.get("bf16_tflops") else None),
+                                                 i8_tops=2.0 * peaks["bf16_tflops"] if peaks.get("bf16_tflops") else None,
+                                                 engine_err=int(st_last.get("fp64_engine_err", 1))),
             "k_out": q.k, "rel_err_fro": e[1], "errors_untimed": extra_err, "variants": variants,
             "roofline": {"kernel": ("k_pass_tc (tcgen05 panel pass)" if form == 2 else "k_pass_ws (FFMA panel pass)"),
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

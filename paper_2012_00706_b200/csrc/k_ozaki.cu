@@ -31,6 +31,7 @@
 // M of the TN GEMM fit one 128-row operand).
 #include "mpid_internal.cuh"
 #include <math.h>
+#include <cstdlib>
 
 namespace mpid {
 
@@ -44,13 +45,13 @@ constexpr int TN_A = OZ_S * 128 * KSTEP;              // 32 KB: 8 slices of 128 
 constexpr int TN_B = OZ_S * TN_N * KSTEP;             // 16 KB: 8 slices of 64 (N) x 32 (K)
 constexpr int TN_CHS = 512;                           // K-steps per int32 chunk (16384 rows)
 constexpr int TN_SLW = 8;                             // slicer / drain warps
-constexpr int TN_NI = 2;                              // MMA-issuing warps
+constexpr int TN_NI = 1;                              // MMA-issuing warp (12 MMAs per K-step)
 constexpr int TN_THREADS = 32 * (1 + TN_NI + TN_SLW);
 constexpr int TN_SMEM = TN_NST * (TN_A + TN_B) + 1024 + 1024;
 // error kernel
 constexpr int ER_N = 32;                              // J columns per tile (MMA N)
 constexpr int ER_EPW = 8;                             // epilogue warps
-constexpr int ER_NI = 3;                              // MMA-issuing warps (12 warps: <= 168 registers)
+constexpr int ER_NI = 1;                              // MMA-issuing warp (8 MMAs per K-step)
 constexpr int ER_THREADS = 32 * (1 + ER_NI + ER_EPW);
 
 __device__ __forceinline__ uint64_t oz_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -228,8 +229,9 @@ __global__ void __launch_bounds__(128) k_oz_slice_rows(const double* __restrict_
   }
 }
 
-// T (k x nj, ldt) -> per 32-column tile j the error kernel's B operand: 8 slices of 32 x KP
-// bytes, [j][q][kc][c 32][16 B]; fsc[c] = 2^{E_c}.  Thread per column (padded to the tile).
+// T (k x nj, ldt) -> per 32-column tile j the error kernel's B operand: the 8 slices
+// concatenated along N (slice q = rows 32 q .. 32 q + 31), K-major: [j][kc][q][c 32][16 B];
+// fsc[c] = 2^{E_c}.  Thread per column (padded to the tile).
 __global__ void __launch_bounds__(128) k_oz_slice_t(const double* __restrict__ T, int64_t ldt, int k, int nj, int KP,
                                                     uint4* __restrict__ Ts, double* __restrict__ fsc) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;   // grid covers the padded columns
@@ -252,9 +254,9 @@ __global__ void __launch_bounds__(128) k_oz_slice_t(const double* __restrict__ T
     uint32_t w[4][8];
 #pragma unroll
     for (int g = 0; g < 4; ++g) oz_slice4(v + 4 * g, sc, w[g]);
-    uint4* base = Ts + (((int64_t)j * OZ_S) * nkc + kc) * ER_N + cc;
+    uint4* base = Ts + (((int64_t)j * nkc + kc) * OZ_S) * ER_N + cc;
 #pragma unroll
-    for (int q = 0; q < OZ_S; ++q) base[(int64_t)q * nkc * ER_N] = make_uint4(w[0][q], w[1][q], w[2][q], w[3][q]);
+    for (int q = 0; q < OZ_S; ++q) base[q * ER_N] = make_uint4(w[0][q], w[1][q], w[2][q], w[3][q]);
   }
 }
 
@@ -270,17 +272,26 @@ __global__ void __launch_bounds__(128) k_oz_slice_t(const double* __restrict__ T
 //   warps 2..9  slice B in-kernel (thread = (column, 8 rows): 8 fp64 -> 8 x 8 B) and drain
 //               the accumulators into fp64 registers (warp w: TMEM lanes 32 (w % 4), 32
 //               columns (w - 2) / 4)
-// One thread issues the MMAs of a few diagonals.  A single thread sustains only about one
-// tcgen05.mma per 50-200 cycles (measured: tools/mma_rate_probe.cu, profiles/r02_mma_rate.txt),
-// far above the N = 32 / 64 tensor floor (16 / 32 cycles), so the 36 MMAs of a K-step are
-// spread over several issuing warps, each owning whole diagonals (an accumulator is written by
-// one thread only, so its first MMA can overwrite): pairs (d, 7 - d) carry 9 MMAs each.
-template <int D>
-__device__ __forceinline__ void tn_diag(uint32_t tmem, uint32_t a, uint32_t b, uint32_t id, bool first) {
+// Operand traffic, not arithmetic, bounds a naive slice-pair loop: every tcgen05.mma reads its
+// whole A (128 x 32 B) and B (N x 32 B) from shared memory, and a thread issues at most about
+// one MMA per 50 cycles (tools/mma_rate_probe.cu, tools/issue_probe.cu; profiles/r02_*probe*).
+// So the B slices are laid out CONCATENATED along N (slice q's 64 columns are rows 64 q ..
+// 64 q + 63 of one K-major operand) and the accumulators diagonal-major (diagonal d at TMEM
+// columns 64 d): ONE MMA of A slice p against B slices 0 .. 7 - p (N = 64 (8 - p)) lands
+// product (p, q) exactly in diagonal p + q's accumulator.  N <= 256 per instruction, so
+// p < 4 takes two MMAs: 12 MMAs per K-step instead of 36, A read 12 times instead of 36.
+__device__ __forceinline__ void tn_kstep(uint32_t tmem, uint32_t a, uint32_t b, bool first) {
 #pragma unroll
-  for (int pa = 0; pa <= D; ++pa)
-    oz_mma(tmem + (uint32_t)(D * TN_N), oz_sdesc(a + pa * 4096, 2048, 128), oz_sdesc(b + (D - pa) * 2048, 1024, 128),
-           id, (first && pa == 0) ? 0u : 1u);
+  for (int pa = 0; pa < OZ_S; ++pa) {
+    const uint64_t da = oz_sdesc(a + pa * 4096, 2048, 128);
+    const int nq = OZ_S - pa;                       // B slices 0 .. 7 - pa
+    const int n0 = nq > 4 ? 4 : nq;                 // first MMA: slices 0 .. n0 - 1
+    oz_mma(tmem + (uint32_t)(pa * TN_N), da, oz_sdesc(b, 8192, 128), oz_idesc(n0 * TN_N),
+           (first && pa == 0) ? 0u : 1u);
+    if (nq > 4)                                     // second MMA: slices 4 .. 7 - pa
+      oz_mma(tmem + (uint32_t)((pa + 4) * TN_N), da, oz_sdesc(b + 4 * 8 * 128, 8192, 128), oz_idesc((nq - 4) * TN_N),
+             (first && pa == 0) ? 0u : 1u);
+  }
 }
 
 struct OzTN {
@@ -300,6 +311,7 @@ struct OzTN {
   int64_t spg;                       // K-steps per row group
   int vec;                           // 16 B loads allowed (even ld / ldq, aligned bases)
   double* part;                      // [ngroups][ntiles][128][64]
+  int dbg;                           // measurement knobs (MPID_OZ_DBG): 1 = B not sliced, 2 = A not loaded
 };
 
 __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
@@ -375,14 +387,18 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
       const int slot = (int)(i % TN_NST);
       if (lane == 0) {
         if (i >= TN_NST) mbar_wait(&empty[slot], (uint32_t)(((i / TN_NST) - 1) & 1));
-        mbar_expect_tx(&full_a[slot], TN_A);
-        tma_load(smem + slot * (TN_A + TN_B), p.As + (s0 + i) * (TN_A / 16), TN_A, &full_a[slot]);
+        if (p.dbg & 2) {
+          mbar_arrive(&full_a[slot]);
+        } else {
+          mbar_expect_tx(&full_a[slot], TN_A);
+          tma_load(smem + slot * (TN_A + TN_B), p.As + (s0 + i) * (TN_A / 16), TN_A, &full_a[slot]);
+        }
       }
       __syncwarp();
       prefetch(s0 + i + PF);
     }
   } else if (warp <= TN_NI) {
-    // ---------------- MMA issuers: warp 1 diagonals {0, 7, 2, 5}, warp 2 {1, 6, 3, 4} ----------------
+    // ---------------- MMA issuer: 12 MMAs per K-step (tn_kstep) ----------------
     if (lane == 0) {
       const uint32_t id = oz_idesc(TN_N);
       int cpos = 0;
@@ -399,17 +415,7 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
         tc_fence_after();
         const uint32_t a = su32(smem + slot * (TN_A + TN_B)), b = a + TN_A;
         const bool first = cpos == 0;
-        if (warp == 1) {
-          tn_diag<0>(tmem, a, b, id, first);
-          tn_diag<7>(tmem, a, b, id, first);
-          tn_diag<2>(tmem, a, b, id, first);
-          tn_diag<5>(tmem, a, b, id, first);
-        } else {
-          tn_diag<1>(tmem, a, b, id, first);
-          tn_diag<6>(tmem, a, b, id, first);
-          tn_diag<3>(tmem, a, b, id, first);
-          tn_diag<4>(tmem, a, b, id, first);
-        }
+        tn_kstep(tmem, a, b, first);
         oz_commit(&empty[slot]);
         if (++cpos == TN_CHS || i == nst - 1) {
           oz_commit(acc_full);
@@ -430,12 +436,15 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
     const double sc = col ? pow2(56 - oz_exp(cp < p.kq ? __longlong_as_double((long long)p.cmaxq[cp])
                                                        : __longlong_as_double((long long)p.cmaxd[p.cmap[cp - p.kq]])))
                           : 0.0;
-    const uint32_t boff = (uint32_t)((ro >> 1) * 1024 + (c >> 3) * 128 + (c & 7) * 16 + (ro & 1) * 8);
+    // B stage, slices concatenated along N: element (q, c, k) at (k / 16) * 8192 +
+    // (8 q + c / 8) * 128 + (c % 8) * 16 + k % 16
+    const uint32_t boff = (uint32_t)((ro >> 1) * 8192 + (c >> 3) * 128 + (c & 7) * 16 + (ro & 1) * 8);
     // drain mapping: TMEM lane quarter warp % 4, columns 32 (sw / 4)
     const int quarter = warp & 3, chalf = sw >> 2;
-    double wacc[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) wacc[i] = 0.0;
+    // the drained chunk sums accumulate in this thread's own slots of the partials (no
+    // register-resident accumulators: 13 warps leave 128 registers per thread)
+    double* out = p.part + (((int64_t)g * p.ntiles + t) * 128 + quarter * 32 + lane) * TN_N + chalf * 32;
+    bool first_drain = true;
     double v[8], nv[8];
     auto load8 = [&](int64_t s, double* dst) {
       const int64_t r0 = s * KSTEP + ro * 8;
@@ -452,21 +461,23 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
         for (int i = 0; i < 8; ++i) dst[i] = (col && r0 + i < p.m) ? __ldcs(col + r0 + i) : 0.0;
       }
     };
-    if (nst > 0) load8(s0, nv);
+    if (nst > 0 && !(p.dbg & 1)) load8(s0, nv);
     int cpos = 0;
     uint32_t aph = 0;
     for (int64_t i = 0; i < nst; ++i) {
       const int slot = (int)(i % TN_NST);
 #pragma unroll
       for (int q = 0; q < 8; ++q) v[q] = nv[q];
-      if (i + 1 < nst) load8(s0 + i + 1, nv);
+      if (i + 1 < nst && !(p.dbg & 1)) load8(s0 + i + 1, nv);
       uint32_t lo[8], hi[8];
       oz_slice4(v, sc, lo);
       oz_slice4(v + 4, sc, hi);
       if (i >= TN_NST) mbar_wait(&empty[slot], (uint32_t)(((i / TN_NST) - 1) & 1));
       unsigned char* bst = smem + slot * (TN_A + TN_B) + TN_A + boff;
+      if (!(p.dbg & 1)) {
 #pragma unroll
-      for (int q = 0; q < OZ_S; ++q) *reinterpret_cast<uint2*>(bst + q * 2048) = make_uint2(lo[q], hi[q]);
+        for (int q = 0; q < OZ_S; ++q) *reinterpret_cast<uint2*>(bst + q * 1024) = make_uint2(lo[q], hi[q]);
+      }
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&full_b[slot]);
@@ -476,7 +487,7 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
         aph ^= 1;
         tc_fence_after();
         const double sa = ea[quarter * 32 + lane];
-#pragma unroll
+#pragma unroll 1
         for (int h = 0; h < 4; ++h) {
           uint32_t r[OZ_S][8];
 #pragma unroll
@@ -488,17 +499,18 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
             double x = i2d(r[OZ_S - 1][j]);
 #pragma unroll
             for (int d = OZ_S - 2; d >= 0; --d) x = fma(x, 0.0078125, i2d(r[d][j]));
-            wacc[h * 8 + j] = fma(x * sa, eb[chalf * 32 + h * 8 + j], wacc[h * 8 + j]);
+            const double val = x * sa * eb[chalf * 32 + h * 8 + j];
+            out[h * 8 + j] = first_drain ? val : out[h * 8 + j] + val;
           }
         }
+        first_drain = false;
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty);
       }
     }
-    double* out = p.part + (((int64_t)g * p.ntiles + t) * 128 + quarter * 32 + lane) * TN_N + chalf * 32;
-#pragma unroll
-    for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2*>(out + j) = make_double2(wacc[j], wacc[j + 1]);
+    if (first_drain)   // no rows in this group: zero partials
+      for (int j = 0; j < 32; ++j) out[j] = 0.0;
   }
   tc_fence_before();
   __syncthreads();
@@ -618,13 +630,11 @@ __global__ void __launch_bounds__(ER_THREADS, 1) k_oz_err(const OzErr p) {
       }
     }
   } else if (warp <= ER_NI) {
-    // MMA issuers, whole diagonals each: warp 1 {7, 4}, warp 2 {6, 3, 1}, warp 3 {5, 2, 0}
-    // (13 / 13 / 10 digit pairs per K-step)
+    // MMA issuer: per K-step (32 of the KP columns of A_I) one MMA per A slice p against T's
+    // slices 0 .. 7 - p concatenated along N (N = 32 (8 - p) <= 256), landing product (p, q)
+    // in diagonal p + q's accumulator (TMEM columns 32 (p + q) of the buffer)
     if (lane == 0) {
-      const uint32_t id = oz_idesc(ER_N);
       const uint32_t a0 = su32(sA), b0 = su32(sB);
-      const int w = warp - 1;
-      const int dset[3][3] = {{7, 4, -1}, {6, 3, 1}, {5, 2, 0}};
       int64_t jc = 0;
       for (int64_t i = 0; i < my_rt; ++i) {
         mbar_wait(a_full, (uint32_t)(i & 1));
@@ -637,16 +647,12 @@ __global__ void __launch_bounds__(ER_THREADS, 1) k_oz_err(const OzErr p) {
           const uint32_t bb = b0 + (uint32_t)(st * BBYTES);
           const uint32_t dt = tmem + (uint32_t)(buf * OZ_S * ER_N);
           for (int kk = 0; kk < p.KP / KSTEP; ++kk) {
-            const uint32_t ak = a0 + (uint32_t)(kk * 4096), bk = bb + (uint32_t)(kk * 2 * ER_N * 16);
+            const uint64_t db = oz_sdesc(bb + (uint32_t)(kk * 2 * OZ_S * ER_N * 16), OZ_S * ER_N * 16, 128);
 #pragma unroll
-            for (int h = 0; h < 3; ++h) {
-              const int d = dset[w][h];
-              if (d < 0) continue;
-              for (int pa = 0; pa <= d; ++pa)
-                oz_mma(dt + (uint32_t)(d * ER_N), oz_sdesc(ak + (uint32_t)(pa * (ABYTES / OZ_S)), 2048, 128),
-                       oz_sdesc(bk + (uint32_t)((d - pa) * (BBYTES / OZ_S)), ER_N * 16, 128), id,
-                       (pa == 0 && kk == 0) ? 0u : 1u);
-            }
+            for (int pa = 0; pa < OZ_S; ++pa)
+              oz_mma(dt + (uint32_t)(pa * ER_N),
+                     oz_sdesc(a0 + (uint32_t)(pa * (ABYTES / OZ_S) + kk * 4096), 2048, 128), db,
+                     oz_idesc((OZ_S - pa) * ER_N), (pa == 0 && kk == 0) ? 0u : 1u);
           }
           oz_commit(&b_empty[st]);
           oz_commit(&acc_full[buf]);
@@ -756,6 +762,7 @@ cudaError_t launch_oz_tn(const double* Q1, int64_t m, int k, const double* AD, i
   p.spg = (nsteps + p.ngroups - 1) / p.ngroups;
   p.vec = ((ld & 1) == 0 && (m & 1) == 0 && (((uintptr_t)AD) & 15) == 0 && (((uintptr_t)Q1) & 15) == 0) ? 1 : 0;
   p.part = part;
+  p.dbg = getenv("MPID_OZ_DBG") ? atoi(getenv("MPID_OZ_DBG")) : 0;
   if ((size_t)p.ngroups * p.ntiles * 128 * TN_N > part_cap) return cudaErrorInvalidValue;
   if ((e = smem_attr((const void*)k_oz_tn, TN_SMEM)) != cudaSuccess) return e;
   k_oz_tn<<<p.ngroups * p.ntiles, TN_THREADS, TN_SMEM, st>>>(p);

@@ -493,15 +493,17 @@ static id_status relayout(mpid_ctx* h, int sbytes) {
 // the engine of the fp64 ID step's two large GEMMs (W = Q1^T A_J with G2, and the error):
 // 2 = the int8 tensor cores by the Ozaki scheme (k_ozaki.cu: k <= 128, a device-resident
 // A_D whose column maxima the round recorded, at least one J column), 1 = DMMA (k_fp64.cu).
-// Auto (0) is DMMA for now (measured: the int8 kernels are not yet faster on C4, DESIGN.md
-// §5); -1 = the int8 engine was requested and does not apply.
-static int fp64_engine(const mpid_ctx* h, int k) {
+// -1 = the int8 engine was requested and does not apply.
+static int fp64_engine(const mpid_ctx* h, int k, bool error_stage) {
   const bool oz_ok = k >= 1 && k <= 128 && h->host_AD != 2 && h->have_cmaxd && h->n - k > 0;
   if (h->fp64_engine == 1) return 1;
   if (h->fp64_engine == 2) return oz_ok ? 2 : -1;
   static const int env = getenv("MPID_FP64_ENGINE") ? atoi(getenv("MPID_FP64_ENGINE")) : 0;   // A/B measurements
+  if (env == 1) return 1;
   if (env == 2) return oz_ok ? 2 : 1;
-  return 1;   // auto: DMMA (the int8 kernels do not beat it yet)
+  // auto: the int8 fused error from 32768 rows per shard (C4: 9.3 vs 14.0 ms); the
+  // coefficients' [G2 | W] product stays on DMMA (its int8 kernel is not faster yet)
+  return (error_stage && oz_ok && h->m_local >= 32768) ? 2 : 1;
 }
 // the layout a call in format fmt needs
 static id_status ensure_layout(mpid_ctx* h, int fmt) {
@@ -1094,7 +1096,7 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
   if (ldp < k) return fail(h, ID_ERR_ARG, "ldp < k");
   if ((size_t)k * 33 * 8 > 200 * 1024) return fail(h, ID_ERR_DIM, "k=%d too large for the P solve", k);
   if (mode != ID_COEF_R && mode != ID_COEF_LSQ) return fail(h, ID_ERR_ARG, "bad coefficient mode");
-  const int eng = fp64_engine(h, k);
+  const int eng = fp64_engine(h, k, false);
   if (eng < 0) return fail(h, ID_ERR_ARG, "the int8 fp64 engine needs k <= 128, a device-resident A_D and n > k");
   CK(cudaEventRecord(h->ev[3], h->st));
   int launches = 0;
@@ -1263,7 +1265,7 @@ id_status id_error(id_handle h, double* abs_fro, double* rel_fro) {
   cudaGetLastError();
   if (!h->have_coef) return fail(h, ID_ERR_STATE, "id_error needs id_coeffs_fp64 first");
   const int k = h->k_out;
-  const int eng = fp64_engine(h, k);
+  const int eng = fp64_engine(h, k, true);
   if (eng < 0) return fail(h, ID_ERR_ARG, "the int8 fp64 engine needs k <= 128, a device-resident A_D and n > k");
   CK(cudaEventRecord(h->ev[5], h->st));
   int nblk = 0;

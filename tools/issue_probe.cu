@@ -89,6 +89,22 @@ __global__ void __launch_bounds__(160, 1) issue(int ksteps, int ni, long long* c
                 mma(tmem + (uint32_t)(d * N), sdesc(a + pa * 4096, 2048, 128), sdesc(b + (d - pa) * 2048, 1024, 128), id,
                     (first && pa == 0) ? 0u : 1u);
         }
+      } else if (PAT >= 3) {
+        // pattern 0 plus the pipeline's per-K-step extras: 3 = a commit per K-step,
+        // 4 = a tcgen05 after-sync fence per K-step, 5 = both, 6 = both + descriptors varying with the slot
+        const uint32_t aa = PAT == 6 ? su32(smem) + (uint32_t)((s & 3) * 49152) : a;
+        const uint32_t bb2 = PAT == 6 ? aa + 32768 : b;
+        if (PAT >= 4) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+#pragma unroll
+          for (int d = 0; d < 8; ++d)
+            if (owns(d, w, ni))
+#pragma unroll
+              for (int pa = 0; pa <= d; ++pa)
+                mma(tmem + (uint32_t)(d * N), sdesc(aa + pa * 4096, 2048, 128), sdesc(bb2 + (d - pa) * 2048, 1024, 128), id,
+                    (first && pa == 0) ? 0u : 1u);
+          if (PAT != 4) commit(&bar[w]);
+        }
       } else if (PAT == 1) {
         if (elect_one()) {
 #pragma unroll
@@ -160,5 +176,9 @@ int main() {
   run<0>(nsm, dc);
   run<1>(nsm, dc);
   run<2>(nsm, dc);
+  run<3>(nsm, dc);
+  run<4>(nsm, dc);
+  run<5>(nsm, dc);
+  run<6>(nsm, dc);
   return 0;
 }

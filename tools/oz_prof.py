@@ -14,7 +14,10 @@ h = MPID(A, k_max=100)
 h.qrcp("fp16", "pow2", k=100)
 for eng in ("int8", "dmma", "int8"):
     h.set_fp64_engine(eng)
-    h.coeffs("lsq")
-    e = h.error()
+    try:
+        h.coeffs("lsq")
+        e = h.error()
+    except Exception as ex:   # measurement knobs (MPID_OZ_DBG) produce garbage coefficients
+        e = str(ex)[:60]
     st = h.stats()
     print(eng, st["fp64_engine"], st["fp64_engine_err"], "coef", st["t_coef_ms"], "err", st["t_err_ms"], e)
