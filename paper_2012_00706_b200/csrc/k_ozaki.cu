@@ -79,9 +79,6 @@ __device__ __forceinline__ void oz_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
                : "memory");
 }
-__device__ __forceinline__ void l2_prefetch(const void* g, uint32_t bytes) {   // 16 B aligned, bytes % 16 == 0
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
@@ -362,27 +359,9 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- A producer; the warp's lanes prefetch B's fp64 rows into L2 ----------------
-    // (the slicers' own loads run one K-step ahead: HBM latency would bound them without it)
-    constexpr int PF = 12;                                       // K-steps ahead
-    const double* pcol[2] = {nullptr, nullptr};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int cp = t * TN_N + lane * 2 + h;
-      if (p.vec) {
-        if (cp < p.kq) pcol[h] = p.Q1 + (int64_t)cp * p.ldq;
-        else if (cp < p.ncol) pcol[h] = p.AD + (int64_t)p.cmap[cp - p.kq] * p.ld;
-      }
-    }
-    auto prefetch = [&](int64_t s) {
-      if (s >= s1) return;
-      const int64_t r0 = s * KSTEP;
-      const uint32_t bytes = (uint32_t)(min((int64_t)KSTEP, p.m - r0) * 8) & ~15u;
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        if (pcol[h] && bytes) l2_prefetch(pcol[h] + r0, bytes);
-    };
-    for (int64_t i = 0; i < PF && i < nst; ++i) prefetch(s0 + i);
+    // ---------------- A producer ----------------
+    // (an L2 prefetch of B's fp64 rows by this warp's lanes, cp.async.bulk.prefetch, made the
+    // kernel slower: the prefetches queue in the SM's TMA unit ahead of the A loads)
     for (int64_t i = 0; i < nst; ++i) {
       const int slot = (int)(i % TN_NST);
       if (lane == 0) {
@@ -394,13 +373,11 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
           tma_load(smem + slot * (TN_A + TN_B), p.As + (s0 + i) * (TN_A / 16), TN_A, &full_a[slot]);
         }
       }
-      __syncwarp();
-      prefetch(s0 + i + PF);
     }
   } else if (warp <= TN_NI) {
     // ---------------- MMA issuer: 12 MMAs per K-step (tn_kstep) ----------------
     if (lane == 0) {
-      const uint32_t id = oz_idesc(TN_N);
+      
       int cpos = 0;
       uint32_t aph = 0;
       for (int64_t i = 0; i < nst; ++i) {
@@ -445,7 +422,7 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
     // register-resident accumulators: 13 warps leave 128 registers per thread)
     double* out = p.part + (((int64_t)g * p.ntiles + t) * 128 + quarter * 32 + lane) * TN_N + chalf * 32;
     bool first_drain = true;
-    double v[8], nv[8];
+    double v[8], n1[8], n2[8];   // the current K-step's values and the next two (loads 2 K-steps ahead)
     auto load8 = [&](int64_t s, double* dst) {
       const int64_t r0 = s * KSTEP + ro * 8;
       if (col && r0 + 8 <= p.m && p.vec) {
@@ -461,14 +438,18 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
         for (int i = 0; i < 8; ++i) dst[i] = (col && r0 + i < p.m) ? __ldcs(col + r0 + i) : 0.0;
       }
     };
-    if (nst > 0 && !(p.dbg & 1)) load8(s0, nv);
+    if (nst > 0 && !(p.dbg & 1)) load8(s0, n1);
+    if (nst > 1 && !(p.dbg & 1)) load8(s0 + 1, n2);
     int cpos = 0;
     uint32_t aph = 0;
     for (int64_t i = 0; i < nst; ++i) {
       const int slot = (int)(i % TN_NST);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = nv[q];
-      if (i + 1 < nst && !(p.dbg & 1)) load8(s0 + i + 1, nv);
+      for (int q = 0; q < 8; ++q) {
+        v[q] = n1[q];
+        n1[q] = n2[q];
+      }
+      if (i + 2 < nst && !(p.dbg & 1)) load8(s0 + i + 2, n2);
       uint32_t lo[8], hi[8];
       oz_slice4(v, sc, lo);
       oz_slice4(v + 4, sc, hi);
@@ -550,6 +531,7 @@ struct OzErr {
   int64_t m;
   int nj, KP;
   int vec;                // A_D rows 16 B aligned (even ld, aligned base): L2 prefetch allowed
+  int dbg;                // measurement knobs (MPID_OZ_DBG): 4 = no L2 prefetch
   int64_t nrt;            // row tiles
   int njt;                // J tiles
   double* part;           // [gridDim.x]
@@ -570,6 +552,10 @@ __global__ void __launch_bounds__(ER_THREADS, 1) k_oz_err(const OzErr p) {
   uint64_t* acc_empty = bars + 8;   // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
   double* red = reinterpret_cast<double*>(bars + 12);
+  // element offsets of the J columns in A_D (cmap[c] * ld), staged once: the epilogue's A_D
+  // loads then depend on a shared-memory read, not on a global load of the column map
+  int64_t* coff = reinterpret_cast<int64_t*>(bars + 32);
+  for (int c = threadIdx.x; c < p.njt * ER_N; c += blockDim.x) coff[c] = c < p.nj ? (int64_t)p.cmap[c] * p.ld : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t my_rt = blockIdx.x < p.nrt ? (p.nrt - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
@@ -611,21 +597,6 @@ __global__ void __launch_bounds__(ER_THREADS, 1) k_oz_err(const OzErr p) {
           if (jc >= 2) mbar_wait(&b_empty[st], (uint32_t)(((jc >> 1) - 1) & 1));
           mbar_expect_tx(&b_full[st], (uint32_t)BBYTES);
           tma_load(sB + st * BBYTES, p.Ts + (int64_t)jt * (BBYTES / 16), (uint32_t)BBYTES, &b_full[st]);
-        }
-      }
-    } else if (p.vec) {
-      // lanes 1..31: L2 prefetch of the epilogue's A_D blocks, two J tiles ahead of the MMAs
-      // (one 128-row column segment, 1 KB, per column and tile): the epilogue's loads would
-      // otherwise wait on HBM latency
-      int64_t jc = 0;
-      for (int64_t i = 0; i < my_rt; ++i) {
-        const int64_t rt = blockIdx.x + i * gridDim.x;
-        const int64_t r0 = rt * 128;
-        const uint32_t bytes = (uint32_t)(min((int64_t)128, p.m - r0) * 8) & ~15u;
-        for (int jt = 0; jt < p.njt; ++jt, ++jc) {
-          if (jc >= 2) mbar_wait(&acc_full[jc & 1], (uint32_t)(((jc >> 1) - 1) & 1));   // tile jc - 2's MMAs done
-          for (int c = jt * ER_N + lane - 1; c < min(p.nj, (jt + 1) * ER_N); c += 31)
-            if (bytes) l2_prefetch(p.AD + (int64_t)p.cmap[c] * p.ld + r0, bytes);
         }
       }
     }
@@ -675,7 +646,16 @@ __global__ void __launch_bounds__(ER_THREADS, 1) k_oz_err(const OzErr p) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int c = c0 + j;
-          a[j] = (live && c < p.nj) ? __ldcs(p.AD + (int64_t)p.cmap[c] * p.ld + r) : 0.0;
+          a[j] = (live && c < p.nj) ? __ldcs(p.AD + coff[c] + r) : 0.0;
+        }
+        // the next J tile's A_D elements of this thread into L2 (no registers held): its
+        // loads, issued one tile from now, then wait on L2 instead of HBM
+        if (live && jt + 1 < p.njt) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int c = c0 + ER_N + j;
+            if (c < p.nj) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.AD + coff[c] + r));
+          }
         }
         mbar_wait(&acc_full[buf], (uint32_t)((jc >> 1) & 1));
         tc_fence_after();
@@ -797,10 +777,12 @@ cudaError_t launch_oz_error(const double* AD, int64_t m, int64_t ld, int nj, con
   p.nj = nj;
   p.KP = KP;
   p.vec = ((ld & 1) == 0 && (((uintptr_t)AD) & 15) == 0) ? 1 : 0;
+  p.dbg = getenv("MPID_OZ_DBG") ? atoi(getenv("MPID_OZ_DBG")) : 0;
   p.nrt = nrt;
   p.njt = njt;
   p.part = part;
-  const int smem = OZ_S * 128 * KP + 2 * OZ_S * ER_N * KP + 256 + 1024;
+  const int smem = OZ_S * 128 * KP + 2 * OZ_S * ER_N * KP + 256 + njt * ER_N * 8 + 1024;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   if ((e = smem_attr((const void*)k_oz_err, smem)) != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(nrt, num_sms);
   *nblk_out = grid;
