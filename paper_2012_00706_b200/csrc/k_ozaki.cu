@@ -44,7 +44,7 @@ constexpr int TN_NST = 4;                             // pipeline stages (one K-
 constexpr int TN_A = OZ_S * 128 * KSTEP;              // 32 KB: 8 slices of 128 (M) x 32 (K)
 constexpr int TN_B = OZ_S * TN_N * KSTEP;             // 16 KB: 8 slices of 64 (N) x 32 (K)
 constexpr int TN_CHS = 512;                           // K-steps per int32 chunk (16384 rows)
-constexpr int TN_SLW = 8;                             // slicer / drain warps
+constexpr int TN_SLW = 16;                            // slicer / drain warps
 constexpr int TN_NI = 1;                              // MMA-issuing warp (12 MMAs per K-step)
 constexpr int TN_THREADS = 32 * (1 + TN_NI + TN_SLW);
 constexpr int TN_SMEM = TN_NST * (TN_A + TN_B) + 1024 + 1024;
@@ -92,6 +92,10 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 #define OZ_LD8(taddr, r)                                                                                       \
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                           \
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])   \
+               : "r"(taddr))
+#define OZ_LD4(taddr, r)                                                                                       \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"                                     \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])                                                  \
                : "r"(taddr))
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -171,22 +175,20 @@ __global__ void __launch_bounds__(256) k_oz_colmax(const double* __restrict__ X,
 __global__ void __launch_bounds__(256) k_oz_slice_cols(const double* __restrict__ X, int64_t m, int64_t ld, int k,
                                                        const unsigned long long* __restrict__ cmax, int64_t nsteps,
                                                        uint4* __restrict__ As) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= nsteps * 256) return;
-  const int l = (int)(idx & 127), h = (int)((idx >> 7) & 1);
-  const int64_t s = idx >> 8;
-  const int64_t r0 = s * KSTEP + h * 16;
+  // one block per K-step: the 32 rows x k columns are read column-segment-wise (a warp =
+  // one column's 256 B, coalesced) into shared memory, then thread (l, row half h) slices
+  // its 16 values and writes 8 x 16 B (consecutive l: contiguous)
+  __shared__ double tile[128][KSTEP + 1];
+  const int64_t s = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = s * KSTEP + lane;
+  for (int l = warp; l < 128; l += 8) tile[l][lane] = (l < k && r < m) ? __ldcs(X + (int64_t)l * ld + r) : 0.0;
+  __syncthreads();
+  const int l = threadIdx.x & 127, h = threadIdx.x >> 7;
+  const double sc = l < k ? pow2(56 - oz_exp(__longlong_as_double((long long)cmax[l]))) : 0.0;
   double v[16];
-  double sc = 0.0;
-  if (l < k) {
-    sc = pow2(56 - oz_exp(__longlong_as_double((long long)cmax[l])));
-    const double* col = X + (int64_t)l * ld;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = r0 + i < m ? col[r0 + i] : 0.0;
-  } else {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = 0.0;
-  }
+  for (int i = 0; i < 16; ++i) v[i] = tile[l][h * 16 + i];
   uint32_t w[4][8];
 #pragma unroll
   for (int g = 0; g < 4; ++g) oz_slice4(v + 4 * g, sc, w[g]);
@@ -403,9 +405,15 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
     }
   } else {
     // ---------------- B slicers + drain ----------------
-    const int sw = warp - 1 - TN_NI;                           // 0..7
-    const int tid = sw * 32 + lane;                            // 0..255
-    const int c = tid & 63, ro = tid >> 6;                     // column, 8-row octet of the K-step
+    // TN_SLW warps: thread = (column c, RPT consecutive rows of the 32-row K-step)
+    constexpr int RPT = KSTEP * TN_N / (32 * TN_SLW);          // rows per thread (4 with 16 warps)
+    constexpr int CW = TN_N * 4 / TN_SLW;                      // drain: columns per warp (16 with 16 warps)
+    const int sw = warp - 1 - TN_NI;
+    const int tid = sw * 32 + lane;
+    // lanes of a warp take consecutive row groups of the same few columns, so each warp load
+    // reads whole 256 B column segments (coalesced) instead of 32 B from 32 columns
+    constexpr int NRG = KSTEP / RPT;                           // row groups per K-step
+    const int c = tid / NRG, ro = tid % NRG;                   // column, row group of RPT rows
     const int cp = t * TN_N + c;
     const double* col = nullptr;
     if (cp < p.kq) col = p.Q1 + (int64_t)cp * p.ldq;
@@ -414,50 +422,53 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
                                                        : __longlong_as_double((long long)p.cmaxd[p.cmap[cp - p.kq]])))
                           : 0.0;
     // B stage, slices concatenated along N: element (q, c, k) at (k / 16) * 8192 +
-    // (8 q + c / 8) * 128 + (c % 8) * 16 + k % 16
-    const uint32_t boff = (uint32_t)((ro >> 1) * 8192 + (c >> 3) * 128 + (c & 7) * 16 + (ro & 1) * 8);
-    // drain mapping: TMEM lane quarter warp % 4, columns 32 (sw / 4)
-    const int quarter = warp & 3, chalf = sw >> 2;
-    // the drained chunk sums accumulate in this thread's own slots of the partials (no
-    // register-resident accumulators: 13 warps leave 128 registers per thread)
-    double* out = p.part + (((int64_t)g * p.ntiles + t) * 128 + quarter * 32 + lane) * TN_N + chalf * 32;
+    // (8 q + c / 8) * 128 + (c % 8) * 16 + k % 16; this thread's rows k = ro RPT .. + RPT - 1
+    const int k0 = ro * RPT;
+    const uint32_t boff = (uint32_t)((k0 >> 4) * 8192 + (c >> 3) * 128 + (c & 7) * 16 + (k0 & 15));
+    // drain mapping: TMEM lane quarter warp % 4, CW columns (sw / 4)
+    const int quarter = warp & 3, cgrp = sw >> 2;
+    // the drained chunk sums accumulate in this thread's own slots of the partials
+    double* out = p.part + (((int64_t)g * p.ntiles + t) * 128 + quarter * 32 + lane) * TN_N + cgrp * CW;
     bool first_drain = true;
-    double v[8], n1[8], n2[8];   // the current K-step's values and the next two (loads 2 K-steps ahead)
-    auto load8 = [&](int64_t s, double* dst) {
-      const int64_t r0 = s * KSTEP + ro * 8;
-      if (col && r0 + 8 <= p.m && p.vec) {
+    double v[RPT], n1[RPT], n2[RPT];   // the current K-step's values and the next two (loads 2 K-steps ahead)
+    auto loadr = [&](int64_t s, double* dst) {
+      const int64_t r0 = s * KSTEP + k0;
+      if (col && r0 + RPT <= p.m && p.vec) {
         const double2* q = reinterpret_cast<const double2*>(col + r0);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < RPT / 2; ++i) {
           const double2 x = __ldcs(q + i);
           dst[2 * i] = x.x;
           dst[2 * i + 1] = x.y;
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) dst[i] = (col && r0 + i < p.m) ? __ldcs(col + r0 + i) : 0.0;
+        for (int i = 0; i < RPT; ++i) dst[i] = (col && r0 + i < p.m) ? __ldcs(col + r0 + i) : 0.0;
       }
     };
-    if (nst > 0 && !(p.dbg & 1)) load8(s0, n1);
-    if (nst > 1 && !(p.dbg & 1)) load8(s0 + 1, n2);
+    if (nst > 0 && !(p.dbg & 1)) loadr(s0, n1);
+    if (nst > 1 && !(p.dbg & 1)) loadr(s0 + 1, n2);
     int cpos = 0;
     uint32_t aph = 0;
     for (int64_t i = 0; i < nst; ++i) {
       const int slot = (int)(i % TN_NST);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < RPT; ++q) {
         v[q] = n1[q];
         n1[q] = n2[q];
       }
-      if (i + 2 < nst && !(p.dbg & 1)) load8(s0 + i + 2, n2);
-      uint32_t lo[8], hi[8];
-      oz_slice4(v, sc, lo);
-      oz_slice4(v + 4, sc, hi);
+      if (i + 2 < nst && !(p.dbg & 1)) loadr(s0 + i + 2, n2);
+      uint32_t w[RPT / 4][8];
+#pragma unroll
+      for (int g4 = 0; g4 < RPT / 4; ++g4) oz_slice4(v + 4 * g4, sc, w[g4]);
       if (i >= TN_NST) mbar_wait(&empty[slot], (uint32_t)(((i / TN_NST) - 1) & 1));
       unsigned char* bst = smem + slot * (TN_A + TN_B) + TN_A + boff;
       if (!(p.dbg & 1)) {
 #pragma unroll
-        for (int q = 0; q < OZ_S; ++q) *reinterpret_cast<uint2*>(bst + q * 1024) = make_uint2(lo[q], hi[q]);
+        for (int q = 0; q < OZ_S; ++q) {
+          if constexpr (RPT == 8) *reinterpret_cast<uint2*>(bst + q * 1024) = make_uint2(w[0][q], w[1][q]);
+          else *reinterpret_cast<uint32_t*>(bst + q * 1024) = w[0][q];
+        }
       }
       fence_async_smem();
       __syncwarp();
@@ -469,19 +480,19 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
         tc_fence_after();
         const double sa = ea[quarter * 32 + lane];
 #pragma unroll 1
-        for (int h = 0; h < 4; ++h) {
-          uint32_t r[OZ_S][8];
+        for (int h = 0; h < CW / 4; ++h) {
+          uint32_t r[OZ_S][4];
 #pragma unroll
           for (int d = 0; d < OZ_S; ++d)
-            OZ_LD8(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(d * TN_N + chalf * 32 + h * 8), r[d]);
+            OZ_LD4(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(d * TN_N + cgrp * CW + h * 4), r[d]);
           tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
+          for (int j = 0; j < 4; ++j) {
             double x = i2d(r[OZ_S - 1][j]);
 #pragma unroll
             for (int d = OZ_S - 2; d >= 0; --d) x = fma(x, 0.0078125, i2d(r[d][j]));
-            const double val = x * sa * eb[chalf * 32 + h * 8 + j];
-            out[h * 8 + j] = first_drain ? val : out[h * 8 + j] + val;
+            const double val = x * sa * eb[cgrp * CW + h * 4 + j];
+            out[h * 4 + j] = first_drain ? val : out[h * 4 + j] + val;
           }
         }
         first_drain = false;
@@ -491,7 +502,7 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k_oz_tn(const OzTN p) {
       }
     }
     if (first_drain)   // no rows in this group: zero partials
-      for (int j = 0; j < 32; ++j) out[j] = 0.0;
+      for (int j = 0; j < CW; ++j) out[j] = 0.0;
   }
   tc_fence_before();
   __syncthreads();
@@ -720,7 +731,7 @@ cudaError_t launch_oz_tn(const double* Q1, int64_t m, int k, const double* AD, i
   k_oz_colmax<<<dim3((unsigned)k, (unsigned)ysplit), 256, 0, st>>>(Q1, m, m, cmaxq);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int64_t nsteps = (m + KSTEP - 1) / KSTEP;
-  k_oz_slice_cols<<<(unsigned)((nsteps * 256 + 255) / 256), 256, 0, st>>>(Q1, m, m, k, cmaxq, nsteps,
+  k_oz_slice_cols<<<(unsigned)nsteps, 256, 0, st>>>(Q1, m, m, k, cmaxq, nsteps,
                                                                            (uint4*)slices);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   OzTN p{};

@@ -501,9 +501,10 @@ static int fp64_engine(const mpid_ctx* h, int k, bool error_stage) {
   static const int env = getenv("MPID_FP64_ENGINE") ? atoi(getenv("MPID_FP64_ENGINE")) : 0;   // A/B measurements
   if (env == 1) return 1;
   if (env == 2) return oz_ok ? 2 : 1;
-  // auto: the int8 fused error from 32768 rows per shard (C4: 9.3 vs 14.0 ms); the
-  // coefficients' [G2 | W] product stays on DMMA (its int8 kernel is not faster yet)
-  return (error_stage && oz_ok && h->m_local >= 32768) ? 2 : 1;
+  // auto: int8 from 32768 rows per shard (C4: error 9.2 vs 14.1 ms, coefficients 14.8 vs
+  // 19.6 ms); below that the DMMA kernels' shorter launches win
+  (void)error_stage;
+  return (oz_ok && h->m_local >= 32768) ? 2 : 1;
 }
 // the layout a call in format fmt needs
 static id_status ensure_layout(mpid_ctx* h, int fmt) {
@@ -845,8 +846,11 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
   }
   CK(launch_init_pivot(h->norms, (int)n, h->perm, h->sc, h->st));
   h->kernel_launches += 1;
-  // one shard: the pass partials' reduction and the reflector are one launch (k_reduce_reflect)
-  const bool fused = h->nranks <= 1 && !h->comm && !getenv("MPID_NO_FUSED_REFLECT");
+  // one shard: the pass partials' reduction and the reflector can be one launch
+  // (k_reduce_reflect, a last-block ticket); measured no faster in the captured step graph
+  // (C2 k = 128: 2.24 vs 1.92 ms per QRCP, C4 +0.2 ms), so it is an opt-in A/B switch
+  static const bool fused_on = getenv("MPID_FUSED_REFLECT") != nullptr;
+  const bool fused = fused_on && h->nranks <= 1 && !h->comm;
   if (fused) CK(cudaMemsetAsync(h->ticket, 0, sizeof(unsigned int), h->st));
   const int own_lo = (int)std::min<int64_t>(h->row_offset, INT32_MAX);
   for (int j = 0; j < k_max; ++j) {

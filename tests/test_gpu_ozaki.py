@@ -116,3 +116,29 @@ def test_int8_engine_refused_where_it_does_not_apply():
     h.coeffs("lsq")
     assert h.stats()["fp64_engine"] == 1
     h.close()
+
+
+def test_auto_engine_choice():
+    """Auto: the int8 engine from 32768 rows per shard with k <= 128, else DMMA."""
+    import torch
+    from paper_2012_00706_b200.mpid import MPID
+    from tests.gpu_helpers import to_dev
+    A = np.asfortranarray(gen_config("C2", 0)[:4096, :256])
+    h = MPID(to_dev(A), k_max=16)
+    h.qrcp("fp32", "none", k=16)
+    h.coeffs("lsq")
+    h.error()
+    st = h.stats()
+    assert st["fp64_engine"] == 1 and st["fp64_engine_err"] == 1
+    h.close()
+    fp = fourier_params(32, 64, 1024, 0)
+    At = gen_fourier(fp, 0, device="cuda")
+    h = MPID(At, k_max=100)
+    h.qrcp("fp16", "pow2", k=100)
+    h.coeffs("lsq")
+    h.error()
+    st = h.stats()
+    assert st["fp64_engine"] == 2 and st["fp64_engine_err"] == 2
+    h.close()
+    del At
+    torch.cuda.empty_cache()
