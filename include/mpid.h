@@ -104,8 +104,14 @@ typedef struct {
                         5 = the whole QRCP in ONE launch in one SM's shared memory (fp16 /
                         fp32, a single shard with m x n x 4 B <= ~220 KB, e.g. C1), in the
                         oracle's paper model (per-operation RNE update, fp64 row-order
-                        sums) bit for bit.  Default: 5 when it applies, else 2 for fp16 with
-                        range scaling, n <= 2048 and >= 16384 rows per shard, else 1. */
+                        sums) bit for bit.
+                        6 = the whole QRCP in ONE cooperative launch with the matrix held in
+                        the shared memory of all SMs (fp16 / fp32, a single shard with m x n x 4 B
+                        <= ~32 MB, e.g. C2): the same paper model, with each column's fp64 sums
+                        formed per row slab and the slab partials added by a fixed warp tree
+                        (opt-in: on C2 it is slower than the captured multi-kernel step).
+                        Default: 5 when it applies, else 2 for fp16 with range scaling,
+                        n <= 2048 and >= 16384 rows per shard, else 1. */
   int32_t sketch_oversample; /* formation 4: l = k_max + sketch_oversample; 0 = fill the
                                 128-row MMA tile that k_max + 10 needs (l = 128 for k = 100) */
   int32_t sketch_seed;       /* formation 4: seed of the Rademacher sketch */

@@ -10,7 +10,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["mpid_api.cu", "k_round.cu", "k_qrcp.cu", "k_pass.cu", "k_pass_tc.cu", "k_qrcp_smem.cu", "k_fp64.cu", "k_norm2.cu", "k_gram.cu", "k_ozaki.cu"]
+SOURCES = ["mpid_api.cu", "k_round.cu", "k_qrcp.cu", "k_pass.cu", "k_pass_tc.cu", "k_qrcp_smem.cu", "k_fp64.cu", "k_norm2.cu", "k_gram.cu", "k_ozaki.cu", "k_qrcp_coop.cu"]
 LIB = os.path.join(HERE, "libmpid.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -836,6 +836,15 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     CK(rec(h, h->ev[2]));
     return ID_OK;
   }
+  if (formation == 6) {
+    // the whole QRCP in one cooperative launch, the matrix in all SMs' shared memory
+    CK(launch_qrcp_coop(fmt, h->S, h->m_local, (int)n, k_max, nb, eps, h->perm, (float*)h->R, h->part,
+                        h->part + (size_t)pass_gx_cap() * n, h->sc, num_sms(), h->st));
+    h->kernel_launches += 1;
+    h->pass_launches = 0;
+    CK(rec(h, h->ev[2]));
+    return ID_OK;
+  }
   if (formation == 5) {
     // the whole QRCP in one CTA's shared memory (the oracle's paper model, bit for bit)
     CK(launch_qrcp_smem(fmt, h->S, h->m_local, (int)n, k_max, nb, eps, h->perm, (float*)h->R, h->sc, h->st));
@@ -963,13 +972,19 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
   // 5 = the one-launch shared-memory QRCP (the paper model), default when one shard fits an SM
   const bool smem_ok = (fmt == ID_FP16 || fmt == ID_FP32) && h->nranks == 1 && !h->comm &&
                        qrcp_smem_bytes(h->m_local, (int)h->n, k_max) <= 227 * 1024;
+  // 6 = the one-launch cooperative QRCP (the matrix in all SMs' shared memory, e.g. C2): opt-in —
+  // measured ~19 us per step on C2 against ~15 us for the captured multi-kernel step
+  const bool coop_ok = (fmt == ID_FP16 || fmt == ID_FP32) && h->nranks == 1 && !h->comm &&
+                       qrcp_coop_rows(h->m_local, (int)h->n, num_sms()) > 0;
   int formation = opts ? opts->formation : 0;
   if (formation == 0) formation = smem_ok ? 5 : (tc_default ? 2 : 1);
+  if (formation == 6 && !coop_ok)
+    return fail(h, ID_ERR_ARG, "the cooperative QRCP needs fp16 / fp32, one shard and m x n x 4 B <= ~32 MB");
   if (formation == 5 && !smem_ok)
     return fail(h, ID_ERR_ARG, "the shared-memory QRCP needs fp16 / fp32, one shard and m x n x 4 B <= ~220 KB");
   if (formation == 2 && !tc_ok)
     return fail(h, ID_ERR_ARG, "the tcgen05 pass needs fp16 storage with range scaling, n <= 2048, m < 4.4e8");
-  if (formation < 1 || formation > 5) return fail(h, ID_ERR_ARG, "bad formation %d", formation);
+  if (formation < 1 || formation > 6) return fail(h, ID_ERR_ARG, "bad formation %d", formation);
   if ((formation == 3 || formation == 4) && fmt != ID_FP16)
     return fail(h, ID_ERR_ARG, "Gram / sketched pivoting (formation 3, 4) run on fp16 A_L (tcgen05 kind::f16)");
   if (formation == 4) {
@@ -984,7 +999,7 @@ id_status id_qrcp_lowprec(id_handle h, id_format fmt, id_scaling scaling, int32_
     const int r = encode_tmap_gram(h->tmapO, (char*)h->S + (size_t)h->m_pad * h->n * 2, h->m_pad / 8, h->sk_lw);
     if (r != 0) return fail(h, ID_ERR_CUDA, "cuTensorMapEncodeTiled (sketch) failed (%d)", r);
   }
-  int nb = opts && opts->nb > 0 ? opts->nb : ((formation == 2 || formation == 5) ? 16 : 4);
+  int nb = opts && opts->nb > 0 ? opts->nb : ((formation == 2 || formation == 5 || formation == 6) ? 16 : 4);
   if (nb > NB_MAX || (formation == 1 && nb > 16) || (fmt == ID_FP64 && nb > 8))
     return fail(h, ID_ERR_ARG, "nb=%d too large for formation %d / format %d", nb, formation, (int)fmt);
   // no graph capture for a loopback group (host-side reductions) or a host-streamed A_D

@@ -154,6 +154,11 @@ cudaError_t launch_pass_tma(int fmt, PassParams p, int num_sms, int* gx_out, cud
 size_t qrcp_smem_bytes(int64_t m, int n, int k);
 cudaError_t launch_qrcp_smem(int fmt, const void* S, int64_t m, int n, int k_max, int nb, double eps, int* perm,
                              float* R, DevScalars* sc, cudaStream_t st);
+// the one-launch cooperative QRCP of a matrix that fits all SMs' shared memory (k_qrcp_coop.cu;
+// the paper model with slab-partial fp64 sums); rows per slab or 0 when it does not apply
+int qrcp_coop_rows(int64_t m, int n, int num_sms);
+cudaError_t launch_qrcp_coop(int fmt, const void* S, int64_t m, int n, int k_max, int nb, double eps, int* perm,
+                             float* R, double* part, double* red, DevScalars* sc, int num_sms, cudaStream_t st);
 // tcgen05 pass (fp16 storage; k_pass_tc.cu): operands, launch, tensor map of S
 int tc_kchw(int nb);
 size_t tc_vop_bytes(int64_t m_pad, int nb);

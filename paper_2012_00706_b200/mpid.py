@@ -280,7 +280,7 @@ class MPID:
     def qrcp(self, fmt="fp16", scaling="pow2", k=None, eps=0.0, nb=0, use_graph=True,
              profile=False, allow_underflow=False, formation=0, oversample=0, seed=0) -> QRCPOut:
         """formation: 0 auto, 1 / "ffma" CUDA-core FFMA, 2 / "tc" tcgen05, 3 / "gram" Gram pivoting (include/mpid.h)."""
-        formation = {"auto": 0, "ffma": 1, "tc": 2, "gram": 3, "sketch": 4, "smem": 5}.get(formation, formation)
+        formation = {"auto": 0, "ffma": 1, "tc": 2, "gram": 3, "sketch": 4, "smem": 5, "coop": 6}.get(formation, formation)
         o = QRCPOpts(nb=nb, use_graph=1 if use_graph else -1, profile_pass=1 if profile else 0,
                      formation=formation, sketch_oversample=oversample, sketch_seed=seed)
         k = self.k_max if k is None else k
