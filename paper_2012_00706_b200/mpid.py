@@ -18,7 +18,8 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmpid.so")
+# MPID_LIB = another in-tree build of the library (A/B measurements of two builds)
+LIB_PATH = os.path.join(HERE, os.environ.get("MPID_LIB", "libmpid.so"))
 
 ID_FP16, ID_FP32, ID_FP64 = 1, 2, 3
 ID_SCALE_NONE, ID_SCALE_MAXABS, ID_SCALE_POW2 = 0, 1, 2
