@@ -897,7 +897,11 @@ static id_status enqueue_qrcp(mpid_ctx* h, int fmt, int scaling, int k_max, doub
     if (formation == 2 && h->tmap_ok != 0) return fail(h, ID_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", h->tmap_ok);
     if (profile) CK(rec(h, h->pass_ev[2 * j]));
     if (formation == 2) CK(launch_pass_tc(p, nb, h->Vop, h->Fop, h->tmapS, h->tmapC, pass_gx_cap(), &gx_used, h->st));
-    else CK(launch_pass_tma(fmt, p, num_sms(), &gx_used, h->st));
+    else {
+      static const int cap_env = getenv("MPID_PASS_MAXCTAS") ? atoi(getenv("MPID_PASS_MAXCTAS")) : 0;   // measurements
+      const int cap = cap_env > 0 ? std::min(cap_env, num_sms()) : num_sms();
+      CK(launch_pass_tma(fmt, p, cap, &gx_used, h->st));
+    }
     if (gx_used < 1 || gx_used > pass_gx_cap())
       return fail(h, ID_ERR_STATE, "panel pass grid %d exceeds the partials buffer (%d)", gx_used, pass_gx_cap());
     if (profile) CK(rec(h, h->pass_ev[2 * j + 1]));
