@@ -50,7 +50,7 @@ constexpr int TN_THREADS = 32 * (1 + TN_NI + TN_SLW);
 constexpr int TN_SMEM = TN_NST * (TN_A + TN_B) + 1024 + 1024;
 // error kernel
 constexpr int ER_N = 32;                              // J columns per tile (MMA N)
-constexpr int ER_EPW = 8;                             // epilogue warps
+constexpr int ER_EPW = 8;                             // epilogue warps (16: more spills, slower)
 constexpr int ER_NI = 1;                              // MMA-issuing warp (8 MMAs per K-step)
 constexpr int ER_THREADS = 32 * (1 + ER_NI + ER_EPW);
 
@@ -104,6 +104,17 @@ __device__ __forceinline__ double i2d(uint32_t a) {
   return __hiloint2double(0x43380000, (int)(a ^ 0x80000000u)) - 6755401588539392.0;
 }
 
+// the 8 diagonal accumulators (|acc_d| < 2^24 for K <= 128) combined exactly in two int64
+// Horner halves H = sum_{d<4} acc_d 2^{7(3-d)}, L = sum_{d>=4} acc_d 2^{7(7-d)} (|H|, |L| < 2^46),
+// each converted exactly with the 1.5 2^52 bit-pattern add: sum_d acc_d 2^{-7d} =
+// (H + L 2^{-28}) 2^{-21} — 2 fp64 adds and 1 fma instead of 8 conversions and 7 fmas
+__device__ __forceinline__ double oz_combine8(const uint32_t* a) {
+  const long long H = ((((long long)(int)a[0] * 128 + (int)a[1]) * 128 + (int)a[2]) * 128) + (int)a[3];
+  const long long L = ((((long long)(int)a[4] * 128 + (int)a[5]) * 128 + (int)a[6]) * 128) + (int)a[7];
+  const double hd = __longlong_as_double(0x4338000000000000LL + H) - 6755399441055744.0;
+  const double ld = __longlong_as_double(0x4338000000000000LL + L) - 6755399441055744.0;
+  return fma(ld, 3.7252902984619140625e-09, hd);   // 2^-28
+}
 // the smallest E with mx < 2^E (mx > 0; 0 for mx == 0)
 __device__ __forceinline__ int oz_exp(double mx) {
   if (!(mx > 0.0)) return 0;
@@ -198,7 +209,7 @@ __global__ void __launch_bounds__(256) k_oz_slice_cols(const double* __restrict_
 }
 
 // A_I (m x k, ldx) -> per 128-row tile t the error kernel's A operand: 8 slices of
-// 128 x KP bytes, [t][p][kc KP/16][r 128][16 B]; rsc[r] = 2^{E_r - 14}.  Thread per row.
+// 128 x KP bytes, [t][p][kc KP/16][r 128][16 B]; rsc[r] = 2^{E_r - 35}.  Thread per row.
 __global__ void __launch_bounds__(128) k_oz_slice_rows(const double* __restrict__ X, int64_t m, int64_t ldx, int k,
                                                        int KP, uint4* __restrict__ As, double* __restrict__ rsc) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // grid covers the padded rows
@@ -208,7 +219,7 @@ __global__ void __launch_bounds__(128) k_oz_slice_rows(const double* __restrict_
     for (int l = 0; l < k; ++l) mx = fmax(mx, fabs(X[(int64_t)l * ldx + r]));
   const int E = oz_exp(mx);
   const double sc = pow2(56 - E);
-  rsc[r] = live ? pow2(E - 14) : 0.0;
+  rsc[r] = live ? pow2(E - 35) : 0.0;   // 2^{E-14} times the 2^{-21} of oz_combine8
   const int64_t t = r >> 7;
   const int rr = (int)(r & 127);
   const int nkc = KP / 16;
@@ -533,7 +544,7 @@ __global__ void k_oz_tn_reduce(const double* __restrict__ part, int ngroups, int
 //               A_D(r, J_c) (loaded before the wait), squares summed in fp64
 struct OzErr {
   const uint4* As;        // A_I slices per row tile
-  const double* rsc;      // per row 2^{E_r - 14}
+  const double* rsc;      // per row 2^{E_r - 35} (2^{E_r - 14} and oz_combine8's 2^{-21})
   const uint4* Ts;        // T slices per J tile
   const double* fsc;      // per column 2^{E_c}
   const double* AD;
@@ -643,7 +654,9 @@ __global__ void __launch_bounds__(ER_THREADS, 1) k_oz_err(const OzErr p) {
       }
     }
   } else {
-    const int ew = warp - 1 - ER_NI, quarter = warp & 3, chalf = ew >> 2;
+    // warp: TMEM lane quarter warp % 4 (rows), ECW columns of each tile (ew / 4)
+    constexpr int ECW = ER_N * 4 / ER_EPW;            // columns per epilogue warp (8 with 16 warps)
+    const int ew = warp - 1 - ER_NI, quarter = warp & 3, cg = ew >> 2;
     int64_t jc = 0;
     for (int64_t i = 0; i < my_rt; ++i) {
       const int64_t rt = blockIdx.x + i * gridDim.x;
@@ -652,10 +665,10 @@ __global__ void __launch_bounds__(ER_THREADS, 1) k_oz_err(const OzErr p) {
       const double rs = live ? p.rsc[r] : 0.0;
       for (int jt = 0; jt < p.njt; ++jt, ++jc) {
         const int buf = (int)(jc & 1);
-        const int c0 = jt * ER_N + chalf * 16;
-        double a[16];
+        const int c0 = jt * ER_N + cg * ECW;
+        double a[ECW];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < ECW; ++j) {
           const int c = c0 + j;
           a[j] = (live && c < p.nj) ? __ldcs(p.AD + coff[c] + r) : 0.0;
         }
@@ -663,21 +676,21 @@ __global__ void __launch_bounds__(ER_THREADS, 1) k_oz_err(const OzErr p) {
         // loads, issued one tile from now, then wait on L2 instead of HBM
         if (live && jt + 1 < p.njt) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
+          for (int j = 0; j < ECW; ++j) {
             const int c = c0 + ER_N + j;
             if (c < p.nj) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.AD + coff[c] + r));
           }
         }
         mbar_wait(&acc_full[buf], (uint32_t)((jc >> 1) & 1));
         tc_fence_after();
-        const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * OZ_S * ER_N + chalf * 16);
+        const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * OZ_S * ER_N + cg * ECW);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < ECW / 8; ++h) {
           uint32_t acc[OZ_S][8];
 #pragma unroll
           for (int d = 0; d < OZ_S; ++d) OZ_LD8(ta + (uint32_t)(d * ER_N + h * 8), acc[d]);
           tmem_wait_ld();
-          if (h == 1) {
+          if (h == ECW / 8 - 1) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[buf]);
@@ -685,11 +698,12 @@ __global__ void __launch_bounds__(ER_THREADS, 1) k_oz_err(const OzErr p) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int c = c0 + h * 8 + j;
-            double x = i2d(acc[OZ_S - 1][j]);
+            uint32_t dg[OZ_S];
 #pragma unroll
-            for (int d = OZ_S - 2; d >= 0; --d) x = fma(x, 0.0078125, i2d(acc[d][j]));
+            for (int d = 0; d < OZ_S; ++d) dg[d] = acc[d][j];
+            const double x = oz_combine8(dg);               // sum_d acc_d 2^{-7d} times 2^21
             const double fs = c < p.nj ? __ldg(p.fsc + c) : 0.0;
-            const double e = a[h * 8 + j] - x * rs * fs;
+            const double e = fma(-x, rs * fs, a[h * 8 + j]);
             ss = fma(e, e, ss);
           }
         }
