@@ -225,7 +225,8 @@ id_status id_error(id_handle h, double* abs_fro, double* rel_fro);
  *       split into eight 7-bit slices under one power-of-two exponent, the 36 slice products
  *       with p + q <= 7 accumulated exactly in int32 and recombined in fp64 — per-product
  *       error < 1.3e-16 relative to 2^(Ea+Eb); needs k <= 128, a device-
- *       resident A_D (not ID_CREATE_STREAM_HOST) and n > k (else ID_ERR_ARG at the call);
+ *       resident A_D (not ID_CREATE_STREAM_HOST), k < n <= 64 x SMs and the error kernel's
+ *       shared memory (n - k <= ~4000 at k = 128) (else ID_ERR_ARG at the call);
  *   0 = automatic (default): 2 where it applies with >= 32768 rows per shard (faster on
  *       C4: coefficients 14.8 vs 19.6 ms, error 9.2 vs 14.1 ms), else 1.
  * Takes effect from the next id_coeffs_fp64 / id_error; id_stats reports the engine used. */

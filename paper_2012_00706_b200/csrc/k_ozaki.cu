@@ -733,6 +733,17 @@ size_t oz_tslice_bytes(int64_t n) { return (size_t)((n + ER_N - 1) / ER_N + 1) *
 size_t oz_part_doubles(int num_sms) { return (size_t)num_sms * 128 * TN_N; }
 
 static int oz_kp(int k) { return (k + KSTEP - 1) / KSTEP * KSTEP; }
+static size_t oz_err_smem(int k, int nj) {
+  const int KP = oz_kp(k), njt = (nj + ER_N - 1) / ER_N;
+  return (size_t)OZ_S * 128 * KP + 2 * (size_t)OZ_S * ER_N * KP + 256 + (size_t)njt * ER_N * 8 + 1024;
+}
+// the shapes the int8 kernels take: k <= 128, the TN grid within one CTA per SM, the error
+// kernel's shared memory (A slices, two B stages, the J columns' offsets) within 227 KB
+bool oz_fits(int64_t n, int k, int num_sms) {
+  if (k < 1 || k > 128 || n <= k) return false;
+  if ((n + TN_N - 1) / TN_N > num_sms) return false;
+  return oz_err_smem(k, (int)(n - k)) <= 227 * 1024;
+}
 
 // [G2 | W] = Q1^T [Q1 | A_D(:, J)]; cmaxq (k entries) is computed here; cmaxd = A_D's column maxima
 cudaError_t launch_oz_tn(const double* Q1, int64_t m, int k, const double* AD, int64_t ld, const int* cmapJ, int nj,
@@ -806,7 +817,7 @@ cudaError_t launch_oz_error(const double* AD, int64_t m, int64_t ld, int nj, con
   p.nrt = nrt;
   p.njt = njt;
   p.part = part;
-  const int smem = OZ_S * 128 * KP + 2 * OZ_S * ER_N * KP + 256 + njt * ER_N * 8 + 1024;
+  const int smem = (int)oz_err_smem(k, nj);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   if ((e = smem_attr((const void*)k_oz_err, smem)) != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(nrt, num_sms);

@@ -495,7 +495,7 @@ static id_status relayout(mpid_ctx* h, int sbytes) {
 // A_D whose column maxima the round recorded, at least one J column), 1 = DMMA (k_fp64.cu).
 // -1 = the int8 engine was requested and does not apply.
 static int fp64_engine(const mpid_ctx* h, int k, bool error_stage) {
-  const bool oz_ok = k >= 1 && k <= 128 && h->host_AD != 2 && h->have_cmaxd && h->n - k > 0;
+  const bool oz_ok = h->host_AD != 2 && h->have_cmaxd && oz_fits(h->n, k, num_sms());
   if (h->fp64_engine == 1) return 1;
   if (h->fp64_engine == 2) return oz_ok ? 2 : -1;
   static const int env = getenv("MPID_FP64_ENGINE") ? atoi(getenv("MPID_FP64_ENGINE")) : 0;   // A/B measurements
@@ -1120,7 +1120,7 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
   if ((size_t)k * 33 * 8 > 200 * 1024) return fail(h, ID_ERR_DIM, "k=%d too large for the P solve", k);
   if (mode != ID_COEF_R && mode != ID_COEF_LSQ) return fail(h, ID_ERR_ARG, "bad coefficient mode");
   const int eng = fp64_engine(h, k, false);
-  if (eng < 0) return fail(h, ID_ERR_ARG, "the int8 fp64 engine needs k <= 128, a device-resident A_D and n > k");
+  if (eng < 0) return fail(h, ID_ERR_ARG, "the int8 fp64 engine needs k <= 128, a device-resident A_D and k < n within its kernels' limits");
   CK(cudaEventRecord(h->ev[3], h->st));
   int launches = 0;
   const size_t tcap = tpart_doubles(m, n, h->k_cap);
@@ -1289,7 +1289,7 @@ id_status id_error(id_handle h, double* abs_fro, double* rel_fro) {
   if (!h->have_coef) return fail(h, ID_ERR_STATE, "id_error needs id_coeffs_fp64 first");
   const int k = h->k_out;
   const int eng = fp64_engine(h, k, true);
-  if (eng < 0) return fail(h, ID_ERR_ARG, "the int8 fp64 engine needs k <= 128, a device-resident A_D and n > k");
+  if (eng < 0) return fail(h, ID_ERR_ARG, "the int8 fp64 engine needs k <= 128, a device-resident A_D and k < n within its kernels' limits");
   CK(cudaEventRecord(h->ev[5], h->st));
   int nblk = 0;
   // skeleton columns contribute exactly 0 (P(:, I) = I_k): sum over J = perm[k:] only

@@ -253,6 +253,7 @@ cudaError_t launch_pchol(const double* G, double* Gc, int n, int k_max, double* 
 size_t oz_slice_bytes(int64_t m_local);
 size_t oz_tslice_bytes(int64_t n);
 size_t oz_part_doubles(int num_sms);
+bool oz_fits(int64_t n, int k, int num_sms);   // k <= 128, grid and shared memory of the int8 kernels
 cudaError_t launch_oz_tn(const double* Q1, int64_t m, int k, const double* AD, int64_t ld, const int* cmapJ, int nj,
                          const unsigned long long* cmaxd, unsigned long long* cmaxq, void* slices, double* part,
                          size_t part_cap, double* G2, double* W, int num_sms, cudaStream_t st);

@@ -142,3 +142,28 @@ def test_auto_engine_choice():
     h.close()
     del At
     torch.cuda.empty_cache()
+
+
+def test_engine_limits_fall_back_to_dmma():
+    """n beyond 64 x SMs (the TN kernel's one-CTA-per-(row group, tile) grid): the automatic
+    engine is DMMA, a forced int8 engine is refused, and P still matches the oracle."""
+    import torch
+    from paper_2012_00706_b200.mpid import MPID, IDError
+    from tests.gpu_helpers import to_dev
+    rng = np.random.default_rng(5)
+    m, n, k = 32768, 9600, 16
+    A = np.asfortranarray(rng.standard_normal((m, 40)) @ rng.standard_normal((40, n))
+                          + 1e-3 * rng.standard_normal((m, n)))
+    h = MPID(to_dev(A), k_max=k)
+    q = h.qrcp("fp32", "none", k=k)
+    P = h.coeffs("lsq").cpu().numpy()
+    h.error()
+    st = h.stats()
+    assert st["fp64_engine"] == 1 and st["fp64_engine_err"] == 1
+    h.set_fp64_engine("int8")
+    with pytest.raises(IDError):
+        h.coeffs("lsq")
+    h.close()
+    P_ref = coeffs_lsq(A, q.piv)
+    assert np.linalg.norm(P - P_ref) <= 1e-10 * np.linalg.norm(P_ref)
+    torch.cuda.empty_cache()
