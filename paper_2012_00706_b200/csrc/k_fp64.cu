@@ -81,6 +81,7 @@ struct GemmArgs {
   int64_t lda;
   const int* cmap;
   const int* ycmap;  // TN: column c of Y is Y's column ycmap[c] (nullptr = identity)
+  unsigned long long* cmax;   // NN store (k_err_ws<true>): atomicMax of each column's max |out| (bit patterns) or null
   int d_tma;         // NN_ERROR: 1 = the A_D tile may be prefetched with bulk copies (16 B aligned rows)
 };
 constexpr int DLD = GT + 2;      // NN_ERROR: smem A_D tile [c][r], 130 doubles per column (16 B aligned,
@@ -618,11 +619,20 @@ __global__ void __launch_bounds__(EW_THREADS, 1) k_err_ws(GemmArgs g, const doub
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int64_t c = n0 + wn * 32 + nt * 8 + tq * 2 + h;
+            double cm = 0.0;
 #pragma unroll
             for (int mt = 0; mt < ERR_MT; ++mt) {
               const int64_t r = m0 + wm * ERR_WM + mt * 8 + gq;
-              if (r < g.M && c < g.N) g.out[c * g.ldo + r] = acc[mt][nt][h];
+              if (r < g.M && c < g.N) {
+                g.out[c * g.ldo + r] = acc[mt][nt][h];
+                cm = fmax(cm, fabs(acc[mt][nt][h]));
+              }
               acc[mt][nt][h] = 0.0;
+            }
+            if (g.cmax) {   // the column max for the int8 engine's slicing (lanes gq share c)
+#pragma unroll
+              for (int o = 4; o < 32; o <<= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+              if (gq == 0 && c < g.N) atomicMax(g.cmax + c, (unsigned long long)__double_as_longlong(cm));
             }
           }
         continue;
@@ -1325,7 +1335,9 @@ cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, cons
 }
 
 cudaError_t launch_nn_store(const double* X, int64_t m, int64_t ldx, const double* B, int64_t ldb, int K,
-                            int N, double* out, int64_t ldo, cudaStream_t st, double* tpack, size_t tpack_cap) {
+                            int N, double* out, int64_t ldo, cudaStream_t st, double* tpack, size_t tpack_cap,
+                            unsigned long long* cmax, int* cmax_done) {
+  if (cmax_done) *cmax_done = 0;
   GemmArgs g{};
   g.X = X; g.ldx = ldx;
   g.Y = B; g.ldy = ldb;
@@ -1345,7 +1357,13 @@ cudaError_t launch_nn_store(const double* X, int64_t m, int64_t ldx, const doubl
     const size_t smem_ws = (size_t)(EW_S * (EW_ASZ + EW_BSZ) + GT * DLD) * sizeof(double);
     cudaError_t e = smem_attr((const void*)k_err_ws<true>, (int)smem_ws);
     if (e != cudaSuccess) return e;
+    g.cmax = cmax;
+    if (cmax) {
+      e = cudaMemsetAsync(cmax, 0, (size_t)N * sizeof(unsigned long long), st);
+      if (e != cudaSuccess) return e;
+    }
     k_err_ws<true><<<(unsigned)std::min<int64_t>(ntiles, sms), EW_THREADS, smem_ws, st>>>(g, tpack, ntiles, (int)ncb);
+    if (cmax_done && cmax) *cmax_done = 1;
     return cudaGetLastError();
   }
   dim3 grid((unsigned)((m + GT - 1) / GT), (unsigned)((N + GT - 1) / GT), 1);

@@ -748,13 +748,15 @@ bool oz_fits(int64_t n, int k, int num_sms) {
 // [G2 | W] = Q1^T [Q1 | A_D(:, J)]; cmaxq (k entries) is computed here; cmaxd = A_D's column maxima
 cudaError_t launch_oz_tn(const double* Q1, int64_t m, int k, const double* AD, int64_t ld, const int* cmapJ, int nj,
                          const unsigned long long* cmaxd, unsigned long long* cmaxq, void* slices, double* part,
-                         size_t part_cap, double* G2, double* W, int num_sms, cudaStream_t st) {
+                         size_t part_cap, double* G2, double* W, int num_sms, cudaStream_t st, int cmaxq_ready) {
   if (k < 1 || k > 128) return cudaErrorInvalidValue;
-  cudaError_t e = cudaMemsetAsync(cmaxq, 0, 128 * sizeof(unsigned long long), st);
-  if (e != cudaSuccess) return e;
-  const int ysplit = (int)std::max<int64_t>(1, std::min<int64_t>(64, (2 * num_sms + k - 1) / k));
-  k_oz_colmax<<<dim3((unsigned)k, (unsigned)ysplit), 256, 0, st>>>(Q1, m, m, cmaxq);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  if (!cmaxq_ready) {
+    if ((e = cudaMemsetAsync(cmaxq, 0, 128 * sizeof(unsigned long long), st)) != cudaSuccess) return e;
+    const int ysplit = (int)std::max<int64_t>(1, std::min<int64_t>(64, (2 * num_sms + k - 1) / k));
+    k_oz_colmax<<<dim3((unsigned)k, (unsigned)ysplit), 256, 0, st>>>(Q1, m, m, cmaxq);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   const int64_t nsteps = (m + KSTEP - 1) / KSTEP;
   k_oz_slice_cols<<<(unsigned)nsteps, 256, 0, st>>>(Q1, m, m, k, cmaxq, nsteps,
                                                                            (uint4*)slices);

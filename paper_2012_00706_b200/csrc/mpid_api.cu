@@ -1150,13 +1150,14 @@ id_status id_coeffs_fp64(id_handle h, id_coef_mode mode, double* P_out, int64_t 
     // Q1 = A_I R1^{-1}: the k x k inverse by triangular solves on I_k, then one DMMA GEMM
     CK(launch_eye(h->Ik, k, h->st));
     CK(launch_trsm_left_upper(R1, nullptr, k, h->Ik, k, nullptr, k, h->Rinv, k, 0, h->st));
-    CK(launch_nn_store(h->AI, m, m, h->Rinv, k, k, k, h->Q1, m, h->st, h->Tp,
-                               ew_tpack_doubles(h->n, h->k_cap)));
     const int nj = n - k;
     const bool oz = eng == 2 && mode == ID_COEF_LSQ;
+    int cmaxq_ready = 0;   // the int8 engine's Q1 column maxima come with Q1 when the kernel can
+    CK(launch_nn_store(h->AI, m, m, h->Rinv, k, k, k, h->Q1, m, h->st, h->Tp, ew_tpack_doubles(h->n, h->k_cap),
+                       oz ? h->cmaxq : nullptr, &cmaxq_ready));
     if (oz) {   // [G2 | W] = Q1^T [Q1 | A_D(:, J)] in one pass over A_D on the int8 tensor cores
       CK(launch_oz_tn(h->Q1, m, k, h->AD, h->ld, h->perm + k, nj, h->cmaxd, h->cmaxq, h->ozs, h->ozpart,
-                      oz_part_doubles(num_sms()), h->G2, h->W, num_sms(), h->st));
+                      oz_part_doubles(num_sms()), h->G2, h->W, num_sms(), h->st, cmaxq_ready));
       launches += 5;
     } else {   // G2 = Q1^T Q1
       CK(launch_tsmm(h->Q1, m, k, h->Q1, m, k, m, h->tpart, sp, h->st));

@@ -211,9 +211,11 @@ cudaError_t launch_error(const double* A, int64_t m, int64_t ld, int ncols, cons
                          double* tpack = nullptr, size_t tpack_cap = 0, int64_t ldx = -1, int pack = 1);
 size_t ew_tpack_doubles(int64_t n, int64_t k);   // packed T slabs of the warp-specialised error kernel
 // out(m x N) = X(m x K) B(K x N), all col-major
+// cmax (optional): the column maxima of out (bit patterns) for the int8 engine; *cmax_done = 1
+// when this launch produced them (the warp-specialised path), else the caller computes them
 cudaError_t launch_nn_store(const double* X, int64_t m, int64_t ldx, const double* B, int64_t ldb, int K,
                             int N, double* out, int64_t ldo, cudaStream_t st, double* tpack = nullptr,
-                            size_t tpack_cap = 0);
+                            size_t tpack_cap = 0, unsigned long long* cmax = nullptr, int* cmax_done = nullptr);
 cudaError_t launch_eye(double* I, int k, cudaStream_t st);
 // host-streamed A_D (mpid_api.cu): acc[i] (+)= sum_y part[y * stride + i] for i < len, fixed order
 cudaError_t launch_acc_rows(const double* part, int rows, int64_t stride, int64_t len, double* acc, int add,
@@ -254,9 +256,10 @@ size_t oz_slice_bytes(int64_t m_local);
 size_t oz_tslice_bytes(int64_t n);
 size_t oz_part_doubles(int num_sms);
 bool oz_fits(int64_t n, int k, int num_sms);   // k <= 128, grid and shared memory of the int8 kernels
+// cmaxq_ready: Q1's column maxima are already in cmaxq (launch_nn_store produced them)
 cudaError_t launch_oz_tn(const double* Q1, int64_t m, int k, const double* AD, int64_t ld, const int* cmapJ, int nj,
                          const unsigned long long* cmaxd, unsigned long long* cmaxq, void* slices, double* part,
-                         size_t part_cap, double* G2, double* W, int num_sms, cudaStream_t st);
+                         size_t part_cap, double* G2, double* W, int num_sms, cudaStream_t st, int cmaxq_ready = 0);
 cudaError_t launch_oz_error(const double* AD, int64_t m, int64_t ld, int nj, const int* cmapJ, const double* AI,
                             int k, const double* T, int64_t ldt, void* slices, void* tslices, double* rsc,
                             double* fsc, double* part, int* nblk_out, int num_sms, cudaStream_t st);
