@@ -1031,6 +1031,38 @@ __global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ G, int k
   if (threadIdx.x == 0) *info = bad;
 }
 
+// The same factorisation with ONE block barrier per step (k <= 143, G in shared memory):
+// every thread forms sqrt(d) and 1 / d of the pivot itself, the trailing update uses the
+// unscaled column j with the factor 1 / d, and the scaled column goes straight to its place
+// in R's upper triangle in global memory (never read back during the sweep).
+__global__ void __launch_bounds__(1024) k_cholesky_1bar(double* __restrict__ G, int k, int* __restrict__ info) {
+  extern __shared__ double sG[];
+  double* L = sG;
+  for (int i = threadIdx.x; i < k * k; i += blockDim.x) L[i] = G[i];
+  __syncthreads();
+  int bad = 0;
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = 0; j < k; ++j) {
+    const double d0 = L[j + (int64_t)j * k];
+    const bool ok = d0 > 0.0;
+    if (!ok && !bad) bad = j + 1;
+    const double d = ok ? d0 : 1.0;
+    const double sd = sqrt(d), rs = 1.0 / sd, inv = 1.0 / d;
+    for (int i = j + threadIdx.x; i < k; i += blockDim.x)          // R(j, i) = L(i, j)
+      G[j + (int64_t)i * k] = i == j ? sd : L[i + (int64_t)j * k] * rs;
+    for (int l = j + 1 + (threadIdx.x >> 5); l < k; l += nw) {     // L(i, l) -= L(i, j) L(l, j) / d
+      const double t = L[l + (int64_t)j * k] * inv;
+      for (int i = l + lane; i < k; i += 32) L[i + (int64_t)l * k] = fma(-L[i + (int64_t)j * k], t, L[i + (int64_t)l * k]);
+    }
+    __syncthreads();
+  }
+  for (int64_t idx = threadIdx.x; idx < (int64_t)k * k; idx += blockDim.x) {
+    const int r = (int)(idx % k), c = (int)(idx / k);
+    if (c < r) G[r + (int64_t)c * k] = 0.0;
+  }
+  if (threadIdx.x == 0) *info = bad;
+}
+
 // ---------------------------------------------------------------------------
 // Cholesky for k > 143 (G does not fit shared memory): left-looking, panels of 16
 // columns.  Thread t owns row p0 + t of the panel: the update with the finished
@@ -1164,6 +1196,93 @@ __global__ void __launch_bounds__(1024) k_trsm_left_block(const double* __restri
     for (int r = rg; r < k; r += 32) T[(int64_t)col * ldt + r] = sb[r * 33 + c];
 }
 
+// The same solves for k <= 128 without block barriers: one WARP per right-hand side, each lane
+// holding rows lane + 32 q (q < RPL) of it in registers; step i broadcasts x_i from its owner
+// lane by a shuffle and the lanes update their rows with the column (or row) i of the factor,
+// staged in shared memory with an odd column stride (conflict-free both ways) together with
+// its reciprocal diagonal (multiplications on the sweep's critical path, no divisions).
+// 8 right-hand sides per CTA; the factors are staged one at a time.
+constexpr int TW_WARPS = 8;
+template <int RPL>
+__device__ __forceinline__ void tw_back(double (&b)[RPL], const double* su, const double* dinv, int k, int ldu,
+                                        int lane) {   // U x = b (upper), rows bottom-up
+#pragma unroll
+  for (int qb = RPL - 1; qb >= 0; --qb) {              // the owner slot of row i is compile-time
+    for (int ii = 31; ii >= 0; --ii) {
+      const int i = qb * 32 + ii;
+      if (i >= k) continue;
+      const double xi = __shfl_sync(0xffffffffu, b[qb], ii) * dinv[i];
+      const double* Ui = su + (size_t)i * ldu;
+#pragma unroll
+      for (int q = 0; q <= qb; ++q) {
+        const int r = lane + 32 * q;
+        if (r < i) b[q] = fma(-Ui[r], xi, b[q]);
+        else if (r == i) b[q] = xi;
+      }
+    }
+  }
+}
+template <int RPL>
+__device__ __forceinline__ void tw_fwdT(double (&b)[RPL], const double* su, const double* dinv, int k, int ldu,
+                                        int lane) {   // U^T x = b (lower), rows top-down: U(i, r) = su[i + r ldu]
+#pragma unroll
+  for (int qb = 0; qb < RPL; ++qb) {
+    for (int ii = 0; ii < 32; ++ii) {
+      const int i = qb * 32 + ii;
+      if (i >= k) break;
+      const double xi = __shfl_sync(0xffffffffu, b[qb], ii) * dinv[i];
+#pragma unroll
+      for (int q = qb; q < RPL; ++q) {
+        const int r = lane + 32 * q;
+        if (r > i && r < k) b[q] = fma(-su[i + (size_t)r * ldu], xi, b[q]);
+        else if (r == i) b[q] = xi;
+      }
+    }
+  }
+}
+__device__ __forceinline__ void tw_stage(const double* __restrict__ U, double* su, double* dinv, int k, int ldu) {
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int r = e % k, c = e / k;
+    su[r + (size_t)c * ldu] = U[e];
+  }
+  for (int i = threadIdx.x; i < k; i += blockDim.x) dinv[i] = 1.0 / U[i + (int64_t)i * k];
+  __syncthreads();
+}
+template <int RPL>
+__global__ void __launch_bounds__(TW_WARPS * 32) k_trsm_warp(const double* __restrict__ R1,
+                                                             const double* __restrict__ R2, int k,
+                                                             const double* __restrict__ B, int64_t ldb,
+                                                             const int* __restrict__ map, int ncols,
+                                                             double* __restrict__ T, int64_t ldt, int mode) {
+  extern __shared__ double su[];   // [k][ldu] factor, then [k] reciprocal diagonal
+  const int ldu = (k & 1) ? k : k + 1;
+  double* dinv = su + (size_t)k * ldu;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = blockIdx.x * TW_WARPS + warp;
+  const bool valid = col < ncols;
+  double b[RPL];
+  const int64_t src = valid ? (int64_t)(map ? map[col] : col) : 0;
+#pragma unroll
+  for (int q = 0; q < RPL; ++q) {
+    const int r = lane + 32 * q;
+    b[q] = (valid && r < k) ? B[src * ldb + r] : 0.0;
+  }
+  if (mode == 1) {
+    tw_stage(R2, su, dinv, k, ldu);
+    tw_fwdT<RPL>(b, su, dinv, k, ldu, lane);
+    tw_back<RPL>(b, su, dinv, k, ldu, lane);
+  }
+  tw_stage(R1, su, dinv, k, ldu);
+  tw_back<RPL>(b, su, dinv, k, ldu, lane);
+  if (valid)
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int r = lane + 32 * q;
+      if (r < k) T[(int64_t)col * ldt + r] = b[q];
+    }
+}
+
 // R (k x n, fp32 or fp64, row-major, pivoted order) -> fp64 col-major k x n
 template <typename RT>
 __global__ void k_R_to_fp64(const RT* __restrict__ R, int k, int n, double* __restrict__ Rd) {
@@ -1247,7 +1366,12 @@ cudaError_t launch_cholesky(double* G, int k, int* info, cudaStream_t st) {
   cudaError_t e = smem_attr((const void*)k_cholesky, 160 * 1024);
   if (e == cudaSuccess) e = smem_attr((const void*)k_cholesky_blocked, 200 * 1024);
   if (e != cudaSuccess) return e;
-  if (sm <= 160 * 1024) {
+  static const bool one_bar = !(getenv("MPID_CHOL_3BAR") && atoi(getenv("MPID_CHOL_3BAR")) == 1);
+  if (sm <= 160 * 1024 && one_bar) {
+    e = smem_attr((const void*)k_cholesky_1bar, 160 * 1024);
+    if (e != cudaSuccess) return e;
+    k_cholesky_1bar<<<1, 1024, sm, st>>>(G, k, info);
+  } else if (sm <= 160 * 1024) {
     k_cholesky<<<1, 1024, sm, st>>>(G, k, info);
   } else if (k <= 1024 && (size_t)k * (CH_NB + 1) * 8 <= 200 * 1024 - sizeof(double) * CH_LC * CH_NB) {
     k_cholesky_blocked<<<1, 1024, (size_t)k * (CH_NB + 1) * 8, st>>>(G, k, info);
@@ -1261,6 +1385,20 @@ cudaError_t launch_trsm_left_upper(const double* R1, const double* R2, int k, co
                                    int64_t ldb, const int* map, int ncols, double* T, int64_t ldt,
                                    int mode, cudaStream_t st) {
   if (ncols <= 0) return cudaSuccess;
+  static const bool warp_env = !(getenv("MPID_TRSM_BLOCK") && atoi(getenv("MPID_TRSM_BLOCK")) == 1);
+  if (warp_env && k <= 128) {   // one warp per right-hand side (k_trsm_warp)
+    const size_t sw = ((size_t)k * ((k & 1) ? k : k + 1) + k) * sizeof(double);
+    const unsigned grid = (unsigned)((ncols + TW_WARPS - 1) / TW_WARPS);
+    const void* fn = k <= 32 ? (const void*)k_trsm_warp<1> : k <= 64 ? (const void*)k_trsm_warp<2>
+                   : k <= 96 ? (const void*)k_trsm_warp<3> : (const void*)k_trsm_warp<4>;
+    cudaError_t e = smem_attr(fn, (int)sw);
+    if (e != cudaSuccess) return e;
+    if (k <= 32) k_trsm_warp<1><<<grid, TW_WARPS * 32, sw, st>>>(R1, R2, k, B, ldb, map, ncols, T, ldt, mode);
+    else if (k <= 64) k_trsm_warp<2><<<grid, TW_WARPS * 32, sw, st>>>(R1, R2, k, B, ldb, map, ncols, T, ldt, mode);
+    else if (k <= 96) k_trsm_warp<3><<<grid, TW_WARPS * 32, sw, st>>>(R1, R2, k, B, ldb, map, ncols, T, ldt, mode);
+    else k_trsm_warp<4><<<grid, TW_WARPS * 32, sw, st>>>(R1, R2, k, B, ldb, map, ncols, T, ldt, mode);
+    return cudaGetLastError();
+  }
   const size_t smem = (size_t)k * 33 * sizeof(double) + (k <= 128 ? (size_t)k * k * sizeof(double) : 0);
   cudaError_t e = smem_attr((const void*)k_trsm_left_block, 200 * 1024);
   if (e != cudaSuccess) return e;

@@ -21,7 +21,7 @@
 //   V holds the pending u_l (rows < l zero) and F the pending c_l f_l, so V F^T =
 //   sum_l v_l f_l^T with v_l = c_l u_l (Householder vector, v_l(l) = 1 in exact arithmetic).
 //
-// B200 structure: one persistent CTA per SM, 18 warps, warp-specialised.  A CTA owns a
+// B200 structure: one persistent CTA per SM, 19 warps, warp-specialised.  A CTA owns a
 // contiguous range of 128-row blocks and walks, per row block, all column tiles of 128
 // (tile 0 starts at column j, so its TMEM lane 0 is the pivot column): unit = (row block,
 // tile).
@@ -31,11 +31,11 @@
 //               rounded tile is written back by a tensor-map store before the slot is reused.
 //   warp 1      MMA issuer (one thread): 8 identity MMAs + 3 x ceil(npend / 16) formation
 //               MMAs per unit into one of 4 TMEM accumulators (128 columns each).
-//   warps 2-17  epilogue, 4 groups of 4 warps (one per TMEM lane quarter); group g takes the
-//               tiles t = g mod 4, so each thread owns one column per tile and keeps its
-//               column sums in registers for the whole launch.  Warp 4 (group 0, lane
-//               quarter 0) publishes u of each row block (TMEM lane 0 of tile 0) to shared
-//               memory and to U (global, for the next steps' V operand).
+//   warps 2-17  epilogue, 2 groups of 8 warps (4 TMEM lane quarters x 2 row halves); group g
+//               takes the tiles t = g mod 2, so each thread owns one column per tile and keeps
+//               its column sums in registers for the whole launch.
+//   warp 18     the u warp: each row block's V operand and pivot column, u = S(:, j) - V F(j, :)^T
+//               on CUDA cores, published to shared memory and to the V operand of the next steps.
 // Bound: HBM — (m - j)(n - j) 2 bytes read per step (+ the same written on store steps);
 // tensor work per element: 32 flops (identity) + 6 * 16 * ceil(npend / 16) (formation).
 #include "mpid_internal.cuh"

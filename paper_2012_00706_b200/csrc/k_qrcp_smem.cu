@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
   float* Rs = reinterpret_cast<float*>(pm + n);
   double* u64 = reinterpret_cast<double*>(smem + ((((size_t)n * ldw * 4 + 15) & ~(size_t)15) + (size_t)5 * n * 8 +
                                                    (size_t)m8 * 4 + (size_t)n * 8 + (size_t)k_max * n * 4 + 15) / 16 * 16);
-  __shared__ int sh_p, sh_stop;
+  __shared__ int sh_p, sh_stop, sh_slow;
   __shared__ double sh_beta, sh_cc, sh_normAL;
   const int tid = threadIdx.x, nt = blockDim.x;
 
@@ -86,33 +86,43 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
   }
   __syncthreads();
   int kk = k_max, st = 0;
+  // pivot of step j (warp 0): max vn, ties -> lowest original index (max and min are exact: any
+  // order agrees).  Step 0's here; step j + 1's runs in warp 0 while warps 1-31 update (below).
+  auto argmax = [&](int j) {
+    double best = -INFINITY;
+    int bo = 0x7fffffff, bp = -1;
+    for (int i = j + lane; i < n; i += 32) {
+      const double vi = vn[i];
+      const int oi = pm[i];
+      if (vi > best || (vi == best && oi < bo)) { best = vi; bo = oi; bp = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double vb = __shfl_xor_sync(0xffffffffu, best, o);
+      const int ob = __shfl_xor_sync(0xffffffffu, bo, o);
+      const int pb = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (vb > best || (vb == best && ob < bo)) { best = vb; bo = ob; bp = pb; }
+    }
+    if (lane == 0) sh_p = bp;
+  };
+  if (warp == 0) argmax(0);
+  __syncthreads();
   for (int j = 0; j < k_max; ++j) {
     const int jl = j, g0 = (j / 8) * 8;
-    if (tid < 32) {                                 // pivot: max vn, ties -> lowest original index
-      double best = -INFINITY;                      // (max and min are exact: any order agrees)
-      int bo = 0x7fffffff, bp = -1;
-      for (int i = j + tid; i < n; i += 32) {
-        const double vi = vn[i];
-        const int oi = pm[i];
-        if (vi > best || (vi == best && oi < bo)) { best = vi; bo = oi; bp = i; }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double vb = __shfl_xor_sync(0xffffffffu, best, o);
-        const int ob = __shfl_xor_sync(0xffffffffu, bo, o);
-        const int pb = __shfl_xor_sync(0xffffffffu, bp, o);
-        if (vb > best || (vb == best && ob < bo)) { best = vb; bo = ob; bp = pb; }
-      }
-      if (tid == 0) sh_p = bp;
-    }
-    __syncthreads();
     const int p = sh_p;
-    if (p != j) {
-      for (int r = tid; r < m8; r += nt) {
-        const float a = W[(int64_t)j * ldw + r];
-        W[(int64_t)j * ldw + r] = W[(int64_t)p * ldw + r];
-        W[(int64_t)p * ldw + r] = a;
+    const bool rnd = store16 && j > 0 && j % nb == 0;   // the storage rounding point (reading R4)
+    // swap columns j <-> p with the storage rounding of their rows >= j, u = the new column j
+    for (int r = tid; r < m8; r += nt) {
+      float a = W[(int64_t)j * ldw + r], b = W[(int64_t)p * ldw + r];
+      if (rnd && r >= jl) {
+        a = __half2float(__float2half_rn(a));
+        b = __half2float(__float2half_rn(b));
       }
+      W[(int64_t)j * ldw + r] = b;
+      W[(int64_t)p * ldw + r] = a;
+      if (r >= g0) u64[r] = r < jl ? 0.0 : (double)b;
+    }
+    if (p != j) {
       for (int r = tid; r < j; r += nt) {
         const float a = Rs[(int64_t)r * n + j];
         Rs[(int64_t)r * n + j] = Rs[(int64_t)r * n + p];
@@ -123,61 +133,80 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
         const double tv = vn[j]; vn[j] = vn[p]; vn[p] = tv;
       }
     }
-    __syncthreads();
-    if (store16 && j > 0 && j % nb == 0) {          // the storage rounding point (reading R4)
-      for (int c = j + warp; c < n; c += nw)
+    if (rnd)
+      for (int c = j + warp; c < n; c += nw) {
+        if (c == j || c == p) continue;
         for (int r = jl + lane; r < m8; r += 32) W[c * ldw + r] = __half2float(__float2half_rn(W[c * ldw + r]));
-      __syncthreads();
-    }
-    for (int r = g0 + tid; r < m8; r += nt) u64[r] = r < jl ? 0.0 : (double)W[j * ldw + r];
+      }
     __syncthreads();
-    for (int c = j + tid; c < n; c += nt) {         // s_i, w_i: exact products, fp64, row order
-      double ss = 0.0, ww = 0.0;
+    // s_i, w_i: exact products added in fp64 in row order from row g0 (rows g0..j-1 are exact
+    // zeros: they only turn a leading -0 into +0, applied once); thread 0 owns column j and
+    // forms beta / c unless the step needs the residual mass (a tolerance, the last step, an
+    // underflowing pivot): then the serial block below
+    for (int c = j + tid; c < n; c += nt) {
+      const float* Wc = W + (int64_t)c * ldw;
+      double ss, ww;
+      {
+        const double a = (double)Wc[jl];
+        ss = __dmul_rn(a, a);
+        ww = __dmul_rn(a, u64[jl]);
+        if (g0 < jl) { ss = __dadd_rn(0.0, ss); ww = __dadd_rn(0.0, ww); }
+      }
 #pragma unroll 8
-      for (int r = g0; r < m8; ++r) {
-        const double a = r < jl ? 0.0 : (double)W[c * ldw + r];
-        const double u = u64[r];
-        const double ps = __dmul_rn(a, a), pw = __dmul_rn(a, u);
-        if (r == g0) { ss = ps; ww = pw; }
-        else { ss = __dadd_rn(ss, ps); ww = __dadd_rn(ww, pw); }
+      for (int r = jl + 1; r < m8; ++r) {
+        const double a = (double)Wc[r];
+        ss = __dadd_rn(ss, __dmul_rn(a, a));
+        ww = __dadd_rn(ww, __dmul_rn(a, u64[r]));
       }
       s[c] = ss;
       w[c] = ww;
-      x[c] = (double)W[(int64_t)c * ldw + jl];
-    }
-    __syncthreads();
-    if (tid == 0) {
-      // the residual mass (a sequential sum over the columns) only when a tolerance asks
-      bool stop = false;
-      if ((eps > 0.0 && j > 0) || j == k_max - 1) {   // (the last step's mass: resid when k = min(m, n))
-        double t = 0.0;
-        for (int c = j; c < n; ++c) t = c == j ? s[j] : __dadd_rn(t, s[c]);
-        sc->resid2 = t;
-        stop = eps > 0.0 && j > 0 && __dsqrt_rn(t) <= __dmul_rn(eps, sh_normAL);
-      }
-      if (stop) sh_stop = 1;
-      else if (!(s[j] >= 1.1754943508222875e-38)) {
-        double t = 0.0;
-        for (int c = j; c < n; ++c) t = c == j ? s[j] : __dadd_rn(t, s[c]);
-        sc->resid2 = t;
-        sh_stop = 2;
-      }
-      else {
-        const double u0 = x[j];
-        const double beta = -copysign(__dsqrt_rn(s[j]), u0);
-        sh_beta = beta;
-        sh_cc = __ddiv_rn(1.0, __dadd_rn(u0, -beta));
+      x[c] = (double)Wc[jl];
+      if (c == j) {
+        const bool slow = (eps > 0.0 && j > 0) || j == k_max - 1 || !(ss >= 1.1754943508222875e-38);
+        sh_slow = slow;
+        if (!slow) {
+          const double u0 = x[j];
+          const double beta = -copysign(__dsqrt_rn(ss), u0);
+          sh_beta = beta;
+          sh_cc = __ddiv_rn(1.0, __dadd_rn(u0, -beta));
+        }
       }
     }
     __syncthreads();
-    if (sh_stop) {
-      kk = j;
-      st = sh_stop == 2 ? 4 : 0;
-      break;
+    if (sh_slow) {
+      if (tid == 0) {
+        bool stop = false;
+        if ((eps > 0.0 && j > 0) || j == k_max - 1) {   // (the last step's mass: resid when k = min(m, n))
+          double t = 0.0;
+          for (int c = j; c < n; ++c) t = c == j ? s[j] : __dadd_rn(t, s[c]);
+          sc->resid2 = t;
+          stop = eps > 0.0 && j > 0 && __dsqrt_rn(t) <= __dmul_rn(eps, sh_normAL);
+        }
+        if (stop) sh_stop = 1;
+        else if (!(s[j] >= 1.1754943508222875e-38)) {
+          double t = 0.0;
+          for (int c = j; c < n; ++c) t = c == j ? s[j] : __dadd_rn(t, s[c]);
+          sc->resid2 = t;
+          sh_stop = 2;
+        }
+        else {
+          const double u0 = x[j];
+          const double beta = -copysign(__dsqrt_rn(s[j]), u0);
+          sh_beta = beta;
+          sh_cc = __ddiv_rn(1.0, __dadd_rn(u0, -beta));
+        }
+      }
+      __syncthreads();
+      if (sh_stop) {
+        kk = j;
+        st = sh_stop == 2 ? 4 : 0;
+        break;
+      }
     }
     const double beta = sh_beta, cc = sh_cc;
     const double sgn = copysign(1.0, beta);
-    for (int r = jl + tid; r < m8; r += nt) v[r] = __double2float_rn(__dmul_rn((double)W[(int64_t)j * ldw + r], cc));
+    for (int r = jl + tid; r < m8; r += nt)
+      v[r] = r == jl ? 1.f : __double2float_rn(__dmul_rn((double)W[(int64_t)j * ldw + r], cc));
     for (int c = tid; c < n; c += nt) {
       if (c < j) {
         Rs[(int64_t)j * n + c] = 0.f;
@@ -190,11 +219,13 @@ __global__ void __launch_bounds__(1024, 1) k_qrcp_smem(const T* __restrict__ S, 
       if (c > j) vn[c] = __dadd_rn(s[c], -__dmul_rn(rw, rw));
     }
     __syncthreads();
-    if (tid == 0) v[jl] = 1.f;
-    __syncthreads();
-    for (int c = j + warp; c < n; c += nw) {       // W(j:, j:) <- fl(W - fl(v f))
-      const float fc = f[c];
-      for (int r = jl + lane; r < m8; r += 32) W[c * ldw + r] = __fsub_rn(W[c * ldw + r], __fmul_rn(v[r], fc));
+    if (warp == 0) {
+      if (j + 1 < k_max) argmax(j + 1);                // the next step's pivot (vn is final)
+    } else {
+      for (int c = j + warp - 1; c < n; c += nw - 1) {  // W(j:, j:) <- fl(W - fl(v f))
+        const float fc = f[c];
+        for (int r = jl + lane; r < m8; r += 32) W[c * ldw + r] = __fsub_rn(W[c * ldw + r], __fmul_rn(v[r], fc));
+      }
     }
     __syncthreads();
   }
