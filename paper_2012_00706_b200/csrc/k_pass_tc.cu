@@ -446,11 +446,14 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
       const int ub = rbi & 1;
       const float* uu = ubuf + ub * R_B;
       mbar_wait(&ufull[ub], (uint32_t)((rbi >> 1) & 1));
+      // plain units (no store, no rows above the pivot row, not the pivot row's block — all but
+      // one row block of one CTA on 94 % of the launches) take a branch-free, fully unrolled path
+      const bool plain = !p.store && !mask && !hasj;
+      const float* uh = uu + 64 * hf;                     // this warp's 64 rows of u
       int ti = 0;
       for (int t = grp; t < ntiles; t += NGRP, ++ti) {
-        const int64_t u = (int64_t)rbi * ntiles + t;
-        const int acc = (int)(u % NACC);
-        const int slot = (int)(u % NST);
+        const int u = rbi * ntiles + t;                   // units per CTA < 2^31 (m_pad / 128 x 16)
+        const int acc = u & (NACC - 1);
         mbar_wait(&tfull[acc], (uint32_t)((u / NACC) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int col = t * C_T + q * 32 + lane;          // column offset from j
@@ -459,6 +462,30 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
         float2 w4[4], s4[4];
 #pragma unroll
         for (int a = 0; a < 4; ++a) { w4[a] = make_float2(0.f, 0.f); s4[a] = w4[a]; }
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * R_B + 64 * hf);
+        auto fma16 = [&](const float* x, const float* u16) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            const float4 u4 = *reinterpret_cast<const float4*>(u16 + i);
+            const float2 xa = make_float2(x[i], x[i + 1]);
+            const float2 xb = make_float2(x[i + 2], x[i + 3]);
+            const int a = (i >> 2) & 1;
+            w4[a] = __ffma2_rn(xa, make_float2(u4.x, u4.y), w4[a]);
+            s4[a] = __ffma2_rn(xa, xa, s4[a]);
+            w4[a + 2] = __ffma2_rn(xb, make_float2(u4.z, u4.w), w4[a + 2]);
+            s4[a + 2] = __ffma2_rn(xb, xb, s4[a + 2]);
+          }
+        };
+        int slot = 0;
+        if (plain) {
+#pragma unroll
+          for (int ci = 0; ci < 4; ++ci) {                  // 16-row chunks of this warp's 64 rows
+            float x[16];
+            tmem_ld16(tbase + (uint32_t)(ci * 16), x);
+            fma16(x, uh + ci * 16);
+          }
+        } else {
+        slot = u % NST;
 #pragma unroll 1
         for (int cb = 4 * hf; cb < 4 * hf + 4; ++cb) {      // 16-row chunks of this warp's 64 rows
           float x[16];
@@ -491,23 +518,13 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
             }
           }
           if (mask) {
+            const int nz = (int)(jl - r0) - cb * 16;       // rows of this chunk above the pivot row
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-              if (r0 + cb * 16 + i < jl) x[i] = 0.f;
+              if (i < nz) x[i] = 0.f;
           }
-          {
-#pragma unroll
-            for (int i = 0; i < 16; i += 4) {
-              const float4 u4 = *reinterpret_cast<const float4*>(uu + cb * 16 + i);
-              const float2 xa = make_float2(x[i], x[i + 1]);
-              const float2 xb = make_float2(x[i + 2], x[i + 3]);
-              const int a = (i >> 2) & 1;
-              w4[a] = __ffma2_rn(xa, make_float2(u4.x, u4.y), w4[a]);
-              s4[a] = __ffma2_rn(xa, xa, s4[a]);
-              w4[a + 2] = __ffma2_rn(xb, make_float2(u4.z, u4.w), w4[a + 2]);
-              s4[a + 2] = __ffma2_rn(xb, xb, s4[a + 2]);
-            }
-          }
+          fma16(x, uu + cb * 16);
+        }
         }
         const float2 wp = __fadd2_rn(__fadd2_rn(w4[0], w4[1]), __fadd2_rn(w4[2], w4[3]));
         const float2 sp = __fadd2_rn(__fadd2_rn(s4[0], s4[1]), __fadd2_rn(s4[2], s4[3]));
