@@ -271,26 +271,27 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
         c0 = (j + t * C_T) * 2;                                 // 8-byte units (fp16: 2 per chunk)
         g0 = (int)((p.rb_first + rb0 + rbi) * RG_B);
       };
+      // (incremental counters: no per-unit divisions on this single-warp critical path)
       int slot = 0;
       uint32_t phase = 0;
-      for (int64_t u = 0; u < units; ++u) {
-        const int64_t rbi = u / ntiles;
-        const int t = (int)(u - rbi * ntiles);
+      int t = 0;                                                // tile of unit u
+      int g0 = (int)((p.rb_first + rb0) * RG_B);                // its first row group
+      const int nu = (int)units;
+      for (int u = 0; u < nu; ++u) {
         if (u >= NST) {
           mbar_wait(&empty[slot], phase ^ 1);
           if (p.store) {
-            int c0, g0;
-            unit_coords(u - NST, c0, g0);
+            int c0s, g0s;
+            unit_coords(u - NST, c0s, g0s);
             if (elect_one()) {
-              tma_store_2d(&tmS, c0, g0, smem + (size_t)slot * geo.slot);
+              tma_store_2d(&tmS, c0s, g0s, smem + (size_t)slot * geo.slot);
               bulk_commit();
               bulk_wait_read0();
             }
             __syncwarp();
           }
         }
-        int c0, g0;
-        unit_coords(u, c0, g0);
+        const int c0 = (j + t * C_T) * 2;                       // 8-byte units (fp16: 2 per chunk)
         unsigned char* base = smem + (size_t)slot * geo.slot;
         if (elect_one()) {
           mbar_expect_tx(&full[slot], (uint32_t)S_BYTES + fbytes);
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
         }
         __syncwarp();
         if (++slot == NST) { slot = 0; phase ^= 1; }
+        if (++t == ntiles) { t = 0; g0 += RG_B; }
       }
       if (p.store) {
         for (int64_t u = units > NST ? units - NST : 0; u < units; ++u) {
@@ -320,43 +322,54 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
     // ============================ MMA issuer ============================
     // converged warp, one elected lane issues (descriptors in uniform registers)
     if (units > 0) {
+      // Single-warp critical path: descriptors are (constant high word, low word = constant +
+      // (shared address >> 4)), so a unit's 11 descriptors cost one add each; tile / slot /
+      // accumulator indices and barrier phases are carried incrementally (no divisions).
       const uint32_t id16 = idesc_f16(16), id128 = idesc_f16(R_B);
-      const uint64_t dI = sdesc(su32(smem + geo.ident), 128, 256);
-      int slot = 0;
-      uint32_t phase = 0;
-      for (int64_t u = 0; u < units; ++u) {
-        const int64_t rbi = u / ntiles;
-        const int t = (int)(u - rbi * ntiles);
-        const int acc = (int)(u % NACC);
-        const int vb = (int)(rbi & 1);
-        if (t == 0) mbar_wait(&vfull[vb], (uint32_t)((rbi >> 1) & 1));
+      auto mkdesc = [](uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | (uint64_t)lo; };
+      const uint32_t hi_s = (128u >> 4) | (1u << 14);           // SBO = 128 B, descriptor version
+      const uint32_t hi_o = (256u >> 4) | (1u << 14);           // SBO = 256 B (operand blocks, identity)
+      const uint32_t lo_s = (2048u >> 4) << 16;                 // LBO = 2048 B (S tile)
+      const uint32_t lo_o = (128u >> 4) << 16;                  // LBO = 128 B
+      const uint64_t dI = mkdesc(lo_o | (su32(smem + geo.ident) >> 4), hi_o);
+      const uint32_t slot16 = (uint32_t)geo.slot >> 4, foff16 = (uint32_t)geo.f_off >> 4;
+      const uint32_t ring16 = su32(smem) >> 4;
+      const uint32_t v16a = su32(smem + geo.v0) >> 4, v16b = su32(smem + geo.v0 + geo.vsz) >> 4;
+      int slot = 0, t = 0, acc = 0, vb = 0;
+      uint32_t s16 = ring16;                                    // (address of the ring slot) >> 4
+      uint32_t phase = 0, tphase = 1, vphase = 0;               // full[slot], tempty[acc] (^1), vfull[vb]
+      const int nu = (int)units;
+      for (int u = 0; u < nu; ++u) {
+        if (t == 0) mbar_wait(&vfull[vb], vphase);
         mbar_wait(&full[slot], phase);
-        mbar_wait(&tempty[acc], (uint32_t)(((u / NACC) & 1) ^ 1));
+        mbar_wait(&tempty[acc], tphase);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t sbase = su32(smem + (size_t)slot * geo.slot);
         const uint32_t d = tmem + (uint32_t)(acc * R_B);
-        const uint32_t fb = sbase + (uint32_t)geo.f_off;
-        const uint32_t vbase = su32(smem + geo.v0 + vb * geo.vsz);
+        const bool last = t == ntiles - 1;
         if (elect_one()) {
           // D(c, r) = S(r, c): A = the S tile (M = columns, K = 16 rows = 2 row groups;
           // LBO = 2048 B to the next row group, SBO = 128 B to the next 8 columns)
 #pragma unroll
           for (int b = 0; b < RG_B / 2; ++b)
-            mma_f16(d + (uint32_t)(16 * b), sdesc(sbase + (uint32_t)(b * 2 * 2048), 2048, 128), dI, id16, 0u);
+            mma_f16(d + (uint32_t)(16 * b), mkdesc(lo_s | (s16 + (uint32_t)(b * 256)), hi_s), dI, id16, 0u);
           // D -= F V^T in 3 hi / lo products per K chunk (operands pre-negated)
+          const uint32_t f16 = lo_o | (s16 + foff16), w16 = lo_o | (vb ? v16b : v16a);
           for (int kc = 0; kc < kch; ++kc) {
-            const uint32_t fh = fb + (uint32_t)(kc * 2 * CH_BYTES), fl = fh + CH_BYTES;
-            const uint32_t vh = vbase + (uint32_t)(kc * 2 * CH_BYTES), vl = vh + CH_BYTES;
-            mma_f16(d, sdesc(fh, 128, 256), sdesc(vh, 128, 256), id128, 1u);
-            mma_f16(d, sdesc(fh, 128, 256), sdesc(vl, 128, 256), id128, 1u);
-            mma_f16(d, sdesc(fl, 128, 256), sdesc(vh, 128, 256), id128, 1u);
+            const uint32_t fh = f16 + (uint32_t)(kc * 2 * (CH_BYTES >> 4)), fl = fh + (CH_BYTES >> 4);
+            const uint32_t vh = w16 + (uint32_t)(kc * 2 * (CH_BYTES >> 4)), vl = vh + (CH_BYTES >> 4);
+            mma_f16(d, mkdesc(fh, hi_o), mkdesc(vh, hi_o), id128, 1u);
+            mma_f16(d, mkdesc(fh, hi_o), mkdesc(vl, hi_o), id128, 1u);
+            mma_f16(d, mkdesc(fl, hi_o), mkdesc(vh, hi_o), id128, 1u);
           }
           mma_commit(&tfull[acc]);
           if (!p.store) mma_commit(&empty[slot]);
-          if (t == ntiles - 1) mma_commit(&vempty[vb]);
+          if (last) mma_commit(&vempty[vb]);
         }
         __syncwarp();
-        if (++slot == NST) { slot = 0; phase ^= 1; }
+        s16 += slot16;
+        if (++slot == NST) { slot = 0; phase ^= 1; s16 = ring16; }
+        if (++acc == NACC) { acc = 0; tphase ^= 1; }
+        if (last) { t = 0; if (vb) vphase ^= 1; vb ^= 1; } else ++t;
       }
     }
   } else if (warp == UWARP) {
