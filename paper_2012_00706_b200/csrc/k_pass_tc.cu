@@ -53,12 +53,13 @@ constexpr int EPI_WARPS = 16;
 constexpr int NGRP = 2;             // epilogue groups: group g takes the tiles t = g mod 2
 constexpr int EPI_GW = EPI_WARPS / NGRP;   // warps per group: 4 lane quarters x 2 row halves
 constexpr int TPG_MAX = 8;          // tiles per group (n - j <= 2048)
-constexpr int BLOCK = 32 * (2 + EPI_WARPS + 1);   // + producer, MMA issuer, u warp
+constexpr int BLOCK = 32 * (2 + EPI_WARPS + 2);   // + producer, 2 MMA issuers, u warp
 constexpr int NACC = 4;             // TMEM accumulators
 constexpr int TMEM_COLS = R_B * NACC;
 constexpr int S_BYTES = C_T * R_B * 2;   // one fp16 unit tile (32 KB)
 constexpr int CH_BYTES = 4096;      // one K chunk (16) of a 128-row / 128-column operand, fp16
 constexpr int UWARP = 2 + EPI_WARPS;  // the pivot-column (u) warp
+constexpr int MMA2 = UWARP + 1;       // the second MMA issuer (odd tiles; warp 1 takes the even ones)
 constexpr int TC_SMEM_MAX = 227 * 1024;   // the sm_100 opt-in maximum of dynamic shared memory per block
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&vfull[b], 1);
-      mbar_init(&vempty[b], 1);          // the MMA issuer's commit after the row block's last unit
+      mbar_init(&vempty[b], 2);          // each MMA issuer's commit after its last unit of the row block
       mbar_init(&ufull[b], 1);
       mbar_init(&ufree[b], EPI_WARPS);
     }
@@ -318,13 +319,15 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
       if (elect_one()) bulk_wait0();
       __syncwarp();
     }
-  } else if (warp == 1) {
-    // ============================ MMA issuer ============================
-    // converged warp, one elected lane issues (descriptors in uniform registers)
+  } else if (warp == 1 || warp == MMA2) {
+    // ============================ MMA issuers ============================
+    // Two converged warps, one elected lane each: warp 1 issues the even tiles of every row
+    // block, warp MMA2 the odd ones (a single issuer's instruction stream was the critical
+    // path of the pass: ~1 us per unit).  Units use disjoint accumulators and ring slots, and
+    // tcgen05.commit tracks the issuing thread's own MMAs, so the two need no mutual ordering.
+    // Descriptors are (constant high word, low word = constant + (shared address >> 4)).
     if (units > 0) {
-      // Single-warp critical path: descriptors are (constant high word, low word = constant +
-      // (shared address >> 4)), so a unit's 11 descriptors cost one add each; tile / slot /
-      // accumulator indices and barrier phases are carried incrementally (no divisions).
+      const int w = warp == 1 ? 0 : 1;
       const uint32_t id16 = idesc_f16(16), id128 = idesc_f16(R_B);
       auto mkdesc = [](uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | (uint64_t)lo; };
       const uint32_t hi_s = (128u >> 4) | (1u << 14);           // SBO = 128 B, descriptor version
@@ -335,41 +338,54 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
       const uint32_t slot16 = (uint32_t)geo.slot >> 4, foff16 = (uint32_t)geo.f_off >> 4;
       const uint32_t ring16 = su32(smem) >> 4;
       const uint32_t v16a = su32(smem + geo.v0) >> 4, v16b = su32(smem + geo.v0 + geo.vsz) >> 4;
-      int slot = 0, t = 0, acc = 0, vb = 0;
-      uint32_t s16 = ring16;                                    // (address of the ring slot) >> 4
-      uint32_t phase = 0, tphase = 1, vphase = 0;               // full[slot], tempty[acc] (^1), vfull[vb]
-      const int nu = (int)units;
-      for (int u = 0; u < nu; ++u) {
-        if (t == 0) mbar_wait(&vfull[vb], vphase);
-        mbar_wait(&full[slot], phase);
-        mbar_wait(&tempty[acc], tphase);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t d = tmem + (uint32_t)(acc * R_B);
-        const bool last = t == ntiles - 1;
-        if (elect_one()) {
-          // D(c, r) = S(r, c): A = the S tile (M = columns, K = 16 rows = 2 row groups;
-          // LBO = 2048 B to the next row group, SBO = 128 B to the next 8 columns)
-#pragma unroll
-          for (int b = 0; b < RG_B / 2; ++b)
-            mma_f16(d + (uint32_t)(16 * b), mkdesc(lo_s | (s16 + (uint32_t)(b * 256)), hi_s), dI, id16, 0u);
-          // D -= F V^T in 3 hi / lo products per K chunk (operands pre-negated)
-          const uint32_t f16 = lo_o | (s16 + foff16), w16 = lo_o | (vb ? v16b : v16a);
-          for (int kc = 0; kc < kch; ++kc) {
-            const uint32_t fh = f16 + (uint32_t)(kc * 2 * (CH_BYTES >> 4)), fl = fh + (CH_BYTES >> 4);
-            const uint32_t vh = w16 + (uint32_t)(kc * 2 * (CH_BYTES >> 4)), vl = vh + (CH_BYTES >> 4);
-            mma_f16(d, mkdesc(fh, hi_o), mkdesc(vh, hi_o), id128, 1u);
-            mma_f16(d, mkdesc(fh, hi_o), mkdesc(vl, hi_o), id128, 1u);
-            mma_f16(d, mkdesc(fl, hi_o), mkdesc(vh, hi_o), id128, 1u);
-          }
-          mma_commit(&tfull[acc]);
-          if (!p.store) mma_commit(&empty[slot]);
-          if (last) mma_commit(&vempty[vb]);
+      int slot = w % NST;                                       // ring slot of this warp's next unit
+      uint32_t phase = (uint32_t)((w / NST) & 1);
+      uint32_t vphase = 0;
+      int ubase = 0;                                            // first unit of the row block
+      for (int rbi = 0; rbi < nrbc; ++rbi) {
+        const int vb = rbi & 1;
+        mbar_wait(&vfull[vb], vphase);
+        if (w >= ntiles) {                                      // (one tile per block: nothing for the odd issuer)
+          if (lane == 0) mbar_arrive(&vempty[vb]);
+          __syncwarp();
         }
-        __syncwarp();
-        s16 += slot16;
-        if (++slot == NST) { slot = 0; phase ^= 1; s16 = ring16; }
-        if (++acc == NACC) { acc = 0; tphase ^= 1; }
-        if (last) { t = 0; if (vb) vphase ^= 1; vb ^= 1; } else ++t;
+        const uint32_t w16 = lo_o | (vb ? v16b : v16a);
+        for (int t = w; t < ntiles; t += 2) {
+          const int u = ubase + t;
+          const int acc = u & (NACC - 1);
+          mbar_wait(&full[slot], phase);
+          mbar_wait(&tempty[acc], (uint32_t)(((u >> 2) & 1) ^ 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t d = tmem + (uint32_t)(acc * R_B);
+          const uint32_t s16 = ring16 + (uint32_t)slot * slot16;
+          const bool last = t + 2 >= ntiles;
+          if (elect_one()) {
+            // D(c, r) = S(r, c): A = the S tile (M = columns, K = 16 rows = 2 row groups;
+            // LBO = 2048 B to the next row group, SBO = 128 B to the next 8 columns)
+#pragma unroll
+            for (int b = 0; b < RG_B / 2; ++b)
+              mma_f16(d + (uint32_t)(16 * b), mkdesc(lo_s | (s16 + (uint32_t)(b * 256)), hi_s), dI, id16, 0u);
+            // D -= F V^T in 3 hi / lo products per K chunk (operands pre-negated)
+            const uint32_t f16 = lo_o | (s16 + foff16);
+            for (int kc = 0; kc < kch; ++kc) {
+              const uint32_t fh = f16 + (uint32_t)(kc * 2 * (CH_BYTES >> 4)), fl = fh + (CH_BYTES >> 4);
+              const uint32_t vh = w16 + (uint32_t)(kc * 2 * (CH_BYTES >> 4)), vl = vh + (CH_BYTES >> 4);
+              mma_f16(d, mkdesc(fh, hi_o), mkdesc(vh, hi_o), id128, 1u);
+              mma_f16(d, mkdesc(fh, hi_o), mkdesc(vl, hi_o), id128, 1u);
+              mma_f16(d, mkdesc(fl, hi_o), mkdesc(vh, hi_o), id128, 1u);
+            }
+            mma_commit(&tfull[acc]);
+            if (!p.store) mma_commit(&empty[slot]);
+            if (last) mma_commit(&vempty[vb]);
+          }
+          __syncwarp();
+          // this warp's next unit is 2 further in the block, or its first tile of the next block
+          int step = last ? ntiles - t + w : 2;
+          slot += step;
+          while (slot >= NST) { slot -= NST; phase ^= 1; }
+        }
+        ubase += ntiles;
+        if (vb) vphase ^= 1;
       }
     }
   } else if (warp == UWARP) {
