@@ -55,6 +55,7 @@ constexpr int EPI_GW = EPI_WARPS / NGRP;   // warps per group: 4 lane quarters x
 constexpr int TPG_MAX = 8;          // tiles per group (n - j <= 2048)
 constexpr int BLOCK = 32 * (2 + EPI_WARPS + 2);   // + producer, 2 MMA issuers, u warp
 constexpr int NACC = 4;             // TMEM accumulators
+constexpr int NVB_MAX = 3;          // row-block buffers (V operand + pivot column)
 constexpr int TMEM_COLS = R_B * NACC;
 constexpr int S_BYTES = C_T * R_B * 2;   // one fp16 unit tile (32 KB)
 constexpr int CH_BYTES = 4096;      // one K chunk (16) of a 128-row / 128-column operand, fp16
@@ -138,7 +139,7 @@ __device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
 struct Geo {
   int slot;        // bytes per ring slot: the S unit tile (32 KB), then the tile's F operand (hi, lo)
   int f_off;
-  int v0;          // per-row-block buffers (2): V operand (hi, lo) x kchw chunks, then the pivot column
+  int v0;          // per-row-block buffers (nvb): V operand (hi, lo) x kchw chunks, then the pivot column
   int vsz;         // bytes of one row-block buffer
   int pcol;        // pivot column offset inside a row-block buffer (16 row groups x 16 B)
   int ident;       // 16 x 16 identity operand (512 B)
@@ -147,18 +148,18 @@ struct Geo {
   int bars;
   int total;
 };
-__host__ __device__ inline Geo geo_of(int kchw, int nst) {
+__host__ __device__ inline Geo geo_of(int kchw, int nst, int nvb) {
   Geo g;
   g.f_off = S_BYTES;
   g.slot = S_BYTES + 2 * kchw * CH_BYTES;
   g.v0 = nst * g.slot;
   g.pcol = 2 * kchw * CH_BYTES;
   g.vsz = g.pcol + RG_B * 16;
-  g.ident = g.v0 + 2 * g.vsz;
+  g.ident = g.v0 + nvb * g.vsz;
   g.ubuf = g.ident + 512;
   g.fj = g.ubuf + 2 * R_B * 4;
   g.bars = g.fj + 2 * 32 * 4;
-  g.total = g.bars + (2 * nst + 2 * NACC + 8) * 8 + 16;
+  g.total = g.bars + (2 * nst + 2 * NACC + 2 * NVB_MAX + 4) * 8 + 16;
   return g;
 }
 }  // namespace
@@ -170,6 +171,8 @@ struct TcParams {
   int64_t rb_first;    // first 128-row block holding rows >= j (local)
   int64_t nrb;         // row blocks from rb_first to the end
   int n, j, j0, npend, store, kchw, nst, ntiles;
+  int nvb;                    // row-block buffers: 3 lets the u warp run a block ahead of the MMAs
+  int nmma;                   // MMA issuer warps (2 needs an even ring depth: one consumer per slot)
   unsigned char* Vop;         // [m_pad / 128][kchw][hi 4 KB | lo 4 KB]
   int lnext;                  // V operand column of u_j for the next step (j mod nb)
   const unsigned char* Fop;   // [ntiles][kchw][hi 4 KB | lo 4 KB]
@@ -187,14 +190,15 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
   extern __shared__ __align__(128) unsigned char smem[];
   const int n = p.n, j = p.j, NST = p.nst, kchw = p.kchw, ntiles = p.ntiles, npend = p.npend;
   const int kch = (npend + 15) >> 4;             // K chunks holding pending reflectors
-  const Geo geo = geo_of(kchw, NST);
+  const int NVB = p.nvb;
+  const Geo geo = geo_of(kchw, NST, NVB);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + geo.bars);
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + NACC;
   uint64_t* vfull = tempty + NACC;
-  uint64_t* vempty = vfull + 2;
-  uint64_t* ufull = vempty + 2;
+  uint64_t* vempty = vfull + NVB_MAX;
+  uint64_t* ufull = vempty + NVB_MAX;
   uint64_t* ufree = ufull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ufree + 2);
   float* ubuf = reinterpret_cast<float*>(smem + geo.ubuf);
@@ -217,9 +221,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], EPI_GW);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NVB_MAX; ++b) {
       mbar_init(&vfull[b], 1);
-      mbar_init(&vempty[b], 2);          // each MMA issuer's commit after its last unit of the row block
+      mbar_init(&vempty[b], p.nmma);          // each MMA issuer's commit after its last unit of the row block
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&ufull[b], 1);
       mbar_init(&ufree[b], EPI_WARPS);
     }
@@ -326,8 +332,8 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
     // path of the pass: ~1 us per unit).  Units use disjoint accumulators and ring slots, and
     // tcgen05.commit tracks the issuing thread's own MMAs, so the two need no mutual ordering.
     // Descriptors are (constant high word, low word = constant + (shared address >> 4)).
-    if (units > 0) {
-      const int w = warp == 1 ? 0 : 1;
+    const int w = warp == 1 ? 0 : 1, NM = p.nmma;
+    if (units > 0 && w < NM) {
       const uint32_t id16 = idesc_f16(16), id128 = idesc_f16(R_B);
       auto mkdesc = [](uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | (uint64_t)lo; };
       const uint32_t hi_s = (128u >> 4) | (1u << 14);           // SBO = 128 B, descriptor version
@@ -337,20 +343,20 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
       const uint64_t dI = mkdesc(lo_o | (su32(smem + geo.ident) >> 4), hi_o);
       const uint32_t slot16 = (uint32_t)geo.slot >> 4, foff16 = (uint32_t)geo.f_off >> 4;
       const uint32_t ring16 = su32(smem) >> 4;
-      const uint32_t v16a = su32(smem + geo.v0) >> 4, v16b = su32(smem + geo.v0 + geo.vsz) >> 4;
+      const uint32_t v16 = su32(smem + geo.v0) >> 4, vsz16 = (uint32_t)geo.vsz >> 4;
       int slot = w % NST;                                       // ring slot of this warp's next unit
       uint32_t phase = (uint32_t)((w / NST) & 1);
       uint32_t vphase = 0;
+      int vb = 0;
       int ubase = 0;                                            // first unit of the row block
       for (int rbi = 0; rbi < nrbc; ++rbi) {
-        const int vb = rbi & 1;
         mbar_wait(&vfull[vb], vphase);
         if (w >= ntiles) {                                      // (one tile per block: nothing for the odd issuer)
           if (lane == 0) mbar_arrive(&vempty[vb]);
           __syncwarp();
         }
-        const uint32_t w16 = lo_o | (vb ? v16b : v16a);
-        for (int t = w; t < ntiles; t += 2) {
+        const uint32_t w16 = lo_o | (v16 + (uint32_t)vb * vsz16);
+        for (int t = w; t < ntiles; t += NM) {
           const int u = ubase + t;
           const int acc = u & (NACC - 1);
           mbar_wait(&full[slot], phase);
@@ -358,7 +364,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t d = tmem + (uint32_t)(acc * R_B);
           const uint32_t s16 = ring16 + (uint32_t)slot * slot16;
-          const bool last = t + 2 >= ntiles;
+          const bool last = t + NM >= ntiles;
           if (elect_one()) {
             // D(c, r) = S(r, c): A = the S tile (M = columns, K = 16 rows = 2 row groups;
             // LBO = 2048 B to the next row group, SBO = 128 B to the next 8 columns)
@@ -380,12 +386,12 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
           }
           __syncwarp();
           // this warp's next unit is 2 further in the block, or its first tile of the next block
-          int step = last ? ntiles - t + w : 2;
+          const int step = last ? ntiles - t + w : NM;
           slot += step;
           while (slot >= NST) { slot -= NST; phase ^= 1; }
         }
         ubase += ntiles;
-        if (vb) vphase ^= 1;
+        if (++vb == NVB) { vb = 0; vphase ^= 1; }
       }
     }
   } else if (warp == UWARP) {
@@ -398,8 +404,8 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
     // steps' V operand).
     const uint32_t fbytes = (uint32_t)(kch * 2 * CH_BYTES);
     auto issue_v = [&](int rbi) {
-      const int vb = rbi & 1;
-      if (rbi >= 2) mbar_wait(&vempty[vb], (uint32_t)(((rbi - 2) >> 1) & 1));   // MMA done with rbi - 2
+      const int vb = rbi % NVB;
+      if (rbi >= NVB) mbar_wait(&vempty[vb], (uint32_t)(((rbi - NVB) / NVB) & 1));   // MMAs done with rbi - NVB
       unsigned char* vbuf = smem + geo.v0 + vb * geo.vsz;
       if (elect_one()) {
         mbar_expect_tx(&vfull[vb], fbytes + RG_B * 16);
@@ -411,9 +417,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
     if (nrbc > 0) issue_v(0);
     if (nrbc > 1) issue_v(1);
     for (int rbi = 0; rbi < nrbc; ++rbi) {
-      const int vb = rbi & 1, ub = rbi & 1;
+      const int vb = rbi % NVB, ub = rbi & 1;
       const int64_t r0 = (p.rb_first + rb0 + rbi) * R_B;
-      mbar_wait(&vfull[vb], (uint32_t)((rbi >> 1) & 1));
+      mbar_wait(&vfull[vb], (uint32_t)((rbi / NVB) & 1));
       if (rbi >= 2) mbar_wait(&ufree[ub], (uint32_t)(((rbi - 2) >> 1) & 1));
       const unsigned char* vbuf = smem + geo.v0 + vb * geo.vsz;
       const __half* pc = reinterpret_cast<const __half*>(vbuf + geo.pcol);   // [16 groups][8 rows]
@@ -460,7 +466,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&ufull[ub]);
-      if (rbi + 2 < nrbc) issue_v(rbi + 2);          // into this buffer once the MMA is done with it
+      // the load two blocks ahead: with 2 buffers into this block's own buffer (it waits for the
+      // MMAs of block rbi, so u of block rbi + 1 is formed only after them and the epilogue
+      // idles at every row-block boundary); with 3 into the buffer of block rbi - 1
+      if (rbi + 2 < nrbc) issue_v(rbi + 2);
     }
   } else if (warp >= 2 && warp < 2 + EPI_WARPS) {
     // ============================ epilogue ============================
@@ -621,12 +630,15 @@ int tc_kchw(int nb) { return (nb + 15) / 16; }
 size_t tc_vop_bytes(int64_t m_pad, int nb) { return (size_t)(m_pad / 128 + 1) * tc_kchw(nb) * 2 * CH_BYTES; }
 size_t tc_fop_bytes(int n, int nb) { return (size_t)((n + C_T - 1) / C_T) * tc_kchw(nb) * 2 * CH_BYTES; }
 
-int tc_smem_bytes(int nb, int* nst_out) {
+int tc_smem_bytes(int nb, int nvb, int* nst_out) {
   const int kchw = tc_kchw(nb);
-  int nst = 4;
-  while (nst > 2 && geo_of(kchw, nst).total > TC_SMEM_MAX) --nst;
+  // as deep a ring as shared memory holds (4 slots of 40 KB at nb <= 16; 5 measured < 1 ms better per C4 QRCP and forces one MMA issuer): with ~3 us between a
+  // load's issue and its slot's release, the bytes in flight bound the pass (MPID_TC_NST: A/B)
+  static const int nst_env = getenv("MPID_TC_NST") ? atoi(getenv("MPID_TC_NST")) : 4;
+  int nst = nst_env < 2 ? 2 : (nst_env > 6 ? 6 : nst_env);
+  while (nst > 2 && geo_of(kchw, nst, nvb).total > TC_SMEM_MAX) --nst;
   if (nst_out) *nst_out = nst;
-  return geo_of(kchw, nst).total;
+  return geo_of(kchw, nst, nvb).total;
 }
 
 cudaError_t launch_pass_tc(const PassParams& pp, int nb, void* Vop, const void* Fop, const void* tmap,
@@ -646,8 +658,15 @@ cudaError_t launch_pass_tc(const PassParams& pp, int nb, void* Vop, const void* 
   p.kchw = tc_kchw(nb);
   p.ntiles = (pp.n - pp.j + C_T - 1) / C_T;
   if (p.npend > p.kchw * 16 || p.kchw > 2 || p.ntiles > 16) return cudaErrorInvalidValue;
+  static const int nvb_env = getenv("MPID_TC_NVB") ? atoi(getenv("MPID_TC_NVB")) : 3;   // A/B measurements
+  p.nvb = nvb_env == 2 ? 2 : NVB_MAX;
+  if (p.nvb == 3 && geo_of(p.kchw, 4, 3).total > TC_SMEM_MAX) p.nvb = 2;   // keep the 4-deep ring (nb > 16)
   int nst = 0;
-  const int smem = tc_smem_bytes(nb, &nst);
+  const int smem = tc_smem_bytes(nb, p.nvb, &nst);
+  // two issuers split the tiles by parity; a ring slot must keep ONE consumer warp (an mbarrier
+  // parity wait cannot tell phase k from k + 2), which holds only for an even ring depth
+  static const int nmma_env = getenv("MPID_TC_NMMA") ? atoi(getenv("MPID_TC_NMMA")) : 0;   // A/B measurements
+  p.nmma = (nst & 1) ? 1 : (nmma_env == 1 ? 1 : 2);
   if (smem > TC_SMEM_MAX) return cudaErrorInvalidConfiguration;
   p.nst = nst;
   p.Vop = (unsigned char*)Vop;

@@ -20,7 +20,7 @@ ts.sort()
 print("%%s qrcp min %%.2f median %%.2f ms piv[:6]=%%s" %% (os.environ.get("TAG"), ts[0], ts[len(ts)//2], list(q.piv[:6])), flush=True)
 ''' % ROOT
 # (libmpid_base.so: a build of the previous commit, copied beside libmpid.so by hand)
-combos = [("base", {"MPID_LIB": "libmpid_base.so"}), ("new", {})]
+combos = [("nvb2", {"MPID_TC_NVB": "2"}), ("nvb3", {})]
 for tag, env in combos * int(sys.argv[1] if len(sys.argv) > 1 else 1):
     e = dict(os.environ, TAG=tag, **env)
     r = subprocess.run([sys.executable, "-c", CHILD], env=e, capture_output=True, text=True, timeout=600)
