@@ -21,7 +21,7 @@
 //   V holds the pending u_l (rows < l zero) and F the pending c_l f_l, so V F^T =
 //   sum_l v_l f_l^T with v_l = c_l u_l (Householder vector, v_l(l) = 1 in exact arithmetic).
 //
-// B200 structure: one persistent CTA per SM, 19 warps, warp-specialised.  A CTA owns a
+// B200 structure: one persistent CTA per SM, 20 warps, warp-specialised.  A CTA owns a
 // contiguous range of 128-row blocks and walks, per row block, all column tiles of 128
 // (tile 0 starts at column j, so its TMEM lane 0 is the pivot column): unit = (row block,
 // tile).
@@ -29,13 +29,17 @@
 //               groups = 32 KB) + the tile's F operand (bulk copy, L2-resident); per row
 //               block the V operand (bulk copy).  NST-deep ring; on store steps the
 //               rounded tile is written back by a tensor-map store before the slot is reused.
-//   warp 1      MMA issuer (one thread): 8 identity MMAs + 3 x ceil(npend / 16) formation
-//               MMAs per unit into one of 4 TMEM accumulators (128 columns each).
+//   warps 1, 19 MMA issuers (one elected thread each; even / odd tiles of every row block): 8
+//               identity MMAs + 3 x ceil(npend / 16) formation MMAs per unit into one of 4
+//               TMEM accumulators (128 columns each).  Their per-unit instruction stream is
+//               the pass's critical path: counters are incremental, descriptors constant + address.
 //   warps 2-17  epilogue, 2 groups of 8 warps (4 TMEM lane quarters x 2 row halves); group g
 //               takes the tiles t = g mod 2, so each thread owns one column per tile and keeps
-//               its column sums in registers for the whole launch.
-//   warp 18     the u warp: each row block's V operand and pivot column, u = S(:, j) - V F(j, :)^T
-//               on CUDA cores, published to shared memory and to the V operand of the next steps.
+//               its column sums in registers for the whole launch; units without store, pivot
+//               row or masked rows take a branch-free unrolled path.
+//   warp 18     the u warp: each row block's V operand and pivot column (3 buffers: it runs a block
+//               ahead of the issuers), u = S(:, j) - V F(j, :)^T on CUDA cores, published to
+//               shared memory and to the V operand of the next steps.
 // Bound: HBM — (m - j)(n - j) 2 bytes read per step (+ the same written on store steps);
 // tensor work per element: 32 flops (identity) + 6 * 16 * ceil(npend / 16) (formation).
 #include "mpid_internal.cuh"
@@ -52,7 +56,6 @@ constexpr int RG_B = R_B / 8;       // row groups per row block
 constexpr int EPI_WARPS = 16;
 constexpr int NGRP = 2;             // epilogue groups: group g takes the tiles t = g mod 2
 constexpr int EPI_GW = EPI_WARPS / NGRP;   // warps per group: 4 lane quarters x 2 row halves
-constexpr int TPG_MAX = 8;          // tiles per group (n - j <= 2048)
 constexpr int BLOCK = 32 * (2 + EPI_WARPS + 2);   // + producer, 2 MMA issuers, u warp
 constexpr int NACC = 4;             // TMEM accumulators
 constexpr int NVB_MAX = 3;          // row-block buffers (V operand + pivot column)
@@ -63,16 +66,10 @@ constexpr int UWARP = 2 + EPI_WARPS;  // the pivot-column (u) warp
 constexpr int MMA2 = UWARP + 1;       // the second MMA issuer (odd tiles; warp 1 takes the even ones)
 constexpr int TC_SMEM_MAX = 227 * 1024;   // the sm_100 opt-in maximum of dynamic shared memory per block
 
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  // K-major, no swizzle; LBO = byte stride between core matrices adjacent along K, SBO =
-  // along M / N; bit 46 = the sm_100 descriptor version
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;
-  return d;
-}
+// Shared-memory matrix descriptors (K-major, no swizzle) are built in the issuer loop as two
+// 32-bit words: low = (address >> 4) | (LBO >> 4) << 16 (LBO = byte stride between core
+// matrices adjacent along K), high = (SBO >> 4) | 1 << 14 (SBO = stride along M / N; bit 46 of
+// the descriptor = the sm_100 descriptor version).
 // kind::f16: fp16 A and B, fp32 accumulator, both K-major, M = 128, N given
 __device__ __forceinline__ uint32_t idesc_f16(int N) {
   return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(C_T >> 4) << 24);
@@ -87,18 +84,6 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem, uint64_t da, uint64_t db,
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
                : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-  uint32_t* r = reinterpret_cast<uint32_t*>(v);
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
@@ -329,8 +314,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass_tc(TcParams p, const __grid_c
     // ============================ MMA issuers ============================
     // Two converged warps, one elected lane each: warp 1 issues the even tiles of every row
     // block, warp MMA2 the odd ones (a single issuer's instruction stream was the critical
-    // path of the pass: ~1 us per unit).  Units use disjoint accumulators and ring slots, and
-    // tcgen05.commit tracks the issuing thread's own MMAs, so the two need no mutual ordering.
+    // path of the pass: ~1 us per unit).  With an even tile count and ring depth (the launcher
+    // checks; otherwise NM = 1) the even and odd units use disjoint accumulators, ring slots
+    // and epilogue groups, and tcgen05.commit tracks the issuing thread's own MMAs, so the two
+    // pipelines need no mutual ordering.
     // Descriptors are (constant high word, low word = constant + (shared address >> 4)).
     const int w = warp == 1 ? 0 : 1, NM = p.nmma;
     if (units > 0 && w < NM) {
@@ -632,8 +619,8 @@ size_t tc_fop_bytes(int n, int nb) { return (size_t)((n + C_T - 1) / C_T) * tc_k
 
 int tc_smem_bytes(int nb, int nvb, int* nst_out) {
   const int kchw = tc_kchw(nb);
-  // as deep a ring as shared memory holds (4 slots of 40 KB at nb <= 16; 5 measured < 1 ms better per C4 QRCP and forces one MMA issuer): with ~3 us between a
-  // load's issue and its slot's release, the bytes in flight bound the pass (MPID_TC_NST: A/B)
+  // ring depth 4 (40 KB slots at nb <= 16); 5 fits but measured < 1 ms better per C4 QRCP and,
+  // being odd, forces one MMA issuer (MPID_TC_NST: A/B measurements)
   static const int nst_env = getenv("MPID_TC_NST") ? atoi(getenv("MPID_TC_NST")) : 4;
   int nst = nst_env < 2 ? 2 : (nst_env > 6 ? 6 : nst_env);
   while (nst > 2 && geo_of(kchw, nst, nvb).total > TC_SMEM_MAX) --nst;
@@ -663,10 +650,13 @@ cudaError_t launch_pass_tc(const PassParams& pp, int nb, void* Vop, const void* 
   if (p.nvb == 3 && geo_of(p.kchw, 4, 3).total > TC_SMEM_MAX) p.nvb = 2;   // keep the 4-deep ring (nb > 16)
   int nst = 0;
   const int smem = tc_smem_bytes(nb, p.nvb, &nst);
-  // two issuers split the tiles by parity; a ring slot must keep ONE consumer warp (an mbarrier
-  // parity wait cannot tell phase k from k + 2), which holds only for an even ring depth
+  // Two issuers split the tiles by parity.  A ring slot (u % nst) and an accumulator (u % 4) must
+  // keep ONE issuer warp and ONE epilogue group over their successive uses — an mbarrier parity
+  // wait cannot tell phase k from k + 2, and only a single in-order issuer guarantees that use
+  // k has completed before anyone waits for use k + 1 — which holds when tile parity = unit
+  // parity: an even ring depth AND an even tile count.  Otherwise one issuer takes all tiles.
   static const int nmma_env = getenv("MPID_TC_NMMA") ? atoi(getenv("MPID_TC_NMMA")) : 0;   // A/B measurements
-  p.nmma = (nst & 1) ? 1 : (nmma_env == 1 ? 1 : 2);
+  p.nmma = ((nst & 1) || (p.ntiles & 1)) ? 1 : (nmma_env == 1 ? 1 : 2);
   if (smem > TC_SMEM_MAX) return cudaErrorInvalidConfiguration;
   p.nst = nst;
   p.Vop = (unsigned char*)Vop;
