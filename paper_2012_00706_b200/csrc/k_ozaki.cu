@@ -127,13 +127,22 @@ __device__ __forceinline__ double pow2(int e) {   // 2^e for -1022 <= e <= 1023
 }
 // byte-wise two's complement negation of 4 digits in [0, 127]
 __device__ __forceinline__ uint32_t neg4(uint32_t b) { return (0x80808080u - b) ^ 0x80808080u; }
-// digits of x at scale sc = 2^{56-E}: w0 = slices 0..3 (byte p = slice p), w1 = slices 4..7
+// digits of x at scale sc = 2^{56-E} (or 0): w0 = slices 0..3 (byte p = slice p), w1 = slices 4..7.
+// X = floor(|x| sc) < 2^56 is taken from the bit pattern with integer shifts — the fp64 pipe
+// (a DMUL and a 64-bit F2I per value) was the slicer warps' top stall in ncu's warp-state
+// sampling of k_oz_tn: |x| = M 2^(e-1075) with M the 53-bit significand, sc = 2^(es-1023), so
+// X = M >> (2098 - es - e) (a left shift of at most 3 when |x| is within 2^-3 of 2^E).
 __device__ __forceinline__ void oz_digits(double x, double sc, uint32_t& w0, uint32_t& w1) {
-  const unsigned long long X = __double2ull_rz(fabs(x) * sc);   // < 2^56 (power-of-two scale: exact)
+  const uint32_t xh = (uint32_t)__double2hiint(x), xl = (uint32_t)__double2loint(x);
+  const uint32_t e = (xh >> 20) & 0x7FFu;
+  const int es = (int)(((uint32_t)__double2hiint(sc) >> 20) & 0x7FFu);   // loop-invariant
+  const unsigned long long M = ((unsigned long long)((xh & 0xFFFFFu) | (e ? 0x100000u : 0u)) << 32) | xl;
+  const int sh = 2098 - es - (int)(e ? e : 1u);                          // subnormals: exponent 1, no hidden bit
+  const unsigned long long X = sh >= 64 ? 0ull : (sh >= 0 ? M >> sh : M << (-sh));
   const uint32_t hi = (uint32_t)(X >> 28), lo = (uint32_t)X & 0x0FFFFFFFu;
   uint32_t b0 = (hi >> 21) | (((hi >> 14) & 127u) << 8) | (((hi >> 7) & 127u) << 16) | ((hi & 127u) << 24);
   uint32_t b1 = (lo >> 21) | (((lo >> 14) & 127u) << 8) | (((lo >> 7) & 127u) << 16) | ((lo & 127u) << 24);
-  if (x < 0.0) {
+  if (xh >> 31) {                                  // (-0.0: all digits 0, their negation too)
     b0 = neg4(b0);
     b1 = neg4(b1);
   }
