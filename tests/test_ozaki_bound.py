@@ -97,3 +97,32 @@ def test_int32_to_fp64_magic_conversion_is_exact():
         d = struct.unpack("<d", struct.pack("<Q", bits))[0]
         assert d - const == a
     assert const == 6755401588539392.0       # the constant in k_ozaki.cu's i2d
+
+
+def test_digit_word_from_the_bit_pattern():
+    """Claim 5 (k_ozaki.cu oz_digits): X = floor(|x| 2^(56-E)) equals the 53-bit significand M
+    of x shifted right by 2098 - es - e, with e the biased exponent of x (1 and no hidden bit
+    for subnormals) and es the biased exponent of the scale 2^(56-E); the shift is never below
+    -3 because |x| < 2^E.  Exact integers against the Fraction definition above."""
+    rng = np.random.default_rng(7)
+    for trial in range(60):
+        x = rng.standard_normal(300) * 10.0 ** int(rng.integers(-280, 280))
+        x[rng.integers(0, 300, 10)] = 0.0
+        x[rng.integers(0, 300, 5)] *= 2.0 ** -45
+        if trial % 6 == 0:
+            x = x * 2.0 ** -1000 * 2.0 ** -50            # subnormals
+        if trial % 6 == 1:
+            x[0] = math.ldexp(1.0 - 2.0 ** -53, 10)      # just below a power of two
+        E = exp_of(float(np.abs(x).max()))
+        if not (-1022 <= 56 - E <= 1023):
+            continue
+        es = (struct.unpack("<Q", struct.pack("<d", math.ldexp(1.0, 56 - E)))[0] >> 52) & 0x7FF
+        for v in x:
+            bits = struct.unpack("<Q", struct.pack("<d", float(v)))[0]
+            e = (bits >> 52) & 0x7FF
+            M = (bits & ((1 << 52) - 1)) | ((1 << 52) if e else 0)
+            sh = 2098 - es - (e if e else 1)
+            assert sh >= -3
+            X = 0 if sh >= 64 else (M >> sh if sh >= 0 else M << -sh)
+            assert X == int(Fraction(abs(float(v))) * Fraction(2) ** (56 - E))
+            assert X < 2 ** 56
